@@ -1,0 +1,164 @@
+/* vpx.h -- C ABI of the B200-native voxpar hot path (libvpx.so).
+ *
+ * Every entry point takes plain device pointers, extents and a cudaStream_t
+ * (passed as void*), launches stream-ordered asynchronous work with no hidden
+ * synchronisation, never allocates or frees caller buffers, and returns an int
+ * status: 0 on success, a negative VPX_ERR_* code otherwise, with a message
+ * available from vpx_last_error().  The status codes map 1:1 onto the
+ * reference's exception taxonomy (reference pkg/src/voxpar/errors.py:4-77).
+ *
+ * Layout conventions:
+ *   activations  NDHWC fp32, stored in a halo frame [N][D+2md][H+2mh][W+2mw][C]
+ *                whose margins m* are 1 in partitioned dims and 0 elsewhere;
+ *   conv weights "OTI": [Cout][kd][kh][kw][Cin] fp32 (the reference keeps OIDHW,
+ *                reference layers/reference.py:68; vpx_layout_* converts).
+ *
+ * The reference's kernel boundary this replaces is
+ *   voxpar.kernels.conv3d_fwd / conv3d_bwd_data / conv3d_bwd_filter
+ *   (reference pkg/src/voxpar/kernels/__init__.py:63-72) and its native
+ *   Cython ABI _hot.conv3d_* (reference pkg/src/voxpar/kernels/_hot.pyx:19-93).
+ */
+#ifndef VPX_H_
+#define VPX_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes (errors.py names) */
+#define VPX_OK 0
+#define VPX_ERR_SHAPE_MISMATCH -1   /* errors.ShapeMismatch  (errors.py:23) */
+#define VPX_ERR_NON_DIVISIBLE -2    /* errors.NonDivisible   (errors.py:8)  */
+#define VPX_ERR_OUT_OF_BOUNDS -3    /* errors.OutOfBounds    (errors.py:19) */
+#define VPX_ERR_LENGTH_MISMATCH -4  /* errors.LengthMismatch (errors.py:27) */
+#define VPX_ERR_UNSUPPORTED -5      /* shape outside what the sm_100a kernels implement */
+#define VPX_ERR_CUDA -6             /* CUDA runtime / driver failure */
+
+/* Message for the last non-zero status returned on this thread. */
+const char* vpx_last_error(void);
+/* Library build tag (architecture, git revision). */
+const char* vpx_version(void);
+
+/* ------------------------------------------------------------ convolution --
+ * Frames are described by int[8] = {n, c, d, h, w, md, mh, mw}: interior extents
+ * and per-dimension halo margins (0 or 1); storage [n][d+2md][h+2mh][w+2mw][c].
+ * Weights are OIDHW fp32 [cout][cin][k][k][k] exactly as the reference holds them
+ * (reference layers/reference.py:68). Odd k, stride 1 or 2, "same" padding. */
+
+/* Workspace bytes needed by the three passes for this layer (packed B operand
+ * + filter-gradient partials). ufr describes the upstream-gradient frame. */
+long long vpx_conv3d_workspace_bytes(int cin, int cout, int k, const int* ufr);
+
+/* y = conv(x, w): replaces voxpar.kernels.conv3d_fwd(xpad, w, stride)
+ * (reference kernels/__init__.py:63, _hot.pyx:19-41).  Writes the interior of
+ * the y frame; margins of y are left untouched. */
+int vpx_conv3d_fwd(const float* x, const int* xfr, const float* w, int k, int stride, float* y,
+                   const int* yfr, void* ws, long long ws_bytes, void* stream);
+
+/* xg = adjoint scatter of u through w, over EVERY position of the xg frame
+ * (interior and margins): replaces voxpar.kernels.conv3d_bwd_data(u, w,
+ * stride, pad_spatial) (reference kernels/__init__.py:67, _hot.pyx:44-67). */
+int vpx_conv3d_bwd_data(const float* u, const int* ufr, const float* w, int k, int stride,
+                        float* xg, const int* gfr, void* ws, long long ws_bytes, void* stream);
+
+/* wg (=|+=) sum over voxels of u (x) x-patches; x frame margins must hold the
+ * exchanged halos.  Replaces voxpar.kernels.conv3d_bwd_filter(xpad, u, stride,
+ * kernel) (reference kernels/__init__.py:71, _hot.pyx:70-93).  Deterministic. */
+int vpx_conv3d_bwd_filter(const float* x, const int* xfr, const float* u, const int* ufr, int k,
+                          int stride, float* wg, int accumulate, void* ws, long long ws_bytes,
+                          void* stream);
+
+/* ------------------------------------------------------- pointwise / pool --
+ * reference layers/reference.py:149-236, layers/distributed.py:132-214.
+ * All read/write frame interiors; is_max selects max (ties -> lowest index in
+ * (d,h,w) C order) vs average 2^3 stride-2 pooling. */
+int vpx_leaky_fwd(const float* x, const int* xf, float* y, const int* yf, float slope, void* stream);
+int vpx_leaky_bwd(const float* x, const int* xf, const float* u, const int* uf, float* g,
+                  const int* gf, float slope, void* stream);
+int vpx_pool_fwd(const float* x, const int* xf, float* y, const int* yf, int is_max, void* stream);
+int vpx_pool_bwd(const float* x, const int* xf, const float* u, const int* uf, float* g,
+                 const int* gf, int is_max, void* stream);
+int vpx_concat(const float* a, const int* af, const float* b, const int* bf, float* y, const int* yf,
+               void* stream);
+int vpx_split(const float* u, const int* uf, float* ga, const int* gaf, float* gb, const int* gbf,
+              int acc_b, void* stream);
+int vpx_add(const float* x, const int* xf, float* y, const int* yf, void* stream);
+int vpx_copy(const float* x, const int* xf, float* y, const int* yf, void* stream);
+
+/* -------------------------------------------------------------- batchnorm --
+ * reference layers/reference.py:188-226, layers/distributed.py:152-201.
+ * vpx_bn_sums: mode 0 -> out2c = [sum x, sum x^2]; mode 1 -> [sum u, sum u*xhat]
+ * (xhat recomputed from x, mean, inv).  Local partials only: the caller
+ * allreduces out2c over the tensor's rank group.  ws >= vpx_bn_workspace_bytes. */
+long long vpx_bn_workspace_bytes(int c);
+int vpx_bn_sums(const float* x, const int* xf, const float* u, const int* uf, const float* mean,
+                const float* inv, int mode, float* out2c, void* ws, void* stream);
+int vpx_bn_stats(const float* sums, int c, double count, float eps, float momentum, float* mean,
+                 float* inv, float* run_mean, float* run_var, void* stream);
+int vpx_bn_apply(const float* x, const int* xf, const float* mean, const float* inv,
+                 const float* gamma, const float* beta, float* y, const int* yf, void* stream);
+int vpx_bn_bwd_apply(const float* x, const int* xf, const float* u, const int* uf, const float* mean,
+                     const float* inv, const float* gamma, const float* sums, double count, float* g,
+                     const int* gf, void* stream);
+
+/* ------------------------------------------------- transposed conv k2 s2 --
+ * reference layers/reference.py:99-144 (w is (cin, cout, 2, 2, 2)). */
+long long vpx_deconv_workspace_bytes(int cin, int cout);
+int vpx_deconv_fwd(const float* x, const int* xf, const float* w, float* y, const int* yf,
+                   void* stream);
+int vpx_deconv_bwd_data(const float* u, const int* uf, const float* w, float* g, const int* gf,
+                        void* stream);
+int vpx_deconv_bwd_filter(const float* x, const int* xf, const float* u, const int* uf, float* wg,
+                          int accumulate, void* ws, void* stream);
+
+/* ------------------------------------------------------------------- halo --
+ * Copy the box {z0,y0,x0,ez,ey,ex} (frame coordinates, margins included) of a
+ * frame to a dense (n,z,y,x,c) buffer (mode 0, pack), back (mode 1, unpack) or
+ * accumulate into the frame (mode 2, adjoint unpack).  Replaces the slab copies
+ * of reference fabric.py:404-410,436-442 / tensor.py:388-409. */
+int vpx_halo_copy(float* frame, const int* ff, const int* box6, float* buf, int mode, void* stream);
+
+/* ------------------------------------------------------------------- prng --
+ * Pinned splitmix64 streams (reference prng.py:28-90), bit-exact with numpy:
+ * value i = lo + (hi-lo) * ((mix(key + (i+1)*golden) >> 11) * 2^-53). */
+int vpx_prng_uniform(unsigned long long key, long long n, double lo, double hi, float* out32,
+                     double* out64, void* stream);
+int vpx_prng_mask(unsigned long long key, long long n, double keep, unsigned char* out, void* stream);
+/* Fill a frame interior from the stream whose counter runs over the NCDHW order
+ * of the interior, starting at counter_base (synthetic batches, cli.py:112-125). */
+int vpx_prng_volume(unsigned long long key, const int* ff, long long counter_base, double lo,
+                    double hi, float* frame, void* stream);
+
+/* -------------------------------------------------------------- optimizer --
+ * reference model/optim.py:63-88; c1 = 1-b1^t, c2 = 1-b2^t. */
+int vpx_adam(float* p, const float* g, float* m, float* v, long long n, float lr, float b1, float b2,
+             float c1, float c2, float eps, void* stream);
+int vpx_sgd(float* p, const float* g, long long n, float lr, void* stream);
+
+/* ----------------------------------------------------------------- losses --
+ * Per-voxel softmax cross entropy (reference layers/reference.py:282-307):
+ * g = (softmax - onehot)/count, part[b] = per-block sums of -log p[label]. */
+int vpx_xent(const float* logits, const int* lf, const long long* labels, double count, float* g,
+             const int* gf, double* part, int nparts, void* stream);
+
+/* ----------------------------------------------------------------- layout -- */
+int vpx_layout_ncdhw_to_frame(const float* src, const int* ff, float* frame, void* stream);
+int vpx_layout_frame_to_ncdhw(const float* frame, const int* ff, float* dst, void* stream);
+
+/* ---------------------------------------------------------------- probes --
+ * Test-only entry points used to pin UMMA/TMA semantics on the device. */
+int vpx_probe_umma(const void* img, int img_bytes, const uint64_t* ops, int n_ops, float* out,
+                   int ncols, void* stream);
+int vpx_probe_tma(const void* gsrc, const uint64_t* dims5, const uint64_t* strides4,
+                  const uint32_t* box5, int swizzle, const int32_t* coords5, void* out,
+                  int out_bytes, void* stream);
+int vpx_probe_mma_rate(int N, int n_iter, int a_layout, int n_acc, int bf16, long long* cycles,
+                       void* stream);
+int vpx_probe_mma_rate2(int N, int n_acc, int bf16, int n_iter, long long* cycles, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VPX_H_ */

@@ -1,0 +1,32 @@
+// Shared declarations for the convolution kernels.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace vpx {
+
+// Parameters of one row-window launch (see conv_rowwin.cu).
+struct ConvRowParams {
+  int zlo, zhi;  // output depth range (may extend to -1 / D for dgrad frame margins)
+  int ylo, yhi;  // output row range
+  int nxseg;     // W_out / 128
+  int ngy;       // ceil((yhi - ylo) / R)
+  int num_tiles;
+  int n_groups;  // channel-chunk groups along K
+  // map coordinate of input voxel for output voxel o and tap offset t in {0,1,2}:
+  //   coord = o - 1 + t + in_off
+  int in_off_d, in_off_h, in_off_w;
+  const float* wpack;  // packed B operand, n_groups blocks
+  float* out;
+  long long out_sn, out_sd, out_sh, out_sw;  // element strides of the output frame
+  int out_off_d, out_off_h, out_off_w;       // output voxel o lands at frame index o + off
+};
+
+int num_sms();
+int rowwin_config(int cin, int cout, int* R, int* CG);
+int launch_rowwin_any(const CUtensorMap& xmap, const ConvRowParams& p, int cin, int cout,
+                      cudaStream_t st);
+
+}  // namespace vpx

@@ -1,0 +1,211 @@
+// C-ABI entry points for the convolution passes (include/vpx.h) and the
+// weight-packing kernel that arranges the UMMA B operand for conv_rowwin.cu.
+//
+// Replaces the reference's kernel boundary voxpar.kernels.conv3d_{fwd,
+// bwd_data,bwd_filter} (reference pkg/src/voxpar/kernels/__init__.py:63-72,
+// cyext.py:20-45): same math, device-resident NDHWC halo frames instead of
+// host NCDHW arrays, explicit workspace instead of internal allocation.
+#include "conv_common.h"
+#include "conv_simt.h"
+#include "vpx_host.h"
+
+namespace vpx {
+
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+// Pack OIDHW weights into the row-window B layout.
+//   mode 0 (forward):  Weff[o][i][t] = w[o][i][t]            (O=cout, I=cin)
+//   mode 1 (bwd data): Weff[o][i][t] = w[i][o][26 - t]       (O=cin,  I=cout)
+// non-pair layout [g][t][c<CG][O][4]; pair layout (I == 4) [q<14][h<2][O][4], tap 2q+h.
+__global__ void pack_rowwin_kernel(const float* __restrict__ w, int cout, int cin, int mode,
+                                   int CG, int pair, float* __restrict__ out) {
+  const int O = mode ? cin : cout;
+  const int I = mode ? cout : cin;
+  const long long total = pair ? 28LL * O * 4 : 27LL * I * O;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    long long t = idx;
+    const int e = t % 4;
+    t /= 4;
+    const int o = t % O;
+    t /= O;
+    int tap, i;
+    if (pair) {
+      tap = static_cast<int>(t);  // t = 2q + h
+      i = e;
+    } else {
+      const int c = t % CG;
+      t /= CG;
+      tap = t % 27;
+      const int g = static_cast<int>(t / 27);
+      i = 4 * (g * CG + c) + e;
+    }
+    float v = 0.f;
+    if (tap < 27) {
+      if (mode == 0)
+        v = w[((long long)o * cin + i) * 27 + tap];
+      else
+        v = w[((long long)i * cin + o) * 27 + (26 - tap)];
+    }
+    out[idx] = v;
+  }
+}
+
+static Frame to_frame(const int* f) { return Frame{f[0], f[1], f[2], f[3], f[4], f[5], f[6], f[7]}; }
+
+static int check_frame(const int* f, const char* what) {
+  for (int i = 0; i < 5; ++i)
+    if (f[i] < 1) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "%s: extent %d is %d", what, i, f[i]);
+  for (int i = 5; i < 8; ++i)
+    if (f[i] < 0 || f[i] > 1) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "%s: margin %d is %d", what, i - 5, f[i]);
+  return VPX_OK;
+}
+
+static long long packed_floats(int cin, int cout) {
+  long long a = 27LL * cin * cout, b = 28LL * 4 * (cin > cout ? cin : cout);
+  return a > b ? a : b;
+}
+
+static int encode_frame_map(CUtensorMap* map, const float* base, const Frame& f, int R) {
+  const uint64_t Wf = f.w + 2 * f.mw, Hf = f.h + 2 * f.mh, Df = f.d + 2 * f.md;
+  uint64_t dims[5] = {(uint64_t)f.c, Wf, Hf, Df, (uint64_t)f.n};
+  uint64_t strides[4] = {(uint64_t)f.c * 4, Wf * f.c * 4, Hf * Wf * f.c * 4, Df * Hf * Wf * f.c * 4};
+  uint32_t box[5] = {4, 130, (uint32_t)(R + 2), 3, 1};
+  return encode_tiled(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float*>(base), dims,
+                      strides, box, CU_TENSOR_MAP_SWIZZLE_NONE);
+}
+
+// One row-window launch: output frame region z in [zlo,zhi), y in [ylo,yhi),
+// x in [0, wout) (wout % 128 == 0), input frame `in` (channels cin_eff).
+static int rowwin_run(const float* in, const Frame& inf, const float* wpack, int cin_eff,
+                      int cout_eff, float* out, const Frame& of, int zlo, int zhi, int ylo,
+                      int yhi, int wout, cudaStream_t st) {
+  int R, CG;
+  if (!rowwin_config(cin_eff, cout_eff, &R, &CG)) VPX_FAIL(VPX_ERR_UNSUPPORTED, "rowwin config");
+  CUtensorMap map;
+  int rc = encode_frame_map(&map, in, inf, R);
+  if (rc) return rc;
+  ConvRowParams p{};
+  p.zlo = zlo;
+  p.zhi = zhi;
+  p.ylo = ylo;
+  p.yhi = yhi;
+  p.nxseg = wout / 128;
+  p.ngy = (yhi - ylo + R - 1) / R;
+  p.n_groups = cin_eff == 4 ? 1 : cin_eff / (4 * CG);
+  p.num_tiles = inf.n * (zhi - zlo) * p.ngy * p.nxseg;
+  p.in_off_d = inf.md;
+  p.in_off_h = inf.mh;
+  p.in_off_w = inf.mw;
+  p.wpack = wpack;
+  p.out = out;
+  const long long Wf = of.w + 2 * of.mw, Hf = of.h + 2 * of.mh, Df = of.d + 2 * of.md;
+  p.out_sw = of.c;
+  p.out_sh = Wf * of.c;
+  p.out_sd = Hf * Wf * of.c;
+  p.out_sn = Df * Hf * Wf * of.c;
+  p.out_off_d = of.md;
+  p.out_off_h = of.mh;
+  p.out_off_w = of.mw;
+  return launch_rowwin_any(map, p, cin_eff, cout_eff, st);
+}
+
+static int pack(const float* w, int cout, int cin, int mode, float* dst, cudaStream_t st) {
+  const int I = mode ? cout : cin, O = mode ? cin : cout;
+  int R, CG;
+  if (!rowwin_config(I, O, &R, &CG)) VPX_FAIL(VPX_ERR_UNSUPPORTED, "pack config");
+  const int pair = I == 4;
+  const long long total = pair ? 28LL * O * 4 : 27LL * I * O;
+  int grid = static_cast<int>((total + 255) / 256);
+  if (grid > 4096) grid = 4096;
+  pack_rowwin_kernel<<<grid, 256, 0, st>>>(w, cout, cin, mode, CG, pair, dst);
+  VPX_LAUNCH_CHECK();
+  return VPX_OK;
+}
+
+}  // namespace vpx
+
+using vpx::Frame;
+
+extern "C" long long vpx_conv3d_workspace_bytes(int cin, int cout, int k, const int* ufr) {
+  Frame uf = vpx::to_frame(ufr);
+  const long long k3 = (long long)k * k * k;
+  long long packed = vpx::packed_floats(cin, cout) * 4;
+  long long parts = vpx::wgrad_simt_parts(uf) * cout * cin * k3 * 4;
+  return ((packed + 255) / 256) * 256 + ((parts + 255) / 256) * 256;
+}
+
+extern "C" int vpx_conv3d_fwd(const float* x, const int* xfr, const float* w, int k, int stride,
+                              float* y, const int* yfr, void* ws, long long ws_bytes,
+                              void* stream) {
+  if (int rc = vpx::check_frame(xfr, "conv fwd input")) return rc;
+  if (int rc = vpx::check_frame(yfr, "conv fwd output")) return rc;
+  Frame xf = vpx::to_frame(xfr), yf = vpx::to_frame(yfr);
+  if (k < 1 || k % 2 == 0) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "conv kernels must be odd, got %d", k);
+  if (stride < 1 || stride > 2) VPX_FAIL(VPX_ERR_UNSUPPORTED, "stride %d", stride);
+  if (yf.n != xf.n || yf.d != (xf.d + stride - 1) / stride || yf.h != (xf.h + stride - 1) / stride ||
+      yf.w != (xf.w + stride - 1) / stride)
+    VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "conv fwd: output (%d,%d,%d,%d) does not match input (%d,%d,%d,%d) stride %d",
+             yf.n, yf.d, yf.h, yf.w, xf.n, xf.d, xf.h, xf.w, stride);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int cin = xf.c, cout = yf.c;
+  int R, CG;
+  if (k == 3 && stride == 1 && yf.w % 128 == 0 && vpx::rowwin_config(cin, cout, &R, &CG)) {
+    if (ws_bytes < vpx::packed_floats(cin, cout) * 4) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "workspace too small");
+    float* wpack = static_cast<float*>(ws);
+    if (int rc = vpx::pack(w, cout, cin, 0, wpack, st)) return rc;
+    return vpx::rowwin_run(x, xf, wpack, cin, cout, y, yf, 0, yf.d, 0, yf.h, yf.w, st);
+  }
+  return vpx::conv_fwd_simt(x, xf, w, k, stride, y, yf, st);
+}
+
+extern "C" int vpx_conv3d_bwd_data(const float* u, const int* ufr, const float* w, int k,
+                                   int stride, float* xg, const int* gfr, void* ws,
+                                   long long ws_bytes, void* stream) {
+  if (int rc = vpx::check_frame(ufr, "conv bwd_data upstream")) return rc;
+  if (int rc = vpx::check_frame(gfr, "conv bwd_data output")) return rc;
+  Frame uf = vpx::to_frame(ufr), gf = vpx::to_frame(gfr);
+  if (k < 1 || k % 2 == 0) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "conv kernels must be odd, got %d", k);
+  if (uf.n != gf.n || uf.d != (gf.d + stride - 1) / stride || uf.h != (gf.h + stride - 1) / stride ||
+      uf.w != (gf.w + stride - 1) / stride)
+    VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "conv bwd_data: upstream does not match input extents");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int cout = uf.c, cin = gf.c;
+  int R, CG;
+  if (k == 3 && stride == 1 && gf.mw == 0 && gf.w % 128 == 0 &&
+      vpx::rowwin_config(cout, cin, &R, &CG)) {
+    if (ws_bytes < vpx::packed_floats(cin, cout) * 4) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "workspace too small");
+    float* wpack = static_cast<float*>(ws);
+    if (int rc = vpx::pack(w, cout, cin, 1, wpack, st)) return rc;
+    return vpx::rowwin_run(u, uf, wpack, cout, cin, xg, gf, -gf.md, gf.d + gf.md, -gf.mh,
+                           gf.h + gf.mh, gf.w, st);
+  }
+  return vpx::conv_bwd_data_simt(u, uf, w, k, stride, xg, gf, st);
+}
+
+extern "C" int vpx_conv3d_bwd_filter(const float* x, const int* xfr, const float* u,
+                                     const int* ufr, int k, int stride, float* wg, int accumulate,
+                                     void* ws, long long ws_bytes, void* stream) {
+  if (int rc = vpx::check_frame(xfr, "conv bwd_filter input")) return rc;
+  if (int rc = vpx::check_frame(ufr, "conv bwd_filter upstream")) return rc;
+  Frame xf = vpx::to_frame(xfr), uf = vpx::to_frame(ufr);
+  if (k < 1 || k % 2 == 0) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "conv kernels must be odd, got %d", k);
+  if (uf.n != xf.n || uf.d != (xf.d + stride - 1) / stride || uf.h != (xf.h + stride - 1) / stride ||
+      uf.w != (xf.w + stride - 1) / stride)
+    VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "conv bwd_filter: upstream does not match input extents");
+  long long need = vpx_conv3d_workspace_bytes(xf.c, uf.c, k, ufr);
+  if (ws_bytes < need) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "workspace too small (%lld < %lld)", ws_bytes, need);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  float* part = reinterpret_cast<float*>(static_cast<char*>(ws) +
+                                         ((vpx::packed_floats(xf.c, uf.c) * 4 + 255) / 256) * 256);
+  return vpx::conv_wgrad_simt(x, xf, u, uf, k, stride, wg, accumulate, part, st);
+}

@@ -1,0 +1,22 @@
+// CUDA-core convolution kernels (shapes outside the tcgen05 fast paths).
+#pragma once
+#include <cuda_runtime.h>
+
+namespace vpx {
+
+// NDHWC halo frame: interior extents (n,c,d,h,w) and margins (md,mh,mw).
+// Allocation is [n][d+2md][h+2mh][w+2mw][c], contiguous.
+struct Frame {
+  int n, c, d, h, w, md, mh, mw;
+};
+
+int num_sms();
+int conv_fwd_simt(const float* x, const Frame& xf, const float* w, int k, int s, float* y,
+                  const Frame& yf, cudaStream_t st);
+int conv_bwd_data_simt(const float* u, const Frame& uf, const float* w, int k, int s, float* xg,
+                       const Frame& gf, cudaStream_t st);
+long long wgrad_simt_parts(const Frame& uf);
+int conv_wgrad_simt(const float* x, const Frame& xf, const float* u, const Frame& uf, int k, int s,
+                    float* wg, int accumulate, float* part, cudaStream_t st);
+
+}  // namespace vpx

@@ -1,0 +1,661 @@
+// Memory-bound kernels of the training step: LeakyReLU, 2^3 pooling, batch
+// norm statistics/apply/backward, channel concat, k2s2 transposed conv, halo
+// pack/unpack, the pinned splitmix64 PRNG, Adam/SGD, losses, layout moves.
+//
+// All activations are NDHWC halo frames (Frame = {n,c,d,h,w,md,mh,mw}); every
+// kernel reads/writes frame interiors through fr_off() so producers can write
+// straight into their consumer's halo-wide frame (no reference-style _wrap
+// copy, reference layers/distributed.py:31-33).  Reductions are deterministic:
+// fixed block partition + fixed-order final sum, accumulated in fp64.
+#include "conv_simt.h"
+#include "vpx_host.h"
+
+namespace vpx {
+
+struct VoxIdx {
+  int n, z, y, x;
+};
+
+__device__ __forceinline__ VoxIdx vox_decode(long long v, const Frame& f) {
+  VoxIdx r;
+  r.x = v % f.w;
+  v /= f.w;
+  r.y = v % f.h;
+  v /= f.h;
+  r.z = v % f.d;
+  r.n = static_cast<int>(v / f.d);
+  return r;
+}
+// Element offset of interior voxel (n,z,y,x) channel 0 in frame f.
+__device__ __forceinline__ long long fr_off(const Frame& f, int n, int z, int y, int x) {
+  return ((((long long)n * (f.d + 2 * f.md) + (z + f.md)) * (f.h + 2 * f.mh) + (y + f.mh)) *
+              (f.w + 2 * f.mw) +
+          (x + f.mw)) *
+         f.c;
+}
+__device__ __forceinline__ long long vox_count(const Frame& f) {
+  return (long long)f.n * f.d * f.h * f.w;
+}
+
+static int grid1d(long long total, int block = 256) {
+  long long g = (total + block - 1) / block;
+  long long cap = (long long)num_sms() * 32;
+  if (g < 1) g = 1;
+  return static_cast<int>(g < cap ? g : cap);
+}
+
+#define GRID_STRIDE(i, total)                                                         \
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (total); \
+       i += (long long)gridDim.x * blockDim.x)
+
+// ------------------------------------------------------------------ leaky
+// reference layers/reference.py:231-236: x >= 0 ? x : slope*x; bwd passes u at x == 0.
+__global__ void leaky_fwd_kernel(const float* __restrict__ x, Frame xf, float* __restrict__ y,
+                                 Frame yf, float slope) {
+  const long long total = vox_count(xf) * xf.c;
+  GRID_STRIDE(i, total) {
+    const int c = i % xf.c;
+    const VoxIdx v = vox_decode(i / xf.c, xf);
+    const float a = x[fr_off(xf, v.n, v.z, v.y, v.x) + c];
+    y[fr_off(yf, v.n, v.z, v.y, v.x) + c] = a >= 0.f ? a : slope * a;
+  }
+}
+__global__ void leaky_bwd_kernel(const float* __restrict__ x, Frame xf, const float* __restrict__ u,
+                                 Frame uf, float* __restrict__ g, Frame gf, float slope) {
+  const long long total = vox_count(xf) * xf.c;
+  GRID_STRIDE(i, total) {
+    const int c = i % xf.c;
+    const VoxIdx v = vox_decode(i / xf.c, xf);
+    const float a = x[fr_off(xf, v.n, v.z, v.y, v.x) + c];
+    const float b = u[fr_off(uf, v.n, v.z, v.y, v.x) + c];
+    g[fr_off(gf, v.n, v.z, v.y, v.x) + c] = a >= 0.f ? b : slope * b;
+  }
+}
+
+// ------------------------------------------------------------------- pool
+// reference layers/reference.py:149-183: 2^3 stride 2, window flattened in
+// (d,h,w) C order, max ties -> lowest linear index; avg bwd = u/8 broadcast.
+__global__ void pool_fwd_kernel(const float* __restrict__ x, Frame xf, float* __restrict__ y,
+                                Frame yf, int is_max) {
+  const long long total = vox_count(yf) * yf.c;
+  GRID_STRIDE(i, total) {
+    const int c = i % yf.c;
+    const VoxIdx o = vox_decode(i / yf.c, yf);
+    float best = 0.f, sum = 0.f;
+    int first = 1;
+    for (int w8 = 0; w8 < 8; ++w8) {
+      const int a = w8 >> 2, b = (w8 >> 1) & 1, cc = w8 & 1;
+      const float val = x[fr_off(xf, o.n, 2 * o.z + a, 2 * o.y + b, 2 * o.x + cc) + c];
+      if (first || val > best) best = val;
+      first = 0;
+      sum += val;
+    }
+    y[fr_off(yf, o.n, o.z, o.y, o.x) + c] = is_max ? best : sum / 8.0f;
+  }
+}
+__global__ void pool_bwd_kernel(const float* __restrict__ x, Frame xf, const float* __restrict__ u,
+                                Frame uf, float* __restrict__ g, Frame gf, int is_max) {
+  const long long total = vox_count(uf) * uf.c;
+  GRID_STRIDE(i, total) {
+    const int c = i % uf.c;
+    const VoxIdx o = vox_decode(i / uf.c, uf);
+    const float uv = u[fr_off(uf, o.n, o.z, o.y, o.x) + c];
+    int arg = 0;
+    if (is_max) {
+      float best = 0.f;
+      for (int w8 = 0; w8 < 8; ++w8) {
+        const int a = w8 >> 2, b = (w8 >> 1) & 1, cc = w8 & 1;
+        const float val = x[fr_off(xf, o.n, 2 * o.z + a, 2 * o.y + b, 2 * o.x + cc) + c];
+        if (w8 == 0 || val > best) {
+          best = val;
+          arg = w8;
+        }
+      }
+    }
+    const float avg = uv / 8.0f;
+    for (int w8 = 0; w8 < 8; ++w8) {
+      const int a = w8 >> 2, b = (w8 >> 1) & 1, cc = w8 & 1;
+      g[fr_off(gf, o.n, 2 * o.z + a, 2 * o.y + b, 2 * o.x + cc) + c] =
+          is_max ? (w8 == arg ? uv : 0.f) : avg;
+    }
+  }
+}
+
+// -------------------------------------------------------------- batchnorm
+// Per-channel partial sums over a fixed voxel partition (deterministic).
+// mode 0: (sum x, sum x^2); mode 1: (sum u, sum u*xhat) with xhat=(x-mean)*inv.
+constexpr int kBnParts = 512;
+
+__global__ void bn_partial_kernel(const float* __restrict__ x, Frame xf, const float* __restrict__ u,
+                                  Frame uf, const float* __restrict__ mean,
+                                  const float* __restrict__ inv, int mode,
+                                  double* __restrict__ part) {
+  // block p handles voxels [p*chunk, (p+1)*chunk); threads stride channels x voxels
+  const int C = xf.c;
+  const long long nv = vox_count(xf);
+  const long long chunk = (nv + gridDim.x - 1) / gridDim.x;
+  const long long v0 = blockIdx.x * chunk, v1 = min(nv, v0 + chunk);
+  extern __shared__ double sh[];  // [2][blockDim.x]
+  const int lanes_per_c = blockDim.x / C > 0 ? blockDim.x / C : 1;
+  const int c = threadIdx.x % C;
+  const int lane = threadIdx.x / C;
+  double s1 = 0.0, s2 = 0.0;
+  if (threadIdx.x < lanes_per_c * C) {
+    for (long long v = v0 + lane; v < v1; v += lanes_per_c) {
+      const VoxIdx q = vox_decode(v, xf);
+      const float a = x[fr_off(xf, q.n, q.z, q.y, q.x) + c];
+      if (mode == 0) {
+        s1 += a;
+        s2 += (double)a * a;
+      } else {
+        const float b = u[fr_off(uf, q.n, q.z, q.y, q.x) + c];
+        const float xh = (a - mean[c]) * inv[c];
+        s1 += b;
+        s2 += (double)b * xh;
+      }
+    }
+  }
+  sh[threadIdx.x] = s1;
+  sh[blockDim.x + threadIdx.x] = s2;
+  __syncthreads();
+  if (threadIdx.x < C) {
+    double t1 = 0.0, t2 = 0.0;
+    for (int l = 0; l < lanes_per_c; ++l) {
+      t1 += sh[l * C + threadIdx.x];
+      t2 += sh[blockDim.x + l * C + threadIdx.x];
+    }
+    part[(long long)blockIdx.x * 2 * C + threadIdx.x] = t1;
+    part[(long long)blockIdx.x * 2 * C + C + threadIdx.x] = t2;
+  }
+}
+__global__ void bn_finish_kernel(const double* __restrict__ part, int P, int C,
+                                 float* __restrict__ out2c) {
+  for (int i = threadIdx.x + blockIdx.x * blockDim.x; i < 2 * C; i += blockDim.x * gridDim.x) {
+    double s = 0.0;
+    for (int p = 0; p < P; ++p) s += part[(long long)p * 2 * C + i];
+    out2c[i] = static_cast<float>(s);
+  }
+}
+// y = gamma*(x-mean)*inv + beta (reference layers/reference.py:206-214)
+__global__ void bn_apply_kernel(const float* __restrict__ x, Frame xf, const float* __restrict__ mean,
+                                const float* __restrict__ inv, const float* __restrict__ gamma,
+                                const float* __restrict__ beta, float* __restrict__ y, Frame yf) {
+  const long long total = vox_count(xf) * xf.c;
+  GRID_STRIDE(i, total) {
+    const int c = i % xf.c;
+    const VoxIdx v = vox_decode(i / xf.c, xf);
+    const float xh = (x[fr_off(xf, v.n, v.z, v.y, v.x) + c] - mean[c]) * inv[c];
+    y[fr_off(yf, v.n, v.z, v.y, v.x) + c] = gamma[c] * xh + beta[c];
+  }
+}
+// dx = gamma*inv*(u - (sum_u + xhat*sum_uxhat)/count) (reference layers/reference.py:217-226)
+__global__ void bn_bwd_apply_kernel(const float* __restrict__ x, Frame xf, const float* __restrict__ u,
+                                    Frame uf, const float* __restrict__ mean,
+                                    const float* __restrict__ inv, const float* __restrict__ gamma,
+                                    const float* __restrict__ sums, float inv_count,
+                                    float* __restrict__ g, Frame gf) {
+  const int C = xf.c;
+  const long long total = vox_count(xf) * C;
+  GRID_STRIDE(i, total) {
+    const int c = i % C;
+    const VoxIdx v = vox_decode(i / C, xf);
+    const float xh = (x[fr_off(xf, v.n, v.z, v.y, v.x) + c] - mean[c]) * inv[c];
+    const float b = u[fr_off(uf, v.n, v.z, v.y, v.x) + c];
+    g[fr_off(gf, v.n, v.z, v.y, v.x) + c] =
+        gamma[c] * inv[c] * (b - (sums[c] + xh * sums[C + c]) * inv_count);
+  }
+}
+// mean/var from allreduced sums; running stats update (reference layers/reference.py:188-204)
+__global__ void bn_stats_kernel(const float* __restrict__ sums, int C, double count, float eps,
+                                float momentum, float* __restrict__ mean, float* __restrict__ inv,
+                                float* __restrict__ run_mean, float* __restrict__ run_var) {
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    const double m = (double)sums[c] / count;
+    double var = (double)sums[C + c] / count - m * m;
+    if (var < 0) var = 0;
+    mean[c] = static_cast<float>(m);
+    inv[c] = static_cast<float>(1.0 / sqrt(var + eps));
+    if (run_mean) run_mean[c] = momentum * run_mean[c] + (1.f - momentum) * static_cast<float>(m);
+    if (run_var) run_var[c] = momentum * run_var[c] + (1.f - momentum) * static_cast<float>(var);
+  }
+}
+
+// ----------------------------------------------------------------- concat
+__global__ void concat_kernel(const float* __restrict__ a, Frame af, const float* __restrict__ b,
+                              Frame bf, float* __restrict__ y, Frame yf) {
+  const long long total = vox_count(yf) * yf.c;
+  GRID_STRIDE(i, total) {
+    const int c = i % yf.c;
+    const VoxIdx v = vox_decode(i / yf.c, yf);
+    const float val = c < af.c ? a[fr_off(af, v.n, v.z, v.y, v.x) + c]
+                               : b[fr_off(bf, v.n, v.z, v.y, v.x) + c - af.c];
+    y[fr_off(yf, v.n, v.z, v.y, v.x) + c] = val;
+  }
+}
+// split gradient of a concat: ga (+)= u[:, :ca], gb (+)= u[:, ca:]
+__global__ void split_kernel(const float* __restrict__ u, Frame uf, float* __restrict__ ga, Frame gaf,
+                             float* __restrict__ gb, Frame gbf, int acc_b) {
+  const long long total = vox_count(uf) * uf.c;
+  GRID_STRIDE(i, total) {
+    const int c = i % uf.c;
+    const VoxIdx v = vox_decode(i / uf.c, uf);
+    const float val = u[fr_off(uf, v.n, v.z, v.y, v.x) + c];
+    if (c < gaf.c) {
+      ga[fr_off(gaf, v.n, v.z, v.y, v.x) + c] = val;
+    } else {
+      float* p = gb + fr_off(gbf, v.n, v.z, v.y, v.x) + c - gaf.c;
+      *p = acc_b ? *p + val : val;
+    }
+  }
+}
+// y (+)= x over frame interiors
+__global__ void add_kernel(const float* __restrict__ x, Frame xf, float* __restrict__ y, Frame yf) {
+  const long long total = vox_count(xf) * xf.c;
+  GRID_STRIDE(i, total) {
+    const int c = i % xf.c;
+    const VoxIdx v = vox_decode(i / xf.c, xf);
+    y[fr_off(yf, v.n, v.z, v.y, v.x) + c] += x[fr_off(xf, v.n, v.z, v.y, v.x) + c];
+  }
+}
+__global__ void copy_kernel(const float* __restrict__ x, Frame xf, float* __restrict__ y, Frame yf) {
+  const long long total = vox_count(xf) * xf.c;
+  GRID_STRIDE(i, total) {
+    const int c = i % xf.c;
+    const VoxIdx v = vox_decode(i / xf.c, xf);
+    y[fr_off(yf, v.n, v.z, v.y, v.x) + c] = x[fr_off(xf, v.n, v.z, v.y, v.x) + c];
+  }
+}
+
+// ------------------------------------------------- transposed conv k2 s2
+// reference layers/reference.py:99-144; w is (cin, cout, 2,2,2).
+__global__ void deconv_fwd_kernel(const float* __restrict__ x, Frame xf, const float* __restrict__ w,
+                                  float* __restrict__ y, Frame yf) {
+  const long long total = vox_count(yf) * yf.c;
+  GRID_STRIDE(i, total) {
+    const int co = i % yf.c;
+    const VoxIdx o = vox_decode(i / yf.c, yf);
+    const int k = ((o.z & 1) * 2 + (o.y & 1)) * 2 + (o.x & 1);
+    const float* xp = x + fr_off(xf, o.n, o.z >> 1, o.y >> 1, o.x >> 1);
+    float acc = 0.f;
+    for (int ci = 0; ci < xf.c; ++ci) acc = fmaf(xp[ci], w[((long long)ci * yf.c + co) * 8 + k], acc);
+    y[fr_off(yf, o.n, o.z, o.y, o.x) + co] = acc;
+  }
+}
+__global__ void deconv_bwd_data_kernel(const float* __restrict__ u, Frame uf,
+                                       const float* __restrict__ w, float* __restrict__ g, Frame gf) {
+  const long long total = vox_count(gf) * gf.c;
+  GRID_STRIDE(i, total) {
+    const int ci = i % gf.c;
+    const VoxIdx p = vox_decode(i / gf.c, gf);
+    float acc = 0.f;
+    for (int k = 0; k < 8; ++k) {
+      const int a = k >> 2, b = (k >> 1) & 1, c = k & 1;
+      const float* up = u + fr_off(uf, p.n, 2 * p.z + a, 2 * p.y + b, 2 * p.x + c);
+      for (int co = 0; co < uf.c; ++co) acc = fmaf(up[co], w[((long long)ci * uf.c + co) * 8 + k], acc);
+    }
+    g[fr_off(gf, p.n, p.z, p.y, p.x) + ci] = acc;
+  }
+}
+// wg[ci][co][k] partial over voxel chunks -> part[p][ci][co][k]
+__global__ void deconv_wgrad_kernel(const float* __restrict__ x, Frame xf, const float* __restrict__ u,
+                                    Frame uf, long long chunk, float* __restrict__ part) {
+  const int len = xf.c * uf.c * 8;
+  const long long nv = vox_count(xf);
+  const long long v0 = blockIdx.y * chunk, v1 = min(nv, v0 + chunk);
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < len; e += gridDim.x * blockDim.x) {
+    const int k = e % 8, co = (e / 8) % uf.c, ci = e / (8 * uf.c);
+    const int a = k >> 2, b = (k >> 1) & 1, c = k & 1;
+    float acc = 0.f;
+    for (long long v = v0; v < v1; ++v) {
+      const VoxIdx q = vox_decode(v, xf);
+      acc = fmaf(x[fr_off(xf, q.n, q.z, q.y, q.x) + ci],
+                 u[fr_off(uf, q.n, 2 * q.z + a, 2 * q.y + b, 2 * q.x + c) + co], acc);
+    }
+    part[(long long)blockIdx.y * len + e] = acc;
+  }
+}
+__global__ void reduce_parts_kernel(const float* __restrict__ part, int P, long long len,
+                                    float* __restrict__ out, int accumulate) {
+  GRID_STRIDE(i, len) {
+    float s = 0.f;
+    for (int p = 0; p < P; ++p) s += part[(long long)p * len + i];
+    out[i] = accumulate ? out[i] + s : s;
+  }
+}
+
+// ------------------------------------------------------------------- halo
+// Copy a box of a frame (frame coordinates, i.e. margins included) to/from a
+// dense buffer in (n, z, y, x, c) C order.  mode 0: pack, 1: unpack, 2: unpack-add.
+__global__ void halo_copy_kernel(float* __restrict__ fr, Frame f, int z0, int y0, int x0, int ez,
+                                 int ey, int ex, float* __restrict__ buf, int mode) {
+  const long long total = (long long)f.n * ez * ey * ex * f.c;
+  const long long Wf = f.w + 2 * f.mw, Hf = f.h + 2 * f.mh, Df = f.d + 2 * f.md;
+  GRID_STRIDE(i, total) {
+    long long t = i;
+    const int c = t % f.c;
+    t /= f.c;
+    const int x = t % ex;
+    t /= ex;
+    const int y = t % ey;
+    t /= ey;
+    const int z = t % ez;
+    const int n = t / ez;
+    const long long off = ((((long long)n * Df + z0 + z) * Hf + y0 + y) * Wf + x0 + x) * f.c + c;
+    if (mode == 0)
+      buf[i] = fr[off];
+    else if (mode == 1)
+      fr[off] = buf[i];
+    else
+      fr[off] += buf[i];
+  }
+}
+
+// -------------------------------------------------------------------- prng
+// splitmix64 counter streams (reference prng.py:28-90).  uniform in fp64:
+// lo + (hi-lo) * ((u64 >> 11) * 2^-53), computed with explicit non-fused ops so
+// the result is bit-identical to numpy's.
+__device__ __forceinline__ uint64_t sm_mix(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+__global__ void prng_uniform_kernel(uint64_t key, long long n, double lo, double hi,
+                                    float* __restrict__ out32, double* __restrict__ out64) {
+  GRID_STRIDE(i, n) {
+    const uint64_t r = sm_mix(key + (static_cast<uint64_t>(i) + 1ULL) * 0x9E3779B97F4A7C15ULL);
+    const double u01 = __dmul_rn(static_cast<double>(r >> 11), 1.1102230246251565e-16);
+    const double v = __dadd_rn(lo, __dmul_rn(__dsub_rn(hi, lo), u01));
+    if (out32) out32[i] = static_cast<float>(v);
+    if (out64) out64[i] = v;
+  }
+}
+// keep-mask (uniform01 < keep) for counters base + i
+__global__ void prng_mask_kernel(uint64_t key, long long n, double keep, uint8_t* __restrict__ out) {
+  GRID_STRIDE(i, n) {
+    const uint64_t r = sm_mix(key + (static_cast<uint64_t>(i) + 1ULL) * 0x9E3779B97F4A7C15ULL);
+    const double u01 = __dmul_rn(static_cast<double>(r >> 11), 1.1102230246251565e-16);
+    out[i] = u01 < keep ? 1 : 0;
+  }
+}
+// y = lo + (hi-lo)*uniform placed into an NDHWC frame from an NCDHW-ordered stream
+__global__ void prng_volume_kernel(uint64_t key, Frame f, long long counter_base, double lo, double hi,
+                                   float* __restrict__ fr) {
+  const long long total = vox_count(f) * f.c;
+  GRID_STRIDE(i, total) {
+    // i enumerates NCDHW order of the interior: (n, c, z, y, x)
+    long long t = i;
+    const int x = t % f.w;
+    t /= f.w;
+    const int y = t % f.h;
+    t /= f.h;
+    const int z = t % f.d;
+    t /= f.d;
+    const int c = t % f.c;
+    const int n = t / f.c;
+    const uint64_t ctr = static_cast<uint64_t>(counter_base + i);
+    const uint64_t r = sm_mix(key + (ctr + 1ULL) * 0x9E3779B97F4A7C15ULL);
+    const double u01 = __dmul_rn(static_cast<double>(r >> 11), 1.1102230246251565e-16);
+    const double v = __dadd_rn(lo, __dmul_rn(__dsub_rn(hi, lo), u01));
+    fr[fr_off(f, n, z, y, x) + c] = static_cast<float>(v);
+  }
+}
+
+// --------------------------------------------------------------- optimizer
+// In-place bias-corrected Adam (reference model/optim.py:71-88), fp32 like the
+// reference's fp32 path; c1 = 1-b1^t, c2 = 1-b2^t precomputed on the host.
+__global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
+                            float* __restrict__ v, long long n, float lr, float b1, float b2,
+                            float c1, float c2, float eps) {
+  GRID_STRIDE(i, n) {
+    const float gi = g[i];
+    float mi = m[i] * b1;
+    mi = mi + (1.f - b1) * gi;
+    float vi = v[i] * b2;
+    vi = vi + (1.f - b2) * (gi * gi);
+    m[i] = mi;
+    v[i] = vi;
+    p[i] = p[i] - lr * (mi / c1) / (sqrtf(vi / c2) + eps);
+  }
+}
+__global__ void sgd_kernel(float* __restrict__ p, const float* __restrict__ g, long long n, float lr) {
+  GRID_STRIDE(i, n) p[i] = p[i] - lr * g[i];
+}
+
+// ------------------------------------------------------------------ losses
+// per-voxel softmax cross entropy over K channels; labels int64 (n, d, h, w).
+// writes dlogits = (softmax - onehot) / count into g and per-block loss partials.
+__global__ void xent_kernel(const float* __restrict__ logits, Frame lf, const long long* __restrict__ lab,
+                            double inv_count, float* __restrict__ g, Frame gf, double* __restrict__ part) {
+  const long long nv = vox_count(lf);
+  const int K = lf.c;
+  double local = 0.0;
+  GRID_STRIDE(v, nv) {
+    const VoxIdx q = vox_decode(v, lf);
+    const float* lp = logits + fr_off(lf, q.n, q.z, q.y, q.x);
+    float mx = lp[0];
+    for (int k = 1; k < K; ++k) mx = fmaxf(mx, lp[k]);
+    float se = 0.f;
+    for (int k = 0; k < K; ++k) se += expf(lp[k] - mx);
+    const float lse = logf(se);
+    const long long y = lab[v];
+    local -= (double)(lp[y] - mx - lse);
+    float* gp = g + fr_off(gf, q.n, q.z, q.y, q.x);
+    for (int k = 0; k < K; ++k) {
+      const float pr = expf(lp[k] - mx - lse);
+      gp[k] = static_cast<float>((pr - (k == y ? 1.f : 0.f)) * inv_count);
+    }
+  }
+  __shared__ double sh[256];
+  sh[threadIdx.x] = local;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+}
+
+// ------------------------------------------------------------------ layout
+// NCDHW dense <-> NDHWC frame interior.
+__global__ void ncdhw_to_frame_kernel(const float* __restrict__ src, Frame f, float* __restrict__ fr) {
+  const long long total = vox_count(f) * f.c;
+  GRID_STRIDE(i, total) {
+    long long t = i;
+    const int x = t % f.w;
+    t /= f.w;
+    const int y = t % f.h;
+    t /= f.h;
+    const int z = t % f.d;
+    t /= f.d;
+    const int c = t % f.c;
+    const int n = t / f.c;
+    fr[fr_off(f, n, z, y, x) + c] = src[i];
+  }
+}
+__global__ void frame_to_ncdhw_kernel(const float* __restrict__ fr, Frame f, float* __restrict__ dst) {
+  const long long total = vox_count(f) * f.c;
+  GRID_STRIDE(i, total) {
+    long long t = i;
+    const int x = t % f.w;
+    t /= f.w;
+    const int y = t % f.h;
+    t /= f.h;
+    const int z = t % f.d;
+    t /= f.d;
+    const int c = t % f.c;
+    const int n = t / f.c;
+    dst[i] = fr[fr_off(f, n, z, y, x) + c];
+  }
+}
+
+static Frame F(const int* f) { return Frame{f[0], f[1], f[2], f[3], f[4], f[5], f[6], f[7]}; }
+static long long VC(const Frame& f) { return (long long)f.n * f.d * f.h * f.w; }
+static cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+
+}  // namespace vpx
+
+using namespace vpx;
+
+#define LAUNCH_TAIL \
+  VPX_LAUNCH_CHECK(); \
+  return VPX_OK
+
+extern "C" int vpx_leaky_fwd(const float* x, const int* xf, float* y, const int* yf, float slope,
+                             void* st) {
+  Frame a = F(xf), b = F(yf);
+  leaky_fwd_kernel<<<grid1d(VC(a) * a.c), 256, 0, S(st)>>>(x, a, y, b, slope);
+  LAUNCH_TAIL;
+}
+extern "C" int vpx_leaky_bwd(const float* x, const int* xf, const float* u, const int* uf, float* g,
+                             const int* gf, float slope, void* st) {
+  Frame a = F(xf), b = F(uf), c = F(gf);
+  leaky_bwd_kernel<<<grid1d(VC(a) * a.c), 256, 0, S(st)>>>(x, a, u, b, g, c, slope);
+  LAUNCH_TAIL;
+}
+extern "C" int vpx_pool_fwd(const float* x, const int* xf, float* y, const int* yf, int is_max,
+                            void* st) {
+  Frame a = F(xf), b = F(yf);
+  if (a.d % 2 || a.h % 2 || a.w % 2) VPX_FAIL(VPX_ERR_NON_DIVISIBLE, "pool3d needs even extents");
+  if (b.d * 2 != a.d || b.h * 2 != a.h || b.w * 2 != a.w || a.c != b.c || a.n != b.n)
+    VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "pool output extents");
+  pool_fwd_kernel<<<grid1d(VC(b) * b.c), 256, 0, S(st)>>>(x, a, y, b, is_max);
+  LAUNCH_TAIL;
+}
+extern "C" int vpx_pool_bwd(const float* x, const int* xf, const float* u, const int* uf, float* g,
+                            const int* gf, int is_max, void* st) {
+  Frame a = F(xf), b = F(uf), c = F(gf);
+  pool_bwd_kernel<<<grid1d(VC(b) * b.c), 256, 0, S(st)>>>(x, a, u, b, g, c, is_max);
+  LAUNCH_TAIL;
+}
+extern "C" long long vpx_bn_workspace_bytes(int c) { return (long long)kBnParts * 2 * c * 8; }
+extern "C" int vpx_bn_sums(const float* x, const int* xf, const float* u, const int* uf,
+                           const float* mean, const float* inv, int mode, float* out2c, void* ws,
+                           void* st) {
+  Frame a = F(xf), b = uf ? F(uf) : F(xf);
+  const int threads = a.c >= 256 ? a.c : (256 / a.c) * a.c;
+  if (threads > 1024) VPX_FAIL(VPX_ERR_UNSUPPORTED, "bn channels %d", a.c);
+  bn_partial_kernel<<<kBnParts, threads, 2 * threads * sizeof(double), S(st)>>>(
+      x, a, u ? u : x, b, mean, inv, mode, static_cast<double*>(ws));
+  VPX_LAUNCH_CHECK();
+  bn_finish_kernel<<<1, 256, 0, S(st)>>>(static_cast<double*>(ws), kBnParts, a.c, out2c);
+  LAUNCH_TAIL;
+}
+extern "C" int vpx_bn_stats(const float* sums, int c, double count, float eps, float momentum,
+                            float* mean, float* inv, float* run_mean, float* run_var, void* st) {
+  bn_stats_kernel<<<1, 256, 0, S(st)>>>(sums, c, count, eps, momentum, mean, inv, run_mean, run_var);
+  LAUNCH_TAIL;
+}
+extern "C" int vpx_bn_apply(const float* x, const int* xf, const float* mean, const float* inv,
+                            const float* gamma, const float* beta, float* y, const int* yf, void* st) {
+  Frame a = F(xf), b = F(yf);
+  bn_apply_kernel<<<grid1d(VC(a) * a.c), 256, 0, S(st)>>>(x, a, mean, inv, gamma, beta, y, b);
+  LAUNCH_TAIL;
+}
+extern "C" int vpx_bn_bwd_apply(const float* x, const int* xf, const float* u, const int* uf,
+                                const float* mean, const float* inv, const float* gamma,
+                                const float* sums, double count, float* g, const int* gf, void* st) {
+  Frame a = F(xf), b = F(uf), c = F(gf);
+  bn_bwd_apply_kernel<<<grid1d(VC(a) * a.c), 256, 0, S(st)>>>(
+      x, a, u, b, mean, inv, gamma, sums, static_cast<float>(1.0 / count), g, c);
+  LAUNCH_TAIL;
+}
+extern "C" int vpx_concat(const float* a, const int* af, const float* b, const int* bf, float* y,
+                          const int* yf, void* st) {
+  Frame A = F(af), B = F(bf), Y = F(yf);
+  if (A.c + B.c != Y.c) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "concat channels");
+  concat_kernel<<<grid1d(VC(Y) * Y.c), 256, 0, S(st)>>>(a, A, b, B, y, Y);
+  LAUNCH_TAIL;
+}
+extern "C" int vpx_split(const float* u, const int* uf, float* ga, const int* gaf, float* gb,
+                         const int* gbf, int acc_b, void* st) {
+  Frame U = F(uf), A = F(gaf), B = F(gbf);
+  split_kernel<<<grid1d(VC(U) * U.c), 256, 0, S(st)>>>(u, U, ga, A, gb, B, acc_b);
+  LAUNCH_TAIL;
+}
+extern "C" int vpx_add(const float* x, const int* xf, float* y, const int* yf, void* st) {
+  Frame A = F(xf), B = F(yf);
+  add_kernel<<<grid1d(VC(A) * A.c), 256, 0, S(st)>>>(x, A, y, B);
+  LAUNCH_TAIL;
+}
+extern "C" int vpx_copy(const float* x, const int* xf, float* y, const int* yf, void* st) {
+  Frame A = F(xf), B = F(yf);
+  copy_kernel<<<grid1d(VC(A) * A.c), 256, 0, S(st)>>>(x, A, y, B);
+  LAUNCH_TAIL;
+}
+extern "C" int vpx_deconv_fwd(const float* x, const int* xf, const float* w, float* y, const int* yf,
+                              void* st) {
+  Frame A = F(xf), B = F(yf);
+  deconv_fwd_kernel<<<grid1d(VC(B) * B.c), 256, 0, S(st)>>>(x, A, w, y, B);
+  LAUNCH_TAIL;
+}
+extern "C" int vpx_deconv_bwd_data(const float* u, const int* uf, const float* w, float* g,
+                                   const int* gf, void* st) {
+  Frame A = F(uf), B = F(gf);
+  deconv_bwd_data_kernel<<<grid1d(VC(B) * B.c), 256, 0, S(st)>>>(u, A, w, g, B);
+  LAUNCH_TAIL;
+}
+extern "C" long long vpx_deconv_workspace_bytes(int cin, int cout) {
+  return 256LL * cin * cout * 8 * 4;
+}
+extern "C" int vpx_deconv_bwd_filter(const float* x, const int* xf, const float* u, const int* uf,
+                                     float* wg, int accumulate, void* ws, void* st) {
+  Frame A = F(xf), B = F(uf);
+  const long long nv = VC(A);
+  const int P = static_cast<int>(nv < 256 ? nv : 256);
+  const long long chunk = (nv + P - 1) / P;
+  const int len = A.c * B.c * 8;
+  dim3 grid((len + 255) / 256, P);
+  deconv_wgrad_kernel<<<grid, 256, 0, S(st)>>>(x, A, u, B, chunk, static_cast<float*>(ws));
+  VPX_LAUNCH_CHECK();
+  reduce_parts_kernel<<<grid1d(len), 256, 0, S(st)>>>(static_cast<float*>(ws), P, len, wg, accumulate);
+  LAUNCH_TAIL;
+}
+extern "C" int vpx_halo_copy(float* fr, const int* ff, const int* box6, float* buf, int mode,
+                             void* st) {
+  Frame f = F(ff);
+  const long long total = (long long)f.n * box6[3] * box6[4] * box6[5] * f.c;
+  halo_copy_kernel<<<grid1d(total), 256, 0, S(st)>>>(fr, f, box6[0], box6[1], box6[2], box6[3],
+                                                     box6[4], box6[5], buf, mode);
+  LAUNCH_TAIL;
+}
+extern "C" int vpx_prng_uniform(unsigned long long key, long long n, double lo, double hi,
+                                float* out32, double* out64, void* st) {
+  prng_uniform_kernel<<<grid1d(n), 256, 0, S(st)>>>(key, n, lo, hi, out32, out64);
+  LAUNCH_TAIL;
+}
+extern "C" int vpx_prng_mask(unsigned long long key, long long n, double keep, unsigned char* out,
+                             void* st) {
+  prng_mask_kernel<<<grid1d(n), 256, 0, S(st)>>>(key, n, keep, out);
+  LAUNCH_TAIL;
+}
+extern "C" int vpx_prng_volume(unsigned long long key, const int* ff, long long counter_base,
+                               double lo, double hi, float* fr, void* st) {
+  Frame f = F(ff);
+  prng_volume_kernel<<<grid1d(VC(f) * f.c), 256, 0, S(st)>>>(key, f, counter_base, lo, hi, fr);
+  LAUNCH_TAIL;
+}
+extern "C" int vpx_adam(float* p, const float* g, float* m, float* v, long long n, float lr,
+                        float b1, float b2, float c1, float c2, float eps, void* st) {
+  adam_kernel<<<grid1d(n), 256, 0, S(st)>>>(p, g, m, v, n, lr, b1, b2, c1, c2, eps);
+  LAUNCH_TAIL;
+}
+extern "C" int vpx_sgd(float* p, const float* g, long long n, float lr, void* st) {
+  sgd_kernel<<<grid1d(n), 256, 0, S(st)>>>(p, g, n, lr);
+  LAUNCH_TAIL;
+}
+extern "C" int vpx_xent(const float* logits, const int* lf, const long long* labels, double count,
+                        float* g, const int* gf, double* part, int nparts, void* st) {
+  Frame A = F(lf), B = F(gf);
+  xent_kernel<<<nparts, 256, 0, S(st)>>>(logits, A, labels, 1.0 / count, g, B, part);
+  LAUNCH_TAIL;
+}
+extern "C" int vpx_layout_ncdhw_to_frame(const float* src, const int* ff, float* fr, void* st) {
+  Frame f = F(ff);
+  ncdhw_to_frame_kernel<<<grid1d(VC(f) * f.c), 256, 0, S(st)>>>(src, f, fr);
+  LAUNCH_TAIL;
+}
+extern "C" int vpx_layout_frame_to_ncdhw(const float* fr, const int* ff, float* dst, void* st) {
+  Frame f = F(ff);
+  frame_to_ncdhw_kernel<<<grid1d(VC(f) * f.c), 256, 0, S(st)>>>(fr, f, dst);
+  LAUNCH_TAIL;
+}

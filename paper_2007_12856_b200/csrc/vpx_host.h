@@ -1,0 +1,43 @@
+// Host-side helpers shared by every C-ABI entry point: status codes, the
+// thread-local last-error message and TMA tensor-map encoding.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include "../../include/vpx.h"
+
+namespace vpx {
+
+void set_error(const char* fmt, ...);
+
+#define VPX_FAIL(code, ...)        \
+  do {                             \
+    ::vpx::set_error(__VA_ARGS__); \
+    return (code);                 \
+  } while (0)
+
+#define VPX_CHECK_CUDA(expr)                                                                \
+  do {                                                                                      \
+    cudaError_t _e = (expr);                                                                \
+    if (_e != cudaSuccess) VPX_FAIL(VPX_ERR_CUDA, "%s: %s", #expr, cudaGetErrorString(_e)); \
+  } while (0)
+
+#define VPX_LAUNCH_CHECK()                                                           \
+  do {                                                                               \
+    cudaError_t _e = cudaGetLastError();                                             \
+    if (_e != cudaSuccess) VPX_FAIL(VPX_ERR_CUDA, "launch: %s", cudaGetErrorString(_e)); \
+  } while (0)
+
+// Encode a tiled TMA map. dims/box are innermost-first; strides_bytes has
+// rank-1 entries (stride of dims 1..rank-1).  Returns 0 or VPX_ERR_CUDA.
+int encode_tiled(CUtensorMap* map, CUtensorMapDataType dtype, int rank, void* gaddr,
+                 const uint64_t* dims, const uint64_t* strides_bytes, const uint32_t* box,
+                 CUtensorMapSwizzle swizzle);
+
+}  // namespace vpx

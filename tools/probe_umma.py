@@ -1,0 +1,420 @@
+"""Pin UMMA descriptor / TMA semantics on a real B200 (exploratory probe).
+
+Builds shared-memory images on the host under explicit layout hypotheses,
+runs one tcgen05.mma sequence through vpx_probe_umma and compares the TMEM
+accumulator with numpy.  Prints one line per hypothesis: PASS/FAIL + max err.
+Run on the GPU box: python tools/probe_umma.py
+"""
+
+import ctypes
+import json
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+from paper_2007_12856_b200 import _lib  # noqa: E402
+
+rng = np.random.default_rng(0)
+RESULTS = {}
+
+
+def tf32(a):
+    a = np.asarray(a, dtype=np.float32).copy()
+    a.view(np.uint32)[...] &= np.uint32(0xFFFFE000)
+    return a
+
+
+def sdesc(start, lbo, sbo, layout, base_off=0):
+    d = (start >> 4) & 0x3FFF
+    d |= ((lbo >> 4) & 0x3FFF) << 16
+    d |= ((sbo >> 4) & 0x3FFF) << 32
+    d |= 1 << 46
+    d |= (base_off & 7) << 49
+    d |= (layout & 7) << 61
+    return d
+
+
+def idesc(M, N, a_mn=False, b_mn=False, fmt=2):
+    d = 1 << 4
+    d |= fmt << 7
+    d |= fmt << 10
+    d |= (1 if a_mn else 0) << 15
+    d |= (1 if b_mn else 0) << 16
+    d |= (N >> 3) << 17
+    d |= (M >> 4) << 24
+    return d
+
+
+def run(img_bytes: np.ndarray, ops, ncols=64):
+    img = torch.from_numpy(np.ascontiguousarray(img_bytes).view(np.uint8)).cuda()
+    ops_arr = np.array(ops, dtype=np.uint64).reshape(-1)
+    ops_t = torch.from_numpy(ops_arr.view(np.int64)).cuda()
+    out = torch.zeros(128 * ncols, dtype=torch.float32, device="cuda")
+    _lib.call("vpx_probe_umma", img.data_ptr(), img.numel(), ops_t.data_ptr(), len(ops), out.data_ptr(),
+              ncols, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    return out.cpu().numpy().reshape(128, ncols)
+
+
+def check(name, got, want):
+    err = float(np.max(np.abs(got - want))) if want.size else 0.0
+    scale = float(np.max(np.abs(want))) or 1.0
+    ok = err / scale < 1e-5
+    RESULTS[name] = {"ok": ok, "rel": err / scale}
+    print(f"{'PASS' if ok else 'FAIL'} {name}: rel {err / scale:.3e}")
+    return ok
+
+
+class Img:
+    def __init__(self, nbytes):
+        self.b = np.zeros(nbytes, dtype=np.uint8)
+
+    def put_f32(self, byte_off, val):
+        self.b[byte_off:byte_off + 4] = np.frombuffer(np.float32(val).tobytes(), dtype=np.uint8)
+
+    def f32_view(self):
+        return self.b.view(np.float32)
+
+
+def place_kmajor_interleave(img, base, X, lbo, sbo):
+    R, K = X.shape
+    for r in range(R):
+        for k in range(K):
+            off = base + (r % 8) * 16 + (r // 8) * sbo + (k // 4) * lbo + (k % 4) * 4
+            img.put_f32(off, X[r, k])
+
+
+def swz128(addr):
+    return addr ^ (((addr >> 7) & 7) << 4)
+
+
+def swz(addr, mode):
+    if mode == 128:
+        return addr ^ (((addr >> 7) & 7) << 4)
+    if mode == 64:
+        return addr ^ (((addr >> 7) & 3) << 4)
+    if mode == 32:
+        return addr ^ (((addr >> 7) & 1) << 4)
+    return addr
+
+
+def t_kmajor_interleave():
+    A = tf32(rng.standard_normal((128, 8)))
+    B = tf32(rng.standard_normal((16, 8)))
+    img = Img(16384)
+    place_kmajor_interleave(img, 0, A, lbo=2048, sbo=128)
+    place_kmajor_interleave(img, 4096, B, lbo=256, sbo=128)
+    ops = [(sdesc(0, 2048, 128, 0), sdesc(4096, 256, 128, 0), idesc(128, 16), 1)]
+    ops = [(a, b, c | (0 << 32), 0) for a, b, c, _ in ops]
+    D = run(img.b, ops, 16)
+    check("kmajor_interleave_M128_N16", D[:, :16], A @ B.T)
+
+    # row-shifted window: rows stored contiguously at 16B pitch, A = rows s..s+127
+    # chunk0 = cols 0..3 (plane 0), chunk1 = cols 4..7 = next voxel (LBO=16 overlap)
+    V = tf32(rng.standard_normal((140, 4)))
+    img = Img(16384)
+    for r in range(140):
+        for k in range(4):
+            img.put_f32(r * 16 + k * 4, V[r, k])
+    B = tf32(rng.standard_normal((16, 8)))
+    place_kmajor_interleave(img, 8192, B, lbo=256, sbo=128)
+    for s in (0, 1, 3):
+        A = np.concatenate([V[s:s + 128], V[s + 1:s + 129]], axis=1)
+        ops = [(sdesc(16 * s, 16, 128, 0), sdesc(8192, 256, 128, 0), idesc(128, 16), 0)]
+        D = run(img.b, ops, 16)
+        check(f"kmajor_interleave_shift{s}_lbo16", D[:, :16], A @ B.T)
+    # pair taps at distance 2 rows (LBO = 32) and at a row distance of 130 (LBO=2080)
+    for dist in (2, 7):
+        s = 1
+        A = np.concatenate([V[s:s + 128], V[s + dist:s + dist + 128]], axis=1) if s + dist + 128 <= 140 else None
+        if A is None:
+            continue
+        ops = [(sdesc(16 * s, 16 * dist, 128, 0), sdesc(8192, 256, 128, 0), idesc(128, 16), 0)]
+        D = run(img.b, ops, 16)
+        check(f"kmajor_interleave_lbo{16 * dist}", D[:, :16], A @ B.T)
+
+
+def t_kmajor_sw(mode):
+    # rows of `mode` bytes (mode/4 tf32 channels), 8-row atoms of 8*mode bytes
+    ch = mode // 4
+    nrows = 144
+    V = tf32(rng.standard_normal((nrows, ch)))
+    img = Img(65536)
+    for r in range(nrows):
+        for k in range(ch):
+            la = r * mode + k * 4
+            img.put_f32(swz(la, mode), V[r, k])
+    Bm = tf32(rng.standard_normal((32, ch)))
+    bbase = 32768
+    for r in range(32):
+        for k in range(ch):
+            la = r * mode + k * 4
+            img.put_f32(bbase + swz(la, mode), Bm[r, k])
+    lay = {128: 2, 64: 4, 32: 6}[mode]
+    sbo = 8 * mode
+    for s in (0, 1, 5, 8):
+        for bo_mode in ("zero", "phase"):
+            if s == 0 and bo_mode == "phase":
+                continue
+            ops = []
+            for kk in range(ch // 8):
+                bo = 0 if bo_mode == "zero" else (s & 7)
+                a = sdesc(s * mode + 32 * kk, 16, sbo, lay, bo)
+                b = sdesc(bbase + 32 * kk, 16, sbo, lay, 0)
+                ops.append((a, b, idesc(128, 32), 1 if kk else 0))
+            D = run(img.b, ops, 32)
+            check(f"kmajor_sw{mode}_shift{s}_base{bo_mode}", D[:, :32], V[s:s + 128] @ Bm.T)
+
+
+def t_mnmajor_interleave():
+    # A[m][k] MN-major: core matrix = 8 k-rows x 4 m (16B); m-group at SBO, k-group at LBO
+    A = tf32(rng.standard_normal((128, 16)))
+    B = tf32(rng.standard_normal((16, 16)))
+    img = Img(32768)
+    sbo_a, lbo_a = 128, 4096
+    for m in range(128):
+        for k in range(16):
+            img.put_f32((m // 4) * sbo_a + (k % 8) * 16 + (k // 8) * lbo_a + (m % 4) * 4, A[m, k])
+    bb = 16384
+    sbo_b, lbo_b = 128, 512
+    for n in range(16):
+        for k in range(16):
+            img.put_f32(bb + (n // 4) * sbo_b + (k % 8) * 16 + (k // 8) * lbo_b + (n % 4) * 4, B[n, k])
+    ops = []
+    for kk in range(2):
+        ops.append((sdesc(kk * lbo_a, lbo_a, sbo_a, 0), sdesc(bb + kk * lbo_b, lbo_b, sbo_b, 0),
+                    idesc(128, 16, True, True), 1 if kk else 0))
+    D = run(img.b, ops, 16)
+    check("mnmajor_interleave_A_B", D[:, :16], A @ B.T)
+    # swapped roles of LBO/SBO hypothesis
+    ops = []
+    for kk in range(2):
+        ops.append((sdesc(kk * lbo_a, sbo_a, lbo_a, 0), sdesc(bb + kk * lbo_b, sbo_b, lbo_b, 0),
+                    idesc(128, 16, True, True), 1 if kk else 0))
+    D = run(img.b, ops, 16)
+    check("mnmajor_interleave_swapped_lbo_sbo", D[:, :16], A @ B.T)
+
+
+def t_mnmajor_sw(mode):
+    # MN-major swizzled: rows = k (8 per atom) of `mode` bytes = mode/4 consecutive mn elements.
+    per = mode // 4
+    K = 8
+    M = 128
+    A = tf32(rng.standard_normal((M, K)))
+    B = tf32(rng.standard_normal((32, K)))
+    img = Img(65536)
+    # A: mn-block j (per elements) x 8 k rows -> atom of 8*mode bytes at j*atom
+    atom = 8 * mode
+    for m in range(M):
+        for k in range(K):
+            la = (m // per) * atom + k * mode + (m % per) * 4
+            img.put_f32(swz(la, mode), A[m, k])
+    bb = 32768
+    for n in range(32):
+        for k in range(K):
+            la = (n // per) * atom + k * mode + (n % per) * 4
+            img.put_f32(bb + swz(la, mode), B[n, k])
+    lay = {128: 2, 64: 4, 32: 6}[mode]
+    for name, lbo, sbo in (("lbo=atom", atom, 0), ("sbo=atom", 0, atom), ("both", atom, atom)):
+        ops = [(sdesc(0, lbo, sbo, lay), sdesc(bb, lbo, sbo, lay), idesc(128, 32, True, True), 0)]
+        D = run(img.b, ops, 32)
+        check(f"mnmajor_sw{mode}_{name}", D[:, :32], A @ B.T)
+
+
+def t_m64():
+    A = tf32(rng.standard_normal((64, 8)))
+    B = tf32(rng.standard_normal((16, 8)))
+    img = Img(16384)
+    place_kmajor_interleave(img, 0, A, lbo=1024, sbo=128)
+    place_kmajor_interleave(img, 4096, B, lbo=256, sbo=128)
+    ops = [(sdesc(0, 1024, 128, 0), sdesc(4096, 256, 128, 0), idesc(64, 16), 0)]
+    D = run(img.b, ops, 16)
+    want = A @ B.T
+    # report where rows landed
+    found = {}
+    for r in range(64):
+        for lane in range(128):
+            if np.max(np.abs(D[lane, :16] - want[r])) < 1e-4 * (np.max(np.abs(want[r])) + 1e-6):
+                found[r] = lane
+                break
+    print("M=64 row->lane map (first 16):", [found.get(r) for r in range(16)],
+          "... rows 32..35:", [found.get(r) for r in range(32, 36)])
+    RESULTS["m64_row_lane"] = {r: found.get(r) for r in range(64)}
+
+
+def t_tma():
+    # 5D tensor (N=1, D=3, H=4, W=20, C=4) fp32; box {4, 18, 3, 2, 1} at coords (0,-1,-1,-1,0)
+    C, W, H, D, N = 4, 20, 4, 3, 1
+    X = rng.standard_normal((N, D, H, W, C)).astype(np.float32)
+    g = torch.from_numpy(X).cuda()
+    dims = (ctypes.c_uint64 * 5)(C, W, H, D, N)
+    strides = (ctypes.c_uint64 * 4)(C * 4, W * C * 4, H * W * C * 4, D * H * W * C * 4)
+    box = (ctypes.c_uint32 * 5)(4, 18, 3, 2, 1)
+    coords = (ctypes.c_int32 * 5)(0, -1, -1, -1, 0)
+    nbytes = 4 * 18 * 3 * 2 * 4
+    out = torch.zeros(nbytes // 4, dtype=torch.float32, device="cuda")
+    _lib.call("vpx_probe_tma", g.data_ptr(), ctypes.addressof(dims), ctypes.addressof(strides),
+              ctypes.addressof(box), 0, ctypes.addressof(coords), out.data_ptr(), nbytes,
+              torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    got = out.cpu().numpy().reshape(2, 3, 18, 4)
+    Xp = np.zeros((D + 2, H + 2, W + 2, C), np.float32)
+    Xp[1:-1, 1:-1, 1:-1] = X[0]
+    want = Xp[0:2, 0:3, 0:18]
+    check("tma_5d_oob_zero_inner16", got, want)
+
+    # swizzle-128 box: C=32 channels (128B rows), 8 voxels
+    C2 = 32
+    X2 = rng.standard_normal((1, 1, 1, 16, C2)).astype(np.float32)
+    g2 = torch.from_numpy(X2).cuda()
+    dims = (ctypes.c_uint64 * 5)(C2, 16, 1, 1, 1)
+    strides = (ctypes.c_uint64 * 4)(C2 * 4, 16 * C2 * 4, 16 * C2 * 4, 16 * C2 * 4)
+    box = (ctypes.c_uint32 * 5)(32, 16, 1, 1, 1)
+    coords = (ctypes.c_int32 * 5)(0, 0, 0, 0, 0)
+    nbytes = 16 * 128
+    out = torch.zeros(nbytes // 4, dtype=torch.float32, device="cuda")
+    _lib.call("vpx_probe_tma", g2.data_ptr(), ctypes.addressof(dims), ctypes.addressof(strides),
+              ctypes.addressof(box), 128, ctypes.addressof(coords), out.data_ptr(), nbytes,
+              torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    raw = out.cpu().numpy().view(np.uint8)
+    want_b = np.zeros(nbytes, np.uint8)
+    src = X2.reshape(16, 32).view(np.uint8).reshape(-1)
+    for la in range(0, nbytes, 4):
+        pa = swz(la, 128)
+        want_b[pa:pa + 4] = src[la:la + 4]
+    ok = np.array_equal(raw, want_b)
+    RESULTS["tma_sw128_pattern"] = {"ok": bool(ok)}
+    print(f"{'PASS' if ok else 'FAIL'} tma_sw128_pattern")
+
+
+def t_rate():
+    cyc = torch.zeros(1, dtype=torch.int64, device="cuda")
+    for bf in (0, 1):
+        for N in (16, 32, 64, 128, 256):
+            for nacc in (1, 2, 4, 8, 16):
+                if N * nacc > 512:
+                    continue
+                it = 1024
+                _lib.call("vpx_probe_mma_rate", N, it, 0, nacc, bf, cyc.data_ptr(),
+                          torch.cuda.current_stream().cuda_stream)
+                torch.cuda.synchronize()
+                c = int(cyc.item())
+                k = 16 if bf else 8
+                print(f"RATE {'bf16' if bf else 'tf32'} N={N} nacc={nacc}: {c / it:.2f} cyc/mma, "
+                      f"{128 * N * k * it / c:.0f} MAC/cyc")
+                RESULTS[f"rate_bf{bf}_N{N}_acc{nacc}"] = c / it
+
+
+def t_rate2():
+    cyc = torch.zeros(1, dtype=torch.int64, device="cuda")
+    for bf in (0, 1):
+        for N, accs in ((16, (1, 4, 8)), (32, (1, 4, 8)), (64, (1, 4, 8)), (128, (1, 2)), (256, (1, 2))):
+            for nacc in accs:
+                it = 2048
+                _lib.call("vpx_probe_mma_rate2", N, nacc, bf, it, cyc.data_ptr(),
+                          torch.cuda.current_stream().cuda_stream)
+                torch.cuda.synchronize()
+                c = int(cyc.item())
+                k = 16 if bf else 8
+                print(f"RATE2 {'bf16' if bf else 'tf32'} N={N} nacc={nacc}: {c / it:.2f} cyc/mma, "
+                      f"{128 * N * k * it / c:.0f} MAC/cyc")
+                RESULTS[f"rate2_bf{bf}_N{N}_acc{nacc}"] = c / it
+
+
+def swz32b(addr):
+    # 128B swizzle with 32B atomicity: bits [7,9) xor into [5,7)
+    return addr ^ (((addr >> 7) & 3) << 5)
+
+
+def t_mn32b():
+    """MN-major tf32 with SWIZZLE_128B_BASE32B (layout type 1): rows = k (128 B = 32 mn)."""
+    M, N, K = 128, 32, 16
+    A = tf32(rng.standard_normal((M, K)))
+    B = tf32(rng.standard_normal((N, K)))
+    img = Img(65536)
+    # element (m,k): (m//32)*LBO + (k//4)*SBO + (k%4)*128 + (m%32)*4
+    LBO_A, SBO = 2048, 512
+    for m in range(M):
+        for k in range(K):
+            la = (m // 32) * LBO_A + (k // 4) * SBO + (k % 4) * 128 + (m % 32) * 4
+            img.put_f32(swz32b(la), A[m, k])
+    bb = 32768
+    for n in range(N):
+        for k in range(K):
+            la = (k // 4) * SBO + (k % 4) * 128 + (n % 32) * 4
+            img.put_f32(bb + swz32b(la), B[n, k])
+    for lbo_first in (True, False):
+        ops = []
+        for kk in range(K // 8):
+            la, sa = (LBO_A, SBO) if lbo_first else (SBO, LBO_A)
+            ops.append((sdesc(kk * 2 * SBO, la, sa, 1), sdesc(bb + kk * 2 * SBO, 4096 if lbo_first else SBO, SBO if lbo_first else 4096, 1),
+                        idesc(M, N, True, True), 1 if kk else 0))
+        D = run(img.b, ops, 32)
+        check(f"mn_sw128_32b_lbo_is_mnblock={lbo_first}", D[:, :32], A @ B.T)
+    # dense voxel-row data: rows of 128 B = 8 voxels x 4 ch; sub-row shift by j*16 B
+    V = tf32(rng.standard_normal((1024, 4)))  # voxel-major, 4 ch
+    img = Img(65536)
+    flat = V.reshape(-1)
+    for i in range(flat.size):
+        img.put_f32(swz32b(i * 4), flat[i])
+    Bm = tf32(rng.standard_normal((32, 8)))
+    bb = 32768
+    for n in range(32):
+        for k in range(8):
+            la = (k // 4) * 512 + (k % 4) * 128 + n * 4
+            img.put_f32(bb + swz32b(la), Bm[n, k])
+    for j in (0, 1, 3):
+        # A[m=(c,ci)][k] = V[8k + j + c][ci] for m in 0..127 -> 4 mn-blocks at LBO=...; use M=128
+        # block b (m//32) at LBO = 8*128*? choose LBO = 4096 (voxel 256 offset)
+        Am = np.zeros((128, 8), np.float32)
+        for m in range(128):
+            for k in range(8):
+                Am[m, k] = V[(m // 32) * 256 + 8 * k + j + (m % 32) // 4, m % 4]
+        ops = [(sdesc(16 * j, 4096, 512, 1), sdesc(bb, 4096, 512, 1), idesc(128, 32, True, True), 0)]
+        D = run(img.b, ops, 32)
+        check(f"mn_sw128_32b_subrow_shift{j}", D[:, :32], Am @ Bm.T)
+
+
+def t_tma32b():
+    C2 = 32
+    X2 = rng.standard_normal((1, 1, 1, 16, C2)).astype(np.float32)
+    g2 = torch.from_numpy(X2).cuda()
+    dims = (ctypes.c_uint64 * 5)(C2, 16, 1, 1, 1)
+    strides = (ctypes.c_uint64 * 4)(C2 * 4, 16 * C2 * 4, 16 * C2 * 4, 16 * C2 * 4)
+    box = (ctypes.c_uint32 * 5)(32, 16, 1, 1, 1)
+    coords = (ctypes.c_int32 * 5)(0, 0, 0, 0, 0)
+    nbytes = 16 * 128
+    out = torch.zeros(nbytes // 4, dtype=torch.float32, device="cuda")
+    _lib.call("vpx_probe_tma", g2.data_ptr(), ctypes.addressof(dims), ctypes.addressof(strides),
+              ctypes.addressof(box), 1282, ctypes.addressof(coords), out.data_ptr(), nbytes,
+              torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    raw = out.cpu().numpy().view(np.uint8)
+    want_b = np.zeros(nbytes, np.uint8)
+    src = X2.reshape(16, 32).view(np.uint8).reshape(-1)
+    for la in range(0, nbytes, 4):
+        pa = swz32b(la)
+        want_b[pa:pa + 4] = src[la:la + 4]
+    ok = np.array_equal(raw, want_b)
+    RESULTS["tma_sw128_atom32b_pattern"] = {"ok": bool(ok)}
+    print(f"{'PASS' if ok else 'FAIL'} tma_sw128_atom32b_pattern")
+
+
+TESTS = {"tma": t_tma, "ki": t_kmajor_interleave, "sw128": lambda: t_kmajor_sw(128),
+         "sw64": lambda: t_kmajor_sw(64), "sw32": lambda: t_kmajor_sw(32),
+         "mni": t_mnmajor_interleave, "mnsw128": lambda: t_mnmajor_sw(128),
+         "mnsw64": lambda: t_mnmajor_sw(64), "m64": t_m64, "rate": t_rate,
+         "mn32b": t_mn32b, "rate2": t_rate2, "tma32b": t_tma32b}
+
+if __name__ == "__main__":
+    import os
+    print(_lib.load().vpx_version().decode())
+    names = sys.argv[1:] or list(TESTS)
+    for n in names:
+        TESTS[n]()
+    os.makedirs("gpurun_out", exist_ok=True)
+    with open(f"gpurun_out/probe_{'_'.join(names)}.json", "w") as f:
+        json.dump(RESULTS, f, indent=1, default=str)
