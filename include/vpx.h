@@ -114,11 +114,12 @@ int vpx_deconv_bwd_filter(const float* x, const int* xf, const float* u, const i
                           int accumulate, void* ws, void* stream);
 
 /* ------------------------------------------------------------------- halo --
- * Copy the box {z0,y0,x0,ez,ey,ex} (frame coordinates, margins included) of a
- * frame to a dense (n,z,y,x,c) buffer (mode 0, pack), back (mode 1, unpack) or
- * accumulate into the frame (mode 2, adjoint unpack).  Replaces the slab copies
- * of reference fabric.py:404-410,436-442 / tensor.py:388-409. */
-int vpx_halo_copy(float* frame, const int* ff, const int* box6, float* buf, int mode, void* stream);
+ * Copy the box {n0,z0,y0,x0,en,ez,ey,ex} (frame coordinates, margins included)
+ * of a frame to a dense (n,z,y,x,c) buffer (mode 0, pack), back (mode 1,
+ * unpack) or accumulate into the frame (mode 2, adjoint unpack).  Replaces the
+ * slab copies of reference fabric.py:404-410,436-442 / tensor.py:388-409 and
+ * the block moves of redistribute (reference layers/distributed.py:298-368). */
+int vpx_halo_copy(float* frame, const int* ff, const int* box8, float* buf, int mode, void* stream);
 
 /* ------------------------------------------------------------------- prng --
  * Pinned splitmix64 streams (reference prng.py:28-90), bit-exact with numpy:

@@ -324,11 +324,12 @@ __global__ void reduce_parts_kernel(const float* __restrict__ part, int P, long 
 }
 
 // ------------------------------------------------------------------- halo
-// Copy a box of a frame (frame coordinates, i.e. margins included) to/from a
-// dense buffer in (n, z, y, x, c) C order.  mode 0: pack, 1: unpack, 2: unpack-add.
-__global__ void halo_copy_kernel(float* __restrict__ fr, Frame f, int z0, int y0, int x0, int ez,
-                                 int ey, int ex, float* __restrict__ buf, int mode) {
-  const long long total = (long long)f.n * ez * ey * ex * f.c;
+// Copy a box of a frame (frame coordinates, i.e. margins included; samples
+// n0..n0+en) to/from a dense buffer in (n, z, y, x, c) C order.
+// mode 0: pack, 1: unpack, 2: unpack-add.
+__global__ void halo_copy_kernel(float* __restrict__ fr, Frame f, int n0, int z0, int y0, int x0,
+                                 int en, int ez, int ey, int ex, float* __restrict__ buf, int mode) {
+  const long long total = (long long)en * ez * ey * ex * f.c;
   const long long Wf = f.w + 2 * f.mw, Hf = f.h + 2 * f.mh, Df = f.d + 2 * f.md;
   GRID_STRIDE(i, total) {
     long long t = i;
@@ -339,7 +340,7 @@ __global__ void halo_copy_kernel(float* __restrict__ fr, Frame f, int z0, int y0
     const int y = t % ey;
     t /= ey;
     const int z = t % ez;
-    const int n = t / ez;
+    const int n = n0 + static_cast<int>(t / ez);
     const long long off = ((((long long)n * Df + z0 + z) * Hf + y0 + y) * Wf + x0 + x) * f.c + c;
     if (mode == 0)
       buf[i] = fr[off];
@@ -610,12 +611,17 @@ extern "C" int vpx_deconv_bwd_filter(const float* x, const int* xf, const float*
   reduce_parts_kernel<<<grid1d(len), 256, 0, S(st)>>>(static_cast<float*>(ws), P, len, wg, accumulate);
   LAUNCH_TAIL;
 }
-extern "C" int vpx_halo_copy(float* fr, const int* ff, const int* box6, float* buf, int mode,
+extern "C" int vpx_halo_copy(float* fr, const int* ff, const int* box8, float* buf, int mode,
                              void* st) {
   Frame f = F(ff);
-  const long long total = (long long)f.n * box6[3] * box6[4] * box6[5] * f.c;
-  halo_copy_kernel<<<grid1d(total), 256, 0, S(st)>>>(fr, f, box6[0], box6[1], box6[2], box6[3],
-                                                     box6[4], box6[5], buf, mode);
+  const int* b = box8;
+  if (b[0] < 0 || b[4] < 0 || b[0] + b[4] > f.n || b[1] < 0 || b[1] + b[5] > f.d + 2 * f.md ||
+      b[2] < 0 || b[2] + b[6] > f.h + 2 * f.mh || b[3] < 0 || b[3] + b[7] > f.w + 2 * f.mw)
+    VPX_FAIL(VPX_ERR_OUT_OF_BOUNDS, "halo box outside frame");
+  const long long total = (long long)b[4] * b[5] * b[6] * b[7] * f.c;
+  if (total == 0) return VPX_OK;
+  halo_copy_kernel<<<grid1d(total), 256, 0, S(st)>>>(fr, f, b[0], b[1], b[2], b[3], b[4], b[5],
+                                                     b[6], b[7], buf, mode);
   LAUNCH_TAIL;
 }
 extern "C" int vpx_prng_uniform(unsigned long long key, long long n, double lo, double hi,

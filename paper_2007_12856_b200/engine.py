@@ -1,0 +1,555 @@
+"""Hybrid data x spatial parallel training step on B200s.
+
+Public API mirrors the reference engine (reference
+pkg/src/voxpar/model/engine.py): ``make_plan`` / ``Plan``, ``Batch``,
+``RankState``, ``forward``, ``loss_and_grad``, ``backward``,
+``train_step`` and ``scatter_batch``.  One process drives one GPU; the
+per-rank program is the reference's, with device DistTensors, libvpx
+kernels and NCCL collectives underneath.
+
+Layout decisions (make_plan, reference engine.py:62-176): every layer is
+"spatial" until the redistribution point -- the first layer that cannot run
+partitioned on the grid, or the flatten -- after which it is "collapsed"
+(full spatial extent on one lead rank per data-parallel group) and, past
+the flatten, "flat".  Each edge's partition carries the halo radii its
+consumer needs.
+
+Gradients: every parameter's gradient is written straight into a view of one
+flat fp32 bucket (param_entries order, reference networks.py:133-153), which
+is allreduced once over all ranks (reference engine.py:446-462) -- that sum
+both completes spatial partial sums and averages data-parallel groups,
+because the loss is normalised by the global batch.  Adam then runs as one
+kernel over the flat parameter / moment buffers.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import torch
+
+from . import _lib, prng
+from .accounting import out_shape
+from .comm import RankCtx
+from .errors import NonDivisible, ShapeMismatch
+from .frames import DistTensor, stream_ptr
+from .geometry import DistTensorMeta, ProcessGrid, Shape5D, make_partition
+from . import layers as D
+from .networks import NetworkSpec, param_entries
+
+NO_HALO = (0, 0, 0)
+
+
+# --------------------------------------------------------------------- plan
+
+@dataclass(frozen=True)
+class Plan:
+    net: NetworkSpec
+    grid: ProcessGrid
+    n_global: int
+    w_i: int
+    placement: tuple   # per layer: "spatial" | "collapsed" | "flat"
+    in_meta: tuple     # per layer: DistTensorMeta of its 5D input (None past flatten)
+    out_radii: tuple   # per layer: halo radii of its output
+    redist_idx: int    # layer the redistribution precedes; -1 = never
+    redist_src_meta: DistTensorMeta
+    leads: tuple       # process rank of each group's lead
+    label_meta: DistTensorMeta  # xent label layout; None for mse
+
+    @property
+    def input_meta(self) -> DistTensorMeta:
+        return self.in_meta[0]
+
+
+def _consumer_radii(layer):
+    return layer.params.radii if layer.kind == "conv" else NO_HALO
+
+
+def _why_not_spatial(layer, in_shape, parts):
+    """None if `layer` can run partitioned on `parts`, else the reason
+    (reference engine.py:62-81)."""
+    ext = in_shape[2:]
+    for name, e, p in zip("dhw", ext, parts):
+        if e % p:
+            return f"extent {name}={e} not divisible by {p} partitions"
+    if layer.kind == "conv":
+        for name, e, p, r, s in zip("dhw", ext, parts, layer.params.radii, layer.params.stride):
+            loc = e // p
+            if p > 1 and r > loc:
+                return f"halo radius {r} exceeds local extent {loc} in {name}"
+            if p > 1 and loc % s:
+                return f"local extent {name}={loc} not divisible by stride {s}"
+    elif layer.kind == "pool":
+        for name, e, p in zip("dhw", ext, parts):
+            if (e // p) % 2:
+                return f"local extent {name}={e // p} is odd"
+    return None
+
+
+def make_plan(net: NetworkSpec, grid: ProcessGrid, n_global: int, w_i: int,
+              redistribute_before: str = None) -> Plan:
+    shapes = [(n_global, net.in_channels, w_i, w_i, w_i)]
+    by_name = {}
+    for layer in net.layers:
+        skip = by_name.get(layer.skip) if layer.kind == "concat" else None
+        nxt = out_shape(layer, shapes[-1], skip_shape=skip)
+        by_name[layer.name] = nxt
+        shapes.append(nxt)
+
+    parts = grid.spatial_parts
+    redist, reasons = -1, {}
+    for i, layer in enumerate(net.layers):
+        if layer.kind == "flatten":
+            if redist < 0:
+                redist = i
+            break
+        why = _why_not_spatial(layer, shapes[i], parts)
+        if why is not None and redist < 0:
+            redist, reasons[i] = i, why
+    if redistribute_before is not None:
+        forced = net.layer_index(redistribute_before)
+        if redist >= 0 and forced > redist:
+            bad = net.layers[redist]
+            raise NonDivisible(f"layer {bad.name!r} cannot run spatially on grid {parts}: "
+                               f"{reasons.get(redist, 'needs flat layout')}")
+        redist = forced
+    if redist == 0 and grid.spatial_size > 1:
+        raise NonDivisible(f"layer {net.layers[0].name!r} cannot run spatially on grid {parts}: "
+                           f"{reasons.get(0)}")
+    if redist >= 0:
+        for i, layer in enumerate(net.layers):
+            if layer.kind == "concat" and net.layer_index(layer.skip) < redist <= i:
+                raise NonDivisible(f"redistribution before {net.layers[redist].name!r} would split the "
+                                   f"{layer.name!r} skip connection across layouts")
+
+    leads = tuple(grid.rank_of(g, 0, 0, 0) for g in range(grid.groups))
+    collapsed_grid = ProcessGrid(grid.groups, 1, 1, 1)
+
+    def meta_for(shape, spatial, radii):
+        s5 = Shape5D(*shape)
+        if spatial:
+            return make_partition(s5, grid, radii)
+        return make_partition(s5, collapsed_grid, radii, rank_map=leads)
+
+    placement, in_meta, out_radii = [], [], []
+    flat = False
+    for i, layer in enumerate(net.layers):
+        if layer.kind == "flatten":
+            placement.append("flat")
+            in_meta.append(meta_for(shapes[i], False, NO_HALO))
+            out_radii.append(NO_HALO)
+            flat = True
+            continue
+        if flat:
+            placement.append("flat")
+            in_meta.append(None)
+            out_radii.append(NO_HALO)
+            continue
+        spatial = redist < 0 or i < redist
+        placement.append("spatial" if spatial else "collapsed")
+        in_meta.append(meta_for(shapes[i], spatial, _consumer_radii(layer)))
+        nxt = net.layers[i + 1] if i + 1 < len(net.layers) else None
+        if nxt is None or nxt.kind == "flatten" or (redist >= 0 and i + 1 == redist):
+            out_radii.append(NO_HALO)
+        else:
+            out_radii.append(_consumer_radii(nxt))
+    redist_src = meta_for(shapes[redist], True, NO_HALO) if redist >= 0 else None
+    label_meta = None
+    if net.loss == "xent":
+        o = shapes[-1]
+        label_meta = meta_for((o[0], 1) + tuple(o[2:]), placement[-1] == "spatial", NO_HALO)
+    return Plan(net, grid, n_global, w_i, tuple(placement), tuple(in_meta), tuple(out_radii),
+                redist, redist_src, leads, label_meta)
+
+
+def _meta_like(meta: DistTensorMeta, radii=NO_HALO):
+    return make_partition(meta.global_shape, meta.grid, radii, meta.rank_map)
+
+
+def _grid_rank(meta: DistTensorMeta, rank: int):
+    return meta.rank_map.index(rank) if rank in meta.rank_map else None
+
+
+# -------------------------------------------------------------------- state
+
+@dataclass
+class Batch:
+    """One rank's share of a global batch (reference engine.py:179-194).
+
+    x_block: DistTensor (or NCDHW array) of this rank's input block, None when
+    it holds none.  target: (n_local, out_dim) CUDA tensor (mse).  y_block:
+    int64 CUDA tensor (n_local, d, h, w) labels (xent).
+    """
+
+    x_block: object = None
+    target: torch.Tensor = None
+    y_block: torch.Tensor = None
+    sample_ids: tuple = ()
+    epoch: int = 0
+    iteration: int = 0
+
+
+class FlatParams:
+    """All trainable tensors as views of one flat fp32 buffer (plus a twin
+    gradient bucket and Adam moments), in param_entries order."""
+
+    def __init__(self, net: NetworkSpec, device="cuda"):
+        self.entries = param_entries(net)
+        total = sum(_numel(s) for _, s, _ in self.entries)
+        self.flat = torch.zeros(total, dtype=torch.float32, device=device)
+        self.grad = torch.zeros(total, dtype=torch.float32, device=device)
+        self.views, self.grads, self.offsets = {}, {}, {}
+        pos = 0
+        for name, shape, _ in self.entries:
+            n = _numel(shape)
+            self.views[name] = self.flat[pos:pos + n].view(shape)
+            self.grads[name] = self.grad[pos:pos + n].view(shape)
+            self.offsets[name] = (pos, n)
+            pos += n
+        self.numel = total
+
+
+def _numel(shape):
+    n = 1
+    for s in shape:
+        n *= s
+    return n
+
+
+@dataclass
+class OptimizerState:
+    kind: str = "adam"
+    m: torch.Tensor = None
+    v: torch.Tensor = None
+    t: int = 0
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+
+
+@dataclass
+class RankState:
+    """Per-rank replica of everything training mutates (reference engine.py:197-203)."""
+
+    params: FlatParams
+    bn_states: dict
+    opt: OptimizerState
+
+
+def init_params(net: NetworkSpec, seed: int = 0) -> FlatParams:
+    """Kaiming-uniform U(+-sqrt(6/fan_in)) drawn from prng [seed,-1,i] in fp64
+    on the device then cast; gamma 1, beta/bias 0 (reference optim.py:97-113).
+    Bit-identical to the reference's fp32 initialisation."""
+    fp = FlatParams(net)
+    for i, (name, shape, fan_in) in enumerate(fp.entries):
+        view = fp.views[name]
+        if fan_in == 0:
+            view.fill_(1.0 if name.endswith(".gamma") else 0.0)
+        else:
+            b = (6.0 / fan_in) ** 0.5
+            prng.uniform_device([seed, -1, i], view.numel(), -b, b, out=view.view(-1))
+    return fp
+
+
+def make_state(net: NetworkSpec, seed: int = 0, kind: str = "adam") -> RankState:
+    fp = init_params(net, seed)
+    bn = {}
+    for layer in net.layers:
+        if layer.kind == "bn":
+            bn[layer.name] = D.BNState(fp.views[f"{layer.name}.gamma"], fp.views[f"{layer.name}.beta"])
+    opt = OptimizerState(kind)
+    if kind == "adam":
+        opt.m = torch.zeros_like(fp.flat)
+        opt.v = torch.zeros_like(fp.flat)
+    return RankState(fp, bn, opt)
+
+
+def lr_at(lr0: float, epoch: int, horizon: int = 100, terminal: float = 0.01) -> float:
+    """Linear decay schedule (reference optim.py:20-31)."""
+    e = min(max(epoch, 0), horizon)
+    return lr0 * (1.0 - (1.0 - terminal) * e / horizon)
+
+
+def optimizer_step(state: RankState, lr: float):
+    """Adam (bias corrected, sqrt(v_hat)+eps) or SGD over the flat buffers
+    (reference optim.py:63-93)."""
+    p, opt = state.params, state.opt
+    opt.t += 1
+    st = stream_ptr()
+    if opt.kind == "adam":
+        c1 = 1.0 - opt.beta1 ** opt.t
+        c2 = 1.0 - opt.beta2 ** opt.t
+        _lib.call("vpx_adam", p.flat.data_ptr(), p.grad.data_ptr(), opt.m.data_ptr(), opt.v.data_ptr(),
+                  p.numel, float(lr), opt.beta1, opt.beta2, float(c1), float(c2), opt.eps, st)
+    else:
+        _lib.call("vpx_sgd", p.flat.data_ptr(), p.grad.data_ptr(), p.numel, float(lr), st)
+
+
+# ------------------------------------------------------------------ forward
+
+def _flat_mask(layer_idx, step_key, sample_ids, features, keep):
+    seed, epoch, it = step_key
+    rows = [prng.keep_mask_device([seed, epoch, it, int(s), layer_idx], features, keep) for s in sample_ids]
+    if not rows:
+        return torch.zeros((0, features), dtype=torch.uint8, device="cuda")
+    return torch.stack(rows)
+
+
+def _apply_mask(x, mask, keep):
+    return x * (mask.to(x.dtype) / keep)
+
+
+def _flatten(t: DistTensor):
+    """NCDHW-order flatten of a lead-local block (reference engine.py:249-258)."""
+    return t.to_ncdhw().reshape(t.n, -1)
+
+
+def forward(ctx: RankCtx, plan: Plan, state: RankState, batch: Batch, mode: str, seed: int = 0,
+            trace: dict = None):
+    net = plan.net
+    P, bn = state.params.views, state.bn_states
+    me = ctx.rank
+    step_key = (seed, batch.epoch, batch.iteration)
+    cur = None
+    gr0 = _grid_rank(plan.input_meta, me)
+    if gr0 is not None:
+        if batch.x_block is None:
+            raise ShapeMismatch(f"rank {me} holds an input block but the batch has none")
+        cur = batch.x_block if isinstance(batch.x_block, DistTensor) else \
+            DistTensor(plan.input_meta, gr0, batch.x_block)
+    outputs, stash = {}, []
+    for i, layer in enumerate(net.layers):
+        if i == plan.redist_idx and plan.placement[i] != "flat":
+            cur = D.redistribute(ctx, cur, plan.redist_src_meta, plan.in_meta[i])
+        if plan.placement[i] == "flat":
+            if layer.kind == "flatten":
+                if plan.redist_idx == i:
+                    cur = D.redistribute(ctx, cur, plan.redist_src_meta, plan.in_meta[i])
+                stash.append(None)
+                if cur is not None:
+                    cur = _flatten(cur)
+            elif cur is None:
+                stash.append(None)
+            elif layer.kind == "fc":
+                stash.append(cur)
+                cur = torch.addmm(P[f"{layer.name}.b"], cur, P[f"{layer.name}.w"])
+            elif layer.kind == "leaky":
+                stash.append(cur)
+                cur = torch.where(cur >= 0, cur, cur * layer.slope)
+            elif layer.kind == "dropout":
+                if mode == "train":
+                    m = _flat_mask(i, step_key, batch.sample_ids, cur.shape[1], layer.keep)
+                    cur = _apply_mask(cur, m, layer.keep)
+                    stash.append(m)
+                else:
+                    stash.append(None)
+            else:
+                raise ShapeMismatch(f"layer kind {layer.kind!r} after flatten")
+            outputs[layer.name] = cur
+            continue
+        if cur is None:
+            stash.append(None)
+            outputs[layer.name] = None
+            continue
+        radii = plan.out_radii[i]
+        if layer.kind == "conv":
+            stash.append(cur)
+            cur = D.dist_conv3d(ctx, cur, P[f"{layer.name}.w"], layer.params, radii)
+        elif layer.kind == "deconv":
+            stash.append(cur)
+            cur = D.dist_deconv3d(ctx, cur, P[f"{layer.name}.w"], radii)
+        elif layer.kind == "pool":
+            stash.append(cur)
+            cur = D.dist_pool3d(ctx, cur, layer.pool_kind, radii)
+        elif layer.kind == "bn":
+            cur, cache = D.dist_batchnorm(ctx, cur, bn[layer.name], mode, radii)
+            stash.append(cache)
+        elif layer.kind == "leaky":
+            stash.append(cur)
+            cur = D.dist_leaky_relu(cur, layer.slope, radii)
+        elif layer.kind == "concat":
+            skip = outputs[layer.skip]
+            stash.append((cur.c, skip.c))
+            cur = D.dist_concat_channels(cur, skip, radii)
+        elif layer.kind == "dropout":
+            raise ShapeMismatch("spatial dropout is not part of either network")
+        else:
+            raise ShapeMismatch(f"unknown layer kind {layer.kind!r}")
+        outputs[layer.name] = cur
+    if trace is not None:
+        for name, value in outputs.items():
+            trace[("fwd", name)] = value
+    return cur, stash
+
+
+def loss_and_grad(ctx: RankCtx, plan: Plan, pred, batch: Batch):
+    """(loss as a 1-element fp64 CUDA tensor, identical on every rank; dpred)."""
+    net = plan.net
+    if net.loss == "mse":
+        size = plan.n_global * net.out_dim
+        return D.dist_mse(ctx, pred, batch.target, size, None)
+    gs = plan.label_meta.global_shape
+    count = gs.n * gs.d * gs.h * gs.w
+    if pred is None:
+        local = torch.zeros(1, dtype=torch.float64, device="cuda")
+        ctx.allreduce_sum_(local)
+        return local / count, None
+    loss, g = D.dist_cross_entropy(ctx, pred, batch.y_block, count, None)
+    return loss, g
+
+
+def backward(ctx: RankCtx, plan: Plan, state: RankState, stash, dpred, trace: dict = None):
+    """Backward pass writing gradient partials into the flat bucket."""
+    net = plan.net
+    P, G, bn = state.params.views, state.params.grads, state.bn_states
+    u = dpred
+    extra = {}
+    for i in range(len(net.layers) - 1, -1, -1):
+        layer = net.layers[i]
+        kept = stash[i]
+        if plan.placement[i] == "flat":
+            if layer.kind == "flatten":
+                if u is not None:
+                    m = _meta_like(plan.in_meta[i])
+                    gr = _grid_rank(m, ctx.rank)
+                    ls = m.local_shape(gr)
+                    u = DistTensor(m, gr, u.reshape(ls.n, ls.c, ls.d, ls.h, ls.w))
+                if plan.redist_idx == i:
+                    u = D.redistribute(ctx, u, _meta_like(plan.in_meta[i]), plan.redist_src_meta)
+            elif u is None:
+                pass
+            elif layer.kind == "fc":
+                w = P[f"{layer.name}.w"]
+                torch.mm(kept.t(), u, out=G[f"{layer.name}.w"])
+                torch.sum(u, dim=0, out=G[f"{layer.name}.b"])
+                u = u @ w.t()
+            elif layer.kind == "leaky":
+                u = torch.where(kept >= 0, u, u * layer.slope)
+            elif layer.kind == "dropout":
+                if kept is not None:
+                    u = _apply_mask(u, kept, layer.keep)
+            if trace is not None:
+                trace[("bwd", layer.name)] = u
+            continue
+        if u is not None and layer.name in extra:
+            u = D.add_into(u, extra.pop(layer.name))
+        if u is None:
+            if i == plan.redist_idx:
+                u = D.redistribute(ctx, None, _meta_like(plan.in_meta[i]), plan.redist_src_meta)
+            if trace is not None:
+                trace[("bwd", layer.name)] = u
+            continue
+        in_meta = plan.in_meta[i]
+        if layer.kind == "conv":
+            D.dist_conv3d_bwd_filter(ctx, kept, u, layer.params, reduce=False, out=G[f"{layer.name}.w"])
+            if i == 0 and trace is None:
+                u = None  # nothing consumes the network input's gradient
+            else:
+                u = D.dist_conv3d_bwd_data(ctx, u, P[f"{layer.name}.w"], layer.params, in_meta)
+        elif layer.kind == "deconv":
+            D.dist_deconv3d_bwd_filter(ctx, kept, u, reduce=False, out=G[f"{layer.name}.w"])
+            u = D.dist_deconv3d_bwd_data(ctx, u, P[f"{layer.name}.w"], in_meta)
+        elif layer.kind == "pool":
+            u = D.dist_pool3d_bwd(ctx, kept, u, layer.pool_kind, in_meta)
+        elif layer.kind == "bn":
+            u, _, _ = D.dist_batchnorm_bwd(ctx, u, bn[layer.name], kept, in_meta,
+                                           dgamma=G[f"{layer.name}.gamma"], dbeta=G[f"{layer.name}.beta"])
+        elif layer.kind == "leaky":
+            u = D.dist_leaky_relu_bwd(kept, u, layer.slope, in_meta)
+        elif layer.kind == "concat":
+            c_main, _ = kept
+            main, sk = D.dist_concat_bwd(u, c_main, _meta_like(in_meta),
+                                         _skip_meta(plan, layer), extra.get(layer.skip))
+            extra[layer.skip] = sk
+            u = main
+        if u is not None and i == plan.redist_idx:
+            u = D.redistribute(ctx, u, _meta_like(in_meta), plan.redist_src_meta)
+        if trace is not None:
+            trace[("bwd", layer.name)] = u
+    return G
+
+
+def _skip_meta(plan: Plan, concat_layer):
+    """Layout of the skip source's output (the concat's second operand)."""
+    net = plan.net
+    j = net.layer_index(concat_layer.skip)
+    src_in = plan.in_meta[j]
+    gs = src_in.global_shape
+    o = out_shape(net.layers[j], (gs.n, gs.c, gs.d, gs.h, gs.w))
+    return make_partition(Shape5D(*o), src_in.grid, NO_HALO, src_in.rank_map)
+
+
+def gradient_allreduce(ctx: RankCtx, state: RankState):
+    """One flat allreduce over all ranks (reference engine.py:446-462)."""
+    ctx.allreduce_sum_(state.params.grad, None)
+
+
+def train_step(ctx: RankCtx, plan: Plan, state: RankState, batch: Batch, lr: float, seed: int = 0):
+    """One hybrid-parallel training step; returns the loss as a 1-element
+    fp64 CUDA tensor (identical on every rank).  No host synchronisation."""
+    state.params.grad.zero_()
+    pred, stash = forward(ctx, plan, state, batch, "train", seed)
+    loss, dpred = loss_and_grad(ctx, plan, pred, batch)
+    backward(ctx, plan, state, stash, dpred)
+    gradient_allreduce(ctx, state)
+    optimizer_step(state, lr)
+    return loss
+
+
+# ------------------------------------------------------------------ batches
+
+def synthetic_batch_full(net: NetworkSpec, w_i: int, n: int, seed: int = 0):
+    """The reference's deterministic verify batch (reference cli.py:112-125):
+    x = prng.uniform([seed,-3,0], N*C*W^3, -1, 1) as NCDHW, targets
+    uniform([seed,-3,1]) (mse) or labels randint([seed,-3,1], 0, K) (xent).
+    Generated on the device; bit-identical to the reference's values."""
+    shape = (n, net.in_channels, w_i, w_i, w_i)
+    numel = shape[0] * shape[1] * shape[2] * shape[3] * shape[4]
+    x = prng.uniform_device([seed, -3, 0], numel, -1.0, 1.0).reshape(shape)
+    if net.loss == "mse":
+        y = prng.uniform_device([seed, -3, 1], n * net.out_dim, -1.0, 1.0).reshape(n, net.out_dim)
+    else:
+        y = randint_device([seed, -3, 1], n * w_i ** 3, 0, net.out_dim).reshape(n, w_i, w_i, w_i)
+    return x, y, tuple(range(n))
+
+
+def randint_device(key, n, lo, hi):
+    """prng.randint (modulo-mapped u64) on the host stream; labels are small."""
+    import numpy as np
+
+    from .prng import resolve, GOLDEN, MASK
+
+    k = np.uint64(resolve(key))
+    ctr = np.arange(n, dtype=np.uint64)
+    z = k + (ctr + np.uint64(1)) * np.uint64(GOLDEN)
+    z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+    z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    z = z ^ (z >> np.uint64(31))
+    vals = (z % np.uint64(hi - lo)).astype(np.int64) + lo
+    return torch.from_numpy(vals).cuda()
+
+
+def scatter_batch(plan: Plan, x, y, sample_ids, rank: int, epoch: int = 0, iteration: int = 0) -> Batch:
+    """This rank's Batch from a global NCDHW batch (device or host tensors).
+    Group g owns rows [g*n_local, (g+1)*n_local) (reference engine.py:482-513)."""
+    n_local = plan.n_global // plan.grid.groups
+    g = plan.grid.coords(rank)[0]
+    rows = slice(g * n_local, (g + 1) * n_local)
+    ids = tuple(int(s) for s in sample_ids)[rows]
+    b = Batch(sample_ids=ids, epoch=epoch, iteration=iteration)
+    gin = _grid_rank(plan.input_meta, rank)
+    if gin is not None:
+        meta = plan.input_meta
+        reg = meta.region(gin)
+        lo, hi = meta.sample_range(meta.group_of(gin))
+        sl = (slice(lo, hi), slice(None)) + reg.slices()
+        b.x_block = DistTensor(meta, gin, torch.as_tensor(x)[sl])
+    if plan.net.loss == "mse":
+        b.target = torch.as_tensor(y)[rows].to("cuda", torch.float32)
+    else:
+        gl = _grid_rank(plan.label_meta, rank)
+        if gl is not None:
+            reg = plan.label_meta.region(gl)
+            lo, hi = plan.label_meta.sample_range(plan.label_meta.group_of(gl))
+            b.y_block = torch.as_tensor(y)[(slice(lo, hi),) + reg.slices()].to("cuda", torch.int64).contiguous()
+    return b

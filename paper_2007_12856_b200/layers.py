@@ -1,0 +1,372 @@
+"""Distributed layer ops on device-resident DistTensors.
+
+Same operator names, argument order and semantics as the reference's
+distributed layer library (reference pkg/src/voxpar/layers/distributed.py):
+every op is collective over the ranks in its tensor's rank map, and gathering
+the outputs reproduces the serial oracle.  Arithmetic runs in libvpx.so
+(sm_100a); communication goes through comm.RankCtx (NCCL).  Outputs are
+allocated with the halo margins their *consumer* needs (out_radii), so a
+producer writes directly into the next conv's frame.
+
+Weights are CUDA fp32 tensors in the reference layouts (conv OIDHW, deconv
+(Cin,Cout,2,2,2)); parameter gradients are written into caller-provided
+buffers (views of the flat gradient-allreduce bucket) when `out` is given.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _lib
+from .comm import RankCtx, halo_exchange, reverse_halo_exchange, copy_box
+from .errors import NonDivisible, ShapeMismatch
+from .frames import DistTensor, frame_desc, stream_ptr
+from .geometry import DistTensorMeta, Shape5D, make_partition
+
+NO_HALO = (0, 0, 0)
+
+
+class Workspace:
+    """Grow-only device scratch (packed weights, reduction partials)."""
+
+    def __init__(self):
+        self._t = None
+
+    def get(self, nbytes: int) -> torch.Tensor:
+        nbytes = max(int(nbytes), 256)
+        if self._t is None or self._t.numel() * 4 < nbytes:
+            self._t = torch.empty((nbytes + 3) // 4 + 1024, dtype=torch.float32, device="cuda")
+        return self._t
+
+
+WS = Workspace()
+
+
+def _group(meta: DistTensorMeta):
+    return sorted(set(meta.rank_map))
+
+
+def _out(meta: DistTensorMeta, shape: Shape5D, radii, grid_rank, zero=None) -> DistTensor:
+    return DistTensor(make_partition(shape, meta.grid, radii, meta.rank_map), grid_rank, zero=zero)
+
+
+def _like(t: DistTensor, radii=NO_HALO, channels=None) -> DistTensor:
+    gs = t.meta.global_shape
+    shape = gs if channels is None else Shape5D(gs.n, channels, gs.d, gs.h, gs.w)
+    return _out(t.meta, shape, radii, t.grid_rank)
+
+
+def _cubic(t):
+    if len(set(t)) != 1:
+        raise ShapeMismatch(f"only cubic kernels/strides are implemented, got {t}")
+    return t[0]
+
+
+# -------------------------------------------------------------- convolution
+
+def dist_conv3d(ctx: RankCtx, x: DistTensor, w: torch.Tensor, params, out_radii=NO_HALO) -> DistTensor:
+    """Halo exchange, then the local tcgen05 implicit-GEMM conv on the frame
+    (reference layers/distributed.py:42-69)."""
+    meta = x.meta
+    if tuple(meta.radii) != params.radii:
+        raise ShapeMismatch(f"input partitioned with radii {meta.radii}, conv needs {params.radii}")
+    if x.c != params.cin:
+        raise ShapeMismatch(f"conv input channels {x.c} != {params.cin}")
+    for name, e, p, s in zip("dhw", x.spatial, meta.grid.spatial_parts, params.stride):
+        if p > 1 and e % s:
+            raise NonDivisible(f"local extent {name}={e} not divisible by stride {s}")
+    halo_exchange(ctx, x)
+    k, s = _cubic(params.kernel), _cubic(params.stride)
+    gs = meta.global_shape
+    y = _out(meta, Shape5D(gs.n, params.cout, *(-(-e // s) for e in gs.spatial)), out_radii, x.grid_rank)
+    nb = _lib.load().vpx_conv3d_workspace_bytes(params.cin, params.cout, k, y.desc)
+    ws = WS.get(nb)
+    _lib.call("vpx_conv3d_fwd", x.ptr, x.desc, w.data_ptr(), k, s, y.ptr, y.desc, ws.data_ptr(),
+              ws.numel() * 4, stream_ptr())
+    return y
+
+
+def dist_conv3d_bwd_data(ctx: RankCtx, u: DistTensor, w: torch.Tensor, params,
+                         in_meta: DistTensorMeta) -> DistTensor:
+    """Input gradient over the halo-wide frame, then the adjoint exchange folds
+    margin gradients into their owners (reference layers/distributed.py:72-82).
+    The returned tensor keeps the frame; only its interior is meaningful."""
+    k, s = _cubic(params.kernel), _cubic(params.stride)
+    g = DistTensor(in_meta, u.grid_rank, zero=False)
+    nb = _lib.load().vpx_conv3d_workspace_bytes(params.cin, params.cout, k, u.desc)
+    ws = WS.get(nb)
+    _lib.call("vpx_conv3d_bwd_data", u.ptr, u.desc, w.data_ptr(), k, s, g.ptr, g.desc, ws.data_ptr(),
+              ws.numel() * 4, stream_ptr())
+    reverse_halo_exchange(ctx, in_meta, u.grid_rank, g)
+    return g
+
+
+def dist_conv3d_bwd_filter(ctx: RankCtx, x: DistTensor, u: DistTensor, params, reduce: bool = True,
+                           out: torch.Tensor = None) -> torch.Tensor:
+    """Filter-gradient partial from the exchanged input frame; allreduced over
+    the tensor's group when reduce=True (reference layers/distributed.py:85-98)."""
+    k, s = _cubic(params.kernel), _cubic(params.stride)
+    if out is None:
+        out = torch.empty((params.cout, params.cin, k, k, k), dtype=torch.float32, device="cuda")
+    nb = _lib.load().vpx_conv3d_workspace_bytes(params.cin, params.cout, k, u.desc)
+    ws = WS.get(nb)
+    _lib.call("vpx_conv3d_bwd_filter", x.ptr, x.desc, u.ptr, u.desc, k, s, out.data_ptr(), 0,
+              ws.data_ptr(), ws.numel() * 4, stream_ptr())
+    if reduce:
+        ctx.allreduce_sum_(out.view(-1), _group(x.meta))
+    return out
+
+
+# ------------------------------------------------------------------- deconv
+
+def dist_deconv3d(ctx: RankCtx, x: DistTensor, w: torch.Tensor, out_radii=NO_HALO) -> DistTensor:
+    """k2s2 transposed conv: purely local (reference layers/distributed.py:103-112)."""
+    if tuple(x.meta.radii) != NO_HALO:
+        raise ShapeMismatch("deconv input must carry no halos")
+    gs = x.meta.global_shape
+    y = _out(x.meta, Shape5D(gs.n, w.shape[1], 2 * gs.d, 2 * gs.h, 2 * gs.w), out_radii, x.grid_rank)
+    _lib.call("vpx_deconv_fwd", x.ptr, x.desc, w.data_ptr(), y.ptr, y.desc, stream_ptr())
+    return y
+
+
+def dist_deconv3d_bwd_data(ctx: RankCtx, u: DistTensor, w: torch.Tensor, in_meta) -> DistTensor:
+    g = DistTensor(in_meta, u.grid_rank, zero=False)
+    _lib.call("vpx_deconv_bwd_data", u.ptr, u.desc, w.data_ptr(), g.ptr, g.desc, stream_ptr())
+    return g
+
+
+def dist_deconv3d_bwd_filter(ctx: RankCtx, x: DistTensor, u: DistTensor, reduce: bool = True,
+                             out: torch.Tensor = None) -> torch.Tensor:
+    if out is None:
+        out = torch.empty((x.c, u.c, 2, 2, 2), dtype=torch.float32, device="cuda")
+    ws = WS.get(_lib.load().vpx_deconv_workspace_bytes(x.c, u.c))
+    _lib.call("vpx_deconv_bwd_filter", x.ptr, x.desc, u.ptr, u.desc, out.data_ptr(), 0, ws.data_ptr(),
+              stream_ptr())
+    if reduce:
+        ctx.allreduce_sum_(out.view(-1), _group(x.meta))
+    return out
+
+
+# ------------------------------------------------------------------ pooling
+
+def dist_pool3d(ctx: RankCtx, x: DistTensor, kind: str = "average", out_radii=NO_HALO) -> DistTensor:
+    """2^3 stride-2 pooling; windows never straddle blocks (reference
+    layers/distributed.py:132-140)."""
+    if tuple(x.meta.radii) != NO_HALO:
+        raise ShapeMismatch("pool input must carry no halos")
+    if kind not in ("average", "max"):
+        raise ShapeMismatch(f"unknown pool kind {kind!r}")
+    gs = x.meta.global_shape
+    y = _out(x.meta, Shape5D(gs.n, gs.c, gs.d // 2, gs.h // 2, gs.w // 2), out_radii, x.grid_rank)
+    _lib.call("vpx_pool_fwd", x.ptr, x.desc, y.ptr, y.desc, int(kind == "max"), stream_ptr())
+    return y
+
+
+def dist_pool3d_bwd(ctx: RankCtx, x: DistTensor, u: DistTensor, kind: str, in_meta) -> DistTensor:
+    g = DistTensor(in_meta, u.grid_rank, zero=False)
+    _lib.call("vpx_pool_bwd", x.ptr, x.desc, u.ptr, u.desc, g.ptr, g.desc, int(kind == "max"), stream_ptr())
+    return g
+
+
+# ---------------------------------------------------------------- batchnorm
+
+class BNState:
+    """Per-channel batch-norm state (reference layers/reference.py:39-57);
+    gamma/beta alias the optimizer's parameter storage."""
+
+    def __init__(self, gamma, beta, running_mean=None, running_var=None, eps=1e-5, momentum=0.9):
+        c = gamma.numel()
+        self.gamma, self.beta = gamma, beta
+        self.running_mean = running_mean if running_mean is not None else torch.zeros(c, device="cuda")
+        self.running_var = running_var if running_var is not None else torch.ones(c, device="cuda")
+        self.eps, self.momentum = eps, momentum
+
+
+def _bn_sums(x, u, mean, inv, mode):
+    c = x.c
+    out = torch.empty(2 * c, dtype=torch.float32, device="cuda")
+    ws = WS.get(_lib.load().vpx_bn_workspace_bytes(c))
+    _lib.call("vpx_bn_sums", x.ptr, x.desc, u.ptr if u is not None else 0, u.desc if u is not None else 0,
+              mean.data_ptr() if mean is not None else 0, inv.data_ptr() if inv is not None else 0, mode,
+              out.data_ptr(), ws.data_ptr(), stream_ptr())
+    return out
+
+
+def dist_batchnorm(ctx: RankCtx, x: DistTensor, state: BNState, mode: str = "train",
+                   out_radii=NO_HALO):
+    """Local (sum x, sum x^2) -> allreduce(2C) over the tensor's whole rank
+    group -> normalise (reference layers/distributed.py:152-180).  Returns
+    (y, cache); the cache keeps x and the batch statistics (xhat is recomputed)."""
+    gs = x.meta.global_shape
+    c = gs.c
+    mean = torch.empty(c, dtype=torch.float32, device="cuda")
+    inv = torch.empty(c, dtype=torch.float32, device="cuda")
+    if mode == "train":
+        count = gs.n * gs.d * gs.h * gs.w
+        sums = _bn_sums(x, None, None, None, 0)
+        ctx.allreduce_sum_(sums, _group(x.meta))
+        _lib.call("vpx_bn_stats", sums.data_ptr(), c, float(count), float(state.eps), float(state.momentum),
+                  mean.data_ptr(), inv.data_ptr(), state.running_mean.data_ptr(),
+                  state.running_var.data_ptr(), stream_ptr())
+    elif mode == "eval":
+        count = 0
+        mean.copy_(state.running_mean)
+        inv.copy_(torch.rsqrt(state.running_var + state.eps))
+    else:
+        raise ShapeMismatch(f"unknown bn mode {mode!r}")
+    y = _out(x.meta, gs, out_radii, x.grid_rank)
+    _lib.call("vpx_bn_apply", x.ptr, x.desc, mean.data_ptr(), inv.data_ptr(), state.gamma.data_ptr(),
+              state.beta.data_ptr(), y.ptr, y.desc, stream_ptr())
+    return y, (x, mean, inv, count)
+
+
+def dist_batchnorm_bwd(ctx: RankCtx, u: DistTensor, state: BNState, cache, in_meta,
+                       dgamma: torch.Tensor = None, dbeta: torch.Tensor = None):
+    """(dx, dgamma partial, dbeta partial); the two reduction terms are
+    allreduced for dx, the parameter gradients stay rank-local partials
+    (reference layers/distributed.py:183-201)."""
+    x, mean, inv, count = cache
+    c = x.c
+    local = _bn_sums(x, u, mean, inv, 1)  # [sum u, sum u*xhat]
+    if dgamma is None:
+        dgamma = torch.empty(c, dtype=torch.float32, device="cuda")
+    if dbeta is None:
+        dbeta = torch.empty(c, dtype=torch.float32, device="cuda")
+    dbeta.copy_(local[:c])
+    dgamma.copy_(local[c:])
+    ctx.allreduce_sum_(local, _group(u.meta))
+    g = DistTensor(in_meta, u.grid_rank, zero=False)
+    _lib.call("vpx_bn_bwd_apply", x.ptr, x.desc, u.ptr, u.desc, mean.data_ptr(), inv.data_ptr(),
+              state.gamma.data_ptr(), local.data_ptr(), float(count), g.ptr, g.desc, stream_ptr())
+    return g, dgamma, dbeta
+
+
+# ---------------------------------------------------------------- pointwise
+
+def dist_leaky_relu(x: DistTensor, slope: float, out_radii=NO_HALO) -> DistTensor:
+    y = _out(x.meta, x.meta.global_shape, out_radii, x.grid_rank)
+    _lib.call("vpx_leaky_fwd", x.ptr, x.desc, y.ptr, y.desc, float(slope), stream_ptr())
+    return y
+
+
+def dist_leaky_relu_bwd(x: DistTensor, u: DistTensor, slope: float, in_meta) -> DistTensor:
+    g = DistTensor(in_meta, u.grid_rank, zero=False)
+    _lib.call("vpx_leaky_bwd", x.ptr, x.desc, u.ptr, u.desc, g.ptr, g.desc, float(slope), stream_ptr())
+    return g
+
+
+def dist_concat_channels(a: DistTensor, b: DistTensor, out_radii=NO_HALO) -> DistTensor:
+    if a.meta.grid != b.meta.grid or a.meta.rank_map != b.meta.rank_map:
+        raise ShapeMismatch("concat operands must share a partition layout")
+    ga, gb = a.meta.global_shape, b.meta.global_shape
+    if (ga.n, ga.d, ga.h, ga.w) != (gb.n, gb.d, gb.h, gb.w):
+        raise ShapeMismatch(f"concat shapes {ga} vs {gb}")
+    y = _out(a.meta, Shape5D(ga.n, ga.c + gb.c, ga.d, ga.h, ga.w), out_radii, a.grid_rank)
+    _lib.call("vpx_concat", a.ptr, a.desc, b.ptr, b.desc, y.ptr, y.desc, stream_ptr())
+    return y
+
+
+def dist_concat_bwd(u: DistTensor, c_main: int, main_meta, skip_meta, skip_grad: DistTensor = None):
+    """Split a concat's gradient into (main part, skip part); the skip part is
+    accumulated into skip_grad when given (reference engine.py:432-438)."""
+    ga = DistTensor(main_meta, u.grid_rank, zero=False)
+    acc = skip_grad is not None
+    gb = skip_grad if acc else DistTensor(skip_meta, u.grid_rank, zero=False)
+    _lib.call("vpx_split", u.ptr, u.desc, ga.ptr, ga.desc, gb.ptr, gb.desc, int(acc), stream_ptr())
+    return ga, gb
+
+
+def add_into(dst: DistTensor, src: DistTensor) -> DistTensor:
+    _lib.call("vpx_add", src.ptr, src.desc, dst.ptr, dst.desc, stream_ptr())
+    return dst
+
+
+# ------------------------------------------------------------------- losses
+
+def dist_mse(ctx: RankCtx, pred, target, global_size: int, group=None):
+    """MSE over rank-local rows (pred None -> contributes 0); loss identical on
+    every rank (reference layers/distributed.py:257-270).  Device tensors."""
+    if pred is None:
+        local = torch.zeros(1, dtype=torch.float64, device="cuda")
+        diff = None
+    else:
+        if pred.shape != target.shape:
+            raise ShapeMismatch(f"mse shapes {tuple(pred.shape)} vs {tuple(target.shape)}")
+        diff = pred - target
+        local = (diff.double() * diff.double()).sum().reshape(1)
+    ctx.allreduce_sum_(local, group)
+    return local / global_size, (None if diff is None else diff * (2.0 / global_size))
+
+
+def dist_cross_entropy(ctx: RankCtx, pred: DistTensor, labels: torch.Tensor, count: int, group=None,
+                       nparts: int = 512):
+    """Per-voxel softmax cross entropy over a spatially partitioned prediction;
+    only the scalar is allreduced (reference layers/distributed.py:273-293).
+    labels: int64 CUDA tensor (n_local, d, h, w) of this rank's block."""
+    g = DistTensor(make_partition(pred.meta.global_shape, pred.meta.grid, NO_HALO, pred.meta.rank_map),
+                   pred.grid_rank, zero=False)
+    part = torch.empty(nparts, dtype=torch.float64, device="cuda")
+    _lib.call("vpx_xent", pred.ptr, pred.desc, labels.data_ptr(), float(count), g.ptr, g.desc,
+              part.data_ptr(), nparts, stream_ptr())
+    local = part.sum().reshape(1)
+    ctx.allreduce_sum_(local, group)
+    return local / count, g
+
+
+# ------------------------------------------------------------ redistribution
+
+def redistribute(ctx: RankCtx, x, src_meta: DistTensorMeta, dst_meta: DistTensorMeta, zero=None):
+    """Move a tensor between partition layouts, values preserved exactly
+    (reference layers/distributed.py:298-368).  Collective over the union of
+    both rank maps; x is this rank's source DistTensor (None if it holds no
+    source part).  Returns the destination DistTensor or None."""
+    if src_meta.global_shape != dst_meta.global_shape:
+        raise ShapeMismatch(f"redistribute shapes differ: {src_meta.global_shape} vs {dst_meta.global_shape}")
+    me = ctx.rank
+    src_gr = src_meta.rank_map.index(me) if me in src_meta.rank_map else None
+    dst_gr = dst_meta.rank_map.index(me) if me in dst_meta.rank_map else None
+    if src_gr is not None and x is None:
+        raise ShapeMismatch(f"rank {me} holds a source block but passed none")
+    out = DistTensor(dst_meta, dst_gr, zero=zero) if dst_gr is not None else None
+    ops, unpacks, locals_ = [], [], []
+    for a in range(src_meta.grid.size):
+        a_lo, a_hi = src_meta.sample_range(src_meta.group_of(a))
+        ra = src_meta.region(a)
+        for b in range(dst_meta.grid.size):
+            b_lo, b_hi = dst_meta.sample_range(dst_meta.group_of(b))
+            lo, hi = max(a_lo, b_lo), min(a_hi, b_hi)
+            if hi <= lo:
+                continue
+            rb = dst_meta.region(b)
+            ov = ra.intersect(rb)
+            if ov is None:
+                continue
+            src_rank, dst_rank = src_meta.fabric_rank(a), dst_meta.fabric_rank(b)
+            if me not in (src_rank, dst_rank):
+                continue
+            ext = ov.extent
+            if a == src_gr:
+                m = x.m
+                sbox = (lo - a_lo,) + tuple(o - r + mm for o, r, mm in zip(ov.offset, ra.offset, m)) + (hi - lo,) + ext
+            if b == dst_gr:
+                m = out.m
+                dbox = (lo - b_lo,) + tuple(o - r + mm for o, r, mm in zip(ov.offset, rb.offset, m)) + (hi - lo,) + ext
+            numel = (hi - lo) * ext[0] * ext[1] * ext[2] * src_meta.global_shape.c
+            if src_rank == dst_rank == me:
+                buf = torch.empty(numel, dtype=torch.float32, device="cuda")
+                copy_box(x, sbox, buf, 0)
+                copy_box(out, dbox, buf, 1)
+            elif src_rank == me:
+                buf = torch.empty(numel, dtype=torch.float32, device="cuda")
+                copy_box(x, sbox, buf, 0)
+                ops.append(("send", dst_rank, buf))
+            else:
+                buf = torch.empty(numel, dtype=torch.float32, device="cuda")
+                ops.append(("recv", src_rank, buf))
+                unpacks.append((dbox, buf))
+    ctx.exchange(ops)
+    for dbox, buf in unpacks:
+        copy_box(out, dbox, buf, 1)
+    return out

@@ -1,0 +1,175 @@
+"""Device kernels vs the CPU oracle (GPU).  Conv runs on tcgen05 in TF32:
+tolerance rtol 1e-3 in the reference's metric max|got-ref| / max|ref|
+(reference cli.py:199-202); pointwise/pool/layout/prng/halo are exact."""
+
+import ctypes
+import json
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import serial as O
+from paper_2007_12856_b200 import _lib, prng
+from paper_2007_12856_b200.frames import Frame, stream_ptr
+
+pytestmark = pytest.mark.gpu
+
+TF32_RTOL = 1e-3
+
+
+def rel(got, ref):
+    ref = np.asarray(ref, dtype=np.float64)
+    return float(np.max(np.abs(np.asarray(got, np.float64) - ref)) / max(np.max(np.abs(ref)), 1e-30))
+
+
+def ws(cin, cout, k, fr):
+    nb = _lib.load().vpx_conv3d_workspace_bytes(cin, cout, k, fr.desc)
+    return torch.empty(nb // 4 + 64, device="cuda")
+
+
+def run_conv(x, w, k, s, margins=(0, 0, 0), grad_margins=(0, 0, 0)):
+    n, cin, d, h, wd = x.shape
+    cout = w.shape[0]
+    xf = Frame(n, cin, d, h, wd, margins, zero=True).load_ncdhw(x)
+    od, oh, ow = (-(-e // s) for e in (d, h, wd))
+    yf = Frame(n, cout, od, oh, ow)
+    wt = torch.from_numpy(np.ascontiguousarray(w)).float().cuda()
+    W = ws(cin, cout, k, yf)
+    _lib.call("vpx_conv3d_fwd", xf.ptr, xf.desc, wt.data_ptr(), k, s, yf.ptr, yf.desc, W.data_ptr(),
+              W.numel() * 4, stream_ptr())
+    return xf, yf, wt, W
+
+
+CASES = [
+    # n, cin, cout, d, h, w, k, s   (tcgen05 row-window for W%128==0 stride 1, else CUDA-core)
+    (1, 4, 16, 4, 6, 128, 3, 1),
+    (2, 4, 16, 3, 5, 256, 3, 1),
+    (1, 16, 32, 4, 4, 128, 3, 1),
+    (1, 32, 64, 3, 3, 128, 3, 1),
+    (1, 64, 128, 8, 8, 8, 3, 2),
+    (1, 128, 256, 4, 4, 4, 3, 1),
+    (2, 8, 2, 6, 6, 6, 1, 1),
+]
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_conv_passes_vs_oracle(case):
+    n, cin, cout, d, h, w, k, s = case
+    rng = np.random.default_rng(7)
+    x = rng.uniform(-1, 1, (n, cin, d, h, w)).astype(np.float32)
+    wt = (rng.uniform(-1, 1, (cout, cin, k, k, k)) / np.sqrt(cin * k ** 3)).astype(np.float32)
+    xf, yf, wdev, W = run_conv(x, wt, k, s)
+    y_ref = O.conv3d(x, wt, (k,) * 3, (s,) * 3)
+    assert rel(yf.to_ncdhw().cpu().numpy(), y_ref) < TF32_RTOL
+    u = rng.uniform(-1, 1, y_ref.shape).astype(np.float32)
+    uf = Frame(*u.shape[:1], u.shape[1], *u.shape[2:]).load_ncdhw(u)
+    gf = Frame(n, cin, d, h, w)
+    _lib.call("vpx_conv3d_bwd_data", uf.ptr, uf.desc, wdev.data_ptr(), k, s, gf.ptr, gf.desc, W.data_ptr(),
+              W.numel() * 4, stream_ptr())
+    g_ref = O.conv3d_bwd_data(u, wt, (k,) * 3, (s,) * 3, (d, h, w))
+    assert rel(gf.to_ncdhw().cpu().numpy(), g_ref) < TF32_RTOL
+    wg = torch.zeros_like(wdev)
+    _lib.call("vpx_conv3d_bwd_filter", xf.ptr, xf.desc, uf.ptr, uf.desc, k, s, wg.data_ptr(), 0, W.data_ptr(),
+              W.numel() * 4, stream_ptr())
+    wg_ref = O.conv3d_bwd_filter(x, u, (k,) * 3, (s,) * 3)
+    assert rel(wg.cpu().numpy(), wg_ref) < TF32_RTOL
+
+
+def test_conv_fwd_frame_margins_and_dgrad_margins():
+    """D/H-partitioned frames: the kernel must read the margin rows (here
+    filled with neighbour data) and write dgrad over the margins too."""
+    rng = np.random.default_rng(3)
+    n, cin, cout, d, h, w = 1, 16, 32, 4, 4, 128
+    full = rng.uniform(-1, 1, (n, cin, d + 2, h + 2, w)).astype(np.float32)  # as if halos were received
+    wt = (rng.uniform(-1, 1, (cout, cin, 3, 3, 3)) / 20).astype(np.float32)
+    xf = Frame(n, cin, d, h, w, (1, 1, 0), zero=True)
+    xf.t.copy_(torch.from_numpy(full.transpose(0, 2, 3, 4, 1).copy()).cuda())
+    yf = Frame(n, cout, d, h, w)
+    wdev = torch.from_numpy(wt).cuda()
+    W = ws(cin, cout, 3, yf)
+    _lib.call("vpx_conv3d_fwd", xf.ptr, xf.desc, wdev.data_ptr(), 3, 1, yf.ptr, yf.desc, W.data_ptr(),
+              W.numel() * 4, stream_ptr())
+    # reference: conv over the margin-extended block, keep the interior rows
+    xpad = np.pad(full, ((0, 0), (0, 0), (0, 0), (0, 0), (1, 1)))
+    y_ref = O.k_conv3d_fwd(xpad, wt, (1, 1, 1))
+    assert rel(yf.to_ncdhw().cpu().numpy(), y_ref) < TF32_RTOL
+    u = rng.uniform(-1, 1, (n, cout, d, h, w)).astype(np.float32)
+    uf = Frame(n, cout, d, h, w).load_ncdhw(u)
+    gf = Frame(n, cin, d, h, w, (1, 1, 0), zero=False)
+    _lib.call("vpx_conv3d_bwd_data", uf.ptr, uf.desc, wdev.data_ptr(), 3, 1, gf.ptr, gf.desc, W.data_ptr(),
+              W.numel() * 4, stream_ptr())
+    g_ref = O.k_conv3d_bwd_data(u, wt, (1, 1, 1), (d + 2, h + 2, w + 2))[:, :, :, :, 1:-1]
+    got = gf.t.cpu().numpy().transpose(0, 4, 1, 2, 3)
+    assert rel(got, g_ref) < TF32_RTOL
+
+
+def test_prng_device_streams_bit_exact(golden):
+    g = json.loads((golden / "prng.json").read_text())
+    for k in g["uniform"]:
+        key = json.loads(k)
+        dev = prng.uniform_device(key, 16, -0.5, 2.0, fp64=True).cpu().numpy()
+        assert dev.tolist() == g["uniform"][k]
+    big = prng.uniform_device([0, -3, 0], 1 << 20, -1.0, 1.0).cpu().numpy()
+    import hashlib
+
+    assert hashlib.sha256(big.tobytes()).hexdigest() == g["uniform_1M_f32_bytes_sha"]
+    m = prng.keep_mask_device([0, 1, 2, 3, 4], 64, 0.8).cpu().numpy().astype(bool)
+    assert np.array_equal(m, O.dropout_mask([0, 1, 2, 3, 4], 64, 0.8))
+
+
+def _frame_of(a):
+    return Frame(a.shape[0], a.shape[1], *a.shape[2:]).load_ncdhw(a.astype(np.float32))
+
+
+def test_pool_leaky_bn_deconv_vs_oracle(golden):
+    A = np.load(golden / "layers.npz")
+    x = A["pool_x"].astype(np.float32)
+    xf = _frame_of(x)
+    for kind in ("average", "max"):
+        yf = Frame(x.shape[0], x.shape[1], x.shape[2] // 2, x.shape[3] // 2, x.shape[4] // 2)
+        _lib.call("vpx_pool_fwd", xf.ptr, xf.desc, yf.ptr, yf.desc, int(kind == "max"), stream_ptr())
+        assert rel(yf.to_ncdhw().cpu().numpy(), O.pool3d(x, kind)) < 1e-6
+        u = A[f"pool_{kind}_u"].astype(np.float32)
+        uf = _frame_of(u)
+        gf = Frame(*x.shape[:2], *x.shape[2:])
+        _lib.call("vpx_pool_bwd", xf.ptr, xf.desc, uf.ptr, uf.desc, gf.ptr, gf.desc, int(kind == "max"), stream_ptr())
+        assert np.array_equal(gf.to_ncdhw().cpu().numpy(), O.pool3d_bwd(x, u, kind))
+    # leaky is exact
+    lx = np.random.default_rng(1).standard_normal((2, 3, 4, 4, 4)).astype(np.float32)
+    lx[0, 0, 0, 0, 0] = 0.0
+    lu = np.random.default_rng(2).standard_normal(lx.shape).astype(np.float32)
+    a, b, c = _frame_of(lx), _frame_of(lu), Frame(2, 3, 4, 4, 4)
+    _lib.call("vpx_leaky_fwd", a.ptr, a.desc, c.ptr, c.desc, 0.3, stream_ptr())
+    assert np.array_equal(c.to_ncdhw().cpu().numpy(), O.leaky(lx, 0.3))
+    _lib.call("vpx_leaky_bwd", a.ptr, a.desc, b.ptr, b.desc, c.ptr, c.desc, 0.3, stream_ptr())
+    assert np.array_equal(c.to_ncdhw().cpu().numpy(), O.leaky_bwd(lx, lu, 0.3))
+    # deconv
+    dx, dw, du = A["deconv_x"].astype(np.float32), A["deconv_w"].astype(np.float32), A["deconv_u"].astype(np.float32)
+    xf, uf = _frame_of(dx), _frame_of(du)
+    yf = Frame(dx.shape[0], dw.shape[1], *(2 * e for e in dx.shape[2:]))
+    wdev = torch.from_numpy(dw).cuda()
+    _lib.call("vpx_deconv_fwd", xf.ptr, xf.desc, wdev.data_ptr(), yf.ptr, yf.desc, stream_ptr())
+    assert rel(yf.to_ncdhw().cpu().numpy(), A["deconv_y"]) < 1e-5
+    gf = Frame(*dx.shape[:2], *dx.shape[2:])
+    _lib.call("vpx_deconv_bwd_data", uf.ptr, uf.desc, wdev.data_ptr(), gf.ptr, gf.desc, stream_ptr())
+    assert rel(gf.to_ncdhw().cpu().numpy(), A["deconv_g"]) < 1e-5
+    wg = torch.zeros_like(wdev)
+    W = torch.empty(_lib.load().vpx_deconv_workspace_bytes(dx.shape[1], dw.shape[1]) // 4, device="cuda")
+    _lib.call("vpx_deconv_bwd_filter", xf.ptr, xf.desc, uf.ptr, uf.desc, wg.data_ptr(), 0, W.data_ptr(), stream_ptr())
+    assert rel(wg.cpu().numpy(), A["deconv_wg"]) < 1e-5
+
+
+def test_halo_copy_round_trip():
+    t = Frame(2, 3, 4, 5, 6, (1, 1, 1), zero=True)
+    t.t.copy_(torch.arange(t.t.numel(), dtype=torch.float32, device="cuda").view_as(t.t))
+    box = (1, 0, 1, 2, 1, 4, 3, 5)  # n0, z0, y0, x0, en, ez, ey, ex
+    buf = torch.empty(1 * 4 * 3 * 5 * 3, device="cuda")
+    from paper_2007_12856_b200.comm import copy_box
+
+    copy_box(t, box, buf, 0)
+    ref = t.t[1:2, 0:4, 1:4, 2:7, :].reshape(-1)
+    assert torch.equal(buf, ref)
+    before = t.t.clone()
+    copy_box(t, box, buf, 2)
+    assert torch.equal(t.t[1:2, 0:4, 1:4, 2:7, :], 2 * before[1:2, 0:4, 1:4, 2:7, :])
