@@ -40,6 +40,8 @@ extern "C" {
 const char* vpx_last_error(void);
 /* Library build tag (architecture, git revision). */
 const char* vpx_version(void);
+/* Total number of CUDA kernels this library has launched in this process. */
+long long vpx_launch_count(void);
 
 /* ------------------------------------------------------------ convolution --
  * Frames are described by int[8] = {n, c, d, h, w, md, mh, mw}: interior extents

@@ -4,6 +4,7 @@
 namespace vpx {
 
 static thread_local char g_err[1024] = {0};
+std::atomic<long long> g_launches{0};
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -56,3 +57,4 @@ int encode_tiled(CUtensorMap* map, CUtensorMapDataType dtype, int rank, void* ga
 
 extern "C" const char* vpx_last_error(void) { return vpx::g_err; }
 extern "C" const char* vpx_version(void) { return "libvpx sm_100a " VPX_GIT_REV; }
+extern "C" long long vpx_launch_count(void) { return vpx::g_launches.load(); }

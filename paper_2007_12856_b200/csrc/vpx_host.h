@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <atomic>
 #include <cstdarg>
 #include <cstdint>
 #include <cstdio>
@@ -15,6 +16,8 @@
 namespace vpx {
 
 void set_error(const char* fmt, ...);
+// Number of kernels this library has launched (vpx_launch_count()).
+extern std::atomic<long long> g_launches;
 
 #define VPX_FAIL(code, ...)        \
   do {                             \
@@ -30,6 +33,7 @@ void set_error(const char* fmt, ...);
 
 #define VPX_LAUNCH_CHECK()                                                           \
   do {                                                                               \
+    ::vpx::g_launches.fetch_add(1, std::memory_order_relaxed);                       \
     cudaError_t _e = cudaGetLastError();                                             \
     if (_e != cudaSuccess) VPX_FAIL(VPX_ERR_CUDA, "launch: %s", cudaGetErrorString(_e)); \
   } while (0)

@@ -354,19 +354,19 @@ def forward(ctx: RankCtx, plan: Plan, state: RankState, batch: Batch, mode: str,
         radii = plan.out_radii[i]
         if layer.kind == "conv":
             stash.append(cur)
-            cur = D.dist_conv3d(ctx, cur, P[f"{layer.name}.w"], layer.params, radii)
+            cur = D.dist_conv3d(ctx, cur, P[f"{layer.name}.w"], layer.params, radii, tag=layer.name)
         elif layer.kind == "deconv":
             stash.append(cur)
             cur = D.dist_deconv3d(ctx, cur, P[f"{layer.name}.w"], radii)
         elif layer.kind == "pool":
             stash.append(cur)
-            cur = D.dist_pool3d(ctx, cur, layer.pool_kind, radii)
+            cur = D.dist_pool3d(ctx, cur, layer.pool_kind, radii, tag=layer.name)
         elif layer.kind == "bn":
             cur, cache = D.dist_batchnorm(ctx, cur, bn[layer.name], mode, radii)
             stash.append(cache)
         elif layer.kind == "leaky":
             stash.append(cur)
-            cur = D.dist_leaky_relu(cur, layer.slope, radii)
+            cur = D.dist_leaky_relu(cur, layer.slope, radii, tag=layer.name)
         elif layer.kind == "concat":
             skip = outputs[layer.skip]
             stash.append((cur.c, skip.c))
@@ -432,7 +432,8 @@ def backward(ctx: RankCtx, plan: Plan, state: RankState, stash, dpred, trace: di
                 trace[("bwd", layer.name)] = u
             continue
         if u is not None and layer.name in extra:
-            u = D.add_into(u, extra.pop(layer.name))
+            # in place, unless a trace holds on to u
+            u = D.add_into(u.clone() if trace is not None else u, extra.pop(layer.name))
         if u is None:
             if i == plan.redist_idx:
                 u = D.redistribute(ctx, None, _meta_like(plan.in_meta[i]), plan.redist_src_meta)
@@ -441,21 +442,22 @@ def backward(ctx: RankCtx, plan: Plan, state: RankState, stash, dpred, trace: di
             continue
         in_meta = plan.in_meta[i]
         if layer.kind == "conv":
-            D.dist_conv3d_bwd_filter(ctx, kept, u, layer.params, reduce=False, out=G[f"{layer.name}.w"])
+            D.dist_conv3d_bwd_filter(ctx, kept, u, layer.params, reduce=False, out=G[f"{layer.name}.w"],
+                                     tag=layer.name)
             if i == 0 and trace is None:
                 u = None  # nothing consumes the network input's gradient
             else:
-                u = D.dist_conv3d_bwd_data(ctx, u, P[f"{layer.name}.w"], layer.params, in_meta)
+                u = D.dist_conv3d_bwd_data(ctx, u, P[f"{layer.name}.w"], layer.params, in_meta, tag=layer.name)
         elif layer.kind == "deconv":
             D.dist_deconv3d_bwd_filter(ctx, kept, u, reduce=False, out=G[f"{layer.name}.w"])
             u = D.dist_deconv3d_bwd_data(ctx, u, P[f"{layer.name}.w"], in_meta)
         elif layer.kind == "pool":
-            u = D.dist_pool3d_bwd(ctx, kept, u, layer.pool_kind, in_meta)
+            u = D.dist_pool3d_bwd(ctx, kept, u, layer.pool_kind, in_meta, tag=layer.name)
         elif layer.kind == "bn":
             u, _, _ = D.dist_batchnorm_bwd(ctx, u, bn[layer.name], kept, in_meta,
                                            dgamma=G[f"{layer.name}.gamma"], dbeta=G[f"{layer.name}.beta"])
         elif layer.kind == "leaky":
-            u = D.dist_leaky_relu_bwd(kept, u, layer.slope, in_meta)
+            u = D.dist_leaky_relu_bwd(kept, u, layer.slope, in_meta, tag=layer.name)
         elif layer.kind == "concat":
             c_main, _ = kept
             main, sk = D.dist_concat_bwd(u, c_main, _meta_like(in_meta),

@@ -103,6 +103,12 @@ class DistTensor(Frame):
         if data is not None:
             self.load_ncdhw(data)
 
+    def clone(self) -> "DistTensor":
+        out = DistTensor.__new__(DistTensor)
+        Frame.__init__(out, self.n, self.c, self.d, self.h, self.w, self.m, tensor=self.t.clone())
+        out.meta, out.grid_rank = self.meta, self.grid_rank
+        return out
+
     @property
     def region(self):
         return self.meta.region(self.grid_rank)

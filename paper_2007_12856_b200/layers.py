@@ -24,6 +24,7 @@ from .comm import RankCtx, halo_exchange, reverse_halo_exchange, copy_box
 from .errors import NonDivisible, ShapeMismatch
 from .frames import DistTensor, frame_desc, stream_ptr
 from .geometry import DistTensorMeta, Shape5D, make_partition
+from .timing import region
 
 NO_HALO = (0, 0, 0)
 
@@ -66,7 +67,13 @@ def _cubic(t):
 
 # -------------------------------------------------------------- convolution
 
-def dist_conv3d(ctx: RankCtx, x: DistTensor, w: torch.Tensor, params, out_radii=NO_HALO) -> DistTensor:
+def _conv_flops(params, out_vox):
+    k = _cubic(params.kernel)
+    return 2 * k ** 3 * params.cin * params.cout * out_vox
+
+
+def dist_conv3d(ctx: RankCtx, x: DistTensor, w: torch.Tensor, params, out_radii=NO_HALO,
+                tag: str = "conv") -> DistTensor:
     """Halo exchange, then the local tcgen05 implicit-GEMM conv on the frame
     (reference layers/distributed.py:42-69)."""
     meta = x.meta
@@ -83,13 +90,15 @@ def dist_conv3d(ctx: RankCtx, x: DistTensor, w: torch.Tensor, params, out_radii=
     y = _out(meta, Shape5D(gs.n, params.cout, *(-(-e // s) for e in gs.spatial)), out_radii, x.grid_rank)
     nb = _lib.load().vpx_conv3d_workspace_bytes(params.cin, params.cout, k, y.desc)
     ws = WS.get(nb)
-    _lib.call("vpx_conv3d_fwd", x.ptr, x.desc, w.data_ptr(), k, s, y.ptr, y.desc, ws.data_ptr(),
-              ws.numel() * 4, stream_ptr())
+    with region(f"{tag}.fwd", _conv_flops(params, y.voxels()),
+                4 * (x.voxels() * x.c + y.voxels() * y.c + w.numel())):
+        _lib.call("vpx_conv3d_fwd", x.ptr, x.desc, w.data_ptr(), k, s, y.ptr, y.desc, ws.data_ptr(),
+                  ws.numel() * 4, stream_ptr())
     return y
 
 
 def dist_conv3d_bwd_data(ctx: RankCtx, u: DistTensor, w: torch.Tensor, params,
-                         in_meta: DistTensorMeta) -> DistTensor:
+                         in_meta: DistTensorMeta, tag: str = "conv") -> DistTensor:
     """Input gradient over the halo-wide frame, then the adjoint exchange folds
     margin gradients into their owners (reference layers/distributed.py:72-82).
     The returned tensor keeps the frame; only its interior is meaningful."""
@@ -97,14 +106,16 @@ def dist_conv3d_bwd_data(ctx: RankCtx, u: DistTensor, w: torch.Tensor, params,
     g = DistTensor(in_meta, u.grid_rank, zero=False)
     nb = _lib.load().vpx_conv3d_workspace_bytes(params.cin, params.cout, k, u.desc)
     ws = WS.get(nb)
-    _lib.call("vpx_conv3d_bwd_data", u.ptr, u.desc, w.data_ptr(), k, s, g.ptr, g.desc, ws.data_ptr(),
-              ws.numel() * 4, stream_ptr())
+    with region(f"{tag}.dgrad", _conv_flops(params, u.voxels()),
+                4 * (u.voxels() * u.c + g.t.numel() + w.numel())):
+        _lib.call("vpx_conv3d_bwd_data", u.ptr, u.desc, w.data_ptr(), k, s, g.ptr, g.desc, ws.data_ptr(),
+                  ws.numel() * 4, stream_ptr())
     reverse_halo_exchange(ctx, in_meta, u.grid_rank, g)
     return g
 
 
 def dist_conv3d_bwd_filter(ctx: RankCtx, x: DistTensor, u: DistTensor, params, reduce: bool = True,
-                           out: torch.Tensor = None) -> torch.Tensor:
+                           out: torch.Tensor = None, tag: str = "conv") -> torch.Tensor:
     """Filter-gradient partial from the exchanged input frame; allreduced over
     the tensor's group when reduce=True (reference layers/distributed.py:85-98)."""
     k, s = _cubic(params.kernel), _cubic(params.stride)
@@ -112,8 +123,10 @@ def dist_conv3d_bwd_filter(ctx: RankCtx, x: DistTensor, u: DistTensor, params, r
         out = torch.empty((params.cout, params.cin, k, k, k), dtype=torch.float32, device="cuda")
     nb = _lib.load().vpx_conv3d_workspace_bytes(params.cin, params.cout, k, u.desc)
     ws = WS.get(nb)
-    _lib.call("vpx_conv3d_bwd_filter", x.ptr, x.desc, u.ptr, u.desc, k, s, out.data_ptr(), 0,
-              ws.data_ptr(), ws.numel() * 4, stream_ptr())
+    with region(f"{tag}.wgrad", _conv_flops(params, u.voxels()),
+                4 * (x.t.numel() + u.voxels() * u.c + out.numel())):
+        _lib.call("vpx_conv3d_bwd_filter", x.ptr, x.desc, u.ptr, u.desc, k, s, out.data_ptr(), 0,
+                  ws.data_ptr(), ws.numel() * 4, stream_ptr())
     if reduce:
         ctx.allreduce_sum_(out.view(-1), _group(x.meta))
     return out
@@ -151,7 +164,8 @@ def dist_deconv3d_bwd_filter(ctx: RankCtx, x: DistTensor, u: DistTensor, reduce:
 
 # ------------------------------------------------------------------ pooling
 
-def dist_pool3d(ctx: RankCtx, x: DistTensor, kind: str = "average", out_radii=NO_HALO) -> DistTensor:
+def dist_pool3d(ctx: RankCtx, x: DistTensor, kind: str = "average", out_radii=NO_HALO,
+                tag: str = "pool") -> DistTensor:
     """2^3 stride-2 pooling; windows never straddle blocks (reference
     layers/distributed.py:132-140)."""
     if tuple(x.meta.radii) != NO_HALO:
@@ -160,13 +174,17 @@ def dist_pool3d(ctx: RankCtx, x: DistTensor, kind: str = "average", out_radii=NO
         raise ShapeMismatch(f"unknown pool kind {kind!r}")
     gs = x.meta.global_shape
     y = _out(x.meta, Shape5D(gs.n, gs.c, gs.d // 2, gs.h // 2, gs.w // 2), out_radii, x.grid_rank)
-    _lib.call("vpx_pool_fwd", x.ptr, x.desc, y.ptr, y.desc, int(kind == "max"), stream_ptr())
+    with region(f"{tag}.fwd", 0, 4 * (x.voxels() * x.c + y.voxels() * y.c)):
+        _lib.call("vpx_pool_fwd", x.ptr, x.desc, y.ptr, y.desc, int(kind == "max"), stream_ptr())
     return y
 
 
-def dist_pool3d_bwd(ctx: RankCtx, x: DistTensor, u: DistTensor, kind: str, in_meta) -> DistTensor:
+def dist_pool3d_bwd(ctx: RankCtx, x: DistTensor, u: DistTensor, kind: str, in_meta,
+                    tag: str = "pool") -> DistTensor:
     g = DistTensor(in_meta, u.grid_rank, zero=False)
-    _lib.call("vpx_pool_bwd", x.ptr, x.desc, u.ptr, u.desc, g.ptr, g.desc, int(kind == "max"), stream_ptr())
+    nb = 4 * (u.voxels() * u.c + g.voxels() * g.c + (x.voxels() * x.c if kind == "max" else 0))
+    with region(f"{tag}.bwd", 0, nb):
+        _lib.call("vpx_pool_bwd", x.ptr, x.desc, u.ptr, u.desc, g.ptr, g.desc, int(kind == "max"), stream_ptr())
     return g
 
 
@@ -245,15 +263,17 @@ def dist_batchnorm_bwd(ctx: RankCtx, u: DistTensor, state: BNState, cache, in_me
 
 # ---------------------------------------------------------------- pointwise
 
-def dist_leaky_relu(x: DistTensor, slope: float, out_radii=NO_HALO) -> DistTensor:
+def dist_leaky_relu(x: DistTensor, slope: float, out_radii=NO_HALO, tag: str = "leaky") -> DistTensor:
     y = _out(x.meta, x.meta.global_shape, out_radii, x.grid_rank)
-    _lib.call("vpx_leaky_fwd", x.ptr, x.desc, y.ptr, y.desc, float(slope), stream_ptr())
+    with region(f"{tag}.fwd", 0, 8 * x.voxels() * x.c):
+        _lib.call("vpx_leaky_fwd", x.ptr, x.desc, y.ptr, y.desc, float(slope), stream_ptr())
     return y
 
 
-def dist_leaky_relu_bwd(x: DistTensor, u: DistTensor, slope: float, in_meta) -> DistTensor:
+def dist_leaky_relu_bwd(x: DistTensor, u: DistTensor, slope: float, in_meta, tag: str = "leaky") -> DistTensor:
     g = DistTensor(in_meta, u.grid_rank, zero=False)
-    _lib.call("vpx_leaky_bwd", x.ptr, x.desc, u.ptr, u.desc, g.ptr, g.desc, float(slope), stream_ptr())
+    with region(f"{tag}.bwd", 0, 12 * x.voxels() * x.c):
+        _lib.call("vpx_leaky_bwd", x.ptr, x.desc, u.ptr, u.desc, g.ptr, g.desc, float(slope), stream_ptr())
     return g
 
 

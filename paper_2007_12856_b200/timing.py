@@ -1,0 +1,55 @@
+"""Per-kernel device timing for the roofline report (bench.py).
+
+When a Recorder is active, the layer ops bracket their libvpx launches with
+CUDA events on the launching (current) stream and tag them with the layer
+name, pass and the algorithmic flops / bytes of that launch.  Inactive
+(the default), `region` is a no-op context manager.
+"""
+
+from __future__ import annotations
+
+import contextlib
+from collections import defaultdict
+
+import torch
+
+_ACTIVE = None
+
+
+class Recorder:
+    def __init__(self):
+        self.events = []  # (tag, flops, bytes, start, end)
+
+    def __enter__(self):
+        global _ACTIVE
+        _ACTIVE = self
+        return self
+
+    def __exit__(self, *exc):
+        global _ACTIVE
+        _ACTIVE = None
+
+    def summary(self):
+        """{tag: {"ms": total, "launches": k, "flops": per launch, "bytes": per launch}}"""
+        torch.cuda.synchronize()
+        out = defaultdict(lambda: {"ms": 0.0, "launches": 0, "flops": 0, "bytes": 0})
+        for tag, fl, by, s, e in self.events:
+            d = out[tag]
+            d["ms"] += s.elapsed_time(e)
+            d["launches"] += 1
+            d["flops"], d["bytes"] = fl, by
+        return dict(out)
+
+
+@contextlib.contextmanager
+def region(tag: str, flops: int = 0, nbytes: int = 0):
+    rec = _ACTIVE
+    if rec is None:
+        yield
+        return
+    s = torch.cuda.Event(enable_timing=True)
+    e = torch.cuda.Event(enable_timing=True)
+    s.record()
+    yield
+    e.record()
+    rec.events.append((tag, flops, nbytes, s, e))
