@@ -58,6 +58,12 @@ long long vpx_conv3d_workspace_bytes(int cin, int cout, int k, const int* ufr);
  * the y frame; margins of y are left untouched. */
 int vpx_conv3d_fwd(const float* x, const int* xfr, const float* w, int k, int stride, float* y,
                    const int* yfr, void* ws, long long ws_bytes, void* stream);
+/* Same, with the layer's LeakyReLU fused into the epilogue when act == 1:
+ * y = leaky(conv(x, w), slope).  Because slope > 0, leaky(y) keeps the sign
+ * of its input, so the backward pass needs only y (vpx_leaky_bwd(y, ...)). */
+int vpx_conv3d_fwd_act(const float* x, const int* xfr, const float* w, int k, int stride, float* y,
+                       const int* yfr, int act, float slope, void* ws, long long ws_bytes,
+                       void* stream);
 
 /* xg = adjoint scatter of u through w, over EVERY position of the xg frame
  * (interior and margins): replaces voxpar.kernels.conv3d_bwd_data(u, w,
@@ -155,8 +161,8 @@ int vpx_layout_frame_to_ncdhw(const float* frame, const int* ff, float* dst, voi
 int vpx_probe_umma(const void* img, int img_bytes, const uint64_t* ops, int n_ops, float* out,
                    int ncols, void* stream);
 int vpx_probe_tma(const void* gsrc, const uint64_t* dims5, const uint64_t* strides4,
-                  const uint32_t* box5, int swizzle, const int32_t* coords5, void* out,
-                  int out_bytes, void* stream);
+                  const uint32_t* box5, const uint32_t* estr5, int swizzle, const int32_t* coords5,
+                  void* out, int out_bytes, int* ok, void* stream);
 int vpx_probe_mma_rate(int N, int n_iter, int a_layout, int n_acc, int bf16, long long* cycles,
                        void* stream);
 int vpx_probe_mma_rate2(int N, int n_acc, int bf16, int n_iter, long long* cycles, void* stream);

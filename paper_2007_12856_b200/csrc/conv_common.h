@@ -22,10 +22,17 @@ struct ConvRowParams {
   float* out;
   long long out_sn, out_sd, out_sh, out_sw;  // element strides of the output frame
   int out_off_d, out_off_h, out_off_w;       // output voxel o lands at frame index o + off
+  int act;                                   // 1: fused LeakyReLU epilogue
+  float slope;
 };
 
 int num_sms();
 int rowwin_config(int cin, int cout, int* R, int* CG);
+struct Frame;
+long long tapbox_workspace_bytes(int cin, int cout);
+int tapbox_supported(int cin, int cout, int mode);
+int conv_tapbox(int mode, const float* in, const Frame& inf, const float* w, int cin, int cout, int stride,
+                float* out, const Frame& of, int act, float slope, void* ws, cudaStream_t st);
 int launch_rowwin_any(const CUtensorMap& xmap, const ConvRowParams& p, int cin, int cout,
                       cudaStream_t st);
 

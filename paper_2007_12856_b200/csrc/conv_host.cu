@@ -88,7 +88,7 @@ static int encode_frame_map(CUtensorMap* map, const float* base, const Frame& f,
 // x in [0, wout) (wout % 128 == 0), input frame `in` (channels cin_eff).
 static int rowwin_run(const float* in, const Frame& inf, const float* wpack, int cin_eff,
                       int cout_eff, float* out, const Frame& of, int zlo, int zhi, int ylo,
-                      int yhi, int wout, cudaStream_t st) {
+                      int yhi, int wout, cudaStream_t st, int act = 0, float slope = 0.f) {
   int R, CG;
   if (!rowwin_config(cin_eff, cout_eff, &R, &CG)) VPX_FAIL(VPX_ERR_UNSUPPORTED, "rowwin config");
   CUtensorMap map;
@@ -116,6 +116,8 @@ static int rowwin_run(const float* in, const Frame& inf, const float* wpack, int
   p.out_off_d = of.md;
   p.out_off_h = of.mh;
   p.out_off_w = of.mw;
+  p.act = act;
+  p.slope = slope;
   return launch_rowwin_any(map, p, cin_eff, cout_eff, st);
 }
 
@@ -141,12 +143,16 @@ extern "C" long long vpx_conv3d_workspace_bytes(int cin, int cout, int k, const 
   const long long k3 = (long long)k * k * k;
   long long packed = vpx::packed_floats(cin, cout) * 4;
   long long parts = vpx::wgrad_simt_parts(uf) * cout * cin * k3 * 4;
+  const long long tc = (long long)vpx::num_sms() * cout * cin * 27 * 4;
+  if (tc > parts) parts = tc;
+  const long long tb = vpx::tapbox_workspace_bytes(cin, cout);
+  if (tb > packed) packed = tb;
   return ((packed + 255) / 256) * 256 + ((parts + 255) / 256) * 256;
 }
 
-extern "C" int vpx_conv3d_fwd(const float* x, const int* xfr, const float* w, int k, int stride,
-                              float* y, const int* yfr, void* ws, long long ws_bytes,
-                              void* stream) {
+extern "C" int vpx_conv3d_fwd_act(const float* x, const int* xfr, const float* w, int k, int stride,
+                                  float* y, const int* yfr, int act, float slope, void* ws,
+                                  long long ws_bytes, void* stream) {
   if (int rc = vpx::check_frame(xfr, "conv fwd input")) return rc;
   if (int rc = vpx::check_frame(yfr, "conv fwd output")) return rc;
   Frame xf = vpx::to_frame(xfr), yf = vpx::to_frame(yfr);
@@ -163,9 +169,19 @@ extern "C" int vpx_conv3d_fwd(const float* x, const int* xfr, const float* w, in
     if (ws_bytes < vpx::packed_floats(cin, cout) * 4) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "workspace too small");
     float* wpack = static_cast<float*>(ws);
     if (int rc = vpx::pack(w, cout, cin, 0, wpack, st)) return rc;
-    return vpx::rowwin_run(x, xf, wpack, cin, cout, y, yf, 0, yf.d, 0, yf.h, yf.w, st);
+    return vpx::rowwin_run(x, xf, wpack, cin, cout, y, yf, 0, yf.d, 0, yf.h, yf.w, st, act, slope);
   }
-  return vpx::conv_fwd_simt(x, xf, w, k, stride, y, yf, st);
+  if (k == 3 && cin % 4 == 0 && vpx::tapbox_supported(cin, cout, 0)) {
+    if (ws_bytes < vpx::tapbox_workspace_bytes(cin, cout)) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "workspace too small");
+    return vpx::conv_tapbox(0, x, xf, w, cin, cout, stride, y, yf, act, slope, ws, st);
+  }
+  return vpx::conv_fwd_simt(x, xf, w, k, stride, y, yf, st, act, slope);
+}
+
+extern "C" int vpx_conv3d_fwd(const float* x, const int* xfr, const float* w, int k, int stride,
+                              float* y, const int* yfr, void* ws, long long ws_bytes,
+                              void* stream) {
+  return vpx_conv3d_fwd_act(x, xfr, w, k, stride, y, yfr, 0, 0.f, ws, ws_bytes, stream);
 }
 
 extern "C" int vpx_conv3d_bwd_data(const float* u, const int* ufr, const float* w, int k,
@@ -189,6 +205,10 @@ extern "C" int vpx_conv3d_bwd_data(const float* u, const int* ufr, const float* 
     return vpx::rowwin_run(u, uf, wpack, cout, cin, xg, gf, -gf.md, gf.d + gf.md, -gf.mh,
                            gf.h + gf.mh, gf.w, st);
   }
+  if (k == 3 && cout % 4 == 0 && vpx::tapbox_supported(cin, cout, 1)) {
+    if (ws_bytes < vpx::tapbox_workspace_bytes(cin, cout)) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "workspace too small");
+    return vpx::conv_tapbox(1, u, uf, w, cin, cout, stride, xg, gf, 0, 0.f, ws, st);
+  }
   return vpx::conv_bwd_data_simt(u, uf, w, k, stride, xg, gf, st);
 }
 
@@ -207,5 +227,10 @@ extern "C" int vpx_conv3d_bwd_filter(const float* x, const int* xfr, const float
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   float* part = reinterpret_cast<float*>(static_cast<char*>(ws) +
                                          ((vpx::packed_floats(xf.c, uf.c) * 4 + 255) / 256) * 256);
+  if (k == 3 && stride == 1 && vpx::wgrad_tc_supported(xf, uf)) {
+    if (int rc = vpx::conv_wgrad_tc(x, xf, u, uf, part, st)) return rc;
+    return vpx::reduce_partials(part, vpx::wgrad_tc_parts(xf, uf), (long long)uf.c * xf.c * 27, wg,
+                                accumulate, st);
+  }
   return vpx::conv_wgrad_simt(x, xf, u, uf, k, stride, wg, accumulate, part, st);
 }

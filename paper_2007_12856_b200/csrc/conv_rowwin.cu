@@ -214,6 +214,10 @@ __global__ void __launch_bounds__(256, 1)
           float v[16];
           vpx::tmem_ld16(tbase + (static_cast<uint32_t>(q * 32) << 16) + acc * ACC + r * COUT + cb * 16, v);
           if (y < p.yhi) {
+            if (p.act) {  // fused LeakyReLU (reference layers/reference.py:231-233)
+#pragma unroll
+              for (int i = 0; i < 16; ++i) v[i] = v[i] >= 0.f ? v[i] : p.slope * v[i];
+            }
             float4* o4 = reinterpret_cast<float4*>(o + cb * 16);
 #pragma unroll
             for (int i = 0; i < 4; ++i) o4[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);

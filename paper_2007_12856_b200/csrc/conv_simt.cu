@@ -24,7 +24,7 @@ __device__ __forceinline__ bool fr_inside(const Frame& f, int z, int y, int x) {
 template <int CPT>
 __global__ void conv_fwd_simt_kernel(const float* __restrict__ x, Frame xf,
                                      const float* __restrict__ w, int k, int s,
-                                     float* __restrict__ y, Frame yf) {
+                                     float* __restrict__ y, Frame yf, int act, float slope) {
   const int cq = yf.c / CPT;
   const long long total = (long long)yf.n * yf.d * yf.h * yf.w * cq;
   const int r = (k - 1) / 2;
@@ -63,7 +63,7 @@ __global__ void conv_fwd_simt_kernel(const float* __restrict__ x, Frame xf,
     }
     float* yp = y + fr_index(yf, n, oz, oy, ox) + CPT * c4;
 #pragma unroll
-    for (int j = 0; j < CPT; ++j) yp[j] = acc[j];
+    for (int j = 0; j < CPT; ++j) yp[j] = (act && acc[j] < 0.f) ? slope * acc[j] : acc[j];
   }
 }
 
@@ -196,13 +196,13 @@ static int grid_for(long long total, int block) {
 }
 
 int conv_fwd_simt(const float* x, const Frame& xf, const float* w, int k, int s, float* y,
-                  const Frame& yf, cudaStream_t st) {
+                  const Frame& yf, cudaStream_t st, int act, float slope) {
   if (yf.c % 4 == 0) {
     long long total = (long long)yf.n * yf.d * yf.h * yf.w * (yf.c / 4);
-    conv_fwd_simt_kernel<4><<<grid_for(total, 256), 256, 0, st>>>(x, xf, w, k, s, y, yf);
+    conv_fwd_simt_kernel<4><<<grid_for(total, 256), 256, 0, st>>>(x, xf, w, k, s, y, yf, act, slope);
   } else {
     long long total = (long long)yf.n * yf.d * yf.h * yf.w * yf.c;
-    conv_fwd_simt_kernel<1><<<grid_for(total, 256), 256, 0, st>>>(x, xf, w, k, s, y, yf);
+    conv_fwd_simt_kernel<1><<<grid_for(total, 256), 256, 0, st>>>(x, xf, w, k, s, y, yf, act, slope);
   }
   VPX_LAUNCH_CHECK();
   return VPX_OK;
@@ -221,6 +221,13 @@ long long wgrad_simt_parts(const Frame& uf) {
   const long long nvox = (long long)uf.n * uf.d * uf.h * uf.w;
   long long P = (nvox + 4095) / 4096;
   return P < 256 ? P : 256;
+}
+
+int reduce_partials(const float* part, int P, long long len, float* out, int accumulate,
+                    cudaStream_t st) {
+  reduce_partials_kernel<<<grid_for(len, 256), 256, 0, st>>>(part, P, len, out, accumulate);
+  VPX_LAUNCH_CHECK();
+  return VPX_OK;
 }
 
 int conv_wgrad_simt(const float* x, const Frame& xf, const float* u, const Frame& uf, int k, int s,

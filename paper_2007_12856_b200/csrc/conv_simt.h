@@ -12,10 +12,16 @@ struct Frame {
 
 int num_sms();
 int conv_fwd_simt(const float* x, const Frame& xf, const float* w, int k, int s, float* y,
-                  const Frame& yf, cudaStream_t st);
+                  const Frame& yf, cudaStream_t st, int act = 0, float slope = 0.f);
 int conv_bwd_data_simt(const float* u, const Frame& uf, const float* w, int k, int s, float* xg,
                        const Frame& gf, cudaStream_t st);
 long long wgrad_simt_parts(const Frame& uf);
+int reduce_partials(const float* part, int P, long long len, float* out, int accumulate,
+                    cudaStream_t st);
+int wgrad_tc_supported(const Frame& xf, const Frame& uf);
+int wgrad_tc_parts(const Frame& xf, const Frame& uf);
+int conv_wgrad_tc(const float* x, const Frame& xf, const float* u, const Frame& uf, float* part,
+                  cudaStream_t st);
 int conv_wgrad_simt(const float* x, const Frame& xf, const float* u, const Frame& uf, int k, int s,
                     float* wg, int accumulate, float* part, cudaStream_t st);
 

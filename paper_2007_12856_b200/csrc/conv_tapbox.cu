@@ -1,0 +1,416 @@
+// Implicit-GEMM convolution on tcgen05 for layers whose rows are too short
+// for the row-window kernel (W < 128: CosmoFlow c4..c7, U-Net deep levels,
+// any W-partitioned grid) and for stride 2.
+//
+// M tile = a box of 128 output voxels (Wb x Hb x Db, W fastest).  For each
+// K entry (tap offset, 32-channel chunk) one TMA box of the input lands in
+// shared memory as 128-byte rows (SWIZZLE_128B K-major): the "im2col" is done
+// by the TMA unit, out-of-bounds taps read zeros (= "same" padding), frame
+// margins supply neighbour halos.  Stride-2 forward uses TMA element strides
+// (the box walks every second input voxel).  Stride-2 backward-data is run as
+// eight parity classes of output voxels (p = 2q + P); each class is a
+// stride-1 gather over u with its own list of taps (ConvTapParams.cls_*).
+// B = packed weights [entry][N_total][32] by 2D TMA, N tile <= 256.
+// Reference semantics: reference pkg/src/voxpar/kernels/_hot.pyx:19-67.
+#include "conv_common.h"
+#include "conv_simt.h"
+#include "vpx_host.h"
+#include "vpx_ptx.cuh"
+
+namespace vpx {
+
+constexpr int kMaxEntries = 256;
+
+struct ConvTapParams {
+  int n;                        // samples
+  int qd, qh, qw;               // q-grid origin offsets: q = q0 + tile coords
+  int QD, QH, QW;               // q-grid extents
+  int Db, Hb, Wb;               // tile box (Db*Hb*Wb <= 128)
+  int td, th, tw;               // tiles per dim
+  int ncls;                     // parity classes (1 or 8)
+  int ntn;                      // N tiles
+  int num_tiles;
+  int in_stride;                // 1 or 2 (input coordinate = s*q + off + margin)
+  int in_off_d, in_off_h, in_off_w;
+  int ntot;                     // total N (rows of each packed weight entry)
+  // per K entry: (od+1) | (oh+1)<<2 | (ow+1)<<4 | chunk<<8 | tap<<16
+  int entries[kMaxEntries];
+  int cls_start[9];             // entry ranges per parity class
+  float* out;
+  long long out_sn, out_sd, out_sh, out_sw;
+  int out_off_d, out_off_h, out_off_w;  // frame margins of the output
+  int out_stride;                       // 1 or 2 (p = s*q + P)
+  int pd_lo, pd_hi, ph_lo, ph_hi, pw_lo, pw_hi;  // valid output range (interior coords incl. margins)
+  int act;
+  float slope;
+};
+
+}  // namespace vpx
+
+namespace {
+
+using vpx::ConvTapParams;
+
+template <int NT, int S>
+__global__ void __launch_bounds__(256, 1)
+    conv_tapbox_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap wmap,
+                       const ConvTapParams p) {
+  constexpr int ABYTES = 128 * 128;  // 128 voxel rows x 32 fp32
+  constexpr int BBYTES = NT * 128;
+  constexpr int STAGE = ABYTES + BBYTES;  // multiple of 1024
+  constexpr int TCOLS = NT <= 32 ? 32 : NT <= 64 ? 64 : NT <= 128 ? 128 : 256;
+  static_assert(2 * TCOLS <= 512, "TMEM");
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t full[S], empty[S], tfull[2], tempty[2];
+  __shared__ uint32_t tmem_base;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      vpx::mbar_init(&full[s], 1);
+      vpx::mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      vpx::mbar_init(&tfull[s], 1);
+      vpx::mbar_init(&tempty[s], 128);
+    }
+    vpx::fence_barrier_init();
+    vpx::tma_prefetch_desc(&xmap);
+    vpx::tma_prefetch_desc(&wmap);
+  }
+  if (warp == 2) vpx::tmem_alloc<2 * TCOLS>(&tmem_base);
+  vpx::tc_fence_before();
+  __syncthreads();
+  vpx::tc_fence_after();
+  const uint32_t tbase = tmem_base;
+
+  // tile -> (n-tile, class, n, zt, yt, xt)
+  auto decode = [&](int tile, int& nt, int& cls, int& n, int& zt, int& yt, int& xt) {
+    nt = tile % p.ntn;
+    tile /= p.ntn;
+    cls = tile % p.ncls;
+    tile /= p.ncls;
+    xt = tile % p.tw;
+    tile /= p.tw;
+    yt = tile % p.th;
+    tile /= p.th;
+    zt = tile % p.td;
+    n = tile / p.td;
+  };
+
+  if (warp == 0) {
+    if (vpx::elect_one()) {
+      const uint32_t a_tx = p.Db * p.Hb * p.Wb * 128;
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+        int nt, cls, n, zt, yt, xt;
+        decode(tile, nt, cls, n, zt, yt, xt);
+        const int qz = p.qd + zt * p.Db, qy = p.qh + yt * p.Hb, qx = p.qw + xt * p.Wb;
+        const int e0 = p.cls_start[cls], e1 = p.cls_start[cls + 1];
+        for (int e = e0; e < e1; ++e) {
+          const int ent = p.entries[e];
+          const int od = (ent & 3) - 1, oh = ((ent >> 2) & 3) - 1, ow = ((ent >> 4) & 3) - 1;
+          const int chunk = (ent >> 8) & 0xff;
+          vpx::mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * STAGE;
+          vpx::mbar_arrive_expect_tx(&full[stage], a_tx + BBYTES);
+          vpx::tma_load_5d(sa, &xmap, &full[stage], 32 * chunk, p.in_stride * qx + ow + p.in_off_w,
+                           p.in_stride * qy + oh + p.in_off_h, p.in_stride * qz + od + p.in_off_d, n);
+          vpx::tma_load_2d(sa + ABYTES, &wmap, &full[stage], 0, e * p.ntot + nt * NT);
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = vpx::make_idesc(2, 128, NT, false, false);
+    int stage = 0, acc = 0;
+    uint32_t phase = 0, aphase = 0;
+    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+      int nt, cls, n, zt, yt, xt;
+      decode(tile, nt, cls, n, zt, yt, xt);
+      const int e0 = p.cls_start[cls], e1 = p.cls_start[cls + 1];
+      vpx::mbar_wait(&tempty[acc], aphase ^ 1);
+      vpx::tc_fence_after();
+      const uint32_t d = tbase + acc * TCOLS;
+      for (int e = e0; e < e1; ++e) {
+        vpx::mbar_wait(&full[stage], phase);
+        vpx::tc_fence_after();
+        if (vpx::elect_one()) {
+          const uint32_t a = vpx::smem_u32(smem + stage * STAGE);
+          const uint32_t b = a + ABYTES;
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            vpx::umma_tf32(d, vpx::make_sdesc(a + 32 * k, 16, 1024, 2), vpx::make_sdesc(b + 32 * k, 16, 1024, 2),
+                           idesc, (e > e0 || k > 0) ? 1u : 0u);
+          vpx::umma_commit(&empty[stage]);
+          if (e == e1 - 1) vpx::umma_commit(&tfull[acc]);
+        }
+        __syncwarp();
+        if (++stage == S) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      if (e1 == e0 && vpx::elect_one()) vpx::umma_commit(&tfull[acc]);  // empty class: no MMAs
+      __syncwarp();
+      acc ^= 1;
+      if (acc == 0) aphase ^= 1;
+    }
+  } else if (warp >= 4) {
+    const int q = warp - 4;
+    const int r = q * 32 + lane;  // row of the M tile
+    int acc = 0;
+    uint32_t aphase = 0;
+    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+      int nt, cls, n, zt, yt, xt;
+      decode(tile, nt, cls, n, zt, yt, xt);
+      const bool empty_cls = p.cls_start[cls + 1] == p.cls_start[cls];
+      vpx::mbar_wait(&tfull[acc], aphase);
+      vpx::tc_fence_after();
+      const int dx = r % p.Wb, dy = (r / p.Wb) % p.Hb, dz = r / (p.Wb * p.Hb);
+      const int qz = p.qd + zt * p.Db + dz, qy = p.qh + yt * p.Hb + dy, qx = p.qw + xt * p.Wb + dx;
+      const int Pd = (cls >> 2) & 1, Ph = (cls >> 1) & 1, Pw = cls & 1;
+      const int pz = p.out_stride * qz + Pd, py = p.out_stride * qy + Ph, px = p.out_stride * qx + Pw;
+      const bool valid = dz < p.Db && qz < p.qd + p.QD && qy < p.qh + p.QH && qx < p.qw + p.QW &&
+                         pz >= p.pd_lo && pz < p.pd_hi && py >= p.ph_lo && py < p.ph_hi && px >= p.pw_lo &&
+                         px < p.pw_hi;
+      float* o = p.out + static_cast<long long>(n) * p.out_sn + static_cast<long long>(pz + p.out_off_d) * p.out_sd +
+                 static_cast<long long>(py + p.out_off_h) * p.out_sh + static_cast<long long>(px + p.out_off_w) * p.out_sw +
+                 nt * NT;
+#pragma unroll 1
+      for (int cb = 0; cb < NT; cb += 16) {
+        float v[16];
+        vpx::tmem_ld16(tbase + (static_cast<uint32_t>(q * 32) << 16) + acc * TCOLS + cb, v);
+        if (valid) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            if (empty_cls) v[i] = 0.f;
+            if (p.act) v[i] = v[i] >= 0.f ? v[i] : p.slope * v[i];
+          }
+          float4* o4 = reinterpret_cast<float4*>(o + cb);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) o4[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        }
+      }
+      vpx::tc_fence_before();
+      vpx::mbar_arrive(&tempty[acc]);
+      acc ^= 1;
+      if (acc == 0) aphase ^= 1;
+    }
+  }
+  vpx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) vpx::tmem_dealloc<2 * TCOLS>(tbase);
+}
+
+template <int NT>
+int launch_tapbox(const CUtensorMap& xm, const CUtensorMap& wm, const ConvTapParams& p, cudaStream_t st) {
+  constexpr int STAGE = 128 * 128 + NT * 128;
+  constexpr int S = (200 * 1024) / STAGE >= 6 ? 6 : (200 * 1024) / STAGE;
+  auto kern = conv_tapbox_kernel<NT, S>;
+  const int smem = S * STAGE + 1024;
+  VPX_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  const int grid = p.num_tiles < vpx::num_sms() ? p.num_tiles : vpx::num_sms();
+  kern<<<grid, 256, smem, st>>>(xm, wm, p);
+  VPX_LAUNCH_CHECK();
+  return VPX_OK;
+}
+
+// Packed B: [entry][ntot][32]; value = Weff(o = row, i = 32*chunk + j, tap)
+//   mode 0 fwd:   w[o][i][tap]        (ntot = cout, i over cin)
+//   mode 1 dgrad: w[i][o][tap]        (ntot = cin,  i over cout)
+__global__ void pack_tapbox_kernel(const float* __restrict__ w, int cout, int cin, int mode,
+                                   const __grid_constant__ ConvTapParams tp, int n_entries, int ntot,
+                                   float* __restrict__ out) {
+  const long long total = (long long)n_entries * ntot * 32;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int j = idx % 32;
+    const int o = (idx / 32) % ntot;
+    const int e = static_cast<int>(idx / (32LL * ntot));
+    const int i = 32 * ((tp.entries[e] >> 8) & 0xff) + j;
+    const int tap = tp.entries[e] >> 16;
+    float v = 0.f;
+    if (mode == 0) {
+      if (i < cin) v = w[((long long)o * cin + i) * 27 + tap];
+    } else {
+      if (i < cout) v = w[((long long)i * cin + o) * 27 + tap];
+    }
+    out[idx] = v;
+  }
+}
+
+int encode_in_map(CUtensorMap* map, const float* base, const vpx::Frame& f, int Db, int Hb, int Wb, int s) {
+  const uint64_t Wf = f.w + 2 * f.mw, Hf = f.h + 2 * f.mh, Df = f.d + 2 * f.md;
+  uint64_t dims[5] = {(uint64_t)f.c, Wf, Hf, Df, (uint64_t)f.n};
+  uint64_t strides[4] = {(uint64_t)f.c * 4, Wf * f.c * 4, Hf * Wf * f.c * 4, Df * Hf * Wf * f.c * 4};
+  uint32_t box[5] = {32, (uint32_t)(s * Wb), (uint32_t)(s * Hb), (uint32_t)(s * Db), 1};
+  uint32_t estr[5] = {1, (uint32_t)s, (uint32_t)s, (uint32_t)s, 1};
+  return vpx::encode_tiled_strided(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float*>(base), dims,
+                                   strides, box, estr, CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+int encode_w_map(CUtensorMap* map, const float* base, long long rows, int NT) {
+  uint64_t dims[2] = {32, (uint64_t)rows};
+  uint64_t strides[1] = {32 * 4};
+  uint32_t box[2] = {32, (uint32_t)NT};
+  return vpx::encode_tiled(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box,
+                           CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+void tile_shape(int D, int H, int W, int* Db, int* Hb, int* Wb) {
+  *Wb = W < 128 ? W : 128;
+  *Hb = H < 128 / *Wb ? H : 128 / *Wb;
+  int rest = 128 / (*Wb * *Hb);
+  *Db = D < rest ? D : rest;
+}
+
+}  // namespace
+
+namespace vpx {
+
+// Workspace: the packed weights, [entry <= 256][ntot][32] fp32.
+long long tapbox_workspace_bytes(int cin, int cout) {
+  const long long ntot = cin > cout ? cin : cout;
+  return (long long)kMaxEntries * ntot * 32 * 4;
+}
+
+int tapbox_supported(int cin, int cout, int mode) {
+  const int ntot = mode == 0 ? cout : cin;
+  return ntot % 16 == 0 && (ntot <= 256 || ntot % 256 == 0);
+}
+
+// mode 0: forward (stride 1 or 2); mode 1: backward-data (stride 1 or 2).
+// in: input frame (x for fwd, u for dgrad); out: output frame.
+int conv_tapbox(int mode, const float* in, const Frame& inf, const float* w, int cin, int cout, int stride,
+                float* out, const Frame& of, int act, float slope, void* ws, cudaStream_t st) {
+  const int ntot = mode == 0 ? cout : cin;
+  const int kchan = mode == 0 ? cin : cout;  // channels along K
+  const int nchunks = (kchan + 31) / 32;
+  ConvTapParams p{};
+  int ne = 0;
+  const int ncls = (mode == 1 && stride == 2) ? 8 : 1;
+  for (int cls = 0; cls < ncls; ++cls) {
+    p.cls_start[cls] = ne;
+    for (int tap = 0; tap < 27; ++tap) {
+      const int t[3] = {tap / 9, (tap / 3) % 3, tap % 3};
+      int off[3];
+      bool ok = true;
+      for (int dd = 0; dd < 3; ++dd) {
+        if (mode == 0) {
+          off[dd] = t[dd] - 1;  // input = s*q + t - 1
+        } else if (stride == 1) {
+          off[dd] = 1 - t[dd];  // u index = p + 1 - t
+        } else {
+          const int P = (cls >> (2 - dd)) & 1;
+          const int num = P + 1 - t[dd];
+          if (num & 1) ok = false;
+          off[dd] = num / 2;  // u index = q + (P + 1 - t)/2, in {0, 1}
+        }
+      }
+      if (!ok) continue;
+      for (int ch = 0; ch < nchunks; ++ch) {
+        if (ne >= kMaxEntries) VPX_FAIL(VPX_ERR_UNSUPPORTED, "tapbox: more than %d K entries", kMaxEntries);
+        p.entries[ne++] = (off[0] + 1) | ((off[1] + 1) << 2) | ((off[2] + 1) << 4) | (ch << 8) | (tap << 16);
+      }
+    }
+  }
+  p.cls_start[ncls] = ne;
+  float* wpack = static_cast<float*>(ws);
+  {
+    const long long total = (long long)ne * ntot * 32;
+    int grid = static_cast<int>((total + 255) / 256);
+    if (grid > 8192) grid = 8192;
+    pack_tapbox_kernel<<<grid, 256, 0, st>>>(w, cout, cin, mode, p, ne, ntot, wpack);
+    VPX_LAUNCH_CHECK();
+  }
+  p.n = of.n;
+  // q grid
+  const int s_in = (mode == 0) ? stride : 1;
+  const int s_out = (mode == 1) ? stride : 1;
+  int QD, QH, QW, q0d = 0, q0h = 0, q0w = 0;
+  if (mode == 0) {
+    QD = of.d;
+    QH = of.h;
+    QW = of.w;
+  } else {
+    // cover output positions [-m, e+m) of the xg frame: q in [(-m - 1)/s .. ]
+    const int lo[3] = {-of.md, -of.mh, -of.mw};
+    const int hi[3] = {of.d + of.md, of.h + of.mh, of.w + of.mw};
+    int qlo[3], qhi[3];
+    for (int dd = 0; dd < 3; ++dd) {
+      if (s_out == 1) {
+        qlo[dd] = lo[dd];
+        qhi[dd] = hi[dd];
+      } else {  // p = 2q + P, P in {0,1}: q in [ceil((lo-1)/2), floor((hi-1)/2)]
+        qlo[dd] = -((1 - lo[dd]) / 2);
+        qhi[dd] = (hi[dd] - 1) / 2 + 1;
+      }
+    }
+    q0d = qlo[0];
+    q0h = qlo[1];
+    q0w = qlo[2];
+    QD = qhi[0] - qlo[0];
+    QH = qhi[1] - qlo[1];
+    QW = qhi[2] - qlo[2];
+  }
+  int Db, Hb, Wb;
+  tile_shape(QD, QH, QW, &Db, &Hb, &Wb);
+  p.qd = q0d;
+  p.qh = q0h;
+  p.qw = q0w;
+  p.QD = QD;
+  p.QH = QH;
+  p.QW = QW;
+  p.Db = Db;
+  p.Hb = Hb;
+  p.Wb = Wb;
+  p.td = (QD + Db - 1) / Db;
+  p.th = (QH + Hb - 1) / Hb;
+  p.tw = (QW + Wb - 1) / Wb;
+  p.ncls = ncls;
+  const int NT = ntot <= 256 ? ntot : 256;
+  p.ntn = ntot / NT;
+  p.num_tiles = of.n * p.td * p.th * p.tw * ncls * p.ntn;
+  p.in_stride = s_in;
+  p.in_off_d = inf.md;
+  p.in_off_h = inf.mh;
+  p.in_off_w = inf.mw;
+  p.ntot = ntot;
+  p.out = out;
+  const long long Wf = of.w + 2 * of.mw, Hf = of.h + 2 * of.mh, Df = of.d + 2 * of.md;
+  p.out_sw = of.c;
+  p.out_sh = Wf * of.c;
+  p.out_sd = Hf * Wf * of.c;
+  p.out_sn = Df * Hf * Wf * of.c;
+  p.out_off_d = of.md;
+  p.out_off_h = of.mh;
+  p.out_off_w = of.mw;
+  p.out_stride = s_out;
+  if (mode == 0) {
+    p.pd_lo = 0, p.pd_hi = of.d, p.ph_lo = 0, p.ph_hi = of.h, p.pw_lo = 0, p.pw_hi = of.w;
+  } else {
+    p.pd_lo = -of.md, p.pd_hi = of.d + of.md, p.ph_lo = -of.mh, p.ph_hi = of.h + of.mh;
+    p.pw_lo = -of.mw, p.pw_hi = of.w + of.mw;
+  }
+  p.act = act;
+  p.slope = slope;
+  CUtensorMap xm, wm;
+  if (int rc = encode_in_map(&xm, in, inf, Db, Hb, Wb, s_in)) return rc;
+  if (int rc = encode_w_map(&wm, wpack, (long long)ne * ntot, NT)) return rc;
+  switch (NT) {
+    case 16: return launch_tapbox<16>(xm, wm, p, st);
+    case 32: return launch_tapbox<32>(xm, wm, p, st);
+    case 64: return launch_tapbox<64>(xm, wm, p, st);
+    case 128: return launch_tapbox<128>(xm, wm, p, st);
+    case 256: return launch_tapbox<256>(xm, wm, p, st);
+  }
+  VPX_FAIL(VPX_ERR_UNSUPPORTED, "tapbox N tile %d", NT);
+}
+
+}  // namespace vpx

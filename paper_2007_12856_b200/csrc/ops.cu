@@ -8,6 +8,7 @@
 // copy, reference layers/distributed.py:31-33).  Reductions are deterministic:
 // fixed block partition + fixed-order final sum, accumulated in fp64.
 #include "conv_simt.h"
+#include "ops_vec.h"
 #include "vpx_host.h"
 
 namespace vpx {
@@ -504,12 +505,14 @@ using namespace vpx;
 extern "C" int vpx_leaky_fwd(const float* x, const int* xf, float* y, const int* yf, float slope,
                              void* st) {
   Frame a = F(xf), b = F(yf);
+  if (a.c % 4 == 0) return leaky_fwd_vec(x, a, y, b, slope, S(st));
   leaky_fwd_kernel<<<grid1d(VC(a) * a.c), 256, 0, S(st)>>>(x, a, y, b, slope);
   LAUNCH_TAIL;
 }
 extern "C" int vpx_leaky_bwd(const float* x, const int* xf, const float* u, const int* uf, float* g,
                              const int* gf, float slope, void* st) {
   Frame a = F(xf), b = F(uf), c = F(gf);
+  if (a.c % 4 == 0) return leaky_bwd_vec(x, a, u, b, g, c, slope, S(st));
   leaky_bwd_kernel<<<grid1d(VC(a) * a.c), 256, 0, S(st)>>>(x, a, u, b, g, c, slope);
   LAUNCH_TAIL;
 }
@@ -519,12 +522,14 @@ extern "C" int vpx_pool_fwd(const float* x, const int* xf, float* y, const int* 
   if (a.d % 2 || a.h % 2 || a.w % 2) VPX_FAIL(VPX_ERR_NON_DIVISIBLE, "pool3d needs even extents");
   if (b.d * 2 != a.d || b.h * 2 != a.h || b.w * 2 != a.w || a.c != b.c || a.n != b.n)
     VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "pool output extents");
+  if (a.c % 4 == 0) return pool_fwd_vec(x, a, y, b, is_max, S(st));
   pool_fwd_kernel<<<grid1d(VC(b) * b.c), 256, 0, S(st)>>>(x, a, y, b, is_max);
   LAUNCH_TAIL;
 }
 extern "C" int vpx_pool_bwd(const float* x, const int* xf, const float* u, const int* uf, float* g,
                             const int* gf, int is_max, void* st) {
   Frame a = F(xf), b = F(uf), c = F(gf);
+  if (a.c % 4 == 0) return pool_bwd_vec(x, a, u, b, g, c, is_max, S(st));
   pool_bwd_kernel<<<grid1d(VC(b) * b.c), 256, 0, S(st)>>>(x, a, u, b, g, c, is_max);
   LAUNCH_TAIL;
 }
@@ -549,6 +554,7 @@ extern "C" int vpx_bn_stats(const float* sums, int c, double count, float eps, f
 extern "C" int vpx_bn_apply(const float* x, const int* xf, const float* mean, const float* inv,
                             const float* gamma, const float* beta, float* y, const int* yf, void* st) {
   Frame a = F(xf), b = F(yf);
+  if (a.c % 4 == 0) return bn_apply_vec(x, a, mean, inv, gamma, beta, y, b, S(st));
   bn_apply_kernel<<<grid1d(VC(a) * a.c), 256, 0, S(st)>>>(x, a, mean, inv, gamma, beta, y, b);
   LAUNCH_TAIL;
 }
@@ -556,6 +562,8 @@ extern "C" int vpx_bn_bwd_apply(const float* x, const int* xf, const float* u, c
                                 const float* mean, const float* inv, const float* gamma,
                                 const float* sums, double count, float* g, const int* gf, void* st) {
   Frame a = F(xf), b = F(uf), c = F(gf);
+  if (a.c % 4 == 0)
+    return bn_bwd_apply_vec(x, a, u, b, mean, inv, gamma, sums, static_cast<float>(1.0 / count), g, c, S(st));
   bn_bwd_apply_kernel<<<grid1d(VC(a) * a.c), 256, 0, S(st)>>>(
       x, a, u, b, mean, inv, gamma, sums, static_cast<float>(1.0 / count), g, c);
   LAUNCH_TAIL;

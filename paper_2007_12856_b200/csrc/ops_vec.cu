@@ -1,0 +1,217 @@
+// Vectorised (float4 over channels) variants of the memory-bound kernels in
+// ops.cu, used whenever C % 4 == 0.  Work is enumerated per float4 of an
+// interior row: a row (n, z, y) of every frame is contiguous (margins only sit
+// at the row ends), so one index decode serves 4 channels and all loads and
+// stores are 16-byte and coalesced.
+#include "conv_simt.h"
+#include "ops_vec.h"
+#include "vpx_host.h"
+
+namespace vpx {
+
+namespace {
+
+__device__ __forceinline__ long long row_base(const Frame& f, long long row) {
+  const int y = row % f.h;
+  row /= f.h;
+  const int z = row % f.d;
+  const int n = static_cast<int>(row / f.d);
+  return ((((long long)n * (f.d + 2 * f.md) + (z + f.md)) * (f.h + 2 * f.mh) + (y + f.mh)) *
+              (f.w + 2 * f.mw) +
+          f.mw) *
+         f.c;
+}
+
+__device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+__device__ __forceinline__ float lk(float v, float s) { return v >= 0.f ? v : s * v; }
+
+#define ROW_LOOP(f)                                                                          \
+  const long long per_row = (long long)(f).w * (f).c / 4;                                    \
+  const long long total = (long long)(f).n * (f).d * (f).h * per_row;                        \
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;          \
+       i += (long long)gridDim.x * blockDim.x)
+
+__global__ void leaky_fwd_v(const float* __restrict__ x, Frame xf, float* __restrict__ y, Frame yf, float s) {
+  ROW_LOOP(xf) {
+    const long long row = i / per_row, off = 4 * (i % per_row);
+    float4 v = ld4(x + row_base(xf, row) + off);
+    v = make_float4(lk(v.x, s), lk(v.y, s), lk(v.z, s), lk(v.w, s));
+    st4(y + row_base(yf, row) + off, v);
+  }
+}
+
+__global__ void leaky_bwd_v(const float* __restrict__ x, Frame xf, const float* __restrict__ u, Frame uf,
+                            float* __restrict__ g, Frame gf, float s) {
+  ROW_LOOP(xf) {
+    const long long row = i / per_row, off = 4 * (i % per_row);
+    const float4 a = ld4(x + row_base(xf, row) + off);
+    const float4 b = ld4(u + row_base(uf, row) + off);
+    st4(g + row_base(gf, row) + off, make_float4(a.x >= 0.f ? b.x : s * b.x, a.y >= 0.f ? b.y : s * b.y,
+                                                 a.z >= 0.f ? b.z : s * b.z, a.w >= 0.f ? b.w : s * b.w));
+  }
+}
+
+__device__ __forceinline__ void mx(float4& best, const float4 v) {
+  // strict '>' keeps the first (lowest window index) maximum on ties
+  best.x = v.x > best.x ? v.x : best.x;
+  best.y = v.y > best.y ? v.y : best.y;
+  best.z = v.z > best.z ? v.z : best.z;
+  best.w = v.w > best.w ? v.w : best.w;
+}
+
+// output row (n, zo, yo) of the pooled frame reads input rows (2zo+a, 2yo+b)
+__global__ void pool_fwd_v(const float* __restrict__ x, Frame xf, float* __restrict__ y, Frame yf,
+                           int is_max) {
+  const int C = yf.c;
+  const long long in_row_stride = (long long)(xf.w + 2 * xf.mw) * C;
+  const long long in_plane_stride = (long long)(xf.h + 2 * xf.mh) * in_row_stride;
+  ROW_LOOP(yf) {
+    const long long orow = i / per_row, off = i % per_row;
+    const int xo = static_cast<int>(off / (C / 4)), c4 = static_cast<int>(off % (C / 4));
+    long long t = orow;
+    const int yo = t % yf.h;
+    t /= yf.h;
+    const int zo = t % yf.d;
+    const int n = static_cast<int>(t / yf.d);
+    const float* p = x + ((((long long)n * (xf.d + 2 * xf.md) + (2 * zo + xf.md)) * (xf.h + 2 * xf.mh) +
+                           (2 * yo + xf.mh)) * (xf.w + 2 * xf.mw) + (2 * xo + xf.mw)) * C + 4 * c4;
+    float4 acc = ld4(p);
+    float4 sum = acc;
+#pragma unroll
+    for (int w8 = 1; w8 < 8; ++w8) {
+      const int a = w8 >> 2, b = (w8 >> 1) & 1, cc = w8 & 1;
+      const float4 v = ld4(p + a * in_plane_stride + b * in_row_stride + cc * C);
+      if (is_max) mx(acc, v);
+      sum.x += v.x;
+      sum.y += v.y;
+      sum.z += v.z;
+      sum.w += v.w;
+    }
+    if (!is_max) acc = make_float4(sum.x / 8.0f, sum.y / 8.0f, sum.z / 8.0f, sum.w / 8.0f);
+    st4(y + row_base(yf, orow) + 4 * off, acc);
+  }
+}
+
+// g[input window] from u[pooled voxel]; max: one-hot at the first maximum
+__global__ void pool_bwd_v(const float* __restrict__ x, Frame xf, const float* __restrict__ u, Frame uf,
+                           float* __restrict__ g, Frame gf, int is_max) {
+  const int C = uf.c;
+  ROW_LOOP(uf) {
+    const long long orow = i / per_row, off = i % per_row;
+    const int xo = static_cast<int>(off / (C / 4)), c4 = static_cast<int>(off % (C / 4));
+    long long t = orow;
+    const int yo = t % uf.h;
+    t /= uf.h;
+    const int zo = t % uf.d;
+    const int n = static_cast<int>(t / uf.d);
+    const float4 uv = ld4(u + row_base(uf, orow) + 4 * off);
+    auto foff = [&](const Frame& f, int a, int b, int cc) {
+      return ((((long long)n * (f.d + 2 * f.md) + (2 * zo + a + f.md)) * (f.h + 2 * f.mh) + (2 * yo + b + f.mh)) *
+                  (f.w + 2 * f.mw) + (2 * xo + cc + f.mw)) * C + 4 * c4;
+    };
+    if (!is_max) {
+      const float4 gv = make_float4(uv.x / 8.0f, uv.y / 8.0f, uv.z / 8.0f, uv.w / 8.0f);
+#pragma unroll
+      for (int w8 = 0; w8 < 8; ++w8) st4(g + foff(gf, w8 >> 2, (w8 >> 1) & 1, w8 & 1), gv);
+    } else {
+      float4 best = ld4(x + foff(xf, 0, 0, 0));
+      int ax = 0, ay = 0, az = 0, aw = 0;
+#pragma unroll
+      for (int w8 = 1; w8 < 8; ++w8) {
+        const float4 v = ld4(x + foff(xf, w8 >> 2, (w8 >> 1) & 1, w8 & 1));
+        if (v.x > best.x) { best.x = v.x; ax = w8; }
+        if (v.y > best.y) { best.y = v.y; ay = w8; }
+        if (v.z > best.z) { best.z = v.z; az = w8; }
+        if (v.w > best.w) { best.w = v.w; aw = w8; }
+      }
+#pragma unroll
+      for (int w8 = 0; w8 < 8; ++w8)
+        st4(g + foff(gf, w8 >> 2, (w8 >> 1) & 1, w8 & 1),
+            make_float4(w8 == ax ? uv.x : 0.f, w8 == ay ? uv.y : 0.f, w8 == az ? uv.z : 0.f, w8 == aw ? uv.w : 0.f));
+    }
+  }
+}
+
+__global__ void bn_apply_v(const float* __restrict__ x, Frame xf, const float* __restrict__ mean,
+                           const float* __restrict__ inv, const float* __restrict__ gamma,
+                           const float* __restrict__ beta, float* __restrict__ y, Frame yf) {
+  const int C = xf.c;
+  ROW_LOOP(xf) {
+    const long long row = i / per_row, off = 4 * (i % per_row);
+    const int c = static_cast<int>(off % C);
+    const float4 v = ld4(x + row_base(xf, row) + off);
+    float r[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) r[j] = gamma[c + j] * ((r[j] - mean[c + j]) * inv[c + j]) + beta[c + j];
+    st4(y + row_base(yf, row) + off, make_float4(r[0], r[1], r[2], r[3]));
+  }
+}
+
+__global__ void bn_bwd_apply_v(const float* __restrict__ x, Frame xf, const float* __restrict__ u, Frame uf,
+                               const float* __restrict__ mean, const float* __restrict__ inv,
+                               const float* __restrict__ gamma, const float* __restrict__ sums,
+                               float inv_count, float* __restrict__ g, Frame gf) {
+  const int C = xf.c;
+  ROW_LOOP(xf) {
+    const long long row = i / per_row, off = 4 * (i % per_row);
+    const int c = static_cast<int>(off % C);
+    const float4 a = ld4(x + row_base(xf, row) + off);
+    const float4 b = ld4(u + row_base(uf, row) + off);
+    const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+    float r[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float xh = (av[j] - mean[c + j]) * inv[c + j];
+      r[j] = gamma[c + j] * inv[c + j] * (bv[j] - (sums[c + j] + xh * sums[C + c + j]) * inv_count);
+    }
+    st4(g + row_base(gf, row) + off, make_float4(r[0], r[1], r[2], r[3]));
+  }
+}
+
+int grid_v(const Frame& f) {
+  const long long total = (long long)f.n * f.d * f.h * f.w * f.c / 4;
+  long long g = (total + 255) / 256;
+  const long long cap = (long long)num_sms() * 16;
+  return static_cast<int>(g < 1 ? 1 : (g > cap ? cap : g));
+}
+
+}  // namespace
+
+int leaky_fwd_vec(const float* x, const Frame& xf, float* y, const Frame& yf, float s, cudaStream_t st) {
+  leaky_fwd_v<<<grid_v(xf), 256, 0, st>>>(x, xf, y, yf, s);
+  VPX_LAUNCH_CHECK();
+  return VPX_OK;
+}
+int leaky_bwd_vec(const float* x, const Frame& xf, const float* u, const Frame& uf, float* g, const Frame& gf,
+                  float s, cudaStream_t st) {
+  leaky_bwd_v<<<grid_v(xf), 256, 0, st>>>(x, xf, u, uf, g, gf, s);
+  VPX_LAUNCH_CHECK();
+  return VPX_OK;
+}
+int pool_fwd_vec(const float* x, const Frame& xf, float* y, const Frame& yf, int is_max, cudaStream_t st) {
+  pool_fwd_v<<<grid_v(yf), 256, 0, st>>>(x, xf, y, yf, is_max);
+  VPX_LAUNCH_CHECK();
+  return VPX_OK;
+}
+int pool_bwd_vec(const float* x, const Frame& xf, const float* u, const Frame& uf, float* g, const Frame& gf,
+                 int is_max, cudaStream_t st) {
+  pool_bwd_v<<<grid_v(uf), 256, 0, st>>>(x, xf, u, uf, g, gf, is_max);
+  VPX_LAUNCH_CHECK();
+  return VPX_OK;
+}
+int bn_apply_vec(const float* x, const Frame& xf, const float* mean, const float* inv, const float* gamma,
+                 const float* beta, float* y, const Frame& yf, cudaStream_t st) {
+  bn_apply_v<<<grid_v(xf), 256, 0, st>>>(x, xf, mean, inv, gamma, beta, y, yf);
+  VPX_LAUNCH_CHECK();
+  return VPX_OK;
+}
+int bn_bwd_apply_vec(const float* x, const Frame& xf, const float* u, const Frame& uf, const float* mean,
+                     const float* inv, const float* gamma, const float* sums, float inv_count, float* g,
+                     const Frame& gf, cudaStream_t st) {
+  bn_bwd_apply_v<<<grid_v(xf), 256, 0, st>>>(x, xf, u, uf, mean, inv, gamma, sums, inv_count, g, gf);
+  VPX_LAUNCH_CHECK();
+  return VPX_OK;
+}
+
+}  // namespace vpx

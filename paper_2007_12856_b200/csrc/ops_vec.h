@@ -1,0 +1,19 @@
+// float4-vectorised memory-bound kernels (C % 4 == 0), see ops_vec.cu.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "conv_simt.h"
+
+namespace vpx {
+int leaky_fwd_vec(const float* x, const Frame& xf, float* y, const Frame& yf, float s, cudaStream_t st);
+int leaky_bwd_vec(const float* x, const Frame& xf, const float* u, const Frame& uf, float* g, const Frame& gf,
+                  float s, cudaStream_t st);
+int pool_fwd_vec(const float* x, const Frame& xf, float* y, const Frame& yf, int is_max, cudaStream_t st);
+int pool_bwd_vec(const float* x, const Frame& xf, const float* u, const Frame& uf, float* g, const Frame& gf,
+                 int is_max, cudaStream_t st);
+int bn_apply_vec(const float* x, const Frame& xf, const float* mean, const float* inv, const float* gamma,
+                 const float* beta, float* y, const Frame& yf, cudaStream_t st);
+int bn_bwd_apply_vec(const float* x, const Frame& xf, const float* u, const Frame& uf, const float* mean,
+                     const float* inv, const float* gamma, const float* sums, float inv_count, float* g,
+                     const Frame& gf, cudaStream_t st);
+}  // namespace vpx

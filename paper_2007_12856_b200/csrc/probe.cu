@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(128, 1)
 
 __global__ void __launch_bounds__(128, 1)
     probe_tma_kernel(const __grid_constant__ CUtensorMap map, int c0, int c1, int c2, int c3,
-                     int c4, uint32_t bytes, uint4* __restrict__ out) {
+                     int c4, uint32_t bytes, uint4* __restrict__ out, int* __restrict__ ok) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bar;
   const int tid = threadIdx.x;
@@ -74,7 +74,11 @@ __global__ void __launch_bounds__(128, 1)
     vpx::mbar_arrive_expect_tx(&bar, bytes);
     vpx::tma_load_5d(smem, &map, &bar, c0, c1, c2, c3, c4);
   }
-  vpx::mbar_wait(&bar, 0);
+  // bounded wait: a wrong byte count must not hang the probe
+  bool done = false;
+  for (long long it = 0; it < (1LL << 22) && !done; ++it) done = vpx::mbar_try_wait(&bar, 0);
+  if (tid == 0) ok[0] = done ? 1 : 0;
+  if (!done) return;
   const uint4* s4 = reinterpret_cast<const uint4*>(smem);
   for (uint32_t i = tid; i < bytes / 16; i += blockDim.x) out[i] = s4[i];
 }
@@ -221,23 +225,24 @@ extern "C" int vpx_probe_umma(const void* img, int img_bytes, const uint64_t* op
 }
 
 extern "C" int vpx_probe_tma(const void* gsrc, const uint64_t* dims5, const uint64_t* strides4,
-                             const uint32_t* box5, int swizzle, const int32_t* coords5, void* out,
-                             int out_bytes, void* stream) {
+                             const uint32_t* box5, const uint32_t* estr5, int swizzle,
+                             const int32_t* coords5, void* out, int out_bytes, int* ok,
+                             void* stream) {
   CUtensorMap map;
   CUtensorMapSwizzle sw = swizzle == 1282 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B
                           : swizzle == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
                           : swizzle == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
                           : swizzle == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
                                           : CU_TENSOR_MAP_SWIZZLE_NONE;
-  int rc = vpx::encode_tiled(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<void*>(gsrc),
-                             dims5, strides4, box5, sw);
+  int rc = vpx::encode_tiled_strided(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5,
+                                     const_cast<void*>(gsrc), dims5, strides4, box5, estr5, sw);
   if (rc) return rc;
   if (out_bytes > kProbeSmem || out_bytes % 16) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "out size");
   VPX_CHECK_CUDA(cudaFuncSetAttribute(probe_tma_kernel,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kProbeSmem));
   probe_tma_kernel<<<1, 128, kProbeSmem, static_cast<cudaStream_t>(stream)>>>(
       map, coords5[0], coords5[1], coords5[2], coords5[3], coords5[4],
-      static_cast<uint32_t>(out_bytes), static_cast<uint4*>(out));
+      static_cast<uint32_t>(out_bytes), static_cast<uint4*>(out), ok);
   VPX_LAUNCH_CHECK();
   return VPX_OK;
 }

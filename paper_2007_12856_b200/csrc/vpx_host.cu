@@ -29,9 +29,17 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 int encode_tiled(CUtensorMap* map, CUtensorMapDataType dtype, int rank, void* gaddr,
                  const uint64_t* dims, const uint64_t* strides_bytes, const uint32_t* box,
                  CUtensorMapSwizzle swizzle) {
+  const uint32_t ones[5] = {1, 1, 1, 1, 1};
+  return encode_tiled_strided(map, dtype, rank, gaddr, dims, strides_bytes, box, ones, swizzle);
+}
+
+int encode_tiled_strided(CUtensorMap* map, CUtensorMapDataType dtype, int rank, void* gaddr,
+                         const uint64_t* dims, const uint64_t* strides_bytes, const uint32_t* box,
+                         const uint32_t* elem_strides, CUtensorMapSwizzle swizzle) {
   auto fn = encode_fn();
   if (!fn) VPX_FAIL(VPX_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
   cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  for (int i = 0; i < rank; ++i) estr[i] = elem_strides[i];
   CUresult r = fn(map, dtype, rank, gaddr, reinterpret_cast<const cuuint64_t*>(dims),
                   reinterpret_cast<const cuuint64_t*>(strides_bytes),
                   reinterpret_cast<const cuuint32_t*>(box), estr, CU_TENSOR_MAP_INTERLEAVE_NONE,

@@ -43,5 +43,9 @@ extern std::atomic<long long> g_launches;
 int encode_tiled(CUtensorMap* map, CUtensorMapDataType dtype, int rank, void* gaddr,
                  const uint64_t* dims, const uint64_t* strides_bytes, const uint32_t* box,
                  CUtensorMapSwizzle swizzle);
+// Same with per-dimension element (traversal) strides.
+int encode_tiled_strided(CUtensorMap* map, CUtensorMapDataType dtype, int rank, void* gaddr,
+                         const uint64_t* dims, const uint64_t* strides_bytes, const uint32_t* box,
+                         const uint32_t* elem_strides, CUtensorMapSwizzle swizzle);
 
 }  // namespace vpx

@@ -318,6 +318,7 @@ def forward(ctx: RankCtx, plan: Plan, state: RankState, batch: Batch, mode: str,
         cur = batch.x_block if isinstance(batch.x_block, DistTensor) else \
             DistTensor(plan.input_meta, gr0, batch.x_block)
     outputs, stash = {}, []
+    fused_act = False
     for i, layer in enumerate(net.layers):
         if i == plan.redist_idx and plan.placement[i] != "flat":
             cur = D.redistribute(ctx, cur, plan.redist_src_meta, plan.in_meta[i])
@@ -352,9 +353,21 @@ def forward(ctx: RankCtx, plan: Plan, state: RankState, batch: Batch, mode: str,
             outputs[layer.name] = None
             continue
         radii = plan.out_radii[i]
+        if fused_act:
+            # this LeakyReLU already ran in the previous conv's epilogue; its
+            # backward only needs the activation output (sign-preserving)
+            fused_act = False
+            stash.append(cur)
+            outputs[layer.name] = cur
+            continue
         if layer.kind == "conv":
             stash.append(cur)
-            cur = D.dist_conv3d(ctx, cur, P[f"{layer.name}.w"], layer.params, radii, tag=layer.name)
+            nxt = net.layers[i + 1] if i + 1 < len(net.layers) else None
+            fused_act = (trace is None and nxt is not None and nxt.kind == "leaky"
+                         and plan.placement[i + 1] == plan.placement[i] and plan.redist_idx != i + 1)
+            cur = D.dist_conv3d(ctx, cur, P[f"{layer.name}.w"], layer.params,
+                                plan.out_radii[i + 1] if fused_act else radii, tag=layer.name,
+                                leaky_slope=nxt.slope if fused_act else None)
         elif layer.kind == "deconv":
             stash.append(cur)
             cur = D.dist_deconv3d(ctx, cur, P[f"{layer.name}.w"], radii)

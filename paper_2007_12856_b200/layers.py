@@ -73,9 +73,11 @@ def _conv_flops(params, out_vox):
 
 
 def dist_conv3d(ctx: RankCtx, x: DistTensor, w: torch.Tensor, params, out_radii=NO_HALO,
-                tag: str = "conv") -> DistTensor:
+                tag: str = "conv", leaky_slope: float = None) -> DistTensor:
     """Halo exchange, then the local tcgen05 implicit-GEMM conv on the frame
-    (reference layers/distributed.py:42-69)."""
+    (reference layers/distributed.py:42-69).  With leaky_slope set, the
+    following LeakyReLU is fused into the epilogue and the result is
+    leaky(conv(x)) (engine.forward uses this outside trace mode)."""
     meta = x.meta
     if tuple(meta.radii) != params.radii:
         raise ShapeMismatch(f"input partitioned with radii {meta.radii}, conv needs {params.radii}")
@@ -92,8 +94,9 @@ def dist_conv3d(ctx: RankCtx, x: DistTensor, w: torch.Tensor, params, out_radii=
     ws = WS.get(nb)
     with region(f"{tag}.fwd", _conv_flops(params, y.voxels()),
                 4 * (x.voxels() * x.c + y.voxels() * y.c + w.numel())):
-        _lib.call("vpx_conv3d_fwd", x.ptr, x.desc, w.data_ptr(), k, s, y.ptr, y.desc, ws.data_ptr(),
-                  ws.numel() * 4, stream_ptr())
+        _lib.call("vpx_conv3d_fwd_act", x.ptr, x.desc, w.data_ptr(), k, s, y.ptr, y.desc,
+                  int(leaky_slope is not None), float(leaky_slope or 0.0), ws.data_ptr(), ws.numel() * 4,
+                  stream_ptr())
     return y
 
 

@@ -88,6 +88,38 @@ def test_train_step_matches_oracle(which):
         assert np.mean(d > 1e-2 * lr) < 0.02, (name, float(np.mean(d > 1e-2 * lr)))
 
 
+def test_fused_step_equals_traced_step():
+    """Outside trace mode conv+LeakyReLU run as one kernel; gradients must be
+    identical to the unfused (traced) step."""
+    net = build_cosmoflow(128)
+    ctx = RankCtx(0, 1)
+    plan = engine.make_plan(net, ProcessGrid(1, 1, 1, 1), 1, 128)
+    x, y, ids = engine.synthetic_batch_full(net, 128, 1, 0)
+    grads = []
+    for trace in ({}, None):
+        state = engine.make_state(net, 0)
+        batch = engine.scatter_batch(plan, x, y, ids, 0)
+        state.params.grad.zero_()
+        pred, stash = engine.forward(ctx, plan, state, batch, "train", 0, trace=trace)
+        loss, dpred = engine.loss_and_grad(ctx, plan, pred, batch)
+        engine.backward(ctx, plan, state, stash, dpred, trace=trace)
+        grads.append(state.params.grad.clone())
+    assert torch.equal(grads[0], grads[1])
+
+
+def test_cosmoflow128_traces_vs_oracle():
+    """Exercises the tcgen05 row-window (c1 W=128), tap-box (c2..c7, stride 2)
+    and filter-gradient kernels inside the full step, n=1."""
+    net, wi = build_cosmoflow(128), 128
+    loss, loss_o, trace, trace_o, grads, grads_o, state, po = _run(net, wi, 1)
+    report = [(k, rel(_to_np(trace[k]), v)) for k, v in trace_o.items()]
+    report += [(("grad", k), rel(grads[k].cpu().numpy(), g)) for k, g in grads_o.items()]
+    print("\n".join(f"{k}: {e:.2e}" for k, e in report))
+    assert abs(float(loss.item()) - loss_o) <= 1e-3 * abs(loss_o)
+    for key, e in report:
+        assert e < (RTOL["fwd"] if key[0] == "fwd" else RTOL["bwd"]), (key, e)
+
+
 def test_cosmoflow64_loss_matches_reference_value(golden):
     """One step of CosmoFlow-64, n=2, fp32 on the reference's synthetic verify
     batch: the loss the reference itself computed (tests/golden/nets.npz)."""

@@ -50,7 +50,43 @@ CASES = [
     (1, 64, 128, 8, 8, 8, 3, 2),
     (1, 128, 256, 4, 4, 4, 3, 1),
     (2, 8, 2, 6, 6, 6, 1, 1),
+    # tcgen05 filter gradient: mode A (Cin <= 32, W taps folded into M) ...
+    (1, 4, 16, 3, 4, 32, 3, 1),
+    (2, 16, 32, 3, 3, 16, 3, 1),
+    (1, 32, 64, 2, 5, 8, 3, 1),
+    # ... and mode B (Cin % 128 == 0, W <= 32)
+    (1, 128, 256, 3, 4, 16, 3, 1),
+    (1, 256, 256, 2, 4, 8, 3, 1),
+    # tap-box fwd/dgrad: W < 128, channel chunks padded by TMA zero fill, stride 2
+    (1, 16, 32, 4, 6, 16, 3, 1),
+    (2, 32, 64, 4, 4, 32, 3, 1),
+    (1, 64, 128, 16, 16, 16, 3, 2),
+    (1, 256, 256, 8, 8, 8, 3, 1),
 ]
+
+
+def test_tapbox_dgrad_all_margins():
+    """W-partitioned frames (margins in all three dims) go through the tap-box
+    kernel for both passes."""
+    rng = np.random.default_rng(11)
+    n, cin, cout, d, h, w = 1, 32, 64, 4, 4, 16
+    full = rng.uniform(-1, 1, (n, cin, d + 2, h + 2, w + 2)).astype(np.float32)
+    wt = (rng.uniform(-1, 1, (cout, cin, 3, 3, 3)) / 30).astype(np.float32)
+    xf = Frame(n, cin, d, h, w, (1, 1, 1), zero=True)
+    xf.t.copy_(torch.from_numpy(full.transpose(0, 2, 3, 4, 1).copy()).cuda())
+    yf = Frame(n, cout, d, h, w)
+    wdev = torch.from_numpy(wt).cuda()
+    W = ws(cin, cout, 3, yf)
+    _lib.call("vpx_conv3d_fwd", xf.ptr, xf.desc, wdev.data_ptr(), 3, 1, yf.ptr, yf.desc, W.data_ptr(),
+              W.numel() * 4, stream_ptr())
+    assert rel(yf.to_ncdhw().cpu().numpy(), O.k_conv3d_fwd(full, wt, (1, 1, 1))) < TF32_RTOL
+    u = rng.uniform(-1, 1, (n, cout, d, h, w)).astype(np.float32)
+    uf = Frame(n, cout, d, h, w).load_ncdhw(u)
+    gf = Frame(n, cin, d, h, w, (1, 1, 1), zero=False)
+    _lib.call("vpx_conv3d_bwd_data", uf.ptr, uf.desc, wdev.data_ptr(), 3, 1, gf.ptr, gf.desc, W.data_ptr(),
+              W.numel() * 4, stream_ptr())
+    g_ref = O.k_conv3d_bwd_data(u, wt, (1, 1, 1), (d + 2, h + 2, w + 2))
+    assert rel(gf.t.cpu().numpy().transpose(0, 4, 1, 2, 3), g_ref) < TF32_RTOL
 
 
 @pytest.mark.parametrize("case", CASES)

@@ -18,6 +18,7 @@ from paper_2007_12856_b200 import _lib  # noqa: E402
 
 rng = np.random.default_rng(0)
 RESULTS = {}
+ONES = (ctypes.c_uint32 * 5)(1, 1, 1, 1, 1)
 
 
 def tf32(a):
@@ -255,9 +256,10 @@ def t_tma():
     coords = (ctypes.c_int32 * 5)(0, -1, -1, -1, 0)
     nbytes = 4 * 18 * 3 * 2 * 4
     out = torch.zeros(nbytes // 4, dtype=torch.float32, device="cuda")
+    ok = torch.zeros(1, dtype=torch.int32, device="cuda")
     _lib.call("vpx_probe_tma", g.data_ptr(), ctypes.addressof(dims), ctypes.addressof(strides),
-              ctypes.addressof(box), 0, ctypes.addressof(coords), out.data_ptr(), nbytes,
-              torch.cuda.current_stream().cuda_stream)
+              ctypes.addressof(box), ctypes.addressof(ONES), 0, ctypes.addressof(coords), out.data_ptr(), nbytes,
+              ok.data_ptr(), torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     got = out.cpu().numpy().reshape(2, 3, 18, 4)
     Xp = np.zeros((D + 2, H + 2, W + 2, C), np.float32)
@@ -275,9 +277,10 @@ def t_tma():
     coords = (ctypes.c_int32 * 5)(0, 0, 0, 0, 0)
     nbytes = 16 * 128
     out = torch.zeros(nbytes // 4, dtype=torch.float32, device="cuda")
+    ok = torch.zeros(1, dtype=torch.int32, device="cuda")
     _lib.call("vpx_probe_tma", g2.data_ptr(), ctypes.addressof(dims), ctypes.addressof(strides),
-              ctypes.addressof(box), 128, ctypes.addressof(coords), out.data_ptr(), nbytes,
-              torch.cuda.current_stream().cuda_stream)
+              ctypes.addressof(box), ctypes.addressof(ONES), 128, ctypes.addressof(coords), out.data_ptr(), nbytes,
+              ok.data_ptr(), torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     raw = out.cpu().numpy().view(np.uint8)
     want_b = np.zeros(nbytes, np.uint8)
@@ -388,9 +391,10 @@ def t_tma32b():
     coords = (ctypes.c_int32 * 5)(0, 0, 0, 0, 0)
     nbytes = 16 * 128
     out = torch.zeros(nbytes // 4, dtype=torch.float32, device="cuda")
+    ok = torch.zeros(1, dtype=torch.int32, device="cuda")
     _lib.call("vpx_probe_tma", g2.data_ptr(), ctypes.addressof(dims), ctypes.addressof(strides),
-              ctypes.addressof(box), 1282, ctypes.addressof(coords), out.data_ptr(), nbytes,
-              torch.cuda.current_stream().cuda_stream)
+              ctypes.addressof(box), ctypes.addressof(ONES), 1282, ctypes.addressof(coords), out.data_ptr(), nbytes,
+              ok.data_ptr(), torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     raw = out.cpu().numpy().view(np.uint8)
     want_b = np.zeros(nbytes, np.uint8)
@@ -403,11 +407,50 @@ def t_tma32b():
     print(f"{'PASS' if ok else 'FAIL'} tma_sw128_atom32b_pattern")
 
 
+def t_tma_strided():
+    """elementStrides: box {32, 2Wb, 2Hb, 1, 1} with strides {1,2,2,1,1} -> Wb*Hb rows?"""
+    C, W, H = 32, 20, 12
+    X = rng.standard_normal((1, 1, H, W, C)).astype(np.float32)
+    g = torch.from_numpy(X).cuda()
+    dims = (ctypes.c_uint64 * 5)(C, W, H, 1, 1)
+    strides = (ctypes.c_uint64 * 4)(C * 4, W * C * 4, H * W * C * 4, H * W * C * 4)
+    Wb, Hb = 8, 4
+    box = (ctypes.c_uint32 * 5)(32, 2 * Wb, 2 * Hb, 1, 1)
+    est = (ctypes.c_uint32 * 5)(1, 2, 2, 1, 1)
+    coords = (ctypes.c_int32 * 5)(0, -1, -1, 0, 0)
+    for nbytes in (Wb * Hb * 128, 4 * Wb * Hb * 128):
+        out = torch.zeros(nbytes // 4, dtype=torch.float32, device="cuda")
+        ok = torch.zeros(1, dtype=torch.int32, device="cuda")
+        _lib.call("vpx_probe_tma", g.data_ptr(), ctypes.addressof(dims), ctypes.addressof(strides),
+                  ctypes.addressof(box), ctypes.addressof(est), 128, ctypes.addressof(coords), out.data_ptr(),
+                  nbytes, ok.data_ptr(), torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        done = int(ok.item())
+        print(f"strided box expect {nbytes} bytes: completed={done}")
+        RESULTS[f"tma_strided_{nbytes}"] = done
+        if done and nbytes == Wb * Hb * 128:
+            raw = out.cpu().numpy().view(np.uint8)
+            src = np.zeros((Hb, Wb, C), np.float32)
+            Xp = np.zeros((H + 2, W + 2, C), np.float32)
+            Xp[1:-1, 1:-1] = X[0, 0]
+            for yy in range(Hb):
+                for xx in range(Wb):
+                    src[yy, xx] = Xp[2 * yy, 2 * xx]
+            sb = src.reshape(-1).view(np.uint8)
+            want = np.zeros_like(raw)
+            for la in range(0, nbytes, 4):
+                pa = swz(la, 128)
+                want[pa:pa + 4] = sb[la:la + 4]
+            good = np.array_equal(raw, want)
+            print(f"{'PASS' if good else 'FAIL'} tma_strided_content")
+            RESULTS["tma_strided_content"] = bool(good)
+
+
 TESTS = {"tma": t_tma, "ki": t_kmajor_interleave, "sw128": lambda: t_kmajor_sw(128),
          "sw64": lambda: t_kmajor_sw(64), "sw32": lambda: t_kmajor_sw(32),
          "mni": t_mnmajor_interleave, "mnsw128": lambda: t_mnmajor_sw(128),
          "mnsw64": lambda: t_mnmajor_sw(64), "m64": t_m64, "rate": t_rate,
-         "mn32b": t_mn32b, "rate2": t_rate2, "tma32b": t_tma32b}
+         "mn32b": t_mn32b, "rate2": t_rate2, "tmastride": t_tma_strided, "tma32b": t_tma32b}
 
 if __name__ == "__main__":
     import os
