@@ -42,6 +42,13 @@ const char* vpx_last_error(void);
 const char* vpx_version(void);
 /* Total number of CUDA kernels this library has launched in this process. */
 long long vpx_launch_count(void);
+/* Numeric mode.  0 (default) = TF32: convolutions on tcgen05 tensor cores,
+ * activations/gradients stored rounded to nearest TF32 so the MMA operands
+ * are exact and the rounding unbiased (north-star tolerance rtol 1e-3).
+ * 1 = FP32: every conv pass on CUDA-core direct kernels in fp32, no rounding
+ * (the reference's own fp32 verify tolerance, rel 1e-5, reference cli.py:186). */
+int vpx_set_precision(int mode);
+int vpx_get_precision(void);
 
 /* ------------------------------------------------------------ convolution --
  * Frames are described by int[8] = {n, c, d, h, w, md, mh, mw}: interior extents

@@ -24,6 +24,7 @@ struct ConvRowParams {
   int out_off_d, out_off_h, out_off_w;       // output voxel o lands at frame index o + off
   int act;                                   // 1: fused LeakyReLU epilogue
   float slope;
+  int rnd;                                   // 1: round stores to nearest TF32
 };
 
 int num_sms();

@@ -8,6 +8,7 @@
 #include "conv_common.h"
 #include "conv_simt.h"
 #include "vpx_host.h"
+#include "vpx_round.cuh"
 
 namespace vpx {
 
@@ -56,11 +57,13 @@ __global__ void pack_rowwin_kernel(const float* __restrict__ w, int cout, int ci
       else
         v = w[((long long)i * cin + o) * 27 + (26 - tap)];
     }
-    out[idx] = v;
+    out[idx] = tf32_rn(v);
   }
 }
 
-static Frame to_frame(const int* f) { return Frame{f[0], f[1], f[2], f[3], f[4], f[5], f[6], f[7]}; }
+static Frame to_frame(const int* f) {
+  return Frame{f[0], f[1], f[2], f[3], f[4], f[5], f[6], f[7], precision() == 0 ? 1 : 0};
+}
 
 static int check_frame(const int* f, const char* what) {
   for (int i = 0; i < 5; ++i)
@@ -118,6 +121,7 @@ static int rowwin_run(const float* in, const Frame& inf, const float* wpack, int
   p.out_off_w = of.mw;
   p.act = act;
   p.slope = slope;
+  p.rnd = of.rnd;
   return launch_rowwin_any(map, p, cin_eff, cout_eff, st);
 }
 
@@ -165,13 +169,14 @@ extern "C" int vpx_conv3d_fwd_act(const float* x, const int* xfr, const float* w
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int cin = xf.c, cout = yf.c;
   int R, CG;
-  if (k == 3 && stride == 1 && yf.w % 128 == 0 && vpx::rowwin_config(cin, cout, &R, &CG)) {
+  const bool tc = vpx::precision() == 0;
+  if (tc && k == 3 && stride == 1 && yf.w % 128 == 0 && vpx::rowwin_config(cin, cout, &R, &CG)) {
     if (ws_bytes < vpx::packed_floats(cin, cout) * 4) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "workspace too small");
     float* wpack = static_cast<float*>(ws);
     if (int rc = vpx::pack(w, cout, cin, 0, wpack, st)) return rc;
     return vpx::rowwin_run(x, xf, wpack, cin, cout, y, yf, 0, yf.d, 0, yf.h, yf.w, st, act, slope);
   }
-  if (k == 3 && cin % 4 == 0 && vpx::tapbox_supported(cin, cout, 0)) {
+  if (tc && k == 3 && cin % 4 == 0 && vpx::tapbox_supported(cin, cout, 0)) {
     if (ws_bytes < vpx::tapbox_workspace_bytes(cin, cout)) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "workspace too small");
     return vpx::conv_tapbox(0, x, xf, w, cin, cout, stride, y, yf, act, slope, ws, st);
   }
@@ -197,7 +202,8 @@ extern "C" int vpx_conv3d_bwd_data(const float* u, const int* ufr, const float* 
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int cout = uf.c, cin = gf.c;
   int R, CG;
-  if (k == 3 && stride == 1 && gf.mw == 0 && gf.w % 128 == 0 &&
+  const bool tc = vpx::precision() == 0;
+  if (tc && k == 3 && stride == 1 && gf.mw == 0 && gf.w % 128 == 0 &&
       vpx::rowwin_config(cout, cin, &R, &CG)) {
     if (ws_bytes < vpx::packed_floats(cin, cout) * 4) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "workspace too small");
     float* wpack = static_cast<float*>(ws);
@@ -205,7 +211,7 @@ extern "C" int vpx_conv3d_bwd_data(const float* u, const int* ufr, const float* 
     return vpx::rowwin_run(u, uf, wpack, cout, cin, xg, gf, -gf.md, gf.d + gf.md, -gf.mh,
                            gf.h + gf.mh, gf.w, st);
   }
-  if (k == 3 && cout % 4 == 0 && vpx::tapbox_supported(cin, cout, 1)) {
+  if (tc && k == 3 && cout % 4 == 0 && vpx::tapbox_supported(cin, cout, 1)) {
     if (ws_bytes < vpx::tapbox_workspace_bytes(cin, cout)) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "workspace too small");
     return vpx::conv_tapbox(1, u, uf, w, cin, cout, stride, xg, gf, 0, 0.f, ws, st);
   }
@@ -227,7 +233,7 @@ extern "C" int vpx_conv3d_bwd_filter(const float* x, const int* xfr, const float
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   float* part = reinterpret_cast<float*>(static_cast<char*>(ws) +
                                          ((vpx::packed_floats(xf.c, uf.c) * 4 + 255) / 256) * 256);
-  if (k == 3 && stride == 1 && vpx::wgrad_tc_supported(xf, uf)) {
+  if (vpx::precision() == 0 && k == 3 && stride == 1 && vpx::wgrad_tc_supported(xf, uf)) {
     if (int rc = vpx::conv_wgrad_tc(x, xf, u, uf, part, st)) return rc;
     return vpx::reduce_partials(part, vpx::wgrad_tc_parts(xf, uf), (long long)uf.c * xf.c * 27, wg,
                                 accumulate, st);

@@ -21,6 +21,7 @@
 #include "conv_common.h"
 #include "vpx_host.h"
 #include "vpx_ptx.cuh"
+#include "vpx_round.cuh"
 
 namespace {
 
@@ -217,6 +218,10 @@ __global__ void __launch_bounds__(256, 1)
             if (p.act) {  // fused LeakyReLU (reference layers/reference.py:231-233)
 #pragma unroll
               for (int i = 0; i < 16; ++i) v[i] = v[i] >= 0.f ? v[i] : p.slope * v[i];
+            }
+            if (p.rnd) {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) v[i] = vpx::tf32_rn(v[i]);
             }
             float4* o4 = reinterpret_cast<float4*>(o + cb * 16);
 #pragma unroll

@@ -6,6 +6,7 @@
 // extent ceil(e/stride).  Tensors are NDHWC halo frames (see include/vpx.h).
 #include "conv_simt.h"
 #include "vpx_host.h"
+#include "vpx_round.cuh"
 
 namespace vpx {
 
@@ -63,7 +64,7 @@ __global__ void conv_fwd_simt_kernel(const float* __restrict__ x, Frame xf,
     }
     float* yp = y + fr_index(yf, n, oz, oy, ox) + CPT * c4;
 #pragma unroll
-    for (int j = 0; j < CPT; ++j) yp[j] = (act && acc[j] < 0.f) ? slope * acc[j] : acc[j];
+    for (int j = 0; j < CPT; ++j) yp[j] = rnd(yf, (act && acc[j] < 0.f) ? slope * acc[j] : acc[j]);
   }
 }
 
@@ -111,7 +112,7 @@ __global__ void conv_bwd_data_simt_kernel(const float* __restrict__ u, Frame uf,
         }
       }
     }
-    xg[idx] = acc;
+    xg[idx] = rnd(gf, acc);
   }
 }
 

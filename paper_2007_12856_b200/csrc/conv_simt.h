@@ -8,7 +8,13 @@ namespace vpx {
 // Allocation is [n][d+2md][h+2mh][w+2mw][c], contiguous.
 struct Frame {
   int n, c, d, h, w, md, mh, mw;
+  int rnd;  // 1: values stored into this frame are rounded to nearest TF32
 };
+
+// Numeric mode of the library (vpx_set_precision): 0 = TF32 tensor cores with
+// round-to-nearest TF32 storage of activations/gradients, 1 = FP32 everywhere
+// (CUDA-core direct kernels, no rounding; the strict-parity mode).
+int precision();
 
 int num_sms();
 int conv_fwd_simt(const float* x, const Frame& xf, const float* w, int k, int s, float* y,

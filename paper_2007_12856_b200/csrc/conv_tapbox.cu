@@ -16,6 +16,7 @@
 #include "conv_simt.h"
 #include "vpx_host.h"
 #include "vpx_ptx.cuh"
+#include "vpx_round.cuh"
 
 namespace vpx {
 
@@ -43,6 +44,7 @@ struct ConvTapParams {
   int pd_lo, pd_hi, ph_lo, ph_hi, pw_lo, pw_hi;  // valid output range (interior coords incl. margins)
   int act;
   float slope;
+  int rnd;
 };
 
 }  // namespace vpx
@@ -191,6 +193,7 @@ __global__ void __launch_bounds__(256, 1)
           for (int i = 0; i < 16; ++i) {
             if (empty_cls) v[i] = 0.f;
             if (p.act) v[i] = v[i] >= 0.f ? v[i] : p.slope * v[i];
+            if (p.rnd) v[i] = vpx::tf32_rn(v[i]);
           }
           float4* o4 = reinterpret_cast<float4*>(o + cb);
 #pragma unroll
@@ -241,7 +244,7 @@ __global__ void pack_tapbox_kernel(const float* __restrict__ w, int cout, int ci
     } else {
       if (i < cout) v = w[((long long)i * cin + o) * 27 + tap];
     }
-    out[idx] = v;
+    out[idx] = vpx::tf32_rn(v);
   }
 }
 
@@ -400,6 +403,7 @@ int conv_tapbox(int mode, const float* in, const Frame& inf, const float* w, int
   }
   p.act = act;
   p.slope = slope;
+  p.rnd = of.rnd;
   CUtensorMap xm, wm;
   if (int rc = encode_in_map(&xm, in, inf, Db, Hb, Wb, s_in)) return rc;
   if (int rc = encode_w_map(&wm, wpack, (long long)ne * ntot, NT)) return rc;

@@ -9,6 +9,7 @@
 // fixed block partition + fixed-order final sum, accumulated in fp64.
 #include "conv_simt.h"
 #include "ops_vec.h"
+#include "vpx_round.cuh"
 #include "vpx_host.h"
 
 namespace vpx {
@@ -58,7 +59,7 @@ __global__ void leaky_fwd_kernel(const float* __restrict__ x, Frame xf, float* _
     const int c = i % xf.c;
     const VoxIdx v = vox_decode(i / xf.c, xf);
     const float a = x[fr_off(xf, v.n, v.z, v.y, v.x) + c];
-    y[fr_off(yf, v.n, v.z, v.y, v.x) + c] = a >= 0.f ? a : slope * a;
+    y[fr_off(yf, v.n, v.z, v.y, v.x) + c] = rnd(yf, a >= 0.f ? a : slope * a);
   }
 }
 __global__ void leaky_bwd_kernel(const float* __restrict__ x, Frame xf, const float* __restrict__ u,
@@ -69,7 +70,7 @@ __global__ void leaky_bwd_kernel(const float* __restrict__ x, Frame xf, const fl
     const VoxIdx v = vox_decode(i / xf.c, xf);
     const float a = x[fr_off(xf, v.n, v.z, v.y, v.x) + c];
     const float b = u[fr_off(uf, v.n, v.z, v.y, v.x) + c];
-    g[fr_off(gf, v.n, v.z, v.y, v.x) + c] = a >= 0.f ? b : slope * b;
+    g[fr_off(gf, v.n, v.z, v.y, v.x) + c] = rnd(gf, a >= 0.f ? b : slope * b);
   }
 }
 
@@ -91,7 +92,7 @@ __global__ void pool_fwd_kernel(const float* __restrict__ x, Frame xf, float* __
       first = 0;
       sum += val;
     }
-    y[fr_off(yf, o.n, o.z, o.y, o.x) + c] = is_max ? best : sum / 8.0f;
+    y[fr_off(yf, o.n, o.z, o.y, o.x) + c] = rnd(yf, is_max ? best : sum / 8.0f);
   }
 }
 __global__ void pool_bwd_kernel(const float* __restrict__ x, Frame xf, const float* __restrict__ u,
@@ -117,7 +118,7 @@ __global__ void pool_bwd_kernel(const float* __restrict__ x, Frame xf, const flo
     for (int w8 = 0; w8 < 8; ++w8) {
       const int a = w8 >> 2, b = (w8 >> 1) & 1, cc = w8 & 1;
       g[fr_off(gf, o.n, 2 * o.z + a, 2 * o.y + b, 2 * o.x + cc) + c] =
-          is_max ? (w8 == arg ? uv : 0.f) : avg;
+          rnd(gf, is_max ? (w8 == arg ? uv : 0.f) : avg);
     }
   }
 }
@@ -186,7 +187,7 @@ __global__ void bn_apply_kernel(const float* __restrict__ x, Frame xf, const flo
     const int c = i % xf.c;
     const VoxIdx v = vox_decode(i / xf.c, xf);
     const float xh = (x[fr_off(xf, v.n, v.z, v.y, v.x) + c] - mean[c]) * inv[c];
-    y[fr_off(yf, v.n, v.z, v.y, v.x) + c] = gamma[c] * xh + beta[c];
+    y[fr_off(yf, v.n, v.z, v.y, v.x) + c] = rnd(yf, gamma[c] * xh + beta[c]);
   }
 }
 // dx = gamma*inv*(u - (sum_u + xhat*sum_uxhat)/count) (reference layers/reference.py:217-226)
@@ -203,7 +204,7 @@ __global__ void bn_bwd_apply_kernel(const float* __restrict__ x, Frame xf, const
     const float xh = (x[fr_off(xf, v.n, v.z, v.y, v.x) + c] - mean[c]) * inv[c];
     const float b = u[fr_off(uf, v.n, v.z, v.y, v.x) + c];
     g[fr_off(gf, v.n, v.z, v.y, v.x) + c] =
-        gamma[c] * inv[c] * (b - (sums[c] + xh * sums[C + c]) * inv_count);
+        rnd(gf, gamma[c] * inv[c] * (b - (sums[c] + xh * sums[C + c]) * inv_count));
   }
 }
 // mean/var from allreduced sums; running stats update (reference layers/reference.py:188-204)
@@ -230,7 +231,7 @@ __global__ void concat_kernel(const float* __restrict__ a, Frame af, const float
     const VoxIdx v = vox_decode(i / yf.c, yf);
     const float val = c < af.c ? a[fr_off(af, v.n, v.z, v.y, v.x) + c]
                                : b[fr_off(bf, v.n, v.z, v.y, v.x) + c - af.c];
-    y[fr_off(yf, v.n, v.z, v.y, v.x) + c] = val;
+    y[fr_off(yf, v.n, v.z, v.y, v.x) + c] = rnd(yf, val);
   }
 }
 // split gradient of a concat: ga (+)= u[:, :ca], gb (+)= u[:, ca:]
@@ -245,7 +246,7 @@ __global__ void split_kernel(const float* __restrict__ u, Frame uf, float* __res
       ga[fr_off(gaf, v.n, v.z, v.y, v.x) + c] = val;
     } else {
       float* p = gb + fr_off(gbf, v.n, v.z, v.y, v.x) + c - gaf.c;
-      *p = acc_b ? *p + val : val;
+      *p = rnd(gbf, acc_b ? *p + val : val);
     }
   }
 }
@@ -255,7 +256,8 @@ __global__ void add_kernel(const float* __restrict__ x, Frame xf, float* __restr
   GRID_STRIDE(i, total) {
     const int c = i % xf.c;
     const VoxIdx v = vox_decode(i / xf.c, xf);
-    y[fr_off(yf, v.n, v.z, v.y, v.x) + c] += x[fr_off(xf, v.n, v.z, v.y, v.x) + c];
+    float* q = y + fr_off(yf, v.n, v.z, v.y, v.x) + c;
+    *q = rnd(yf, *q + x[fr_off(xf, v.n, v.z, v.y, v.x) + c]);
   }
 }
 __global__ void copy_kernel(const float* __restrict__ x, Frame xf, float* __restrict__ y, Frame yf) {
@@ -279,7 +281,7 @@ __global__ void deconv_fwd_kernel(const float* __restrict__ x, Frame xf, const f
     const float* xp = x + fr_off(xf, o.n, o.z >> 1, o.y >> 1, o.x >> 1);
     float acc = 0.f;
     for (int ci = 0; ci < xf.c; ++ci) acc = fmaf(xp[ci], w[((long long)ci * yf.c + co) * 8 + k], acc);
-    y[fr_off(yf, o.n, o.z, o.y, o.x) + co] = acc;
+    y[fr_off(yf, o.n, o.z, o.y, o.x) + co] = rnd(yf, acc);
   }
 }
 __global__ void deconv_bwd_data_kernel(const float* __restrict__ u, Frame uf,
@@ -294,7 +296,7 @@ __global__ void deconv_bwd_data_kernel(const float* __restrict__ u, Frame uf,
       const float* up = u + fr_off(uf, p.n, 2 * p.z + a, 2 * p.y + b, 2 * p.x + c);
       for (int co = 0; co < uf.c; ++co) acc = fmaf(up[co], w[((long long)ci * uf.c + co) * 8 + k], acc);
     }
-    g[fr_off(gf, p.n, p.z, p.y, p.x) + ci] = acc;
+    g[fr_off(gf, p.n, p.z, p.y, p.x) + ci] = rnd(gf, acc);
   }
 }
 // wg[ci][co][k] partial over voxel chunks -> part[p][ci][co][k]
@@ -398,7 +400,7 @@ __global__ void prng_volume_kernel(uint64_t key, Frame f, long long counter_base
     const uint64_t r = sm_mix(key + (ctr + 1ULL) * 0x9E3779B97F4A7C15ULL);
     const double u01 = __dmul_rn(static_cast<double>(r >> 11), 1.1102230246251565e-16);
     const double v = __dadd_rn(lo, __dmul_rn(__dsub_rn(hi, lo), u01));
-    fr[fr_off(f, n, z, y, x) + c] = static_cast<float>(v);
+    fr[fr_off(f, n, z, y, x) + c] = rnd(f, static_cast<float>(v));
   }
 }
 
@@ -444,7 +446,7 @@ __global__ void xent_kernel(const float* __restrict__ logits, Frame lf, const lo
     float* gp = g + fr_off(gf, q.n, q.z, q.y, q.x);
     for (int k = 0; k < K; ++k) {
       const float pr = expf(lp[k] - mx - lse);
-      gp[k] = static_cast<float>((pr - (k == y ? 1.f : 0.f)) * inv_count);
+      gp[k] = rnd(gf, static_cast<float>((pr - (k == y ? 1.f : 0.f)) * inv_count));
     }
   }
   __shared__ double sh[256];
@@ -471,7 +473,7 @@ __global__ void ncdhw_to_frame_kernel(const float* __restrict__ src, Frame f, fl
     t /= f.d;
     const int c = t % f.c;
     const int n = t / f.c;
-    fr[fr_off(f, n, z, y, x) + c] = src[i];
+    fr[fr_off(f, n, z, y, x) + c] = rnd(f, src[i]);
   }
 }
 __global__ void frame_to_ncdhw_kernel(const float* __restrict__ fr, Frame f, float* __restrict__ dst) {
@@ -490,7 +492,9 @@ __global__ void frame_to_ncdhw_kernel(const float* __restrict__ fr, Frame f, flo
   }
 }
 
-static Frame F(const int* f) { return Frame{f[0], f[1], f[2], f[3], f[4], f[5], f[6], f[7]}; }
+static Frame F(const int* f) {
+  return Frame{f[0], f[1], f[2], f[3], f[4], f[5], f[6], f[7], precision() == 0 ? 1 : 0};
+}
 static long long VC(const Frame& f) { return (long long)f.n * f.d * f.h * f.w; }
 static cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
 

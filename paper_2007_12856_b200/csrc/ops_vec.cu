@@ -5,6 +5,7 @@
 // stores are 16-byte and coalesced.
 #include "conv_simt.h"
 #include "ops_vec.h"
+#include "vpx_round.cuh"
 #include "vpx_host.h"
 
 namespace vpx {
@@ -23,7 +24,9 @@ __device__ __forceinline__ long long row_base(const Frame& f, long long row) {
 }
 
 __device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
-__device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+__device__ __forceinline__ void st4(const Frame& f, float* p, float4 v) {
+  *reinterpret_cast<float4*>(p) = rnd4(f, v);
+}
 __device__ __forceinline__ float lk(float v, float s) { return v >= 0.f ? v : s * v; }
 
 #define ROW_LOOP(f)                                                                          \
@@ -37,7 +40,7 @@ __global__ void leaky_fwd_v(const float* __restrict__ x, Frame xf, float* __rest
     const long long row = i / per_row, off = 4 * (i % per_row);
     float4 v = ld4(x + row_base(xf, row) + off);
     v = make_float4(lk(v.x, s), lk(v.y, s), lk(v.z, s), lk(v.w, s));
-    st4(y + row_base(yf, row) + off, v);
+    st4(yf, y + row_base(yf, row) + off, v);
   }
 }
 
@@ -47,7 +50,7 @@ __global__ void leaky_bwd_v(const float* __restrict__ x, Frame xf, const float* 
     const long long row = i / per_row, off = 4 * (i % per_row);
     const float4 a = ld4(x + row_base(xf, row) + off);
     const float4 b = ld4(u + row_base(uf, row) + off);
-    st4(g + row_base(gf, row) + off, make_float4(a.x >= 0.f ? b.x : s * b.x, a.y >= 0.f ? b.y : s * b.y,
+    st4(gf, g + row_base(gf, row) + off, make_float4(a.x >= 0.f ? b.x : s * b.x, a.y >= 0.f ? b.y : s * b.y,
                                                  a.z >= 0.f ? b.z : s * b.z, a.w >= 0.f ? b.w : s * b.w));
   }
 }
@@ -89,7 +92,7 @@ __global__ void pool_fwd_v(const float* __restrict__ x, Frame xf, float* __restr
       sum.w += v.w;
     }
     if (!is_max) acc = make_float4(sum.x / 8.0f, sum.y / 8.0f, sum.z / 8.0f, sum.w / 8.0f);
-    st4(y + row_base(yf, orow) + 4 * off, acc);
+    st4(yf, y + row_base(yf, orow) + 4 * off, acc);
   }
 }
 
@@ -113,7 +116,7 @@ __global__ void pool_bwd_v(const float* __restrict__ x, Frame xf, const float* _
     if (!is_max) {
       const float4 gv = make_float4(uv.x / 8.0f, uv.y / 8.0f, uv.z / 8.0f, uv.w / 8.0f);
 #pragma unroll
-      for (int w8 = 0; w8 < 8; ++w8) st4(g + foff(gf, w8 >> 2, (w8 >> 1) & 1, w8 & 1), gv);
+      for (int w8 = 0; w8 < 8; ++w8) st4(gf, g + foff(gf, w8 >> 2, (w8 >> 1) & 1, w8 & 1), gv);
     } else {
       float4 best = ld4(x + foff(xf, 0, 0, 0));
       int ax = 0, ay = 0, az = 0, aw = 0;
@@ -127,7 +130,7 @@ __global__ void pool_bwd_v(const float* __restrict__ x, Frame xf, const float* _
       }
 #pragma unroll
       for (int w8 = 0; w8 < 8; ++w8)
-        st4(g + foff(gf, w8 >> 2, (w8 >> 1) & 1, w8 & 1),
+        st4(gf, g + foff(gf, w8 >> 2, (w8 >> 1) & 1, w8 & 1),
             make_float4(w8 == ax ? uv.x : 0.f, w8 == ay ? uv.y : 0.f, w8 == az ? uv.z : 0.f, w8 == aw ? uv.w : 0.f));
     }
   }
@@ -144,7 +147,7 @@ __global__ void bn_apply_v(const float* __restrict__ x, Frame xf, const float* _
     float r[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
     for (int j = 0; j < 4; ++j) r[j] = gamma[c + j] * ((r[j] - mean[c + j]) * inv[c + j]) + beta[c + j];
-    st4(y + row_base(yf, row) + off, make_float4(r[0], r[1], r[2], r[3]));
+    st4(yf, y + row_base(yf, row) + off, make_float4(r[0], r[1], r[2], r[3]));
   }
 }
 
@@ -165,7 +168,7 @@ __global__ void bn_bwd_apply_v(const float* __restrict__ x, Frame xf, const floa
       const float xh = (av[j] - mean[c + j]) * inv[c + j];
       r[j] = gamma[c + j] * inv[c + j] * (bv[j] - (sums[c + j] + xh * sums[C + c + j]) * inv_count);
     }
-    st4(g + row_base(gf, row) + off, make_float4(r[0], r[1], r[2], r[3]));
+    st4(gf, g + row_base(gf, row) + off, make_float4(r[0], r[1], r[2], r[3]));
   }
 }
 

@@ -16,6 +16,7 @@
 namespace vpx {
 
 void set_error(const char* fmt, ...);
+int precision();
 // Number of kernels this library has launched (vpx_launch_count()).
 extern std::atomic<long long> g_launches;
 
