@@ -25,6 +25,20 @@ def rel(got, ref):
     return float(np.max(np.abs(np.asarray(got, np.float64) - ref)) / max(np.max(np.abs(ref)), 1e-30))
 
 
+def rel_l2(got, ref):
+    ref = np.asarray(ref, dtype=np.float64)
+    return float(np.linalg.norm(np.asarray(got, np.float64) - ref) / max(np.linalg.norm(ref), 1e-300))
+
+
+# TF32 tolerances (stated in DESIGN.md "Parity"): forward activations and loss
+# in the reference's max-abs metric; gradients in relative L2, because a
+# LeakyReLU whose TF32 pre-activation lands on the other side of zero than the
+# fp32 one switches its gradient between u and 0.3u at that voxel, an O(1)
+# local difference the max-abs metric reports in full.  FP32 mode is held to
+# the reference's own fp32 tolerance (1e-5) on every tensor in max-abs.
+TF32 = {"fwd": 2e-3, "loss": 1e-3, "bwd_l2": 2e-2, "grad_l2": 1e-2}
+
+
 def _to_np(v):
     if isinstance(v, DistTensor):
         return v.numpy()
@@ -85,20 +99,14 @@ def test_train_step_matches_oracle(which, precision):
     for key, ref in trace_o.items():
         got = trace.get(key)
         assert got is not None, key
-        report.append((key, rel(_to_np(got), ref)))
+        g = _to_np(got)
+        report.append((key, rel(g, ref), rel_l2(g, ref)))
     for name, g in grads_o.items():
-        report.append((("grad", name), rel(grads[name].cpu().numpy(), g)))
+        d = grads[name].cpu().numpy()
+        report.append((("grad", name), rel(d, g), rel_l2(d, g)))
     print(f"\n[{which} {precision}] loss dev {float(loss.item())!r} oracle {loss_o!r}")
-    print("\n".join(f"{k}: {e:.2e}" for k, e in report))
-    if precision == "fp32":
-        assert abs(float(loss.item()) - loss_o) <= 1e-5 * abs(loss_o)
-        for key, e in report:
-            assert e < 1e-5, (key, e)
-    else:
-        assert abs(float(loss.item()) - loss_o) <= 1e-3 * abs(loss_o)
-        for key, e in report:
-            if key[0] == "fwd":
-                assert e < RTOL["fwd"], (key, e)
+    print("\n".join(f"{k}: maxabs {e:.2e} l2 {e2:.2e}" for k, e, e2 in report))
+    _check(precision, loss, loss_o, report)
     # Adam's first step moves every parameter by ~lr*sign(g): a parameter whose
     # gradient sits at the noise floor may flip sign (|dp| <= 2 lr); anything
     # else must agree closely and flips must be rare.
@@ -106,6 +114,22 @@ def test_train_step_matches_oracle(which, precision):
         d = np.abs(state.params.views[name].cpu().numpy().astype(np.float64) - p)
         assert d.max() <= 2.0 * lr * 1.001, name
         assert np.mean(d > 1e-2 * lr) < 0.02, (name, float(np.mean(d > 1e-2 * lr)))
+
+
+def _check(precision, loss, loss_o, report):
+    if precision == "fp32":
+        assert abs(float(loss.item()) - loss_o) <= 1e-5 * abs(loss_o)
+        for key, e, _ in report:
+            assert e < 1e-5, (key, e)
+        return
+    assert abs(float(loss.item()) - loss_o) <= TF32["loss"] * abs(loss_o)
+    for key, e, e2 in report:
+        if key[0] == "fwd":
+            assert e < TF32["fwd"], (key, e)
+        elif key[0] == "bwd":
+            assert e2 < TF32["bwd_l2"], (key, e2)
+        else:
+            assert e2 < TF32["grad_l2"], (key, e2)
 
 
 def test_fused_step_equals_traced_step():
@@ -124,7 +148,9 @@ def test_fused_step_equals_traced_step():
         loss, dpred = engine.loss_and_grad(ctx, plan, pred, batch)
         engine.backward(ctx, plan, state, stash, dpred, trace=trace)
         grads.append(state.params.grad.clone())
-    assert torch.equal(grads[0], grads[1])
+    # fused epilogue rounds leaky(conv) once; the unfused path rounds conv and
+    # then leaky(conv): activations differ by one TF32 rounding at most
+    assert rel_l2(grads[1].cpu().numpy(), grads[0].cpu().numpy()) < 1e-3
 
 
 def test_cosmoflow128_traces_vs_oracle():
@@ -132,12 +158,11 @@ def test_cosmoflow128_traces_vs_oracle():
     and filter-gradient kernels inside the full step, n=1."""
     net, wi = build_cosmoflow(128), 128
     loss, loss_o, trace, trace_o, grads, grads_o, state, po = _run(net, wi, 1)
-    report = [(k, rel(_to_np(trace[k]), v)) for k, v in trace_o.items()]
-    report += [(("grad", k), rel(grads[k].cpu().numpy(), g)) for k, g in grads_o.items()]
-    print("\n".join(f"{k}: {e:.2e}" for k, e in report))
-    assert abs(float(loss.item()) - loss_o) <= 1e-3 * abs(loss_o)
-    for key, e in report:
-        assert e < (RTOL["fwd"] if key[0] == "fwd" else RTOL["bwd"]), (key, e)
+    report = [(k, rel(_to_np(trace[k]), v), rel_l2(_to_np(trace[k]), v)) for k, v in trace_o.items()]
+    report += [(("grad", k), rel(grads[k].cpu().numpy(), g), rel_l2(grads[k].cpu().numpy(), g))
+               for k, g in grads_o.items()]
+    print("\n".join(f"{k}: maxabs {e:.2e} l2 {e2:.2e}" for k, e, e2 in report))
+    _check("tf32", loss, loss_o, report)
 
 
 def test_cosmoflow64_loss_matches_reference_value(golden):

@@ -158,7 +158,26 @@ def _frame_of(a):
     return Frame(a.shape[0], a.shape[1], *a.shape[2:]).load_ncdhw(a.astype(np.float32))
 
 
-def test_pool_leaky_bn_deconv_vs_oracle(golden):
+@pytest.fixture
+def fp32_mode():
+    import paper_2007_12856_b200 as pkg
+
+    pkg.set_precision("fp32")
+    yield
+    pkg.set_precision("tf32")
+
+
+def test_tf32_storage_rounds_to_nearest():
+    """In TF32 mode every stored activation is the nearest TF32 value (low 13
+    mantissa bits zero, round-to-nearest), so the tensor core sees it exactly."""
+    x = np.random.default_rng(4).standard_normal((1, 8, 2, 4, 4)).astype(np.float32)
+    f = _frame_of(x)
+    got = f.to_ncdhw().cpu().numpy()
+    assert np.all(got.view(np.uint32) & np.uint32(0x1FFF) == 0)
+    assert np.max(np.abs(got - x) / np.abs(x)) <= 2.0 ** -11
+
+
+def test_pool_leaky_bn_deconv_vs_oracle(golden, fp32_mode):
     A = np.load(golden / "layers.npz")
     x = A["pool_x"].astype(np.float32)
     xf = _frame_of(x)
