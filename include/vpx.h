@@ -85,6 +85,17 @@ int vpx_conv3d_bwd_filter(const float* x, const int* xfr, const float* u, const 
                           int stride, float* wg, int accumulate, void* ws, long long ws_bytes,
                           void* stream);
 
+/* First-layer fast path (Cin = 4, Cout = 16, the CosmoFlow c1 block):
+ * vpx_pool_leaky_bwd_blocked fuses the 2^3 pool backward and the LeakyReLU
+ * backward (y = LeakyReLU output = pool input) and writes the conv-output
+ * gradient in the 4-channel-blocked layout [C/4][n][d][h][w][4];
+ * vpx_conv3d_bwd_filter_c4 computes the filter gradient from it on tcgen05.
+ * ufr describes the logical (unblocked) gradient: {n, 16, d, h, w, 0, 0, 0}. */
+int vpx_pool_leaky_bwd_blocked(const float* y, const int* yf, const float* up, const int* upf, float* gb,
+                               float slope, int is_max, void* stream);
+int vpx_conv3d_bwd_filter_c4(const float* x, const int* xfr, const float* ub, const int* ufr, float* wg,
+                             int accumulate, void* ws, long long ws_bytes, void* stream);
+
 /* ------------------------------------------------------- pointwise / pool --
  * reference layers/reference.py:149-236, layers/distributed.py:132-214.
  * All read/write frame interiors; is_max selects max (ties -> lowest index in

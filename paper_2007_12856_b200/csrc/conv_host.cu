@@ -7,6 +7,7 @@
 // host NCDHW arrays, explicit workspace instead of internal allocation.
 #include "conv_common.h"
 #include "conv_simt.h"
+#include "ops_vec.h"
 #include "vpx_host.h"
 #include "vpx_round.cuh"
 
@@ -239,4 +240,28 @@ extern "C" int vpx_conv3d_bwd_filter(const float* x, const int* xfr, const float
                                 accumulate, st);
   }
   return vpx::conv_wgrad_simt(x, xf, u, uf, k, stride, wg, accumulate, part, st);
+}
+
+extern "C" int vpx_pool_leaky_bwd_blocked(const float* y, const int* yfr, const float* up, const int* upfr,
+                                          float* gb, float slope, int is_max, void* stream) {
+  Frame yf = vpx::to_frame(yfr), uf = vpx::to_frame(upfr);
+  if (yf.c % 4 || uf.c != yf.c || uf.d * 2 != yf.d || uf.h * 2 != yf.h || uf.w * 2 != yf.w)
+    VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "pool/leaky blocked backward: extents");
+  return vpx::pool_leaky_bwd_blocked(y, yf, up, uf, gb, slope, is_max, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int vpx_conv3d_bwd_filter_c4(const float* x, const int* xfr, const float* ub, const int* ufr,
+                                        float* wg, int accumulate, void* ws, long long ws_bytes,
+                                        void* stream) {
+  Frame xf = vpx::to_frame(xfr), uf = vpx::to_frame(ufr);
+  if (!vpx::wgrad_c4_supported(xf, uf)) VPX_FAIL(VPX_ERR_UNSUPPORTED, "blocked c4 filter gradient: shape");
+  if (uf.n != xf.n || uf.d != xf.d || uf.h != xf.h || uf.w != xf.w)
+    VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "blocked c4 filter gradient: extents");
+  const int P = vpx::wgrad_c4_parts(uf);
+  const long long need = (long long)P * uf.c * 4 * 27 * 4;
+  if (ws_bytes < need) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "workspace too small");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  float* part = static_cast<float*>(ws);
+  if (int rc = vpx::conv_wgrad_c4(x, xf, ub, uf, part, st)) return rc;
+  return vpx::reduce_partials(part, P, (long long)uf.c * 4 * 27, wg, accumulate, st);
 }

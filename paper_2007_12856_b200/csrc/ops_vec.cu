@@ -218,3 +218,67 @@ int bn_bwd_apply_vec(const float* x, const Frame& xf, const float* u, const Fram
 }
 
 }  // namespace vpx
+
+// Fused 2^3 pool backward + LeakyReLU backward of the first conv block,
+// writing the conv-output gradient in the 4-channel-blocked layout
+// [C/4][n][d][h][w][4] that conv_wgrad_c4.cu consumes.  y is the LeakyReLU
+// output (= pool input; its sign is the pre-activation's sign), up the pooled
+// gradient.  Saves the full-resolution pool-backward tensor (write + read).
+namespace vpx {
+namespace {
+__global__ void pool_leaky_bwd_blocked_v(const float* __restrict__ y, Frame yf, const float* __restrict__ up,
+                                         Frame uf, float* __restrict__ gb, float s, int is_max) {
+  const int C = uf.c;
+  const long long vox_full = (long long)yf.n * yf.d * yf.h * yf.w;
+  ROW_LOOP(uf) {
+    const long long orow = i / per_row, off = i % per_row;
+    const int xo = static_cast<int>(off / (C / 4)), c4 = static_cast<int>(off % (C / 4));
+    long long t = orow;
+    const int yo = t % uf.h;
+    t /= uf.h;
+    const int zo = t % uf.d;
+    const int n = static_cast<int>(t / uf.d);
+    const float4 uv = ld4(up + row_base(uf, orow) + 4 * off);
+    float4 vals[8];
+#pragma unroll
+    for (int w8 = 0; w8 < 8; ++w8) {
+      const int a = w8 >> 2, b = (w8 >> 1) & 1, cc = w8 & 1;
+      vals[w8] = ld4(y + ((((long long)n * (yf.d + 2 * yf.md) + (2 * zo + a + yf.md)) * (yf.h + 2 * yf.mh) +
+                           (2 * yo + b + yf.mh)) * (yf.w + 2 * yf.mw) + (2 * xo + cc + yf.mw)) * C + 4 * c4);
+    }
+    int ax = 0, ay = 0, az = 0, aw = 0;
+    if (is_max) {
+      float4 best = vals[0];
+#pragma unroll
+      for (int w8 = 1; w8 < 8; ++w8) {
+        if (vals[w8].x > best.x) { best.x = vals[w8].x; ax = w8; }
+        if (vals[w8].y > best.y) { best.y = vals[w8].y; ay = w8; }
+        if (vals[w8].z > best.z) { best.z = vals[w8].z; az = w8; }
+        if (vals[w8].w > best.w) { best.w = vals[w8].w; aw = w8; }
+      }
+    }
+    const float4 avg = make_float4(uv.x / 8.0f, uv.y / 8.0f, uv.z / 8.0f, uv.w / 8.0f);
+#pragma unroll
+    for (int w8 = 0; w8 < 8; ++w8) {
+      const int a = w8 >> 2, b = (w8 >> 1) & 1, cc = w8 & 1;
+      float4 g = is_max ? make_float4(w8 == ax ? uv.x : 0.f, w8 == ay ? uv.y : 0.f, w8 == az ? uv.z : 0.f,
+                                      w8 == aw ? uv.w : 0.f)
+                        : avg;
+      const float4 v = vals[w8];
+      g = make_float4(v.x >= 0.f ? g.x : s * g.x, v.y >= 0.f ? g.y : s * g.y, v.z >= 0.f ? g.z : s * g.z,
+                      v.w >= 0.f ? g.w : s * g.w);
+      const long long vox = (((long long)n * yf.d + 2 * zo + a) * yf.h + 2 * yo + b) * yf.w + 2 * xo + cc;
+      float* dst = gb + ((long long)c4 * vox_full + vox) * 4;
+      *reinterpret_cast<float4*>(dst) = rnd4(yf, g);
+    }
+  }
+}
+}  // namespace
+
+int pool_leaky_bwd_blocked(const float* y, const Frame& yf, const float* up, const Frame& uf, float* gb,
+                           float s, int is_max, cudaStream_t st) {
+  pool_leaky_bwd_blocked_v<<<grid_v(uf), 256, 0, st>>>(y, yf, up, uf, gb, s, is_max);
+  VPX_LAUNCH_CHECK();
+  return VPX_OK;
+}
+}  // namespace vpx

@@ -417,9 +417,22 @@ def backward(ctx: RankCtx, plan: Plan, state: RankState, stash, dpred, trace: di
     P, G, bn = state.params.views, state.params.grads, state.bn_states
     u = dpred
     extra = {}
+    skip_below = None
     for i in range(len(net.layers) - 1, -1, -1):
         layer = net.layers[i]
         kept = stash[i]
+        if skip_below is not None and i >= skip_below:
+            continue
+        if (trace is None and u is not None and layer.kind == "pool" and i == 2
+                and D.first_block_fast_path(net.layers[0], net.layers[1], kept, u, plan.in_meta[0])):
+            # conv(Cin=4) -> leaky -> pool: fused pool/leaky backward in the
+            # blocked layout + the dense c1 filter-gradient kernel; nothing
+            # consumes the network input's gradient
+            D.first_block_wgrad(ctx, stash[0], kept, u, net.layers[1].slope, layer.pool_kind,
+                                G[f"{net.layers[0].name}.w"], tag=net.layers[0].name)
+            u = None
+            skip_below = 0
+            continue
         if plan.placement[i] == "flat":
             if layer.kind == "flatten":
                 if u is not None:

@@ -393,3 +393,35 @@ def redistribute(ctx: RankCtx, x, src_meta: DistTensorMeta, dst_meta: DistTensor
     for dbox, buf in unpacks:
         copy_box(out, dbox, buf, 1)
     return out
+
+
+# ------------------------------------------------- first-block fast path
+
+def first_block_fast_path(conv, act, y: DistTensor, u: DistTensor, x_meta) -> bool:
+    """True when the first conv block (Cin=4 -> 16, LeakyReLU, 2^3 pool) can
+    take the fused backward: blocked pool/leaky backward + dense c1 wgrad."""
+    if conv.kind != "conv" or act.kind != "leaky" or conv.params.cin != 4 or conv.params.cout != 16:
+        return False
+    if tuple(conv.params.kernel) != (3, 3, 3) or tuple(conv.params.stride) != (1, 1, 1):
+        return False
+    return y.m == (0, 0, 0) and u.m == (0, 0, 0) and y.w in (64, 128, 256, 512) and x_meta.margins()[2] == 0
+
+
+def first_block_wgrad(ctx: RankCtx, x: DistTensor, y: DistTensor, u_pool: DistTensor, slope: float,
+                      pool_kind: str, out: torch.Tensor, tag: str = "c1"):
+    """c1 filter gradient straight from the pooled gradient (see
+    vpx_pool_leaky_bwd_blocked / vpx_conv3d_bwd_filter_c4 in include/vpx.h)."""
+    nvox = y.voxels()
+    gb = WS2.get(nvox * y.c * 4)
+    with region(f"{tag}_act.bwd", 0, 4 * (u_pool.voxels() * u_pool.c + 2 * nvox * y.c)):
+        _lib.call("vpx_pool_leaky_bwd_blocked", y.ptr, y.desc, u_pool.ptr, u_pool.desc, gb.data_ptr(),
+                  float(slope), int(pool_kind == "max"), stream_ptr())
+    ufr = frame_desc(y.n, y.c, y.d, y.h, y.w)
+    ws = WS.get(_lib.load().vpx_conv3d_workspace_bytes(x.c, y.c, 3, ctypes.addressof(ufr)))
+    with region(f"{tag}.wgrad", 2 * 27 * x.c * y.c * nvox, 4 * (x.voxels() * x.c + nvox * y.c + out.numel())):
+        _lib.call("vpx_conv3d_bwd_filter_c4", x.ptr, x.desc, gb.data_ptr(), ctypes.addressof(ufr), out.data_ptr(),
+                  0, ws.data_ptr(), ws.numel() * 4, stream_ptr())
+    return out
+
+
+WS2 = Workspace()

@@ -65,6 +65,35 @@ CASES = [
 ]
 
 
+@pytest.mark.parametrize("shape,margins", [((1, 3, 5, 64), (0, 0, 0)), ((2, 4, 3, 128), (1, 0, 0)),
+                                           ((1, 2, 4, 512), (1, 1, 0))])
+def test_first_block_fused_backward_and_c4_wgrad(shape, margins):
+    """c1 fast path: pooled gradient -> (pool bwd + leaky bwd, blocked layout)
+    -> dense Cin=4 filter gradient, against the oracle composition."""
+    n, d, h, w = shape
+    rng = np.random.default_rng(21)
+    x = rng.uniform(-1, 1, (n, 4, d, h, w)).astype(np.float32)
+    y = rng.uniform(-1, 1, (n, 16, d, h, w)).astype(np.float32)   # leaky output (= pool input)
+    up = rng.uniform(-1, 1, (n, 16, d // 2, h // 2, w // 2)).astype(np.float32)
+    xf = Frame(n, 4, d, h, w, margins, zero=True).load_ncdhw(x)
+    yf, uf = _frame_of(y), _frame_of(up)
+    gb = torch.empty(4 * n * d * h * w * 4, device="cuda")
+    _lib.call("vpx_pool_leaky_bwd_blocked", yf.ptr, yf.desc, uf.ptr, uf.desc, gb.data_ptr(), 0.3, 0, stream_ptr())
+    yr = yf.to_ncdhw().cpu().numpy()  # as stored (TF32-rounded)
+    g_ref = O.leaky_bwd(yr, O.pool3d_bwd(yr, uf.to_ncdhw().cpu().numpy(), "average"), 0.3)
+    got = gb.view(4, n, d, h, w, 4).permute(1, 0, 5, 2, 3, 4).reshape(n, 16, d, h, w).cpu().numpy()
+    assert rel(got, g_ref) < 1e-3
+    wg = torch.zeros(16, 4, 3, 3, 3, device="cuda")
+    from paper_2007_12856_b200.frames import frame_desc
+
+    ufr = frame_desc(n, 16, d, h, w)
+    W = ws(4, 16, 3, Frame(n, 16, d, h, w))
+    _lib.call("vpx_conv3d_bwd_filter_c4", xf.ptr, xf.desc, gb.data_ptr(), ctypes.addressof(ufr), wg.data_ptr(), 0,
+              W.data_ptr(), W.numel() * 4, stream_ptr())
+    wg_ref = O.conv3d_bwd_filter(xf.to_ncdhw().cpu().numpy(), got, (3, 3, 3), (1, 1, 1))
+    assert rel(wg.cpu().numpy(), wg_ref) < TF32_RTOL
+
+
 def test_tapbox_dgrad_all_margins():
     """W-partitioned frames (margins in all three dims) go through the tap-box
     kernel for both passes."""

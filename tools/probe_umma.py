@@ -446,11 +446,49 @@ def t_tma_strided():
             RESULTS["tma_strided_content"] = bool(good)
 
 
+def t_tma_narrow_swz():
+    """box {4 ch, 64 voxels} with SWIZZLE_128B_ATOM_32B: 16-byte voxels land at
+    swz32b(16*v), i.e. the swizzle is a pure smem-address transform."""
+    C, W = 4, 80
+    X = rng.standard_normal((1, 1, 1, W, C)).astype(np.float32)
+    g = torch.from_numpy(X).cuda()
+    dims = (ctypes.c_uint64 * 5)(C, W, 1, 1, 1)
+    strides = (ctypes.c_uint64 * 4)(C * 4, W * C * 4, W * C * 4, W * C * 4)
+    for box_w, x0 in ((64, 0), (72, -8)):
+        box = (ctypes.c_uint32 * 5)(4, box_w, 1, 1, 1)
+        coords = (ctypes.c_int32 * 5)(0, x0, 0, 0, 0)
+        nbytes = box_w * 16
+        out = torch.zeros(nbytes // 4, dtype=torch.float32, device="cuda")
+        ok = torch.zeros(1, dtype=torch.int32, device="cuda")
+        _lib.call("vpx_probe_tma", g.data_ptr(), ctypes.addressof(dims), ctypes.addressof(strides),
+                  ctypes.addressof(box), ctypes.addressof(ONES), 1282, ctypes.addressof(coords), out.data_ptr(),
+                  nbytes, ok.data_ptr(), torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        raw = out.cpu().numpy().view(np.uint8)
+        Xp = np.zeros((W + 16, C), np.float32)
+        Xp[8:8 + W] = X[0, 0, 0]
+        src = Xp[8 + x0: 8 + x0 + box_w].reshape(-1).view(np.uint8)
+        want = np.zeros_like(raw)
+        for la in range(0, nbytes, 4):
+            pa = swz32b(la)
+            want[pa:pa + 4] = src[la:la + 4]
+        good = int(ok.item()) == 1 and np.array_equal(raw, want)
+        print(f"{'PASS' if good else 'FAIL'} tma_narrow_swz32b box_w={box_w} x0={x0} ok={int(ok.item())}")
+        got = out.cpu().numpy().reshape(-1, 4)
+        vox = Xp[8 + x0: 8 + x0 + box_w]
+        where = []
+        for ch in range(min(len(got), 40)):
+            hit = [v for v in range(box_w) if np.array_equal(got[ch], vox[v])]
+            where.append(hit[0] if hit else -1)
+        print("smem 16B chunk -> voxel:", where)
+        RESULTS[f"tma_narrow_{box_w}"] = bool(good)
+
+
 TESTS = {"tma": t_tma, "ki": t_kmajor_interleave, "sw128": lambda: t_kmajor_sw(128),
          "sw64": lambda: t_kmajor_sw(64), "sw32": lambda: t_kmajor_sw(32),
          "mni": t_mnmajor_interleave, "mnsw128": lambda: t_mnmajor_sw(128),
          "mnsw64": lambda: t_mnmajor_sw(64), "m64": t_m64, "rate": t_rate,
-         "mn32b": t_mn32b, "rate2": t_rate2, "tmastride": t_tma_strided, "tma32b": t_tma32b}
+         "mn32b": t_mn32b, "rate2": t_rate2, "tmastride": t_tma_strided, "tmanarrow": t_tma_narrow_swz, "tma32b": t_tma32b}
 
 if __name__ == "__main__":
     import os
