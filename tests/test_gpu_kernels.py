@@ -65,7 +65,7 @@ CASES = [
 ]
 
 
-@pytest.mark.parametrize("shape,margins", [((1, 3, 5, 64), (0, 0, 0)), ((2, 4, 3, 128), (1, 0, 0)),
+@pytest.mark.parametrize("shape,margins", [((1, 4, 6, 64), (0, 0, 0)), ((2, 4, 2, 128), (1, 0, 0)),
                                            ((1, 2, 4, 512), (1, 1, 0))])
 def test_first_block_fused_backward_and_c4_wgrad(shape, margins):
     """c1 fast path: pooled gradient -> (pool bwd + leaky bwd, blocked layout)
