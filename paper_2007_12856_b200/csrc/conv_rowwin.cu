@@ -49,9 +49,17 @@ __host__ __device__ constexpr int pow2_cols(int c) {
   return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512;
 }
 
+// Epilogue staging for coalesced stores (COUT <= 32): 4 warps x 32 voxels x
+// (COUT + 4) floats, padded so the per-lane 16-byte stores are conflict free.
+template <int COUT>
+__host__ __device__ constexpr int epi_bytes() {
+  return COUT <= 32 ? 4 * 32 * (COUT + 4) * 4 : 0;
+}
+
 template <int COUT, int R, int CG, bool PAIR, int S>
 __global__ void __launch_bounds__(256, 1)
     conv_rowwin_kernel(const __grid_constant__ CUtensorMap xmap, const ConvRowParams p) {
+  constexpr bool kStaged = epi_bytes<COUT>() > 0;
   constexpr int PLANE = plane_bytes<R>();
   constexpr int ABYTES = CG * PLANE;
   constexpr int BBYTES = b_bytes<COUT, CG, PAIR>();
@@ -189,6 +197,7 @@ __global__ void __launch_bounds__(256, 1)
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
     const int q = warp - 4;  // TMEM lane quarter
+    float* stg = reinterpret_cast<float*>(smem + S * STAGE) + q * 32 * (COUT + 4);
     int acc = 0;
     uint32_t aphase = 0;
     for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
@@ -206,6 +215,8 @@ __global__ void __launch_bounds__(256, 1)
       float* orow = p.out + static_cast<long long>(n) * p.out_sn +
                     static_cast<long long>(z + p.out_off_d) * p.out_sd +
                     static_cast<long long>(x + p.out_off_w) * p.out_sw;
+      // warp's first voxel of the row segment (for the coalesced write-out)
+      float* orow_w = orow - static_cast<long long>(lane) * p.out_sw;
 #pragma unroll 1
       for (int r = 0; r < R; ++r) {
         const int y = y0 + r;
@@ -214,19 +225,40 @@ __global__ void __launch_bounds__(256, 1)
         for (int cb = 0; cb < COUT / 16; ++cb) {
           float v[16];
           vpx::tmem_ld16(tbase + (static_cast<uint32_t>(q * 32) << 16) + acc * ACC + r * COUT + cb * 16, v);
-          if (y < p.yhi) {
-            if (p.act) {  // fused LeakyReLU (reference layers/reference.py:231-233)
+          if (p.act) {  // fused LeakyReLU (reference layers/reference.py:231-233)
 #pragma unroll
-              for (int i = 0; i < 16; ++i) v[i] = v[i] >= 0.f ? v[i] : p.slope * v[i];
-            }
-            if (p.rnd) {
+            for (int i = 0; i < 16; ++i) v[i] = v[i] >= 0.f ? v[i] : p.slope * v[i];
+          }
+          if (p.rnd) {
 #pragma unroll
-              for (int i = 0; i < 16; ++i) v[i] = vpx::tf32_rn(v[i]);
-            }
+            for (int i = 0; i < 16; ++i) v[i] = vpx::tf32_rn(v[i]);
+          }
+          if constexpr (kStaged) {
+            // this lane's voxel row -> padded smem (conflict-free 16-byte stores)
+            float4* s4 = reinterpret_cast<float4*>(stg + lane * (COUT + 4) + cb * 16);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) s4[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+          } else if (y < p.yhi) {
             float4* o4 = reinterpret_cast<float4*>(o + cb * 16);
 #pragma unroll
             for (int i = 0; i < 4; ++i) o4[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
           }
+        }
+        if constexpr (kStaged) {
+          // 32 voxels x COUT channels are contiguous in global memory: write
+          // them out as consecutive 16-byte chunks (fully coalesced)
+          __syncwarp();
+          if (y < p.yhi) {
+            float* ow = orow_w + static_cast<long long>(y + p.out_off_h) * p.out_sh;
+            constexpr int Q = COUT / 4;  // float4 chunks per voxel
+#pragma unroll
+            for (int k = 0; k < Q; ++k) {
+              const int c = k * 32 + lane, vx = c / Q, qq = c % Q;
+              const float4 val = *reinterpret_cast<const float4*>(stg + vx * (COUT + 4) + qq * 4);
+              *reinterpret_cast<float4*>(ow + static_cast<long long>(vx) * p.out_sw + qq * 4) = val;
+            }
+          }
+          __syncwarp();
         }
       }
       vpx::tc_fence_before();
@@ -243,10 +275,10 @@ __global__ void __launch_bounds__(256, 1)
 template <int COUT, int R, int CG, bool PAIR>
 int launch_rowwin(const CUtensorMap& xmap, const ConvRowParams& p, cudaStream_t st) {
   constexpr int STAGE = stage_bytes<COUT, R, CG, PAIR>();
-  constexpr int BUDGET = 220 * 1024;
+  constexpr int BUDGET = 226 * 1024 - epi_bytes<COUT>();
   constexpr int S = (BUDGET - 1024) / STAGE >= 4 ? 4 : (BUDGET - 1024) / STAGE;
   static_assert(S >= 2, "stage too large");
-  constexpr int SMEM = S * STAGE + 1024;
+  constexpr int SMEM = S * STAGE + epi_bytes<COUT>() + 1024;
   auto kern = conv_rowwin_kernel<COUT, R, CG, PAIR, S>;
   VPX_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
   int grid = p.num_tiles < vpx::num_sms() ? p.num_tiles : vpx::num_sms();
