@@ -33,6 +33,7 @@ import torch.distributed as dist
 from . import _lib
 from .errors import OutOfBounds
 from .geometry import round_boxes
+from .timing import region
 
 
 class RankCtx:
@@ -94,8 +95,10 @@ class RankCtx:
             return
         p2p = [dist.P2POp(dist.isend if kind == "send" else dist.irecv, t, peer)
                for kind, peer, t in ops]
-        for req in dist.batch_isend_irecv(p2p):
-            req.wait()
+        nbytes = sum(4 * t.numel() for kind, _, t in ops if kind == "send")
+        with region("comm.p2p", 0, nbytes):
+            for req in dist.batch_isend_irecv(p2p):
+                req.wait()
 
     # ------------------------------------------------------- collectives
     def allreduce_sum_(self, tensor: torch.Tensor, members=None) -> torch.Tensor:
@@ -106,7 +109,9 @@ class RankCtx:
             raise OutOfBounds(f"rank {self.rank} not in allreduce group {sorted(members)}")
         if members is not None and len(members) == 1:
             return tensor
-        dist.all_reduce(tensor, op=dist.ReduceOp.SUM, group=self.group(members or range(self.size)))
+        tag = "comm.allreduce_grad" if tensor.numel() > 65536 else "comm.allreduce_small"
+        with region(tag, 0, tensor.numel() * tensor.element_size()):
+            dist.all_reduce(tensor, op=dist.ReduceOp.SUM, group=self.group(members or range(self.size)))
         return tensor
 
     def allreduce_sum(self, vec, group=None):
