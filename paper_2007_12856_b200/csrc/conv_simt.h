@@ -24,9 +24,9 @@ int conv_bwd_data_simt(const float* u, const Frame& uf, const float* w, int k, i
 long long wgrad_simt_parts(const Frame& uf);
 int reduce_partials(const float* part, int P, long long len, float* out, int accumulate,
                     cudaStream_t st);
-int wgrad_tc_supported(const Frame& xf, const Frame& uf);
+int wgrad_tc_supported(const Frame& xf, const Frame& uf, int stride);
 int wgrad_tc_parts(const Frame& xf, const Frame& uf);
-int conv_wgrad_tc(const float* x, const Frame& xf, const float* u, const Frame& uf, float* part,
+int conv_wgrad_tc(const float* x, const Frame& xf, const float* u, const Frame& uf, int stride, float* part,
                   cudaStream_t st);
 int conv_wgrad_simt(const float* x, const Frame& xf, const float* u, const Frame& uf, int k, int s,
                     float* wg, int accumulate, float* part, cudaStream_t st);

@@ -34,6 +34,7 @@ struct WgradParams {
   long long rows;     // n * d * h * nxseg row tasks
   int nsub, P;        // sub-tasks, row ranges
   int x_off_d, x_off_h, x_off_w;  // x frame margins
+  int stride;                     // 1 or 2 (mode B only): x voxel = stride*o + tap - 1
   int ci_tiles, co_tiles;         // mode B tiling
   float* part;                    // [P][cout][cin][27]
 };
@@ -97,7 +98,14 @@ __global__ void __launch_bounds__(256, 1)
 
   if (warp == 0) {
     if (vpx::elect_one()) {
-      const uint32_t tx = XPL * XROWS * (wseg + 4) * kRow + NCO * wseg * kRow;
+      // mode B: channel planes actually present in this 128-channel tile (the
+      // rest stay stale and only feed discarded D rows); stride-2 boxes walk
+      // every second voxel (TMA element stride), so the W tap is applied in the
+      // coordinate instead of as a shared-memory offset
+      const int npl = MODE_A ? XPL : min(XPL, (p.cin - 128 * cit) / 32);
+      const int xrows = (MODE_A || p.stride == 1) ? wseg + 4 : wseg;
+      const int xw0 = (MODE_A || p.stride == 1) ? -1 : c - 1;
+      const uint32_t tx = npl * XROWS * xrows * kRow + NCO * wseg * kRow;
       int stage = 0;
       uint32_t phase = 0;
       for (long long r = r0; r < r1; ++r) {
@@ -113,10 +121,10 @@ __global__ void __launch_bounds__(256, 1)
         uint8_t* sx = smem + stage * STAGE;
         uint8_t* su = sx + XB;
         vpx::mbar_arrive_expect_tx(&full[stage], tx);
-#pragma unroll
-        for (int pl = 0; pl < XPL; ++pl)
-          vpx::tma_load_5d(sx + pl * XPLANE, &xmap, &full[stage], 32 * (cit * 4 + pl), x0 - 1 + p.x_off_w,
-                           y - 1 + b + p.x_off_h, z - 1 + a + p.x_off_d, n);
+        const int s = MODE_A ? 1 : p.stride;
+        for (int pl = 0; pl < npl; ++pl)
+          vpx::tma_load_5d(sx + pl * XPLANE, &xmap, &full[stage], 32 * (cit * 4 + pl), s * x0 + xw0 + p.x_off_w,
+                           s * y - 1 + b + p.x_off_h, s * z - 1 + a + p.x_off_d, n);
 #pragma unroll
         for (int cb = 0; cb < NCO; ++cb)
           vpx::tma_load_5d(su + cb * UPLANE, &umap, &full[stage], 32 * (cot * NCO + cb), x0, y, z, n);
@@ -146,7 +154,8 @@ __global__ void __launch_bounds__(256, 1)
               vpx::umma_tf32(tbase + bb * NCOUT, adesc, bdesc, idesc, first);
             }
           } else {
-            const uint64_t adesc = vpx::make_sdesc(xb + (k + c) * kRow, XPLANE, 512, 1);
+            const int coff = p.stride == 1 ? c : 0;
+            const uint64_t adesc = vpx::make_sdesc(xb + (k + coff) * kRow, XPLANE, 512, 1);
             vpx::umma_tf32(tbase, adesc, bdesc, idesc, first);
           }
         }
@@ -202,13 +211,15 @@ __global__ void __launch_bounds__(256, 1)
   if (warp == 2) vpx::tmem_dealloc<TCOLS>(tbase);
 }
 
-int encode_ch32_map(CUtensorMap* map, const float* base, const vpx::Frame& f, int box_w, int box_h) {
+int encode_ch32_map(CUtensorMap* map, const float* base, const vpx::Frame& f, int box_w, int box_h,
+                    int w_stride = 1) {
   const uint64_t Wf = f.w + 2 * f.mw, Hf = f.h + 2 * f.mh, Df = f.d + 2 * f.md;
   uint64_t dims[5] = {(uint64_t)f.c, Wf, Hf, Df, (uint64_t)f.n};
   uint64_t strides[4] = {(uint64_t)f.c * 4, Wf * f.c * 4, Hf * Wf * f.c * 4, Df * Hf * Wf * f.c * 4};
-  uint32_t box[5] = {32, (uint32_t)box_w, (uint32_t)box_h, 1, 1};
-  return vpx::encode_tiled(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float*>(base), dims, strides,
-                           box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  uint32_t box[5] = {32, (uint32_t)(box_w * w_stride), (uint32_t)box_h, 1, 1};
+  uint32_t estr[5] = {1, (uint32_t)w_stride, 1, 1, 1};
+  return vpx::encode_tiled_strided(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float*>(base), dims,
+                                   strides, box, estr, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
 }
 
 template <bool MODE_A, int NCOUT>
@@ -231,20 +242,22 @@ int launch_wgrad(const CUtensorMap& xm, const CUtensorMap& um, const WgradParams
 int nsub_of(const vpx::Frame& xf, const vpx::Frame& uf) {
   if (xf.c <= 32) return 3;
   const int nco = uf.c == 128 ? 128 : 256;
-  return 27 * (xf.c / 128) * (uf.c / nco);
+  return 27 * ((xf.c + 127) / 128) * (uf.c / nco);
 }
 
 }  // namespace
 
 namespace vpx {
 
-// 1 if the tcgen05 wgrad handles this layer (stride 1, k = 3 checked by caller).
-int wgrad_tc_supported(const Frame& xf, const Frame& uf) {
+// 1 if the tcgen05 wgrad handles this layer (k = 3 checked by the caller).
+// stride 2 is handled in mode B only (Cin >= 64, the CosmoFlow c4 shape).
+int wgrad_tc_supported(const Frame& xf, const Frame& uf, int stride) {
   if (uf.w % 8 || (uf.w > 128 && uf.w % 128)) return 0;
   if (uf.mw || uf.md || uf.mh) return 0;  // upstream gradients are margin-free
   const int cin = xf.c, cout = uf.c;
-  if (cin <= 32 && cin % 4 == 0) return cout == 16 || cout == 32 || cout == 64;
-  if (cin % 128 == 0 && uf.w <= 32) return cout == 128 || cout % 256 == 0;
+  if (stride == 1 && cin <= 32 && cin % 4 == 0) return cout == 16 || cout == 32 || cout == 64;
+  if (cin % 32 == 0 && cin >= 64 && uf.w <= 32 && (stride == 1 || stride == 2))
+    return cout == 128 || cout % 256 == 0;
   return 0;
 }
 
@@ -259,9 +272,10 @@ int wgrad_tc_parts(const Frame& xf, const Frame& uf) {
   return static_cast<int>(P);
 }
 
-int conv_wgrad_tc(const float* x, const Frame& xf, const float* u, const Frame& uf, float* part,
+int conv_wgrad_tc(const float* x, const Frame& xf, const float* u, const Frame& uf, int stride, float* part,
                   cudaStream_t st) {
   WgradParams p{};
+  p.stride = stride;
   p.n = uf.n;
   p.d = uf.d;
   p.h = uf.h;
@@ -279,11 +293,15 @@ int conv_wgrad_tc(const float* x, const Frame& xf, const float* u, const Frame& 
   p.part = part;
   const bool modeA = xf.c <= 32;
   if (!modeA) {
-    p.ci_tiles = xf.c / 128;
+    p.ci_tiles = (xf.c + 127) / 128;
     p.co_tiles = uf.c / (uf.c == 128 ? 128 : 256);
   }
   CUtensorMap xm, um;
-  if (int rc = encode_ch32_map(&xm, x, xf, p.wseg + 4, modeA ? 3 : 1)) return rc;
+  if (modeA || stride == 1) {
+    if (int rc = encode_ch32_map(&xm, x, xf, p.wseg + 4, modeA ? 3 : 1)) return rc;
+  } else {
+    if (int rc = encode_ch32_map(&xm, x, xf, p.wseg, 1, stride)) return rc;
+  }
   if (int rc = encode_ch32_map(&um, u, uf, p.wseg, 1)) return rc;
   if (modeA) {
     switch (uf.c) {

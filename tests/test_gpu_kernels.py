@@ -57,6 +57,9 @@ CASES = [
     # ... and mode B (Cin % 128 == 0, W <= 32)
     (1, 128, 256, 3, 4, 16, 3, 1),
     (1, 256, 256, 2, 4, 8, 3, 1),
+    (1, 64, 128, 4, 4, 16, 3, 1),      # partial 128-channel tile
+    (1, 64, 128, 8, 16, 32, 3, 2),     # stride 2 (TMA element stride), the c4 shape
+    (2, 192, 128, 4, 8, 16, 3, 2),
     # tap-box fwd/dgrad: W < 128, channel chunks padded by TMA zero fill, stride 2
     (1, 16, 32, 4, 6, 16, 3, 1),
     (2, 32, 64, 4, 4, 32, 3, 1),
