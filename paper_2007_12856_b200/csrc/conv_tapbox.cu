@@ -285,7 +285,8 @@ long long tapbox_workspace_bytes(int cin, int cout) {
 
 int tapbox_supported(int cin, int cout, int mode) {
   const int ntot = mode == 0 ? cout : cin;
-  return ntot % 16 == 0 && (ntot <= 256 || ntot % 256 == 0);
+  // N tiles with a kernel instance: 16/32/64/128/256, or a multiple of 256
+  return ntot == 16 || ntot == 32 || ntot == 64 || ntot == 128 || ntot % 256 == 0;
 }
 
 // mode 0: forward (stride 1 or 2); mode 1: backward-data (stride 1 or 2).
