@@ -43,7 +43,7 @@ N_PER_GROUP = 1
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--width", type=int, default=WIDTH)
@@ -164,10 +164,13 @@ class ClockSampler:
                  "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            t0 = time.time()  # timed work starts only once the sampler is live
+            while not self.samples and time.time() - t0 < 3.0:
+                time.sleep(0.01)
         except Exception:
             self.proc = None
         return self
@@ -194,6 +197,18 @@ class ClockSampler:
                           if len(s) > 3 + i and s[3 + i].lower().startswith("active")})
         return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
                 "samples": len(self.samples)}
+
+
+def ncu_traffic(tag):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the kernel
+    behind `tag`, from the committed `ncu --set full` capture summary
+    (profiles/ncu_traffic.json, written by tools/ncu_summary.py); None if that
+    kernel has not been captured."""
+    f = ROOT / "profiles" / "ncu_traffic.json"
+    if not f.exists():
+        return None
+    ent = json.loads(f.read_text()).get(tag)
+    return None if ent is None else ent["dram_bytes"]
 
 
 def tf32_peak_tflops():
@@ -334,6 +349,7 @@ def run_ours(args):
             roof = {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": f_h, "traffic": None,
                     "kernel": top_tag, "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"}
         roof["share_of_step"] = top["ms"] / ms
+        roof["traffic"] = ncu_traffic(top_tag)
     fl = train_step_flops(net, (n_global, 4, W, W, W))
     breakdown = {k: {"ms_per_step": v["ms"] / args.steps,
                      "tflops": (v["flops"] / (v["ms"] / v["launches"] * 1e-3) / 1e12) if v["flops"] else None,

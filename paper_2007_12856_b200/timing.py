@@ -3,17 +3,21 @@
 When a Recorder is active, the layer ops bracket their libvpx launches with
 CUDA events on the launching (current) stream and tag them with the layer
 name, pass and the algorithmic flops / bytes of that launch.  Inactive
-(the default), `region` is a no-op context manager.
+(the default), `region` is a no-op context manager.  With VPX_NVTX=1 in the
+environment every region is also an NVTX range named by its tag, so a single
+layer's kernel can be selected for `ncu --nvtx --nvtx-include "<tag>/"`.
 """
 
 from __future__ import annotations
 
 import contextlib
+import os
 from collections import defaultdict
 
 import torch
 
 _ACTIVE = None
+_NVTX = os.environ.get("VPX_NVTX") == "1"
 
 
 class Recorder:
@@ -28,6 +32,7 @@ class Recorder:
     def __exit__(self, *exc):
         global _ACTIVE
         _ACTIVE = None
+_NVTX = os.environ.get("VPX_NVTX") == "1"
 
     def summary(self):
         """{tag: {"ms": total, "launches": k, "flops": per launch, "bytes": per launch}}"""
@@ -44,12 +49,22 @@ class Recorder:
 @contextlib.contextmanager
 def region(tag: str, flops: int = 0, nbytes: int = 0):
     rec = _ACTIVE
+    if _NVTX:
+        torch.cuda.nvtx.range_push(tag)
     if rec is None:
-        yield
+        try:
+            yield
+        finally:
+            if _NVTX:
+                torch.cuda.nvtx.range_pop()
         return
     s = torch.cuda.Event(enable_timing=True)
     e = torch.cuda.Event(enable_timing=True)
     s.record()
-    yield
+    try:
+        yield
+    finally:
+        if _NVTX:
+            torch.cuda.nvtx.range_pop()
     e.record()
     rec.events.append((tag, flops, nbytes, s, e))
