@@ -32,7 +32,6 @@ class Recorder:
     def __exit__(self, *exc):
         global _ACTIVE
         _ACTIVE = None
-_NVTX = os.environ.get("VPX_NVTX") == "1"
 
     def summary(self):
         """{tag: {"ms": total, "launches": k, "flops": per launch, "bytes": per launch}}"""
