@@ -10,8 +10,8 @@
  * Layout conventions:
  *   activations  NDHWC fp32, stored in a halo frame [N][D+2md][H+2mh][W+2mw][C]
  *                whose margins m* are 1 in partitioned dims and 0 elsewhere;
- *   conv weights "OTI": [Cout][kd][kh][kw][Cin] fp32 (the reference keeps OIDHW,
- *                reference layers/reference.py:68; vpx_layout_* converts).
+ *   conv weights OIDHW fp32 exactly as the reference keeps them
+ *                (reference layers/reference.py:68); packed per pass internally.
  *
  * The reference's kernel boundary this replaces is
  *   voxpar.kernels.conv3d_fwd / conv3d_bwd_data / conv3d_bwd_filter
