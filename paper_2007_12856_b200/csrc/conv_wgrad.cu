@@ -266,7 +266,9 @@ int wgrad_tc_parts(const Frame& xf, const Frame& uf) {
   const int nsub = nsub_of(xf, uf);
   const int wseg = uf.w < 128 ? uf.w : 128;
   const long long rows = (long long)uf.n * uf.d * uf.h * (uf.w / wseg);
-  long long P = (num_sms() + nsub - 1) / nsub;
+  // one CTA per SM (smem-limited): nsub * P must not exceed the SM count, or the
+  // leftover CTAs run as a second wave and double the kernel time
+  long long P = num_sms() / nsub;
   if (P < 1) P = 1;
   if (P > rows) P = rows;
   return static_cast<int>(P);

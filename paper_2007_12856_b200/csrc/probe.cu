@@ -10,11 +10,13 @@ namespace {
 constexpr int kProbeSmem = 200 * 1024;
 
 // op layout (4 x u64): adesc (start = offset into image), bdesc (same),
-// idesc | (d_col << 32), accumulate flag.
+// idesc | (d_col << 32), accumulate flag | 2 if A comes from TMEM (then the
+// adesc word is the TMEM column of A).  ta[128][ta_cols] (optional) is stored
+// to TMEM columns [256, 256 + ta_cols) before the ops run.
 __global__ void __launch_bounds__(128, 1)
     probe_umma_kernel(const uint4* __restrict__ img, int img_bytes,
                       const uint64_t* __restrict__ ops, int n_ops, float* __restrict__ out,
-                      int ncols) {
+                      int ncols, const float* __restrict__ ta, int ta_cols) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bar;
   __shared__ uint32_t tmem_base;
@@ -31,16 +33,30 @@ __global__ void __launch_bounds__(128, 1)
   __syncthreads();
   vpx::tc_fence_after();
   const uint32_t tbase = tmem_base;
+  if (ta != nullptr) {
+    const int row = 32 * (warp & 3) + (tid & 31);
+    for (int c = 0; c < ta_cols; c += 16) {
+      float v[16];
+      for (int j = 0; j < 16; ++j) v[j] = ta[row * ta_cols + c + j];
+      vpx::tmem_st16(tbase + (static_cast<uint32_t>(32 * (warp & 3)) << 16) + 256 + c, v);
+    }
+    vpx::tmem_st_wait();
+  }
+  vpx::tc_fence_before();
+  __syncthreads();
+  vpx::tc_fence_after();
   const uint64_t sbase = static_cast<uint64_t>(vpx::smem_u32(smem) >> 4);
   if (tid == 0) {
     for (int i = 0; i < n_ops; ++i) {
-      uint64_t a = ops[4 * i + 0] + sbase;
       uint64_t b = ops[4 * i + 1] + sbase;
       uint64_t w = ops[4 * i + 2];
       uint32_t idesc = static_cast<uint32_t>(w & 0xffffffffu);
       uint32_t dcol = static_cast<uint32_t>(w >> 32);
-      uint32_t acc = static_cast<uint32_t>(ops[4 * i + 3]);
-      vpx::umma_tf32(tbase + dcol, a, b, idesc, acc);
+      uint32_t acc = static_cast<uint32_t>(ops[4 * i + 3]) & 1u;
+      if (ops[4 * i + 3] & 2u)
+        vpx::umma_tf32_ta(tbase + dcol, tbase + static_cast<uint32_t>(ops[4 * i + 0]), b, idesc, acc);
+      else
+        vpx::umma_tf32(tbase + dcol, ops[4 * i + 0] + sbase, b, idesc, acc);
     }
     vpx::umma_commit(&bar);
   }
@@ -111,7 +127,10 @@ __global__ void __launch_bounds__(128, 1)
                                : vpx::make_sdesc(s0 + 32768, 16, 1024, 2);
     uint32_t idesc = vpx::make_idesc(bf16 ? 1 : 2, 128, N, false, false);
     long long t0 = clock64();
-    if (bf16) {
+    if (a_layout == 2) {
+      for (int i = 0; i < n_iter; ++i)
+        vpx::umma_tf32_ta(tbase + (i % n_acc) * N, tbase + 256 + 8 * (i & 7), b, idesc, i >= n_acc);
+    } else if (bf16) {
       for (int i = 0; i < n_iter; ++i)
         vpx::umma_f16(tbase + (i % n_acc) * N, a, b, idesc, i >= n_acc);
     } else {
@@ -131,8 +150,9 @@ __global__ void __launch_bounds__(128, 1)
 
 // Same, with the issue loop in the canonical warp-uniform form (whole warp 1
 // iterates; one elected lane issues an unrolled burst of NACC MMAs).
-template <int N, int NACC, bool BF16>
+template <int N, int NACC, int MODE>  // MODE 0 tf32, 1 bf16, 2 tf32 with A in TMEM (cols 256..)
 __global__ void __launch_bounds__(128, 1) probe_rate2_kernel(int n_iter, long long* cycles) {
+  constexpr bool BF16 = MODE == 1;
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bar;
   __shared__ uint32_t tmem_base;
@@ -158,7 +178,9 @@ __global__ void __launch_bounds__(128, 1) probe_rate2_kernel(int n_iter, long lo
       if (vpx::elect_one()) {
 #pragma unroll
         for (int j = 0; j < NACC; ++j) {
-          if (BF16)
+          if (MODE == 2)
+            vpx::umma_tf32_ta(tbase + (j * N) % 256, tbase + 256 + 8 * (j & 7), b, idesc, i > 0);
+          else if (BF16)
             vpx::umma_f16(tbase + j * N, a + 2 * (j & 1), b, idesc, i > 0);
           else
             vpx::umma_tf32(tbase + j * N, a + 2 * (j & 1), b, idesc, i > 0);
@@ -177,11 +199,11 @@ __global__ void __launch_bounds__(128, 1) probe_rate2_kernel(int n_iter, long lo
   if (warp == 0) vpx::tmem_dealloc<512>(tbase);
 }
 
-template <int N, int NACC, bool BF16>
+template <int N, int NACC, int MODE>
 static int launch_rate2(int n_iter, long long* cycles, cudaStream_t st) {
-  VPX_CHECK_CUDA(cudaFuncSetAttribute(probe_rate2_kernel<N, NACC, BF16>,
+  VPX_CHECK_CUDA(cudaFuncSetAttribute(probe_rate2_kernel<N, NACC, MODE>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 65536 + 1024));
-  probe_rate2_kernel<N, NACC, BF16><<<1, 128, 65536 + 1024, st>>>(n_iter, cycles);
+  probe_rate2_kernel<N, NACC, MODE><<<1, 128, 65536 + 1024, st>>>(n_iter, cycles);
   VPX_LAUNCH_CHECK();
   return VPX_OK;
 }
@@ -193,8 +215,9 @@ extern "C" int vpx_probe_mma_rate2(int N, int n_acc, int bf16, int n_iter, long 
   cudaStream_t st = static_cast<cudaStream_t>(stream);
 #define RATE_CASE(n, a)                                                         \
   if (N == n && n_acc == a)                                                     \
-    return bf16 ? launch_rate2<n, a, true>(n_iter, cycles, st)                  \
-                : launch_rate2<n, a, false>(n_iter, cycles, st);
+    return bf16 == 2 ? launch_rate2<n, a, 2>(n_iter, cycles, st)                \
+           : bf16    ? launch_rate2<n, a, 1>(n_iter, cycles, st)                \
+                     : launch_rate2<n, a, 0>(n_iter, cycles, st);
   RATE_CASE(16, 1) RATE_CASE(16, 4) RATE_CASE(16, 8) RATE_CASE(32, 1) RATE_CASE(32, 4)
   RATE_CASE(32, 8) RATE_CASE(64, 1) RATE_CASE(64, 4) RATE_CASE(64, 8) RATE_CASE(128, 1)
   RATE_CASE(128, 2) RATE_CASE(256, 1) RATE_CASE(256, 2)
@@ -219,7 +242,19 @@ extern "C" int vpx_probe_umma(const void* img, int img_bytes, const uint64_t* op
   VPX_CHECK_CUDA(cudaFuncSetAttribute(probe_umma_kernel,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kProbeSmem));
   probe_umma_kernel<<<1, 128, kProbeSmem, static_cast<cudaStream_t>(stream)>>>(
-      static_cast<const uint4*>(img), img_bytes, ops, n_ops, out, ncols);
+      static_cast<const uint4*>(img), img_bytes, ops, n_ops, out, ncols, nullptr, 0);
+  VPX_LAUNCH_CHECK();
+  return VPX_OK;
+}
+
+extern "C" int vpx_probe_umma_ta(const void* img, int img_bytes, const uint64_t* ops, int n_ops,
+                                 const float* ta, int ta_cols, float* out, int ncols, void* stream) {
+  if (img_bytes > kProbeSmem || img_bytes % 16) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "image size");
+  if (ncols % 16 || ncols > 256 || ta_cols % 16 || ta_cols > 256) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "cols");
+  VPX_CHECK_CUDA(cudaFuncSetAttribute(probe_umma_kernel,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kProbeSmem));
+  probe_umma_kernel<<<1, 128, kProbeSmem, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const uint4*>(img), img_bytes, ops, n_ops, out, ncols, ta, ta_cols);
   VPX_LAUNCH_CHECK();
   return VPX_OK;
 }

@@ -581,3 +581,63 @@ def scatter_batch(plan: Plan, x, y, sample_ids, rank: int, epoch: int = 0, itera
             lo, hi = plan.label_meta.sample_range(plan.label_meta.group_of(gl))
             b.y_block = torch.as_tensor(y)[(slice(lo, hi),) + reg.slices()].to("cuda", torch.int64).contiguous()
     return b
+
+
+class HostInputPipeline:
+    """Streams per-step input blocks from pinned host memory into a Batch.
+
+    The reference reads each step's block from its datastore on the host
+    (reference data/datastore.py:156-179) and hands numpy arrays to the step.
+    Here the block is copied host->device on a dedicated copy stream into one
+    of two staging buffers while the previous step computes; `load(batch)`
+    makes the compute stream wait for that copy, converts the staged NCDHW
+    block into the batch's halo frame (vpx_layout_ncdhw_to_frame) and queues
+    the next copy.  Copies therefore overlap compute and the step itself sees
+    no host synchronisation.
+
+    host_blocks: a callable step -> pinned NCDHW host tensor (this rank's
+    block), or a single tensor reused every step.
+    """
+
+    def __init__(self, host_blocks, device=None):
+        self._src = host_blocks if callable(host_blocks) else (lambda i, t=host_blocks: t)
+        first = self._src(0)
+        self.shape = tuple(first.shape)
+        self.bytes_per_step = first.numel() * first.element_size()
+        self.copy_stream = torch.cuda.Stream(device=device)
+        self._buf = [torch.empty(self.shape, dtype=first.dtype, device="cuda") for _ in range(2)]
+        self._ready = [torch.cuda.Event() for _ in range(2)]
+        self._free = [torch.cuda.Event() for _ in range(2)]
+        self._free_recorded = [False, False]
+        self._step = 0
+        self._issued = -1
+
+    def _issue(self, i):
+        slot = i % 2
+        with torch.cuda.stream(self.copy_stream):
+            if self._free_recorded[slot]:
+                self.copy_stream.wait_event(self._free[slot])
+            self._buf[slot].copy_(self._src(i), non_blocking=True)
+            self._ready[slot].record(self.copy_stream)
+        self._issued = i
+
+    def start(self, after: torch.cuda.Event = None):
+        """Queue the first copy (optionally after `after` on the copy stream)."""
+        if after is not None:
+            self.copy_stream.wait_event(after)
+        self._issue(self._step)
+
+    def load(self, batch: "Batch", prefetch_next: bool = True) -> "Batch":
+        i = self._step
+        if self._issued < i:
+            self._issue(i)
+        slot = i % 2
+        cur = torch.cuda.current_stream()
+        cur.wait_event(self._ready[slot])
+        batch.x_block.load_ncdhw(self._buf[slot])
+        self._free[slot].record(cur)
+        self._free_recorded[slot] = True
+        self._step += 1
+        if prefetch_next:
+            self._issue(self._step)
+        return batch
