@@ -95,6 +95,15 @@ int vpx_pool_leaky_bwd_blocked(const float* y, const int* yf, const float* up, c
                                float slope, int is_max, void* stream);
 int vpx_conv3d_bwd_filter_c4(const float* x, const int* xfr, const float* ub, const int* ufr, float* wg,
                              int accumulate, void* ws, long long ws_bytes, void* stream);
+/* The same filter gradient computed straight from the POOLED gradient `up`
+ * (average pool only): u = leaky'(y) * up/8 is produced inside the kernel
+ * (into TMEM, the MMA's A operand) and never written to memory; replaces the
+ * pair above for TF32 mode (conv_c1bwd.cu).  y: LeakyReLU output frame,
+ * up: pooled-gradient frame (half extents).  Frames may carry D/H margins,
+ * not W margins.  VPX_ERR_UNSUPPORTED for max pooling or FP32 mode. */
+int vpx_conv3d_bwd_filter_c4_pooled(const float* x, const int* xfr, const float* y, const int* yfr,
+                                    const float* up, const int* upfr, float slope, int is_max, float* wg,
+                                    int accumulate, void* ws, long long ws_bytes, void* stream);
 
 /* ------------------------------------------------------- pointwise / pool --
  * reference layers/reference.py:149-236, layers/distributed.py:132-214.

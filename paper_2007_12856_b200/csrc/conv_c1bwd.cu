@@ -1,0 +1,348 @@
+// Backward of the first CosmoFlow block (Conv3d 4 -> 16, LeakyReLU, 2^3 average
+// pool) in ONE kernel: the filter gradient is computed straight from the pooled
+// gradient, without materialising the 16-channel full-resolution gradient.
+//
+//   u[v][co]  = leaky'(y[v][co]) * up[v/2][co] / 8        (pool + LeakyReLU bwd)
+//   wg[co][ci][a][b][c] = sum_v u[v][co] * x[v + (a,b,c) - 1][ci]
+//
+// tcgen05 with the A operand in TMEM: the producer warps compute u for 64
+// voxels at a time and store it with tcgen05.st as A[m = (d, co)][k] =
+// u[8k + d + 1][co] (8 W-shifts d x 16 channels = 128 lanes, one column per
+// 8-voxel group k); B is the input row as 128-byte rows of 8 voxels x 4
+// channels (MN-major SWIZZLE_128B_BASE32B, N = 48: rows k and k+1).  Entry
+// (d, co) x (e, ci) of D_ab accumulates u[8k+d+1][co] * x[8k+e][ci], i.e. W tap
+// c = e - d of the filter gradient when 0 <= c <= 2 (the rest is discarded).
+// Each of the 9 (depth, height) taps is one MMA on its own x row into its own
+// 48-column accumulator (432 TMEM columns); A cycles through an 8-slot ring
+// in the remaining 64 columns.  The MMA reads only B from shared memory, so a
+// K=8 step costs ~N/2 cycles instead of the (A + B)/128 B/clk of a
+// shared-memory A operand.
+//
+// Warp roles: w0 TMA (x rows into a 4-row ring per depth tap, y and pooled
+// gradient rows), w1 MMA issuer, w2 TMEM owner, w4..w7 u producers and
+// epilogue (fold D into wg, split-K partial per CTA, fixed-order reduction
+// afterwards -> deterministic).
+// Reference semantics: reference pkg/src/voxpar/kernels/_hot.pyx:70-93 (filter
+// gradient), layers/reference.py:170-173 (avg pool bwd), :231-236 (leaky bwd).
+#include "conv_common.h"
+#include "conv_simt.h"
+#include "vpx_host.h"
+#include "vpx_ptx.cuh"
+#include "vpx_round.cuh"
+
+namespace {
+
+struct C1Params {
+  int n, d, h;              // u (= y) interior extents, W is the template parameter
+  long long rows;           // n * d * h
+  int P;                    // CTAs (row ranges)
+  int x_off_d, x_off_h;     // x frame margins
+  int y_off_d, y_off_h;     // y frame margins
+  int up_off_d, up_off_h;   // pooled-gradient frame margins
+  float slope;
+  int rnd;                  // round u to nearest TF32
+  float* part;              // [P][16][4][27]
+};
+
+constexpr int kNA = 48;          // N per tap (x chunks k, k+1: 64 > 48 used columns)
+constexpr int kACol = 9 * kNA;   // first A column (432)
+constexpr int kASlots = 8;       // A ring: 8 slots x 8 columns
+
+template <int W>
+struct C1Cfg {
+  static constexpr int KS = (W / 8 + 1 + 7) / 8;           // K-steps per row (k = -1 .. 8KS-2)
+  static constexpr int XCH = 8 * KS + 1;                   // x chunks per row (-1 .. 8KS-1)
+  static constexpr int XROW = (XCH * 128 + 1023) / 1024 * 1024;
+  static constexpr int XS = 12 * XROW;                     // 3 depth taps x 4-row ring
+  static constexpr int YB = W * 16 * 4;                    // y row
+  static constexpr int UB = W / 2 * 16 * 4;                // pooled-gradient row
+  static constexpr int PIPE = XS + 2 * YB + 2 * UB;
+  static constexpr int SCRATCH = 128 * 108 * 4;            // epilogue fold, reuses the pipeline buffers
+  static constexpr int SMEM = PIPE > SCRATCH ? PIPE : SCRATCH;
+};
+
+template <int W>
+__global__ void __launch_bounds__(256, 1)
+    c1_pooled_wgrad_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap ymap,
+                           const __grid_constant__ CUtensorMap upmap, const C1Params p) {
+  using Cfg = C1Cfg<W>;
+  constexpr int KS = Cfg::KS, XROW = Cfg::XROW;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* xs = smem;
+  uint8_t* ys = smem + Cfg::XS;
+  uint8_t* us = ys + 2 * Cfg::YB;
+  __shared__ __align__(8) uint64_t xfull[2], yfull[2], yempty[2], rowdone[2], fullA[kASlots], emptyA[kASlots],
+      tfull;
+  __shared__ uint32_t tmem_base;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int pidx = blockIdx.x;
+  const long long r0 = p.rows * pidx / p.P, r1 = p.rows * (pidx + 1) / p.P;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2; ++i) {
+      vpx::mbar_init(&xfull[i], 1);
+      vpx::mbar_init(&yfull[i], 1);
+      vpx::mbar_init(&yempty[i], 4);
+      vpx::mbar_init(&rowdone[i], 1);
+    }
+    for (int i = 0; i < kASlots; ++i) {
+      vpx::mbar_init(&fullA[i], 4);
+      vpx::mbar_init(&emptyA[i], 1);
+    }
+    vpx::mbar_init(&tfull, 1);
+    vpx::fence_barrier_init();
+    vpx::tma_prefetch_desc(&xmap);
+    vpx::tma_prefetch_desc(&ymap);
+    vpx::tma_prefetch_desc(&upmap);
+  }
+  if (warp == 2) vpx::tmem_alloc<512>(&tmem_base);
+  vpx::tc_fence_before();
+  __syncthreads();
+  vpx::tc_fence_after();
+  const uint32_t tbase = tmem_base;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    if (vpx::elect_one()) {
+      for (long long r = r0; r < r1; ++r) {
+        const int i = static_cast<int>(r - r0);
+        long long t = r;
+        const int y = t % p.h;
+        t /= p.h;
+        const int z = t % p.d;
+        const int n = static_cast<int>(t / p.d);
+        const bool reset = (i == 0) || (y == 0);
+        // the x ring slot of row y+1 last served u row i-2; a reset reloads all
+        // three rows per depth tap, so u row i-1 must be done
+        if (reset && i >= 1) vpx::mbar_wait(&rowdone[(i - 1) & 1], ((i - 1) >> 1) & 1);
+        else if (i >= 2) vpx::mbar_wait(&rowdone[i & 1], ((i - 2) >> 1) & 1);
+        const int nrow = reset ? 3 : 1;
+        vpx::mbar_arrive_expect_tx(&xfull[i & 1], 3 * nrow * Cfg::XCH * 128);
+#pragma unroll 1
+        for (int a = 0; a < 3; ++a) {
+          for (int j = 0; j < nrow; ++j) {
+            const int yy = reset ? y - 1 + j : y + 1;
+            vpx::tma_load_5d(xs + (a * 4 + (yy & 3)) * XROW, &xmap, &xfull[i & 1], 0, -1, yy + p.x_off_h,
+                             z - 1 + a + p.x_off_d, n);
+          }
+        }
+        vpx::mbar_wait(&yempty[i & 1], ((i >> 1) & 1) ^ 1);
+        vpx::mbar_arrive_expect_tx(&yfull[i & 1], Cfg::YB + Cfg::UB);
+        vpx::tma_load_5d(ys + (i & 1) * Cfg::YB, &ymap, &yfull[i & 1], 0, 0, y + p.y_off_h, z + p.y_off_d, n);
+        vpx::tma_load_5d(us + (i & 1) * Cfg::UB, &upmap, &yfull[i & 1], 0, 0, (y >> 1) + p.up_off_h,
+                         (z >> 1) + p.up_off_d, n);
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------------- MMA
+    constexpr uint32_t idesc = vpx::make_idesc(2, 128, kNA, false, true);
+    const uint32_t xb = vpx::smem_u32(xs);
+    for (long long r = r0; r < r1; ++r) {
+      const int i = static_cast<int>(r - r0);
+      const int y = static_cast<int>(r % p.h);
+      vpx::mbar_wait(&xfull[i & 1], (i >> 1) & 1);
+      for (int s = 0; s < KS; ++s) {
+        const int g = i * KS + s, slot = g & (kASlots - 1);
+        vpx::mbar_wait(&fullA[slot], (g >> 3) & 1);
+        vpx::tc_fence_after();
+        if (vpx::elect_one()) {
+          const uint32_t acol = tbase + kACol + slot * 8;
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+#pragma unroll
+            for (int b = 0; b < 3; ++b) {
+              const uint32_t row = xb + (a * 4 + ((y - 1 + b) & 3)) * XROW + s * 8 * 128;
+              const uint64_t bdesc = vpx::make_sdesc(row, 128, 512, 1);
+              vpx::umma_tf32_ta(tbase + (a * 3 + b) * kNA, acol, bdesc, idesc, (i > 0 || s > 0) ? 1u : 0u);
+            }
+          }
+          vpx::umma_commit(&emptyA[slot]);
+          if (s == KS - 1) {
+            vpx::umma_commit(&rowdone[i & 1]);
+            if (r == r1 - 1) vpx::umma_commit(&tfull);
+          }
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------- u producers
+    const int q = warp - 4, m = q * 32 + lane, dd = m >> 4, co = m & 15;
+    const uint32_t lane_addr = tbase + (static_cast<uint32_t>(q * 32) << 16) + kACol;
+    for (long long r = r0; r < r1; ++r) {
+      const int i = static_cast<int>(r - r0);
+      vpx::mbar_wait(&yfull[i & 1], (i >> 1) & 1);
+      const float* yrow = reinterpret_cast<const float*>(ys + (i & 1) * Cfg::YB);
+      const float* urow = reinterpret_cast<const float*>(us + (i & 1) * Cfg::UB);
+      for (int s = 0; s < KS; ++s) {
+        const int g = i * KS + s, slot = g & (kASlots - 1);
+        float v[8];
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const int vox = 64 * s + 8 * kk - 7 + dd;  // u voxel 8k + d + 1, k = 8s + kk - 1
+          float val = 0.f;
+          if (vox >= 0 && vox < W) {
+            const float gp = urow[(vox >> 1) * 16 + co] / 8.0f;
+            val = yrow[vox * 16 + co] >= 0.f ? gp : p.slope * gp;
+            if (p.rnd) val = vpx::tf32_rn(val);
+          }
+          v[kk] = val;
+        }
+        vpx::mbar_wait(&emptyA[slot], ((g >> 3) & 1) ^ 1);
+        vpx::tmem_st8(lane_addr + slot * 8, v);
+        vpx::tmem_st_wait();
+        vpx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) vpx::mbar_arrive(&fullA[slot]);
+      }
+      __syncwarp();
+      if (lane == 0) vpx::mbar_arrive(&yempty[i & 1]);
+    }
+  }
+
+  // ---------------------------------------------------------------- epilogue
+  const bool have = r1 > r0;
+  if (warp >= 4 && have) {
+    vpx::mbar_wait(&tfull, 0);
+    vpx::tc_fence_after();
+  }
+  __syncthreads();  // all TMA landed and consumed, all MMAs retired: reuse the x ring
+  float* red = reinterpret_cast<float*>(smem);  // [d][co][ci][27]
+  if (warp >= 4) {
+    const int q = warp - 4, m = q * 32 + lane, dd = m >> 4;
+#pragma unroll 1
+    for (int ab = 0; ab < 9; ++ab) {
+      float v[kNA];
+      if (have) {
+#pragma unroll
+        for (int c16 = 0; c16 < kNA / 16; ++c16) {
+          float t16[16];
+          vpx::tmem_ld16(tbase + (static_cast<uint32_t>(q * 32) << 16) + ab * kNA + 16 * c16, t16);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[16 * c16 + j] = t16[j];
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < kNA; ++j) v[j] = 0.f;
+      }
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const int t = dd + c;  // x voxel offset e (+8 for chunk k+1) = d + c
+        const int nb = (t >> 3) * 32 + (t & 7) * 4;
+#pragma unroll
+        for (int ci = 0; ci < 4; ++ci) red[(m * 4 + ci) * 27 + ab * 3 + c] = v[nb + ci];
+      }
+    }
+  }
+  __syncthreads();
+  float* base = p.part + static_cast<long long>(pidx) * 16 * 4 * 27;
+  for (int o = threadIdx.x; o < 16 * 4 * 27; o += blockDim.x) {
+    const int co = o / 108, rem = o % 108;
+    float s = 0.f;
+#pragma unroll
+    for (int dd = 0; dd < 8; ++dd) s += red[(dd * 16 + co) * 108 + rem];
+    base[o] = s;
+  }
+  vpx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) vpx::tmem_dealloc<512>(tbase);
+}
+
+template <int W>
+int launch_c1(const CUtensorMap& xm, const CUtensorMap& ym, const CUtensorMap& um, const C1Params& p,
+              cudaStream_t st) {
+  constexpr int smem = C1Cfg<W>::SMEM + 1024;
+  static_assert(smem <= 227 * 1024, "smem");
+  auto kern = c1_pooled_wgrad_kernel<W>;
+  VPX_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  kern<<<p.P, 256, smem, st>>>(xm, ym, um, p);
+  VPX_LAUNCH_CHECK();
+  return VPX_OK;
+}
+
+}  // namespace
+
+namespace vpx {
+
+int c1_pooled_supported(const Frame& xf, const Frame& yf, const Frame& uf) {
+  if (precision() != 0) return 0;
+  if (xf.c != 4 || yf.c != 16 || uf.c != 16) return 0;
+  if (xf.mw || yf.mw || uf.mw) return 0;
+  if (!(yf.w == 64 || yf.w == 128 || yf.w == 256 || yf.w == 512)) return 0;
+  if (xf.n != yf.n || xf.d != yf.d || xf.h != yf.h || xf.w != yf.w) return 0;
+  if (yf.d % 2 || yf.h % 2 || uf.n != yf.n || uf.d * 2 != yf.d || uf.h * 2 != yf.h || uf.w * 2 != yf.w) return 0;
+  return 1;
+}
+
+int c1_pooled_parts(const Frame& yf) {
+  const long long rows = (long long)yf.n * yf.d * yf.h;
+  long long P = num_sms();
+  if (P > rows) P = rows;
+  return static_cast<int>(P < 1 ? 1 : P);
+}
+
+int conv_wgrad_c1_pooled(const float* x, const Frame& xf, const float* y, const Frame& yf, const float* up,
+                         const Frame& uf, float slope, float* part, cudaStream_t st) {
+  C1Params p{};
+  p.n = yf.n;
+  p.d = yf.d;
+  p.h = yf.h;
+  p.rows = (long long)yf.n * yf.d * yf.h;
+  p.P = c1_pooled_parts(yf);
+  p.x_off_d = xf.md;
+  p.x_off_h = xf.mh;
+  p.y_off_d = yf.md;
+  p.y_off_h = yf.mh;
+  p.up_off_d = uf.md;
+  p.up_off_h = uf.mh;
+  p.slope = slope;
+  p.rnd = 1;
+  p.part = part;
+  const int W = yf.w;
+  int xch = 0;
+  switch (W) {
+    case 512: xch = C1Cfg<512>::XCH; break;
+    case 256: xch = C1Cfg<256>::XCH; break;
+    case 128: xch = C1Cfg<128>::XCH; break;
+    case 64: xch = C1Cfg<64>::XCH; break;
+  }
+  CUtensorMap xm, ym, um;
+  {
+    const uint64_t Hf = xf.h + 2 * xf.mh, Df = xf.d + 2 * xf.md;
+    uint64_t dims[5] = {32, (uint64_t)W / 8, Hf, Df, (uint64_t)xf.n};
+    uint64_t strides[4] = {128, (uint64_t)W * 16, Hf * W * 16, Df * Hf * W * 16};
+    uint32_t box[5] = {32, (uint32_t)xch, 1, 1, 1};
+    if (int rc = encode_tiled(&xm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float*>(x), dims, strides, box,
+                              CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
+      return rc;
+  }
+  {
+    const uint64_t Hf = yf.h + 2 * yf.mh, Df = yf.d + 2 * yf.md;
+    uint64_t dims[5] = {64, (uint64_t)W / 4, Hf, Df, (uint64_t)yf.n};
+    uint64_t strides[4] = {256, (uint64_t)W * 64, Hf * W * 64, Df * Hf * W * 64};
+    uint32_t box[5] = {64, (uint32_t)(W / 4), 1, 1, 1};
+    if (int rc = encode_tiled(&ym, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float*>(y), dims, strides, box,
+                              CU_TENSOR_MAP_SWIZZLE_NONE))
+      return rc;
+  }
+  {
+    const uint64_t Wu = uf.w, Hf = uf.h + 2 * uf.mh, Df = uf.d + 2 * uf.md;
+    uint64_t dims[5] = {64, Wu / 4, Hf, Df, (uint64_t)uf.n};
+    uint64_t strides[4] = {256, Wu * 64, Hf * Wu * 64, Df * Hf * Wu * 64};
+    uint32_t box[5] = {64, (uint32_t)(Wu / 4), 1, 1, 1};
+    if (int rc = encode_tiled(&um, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float*>(up), dims, strides, box,
+                              CU_TENSOR_MAP_SWIZZLE_NONE))
+      return rc;
+  }
+  switch (W) {
+    case 512: return launch_c1<512>(xm, ym, um, p, st);
+    case 256: return launch_c1<256>(xm, ym, um, p, st);
+    case 128: return launch_c1<128>(xm, ym, um, p, st);
+    case 64: return launch_c1<64>(xm, ym, um, p, st);
+  }
+  VPX_FAIL(VPX_ERR_UNSUPPORTED, "c1 pooled filter gradient: W=%d", W);
+}
+
+}  // namespace vpx
+

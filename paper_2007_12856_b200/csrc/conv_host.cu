@@ -265,3 +265,20 @@ extern "C" int vpx_conv3d_bwd_filter_c4(const float* x, const int* xfr, const fl
   if (int rc = vpx::conv_wgrad_c4(x, xf, ub, uf, part, st)) return rc;
   return vpx::reduce_partials(part, P, (long long)uf.c * 4 * 27, wg, accumulate, st);
 }
+
+// First-block filter gradient straight from the pooled gradient (avg pool).
+extern "C" int vpx_conv3d_bwd_filter_c4_pooled(const float* x, const int* xfr, const float* y, const int* yfr,
+                                               const float* up, const int* upfr, float slope, int is_max,
+                                               float* wg, int accumulate, void* ws, long long ws_bytes,
+                                               void* stream) {
+  Frame xf = vpx::to_frame(xfr), yf = vpx::to_frame(yfr), uf = vpx::to_frame(upfr);
+  if (is_max || !vpx::c1_pooled_supported(xf, yf, uf))
+    VPX_FAIL(VPX_ERR_UNSUPPORTED, "pooled c1 filter gradient: shape/mode");
+  const int P = vpx::c1_pooled_parts(yf);
+  const long long need = (long long)P * 16 * 4 * 27 * 4;
+  if (ws_bytes < need) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "workspace too small");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  float* part = static_cast<float*>(ws);
+  if (int rc = vpx::conv_wgrad_c1_pooled(x, xf, y, yf, up, uf, slope, part, st)) return rc;
+  return vpx::reduce_partials(part, P, 16 * 4 * 27, wg, accumulate, st);
+}

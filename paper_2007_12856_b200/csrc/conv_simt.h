@@ -28,6 +28,10 @@ int wgrad_tc_supported(const Frame& xf, const Frame& uf, int stride);
 int wgrad_tc_parts(const Frame& xf, const Frame& uf);
 int conv_wgrad_tc(const float* x, const Frame& xf, const float* u, const Frame& uf, int stride, float* part,
                   cudaStream_t st);
+int c1_pooled_supported(const Frame& xf, const Frame& yf, const Frame& uf);
+int c1_pooled_parts(const Frame& yf);
+int conv_wgrad_c1_pooled(const float* x, const Frame& xf, const float* y, const Frame& yf, const float* up,
+                         const Frame& uf, float slope, float* part, cudaStream_t st);
 int conv_wgrad_simt(const float* x, const Frame& xf, const float* u, const Frame& uf, int k, int s,
                     float* wg, int accumulate, float* part, cudaStream_t st);
 

@@ -414,13 +414,20 @@ def first_block_wgrad(ctx: RankCtx, x: DistTensor, y: DistTensor, u_pool: DistTe
     """c1 filter gradient straight from the pooled gradient (see
     vpx_pool_leaky_bwd_blocked / vpx_conv3d_bwd_filter_c4 in include/vpx.h)."""
     nvox = y.voxels()
+    ufr = frame_desc(y.n, y.c, y.d, y.h, y.w)
+    ws = WS.get(_lib.load().vpx_conv3d_workspace_bytes(x.c, y.c, 3, ctypes.addressof(ufr)))
+    flops = 2 * 27 * x.c * y.c * nvox
+    if pool_kind != "max" and _lib.load().vpx_get_precision() == 0:
+        # one kernel: pooled gradient -> u (in TMEM) -> filter gradient
+        with region(f"{tag}.wgrad", flops, 4 * (x.voxels() * x.c + nvox * y.c + u_pool.voxels() * u_pool.c)):
+            _lib.call("vpx_conv3d_bwd_filter_c4_pooled", x.ptr, x.desc, y.ptr, y.desc, u_pool.ptr, u_pool.desc,
+                      float(slope), 0, out.data_ptr(), 0, ws.data_ptr(), ws.numel() * 4, stream_ptr())
+        return out
     gb = WS2.get(nvox * y.c * 4)
     with region(f"{tag}_act.bwd", 0, 4 * (u_pool.voxels() * u_pool.c + 2 * nvox * y.c)):
         _lib.call("vpx_pool_leaky_bwd_blocked", y.ptr, y.desc, u_pool.ptr, u_pool.desc, gb.data_ptr(),
                   float(slope), int(pool_kind == "max"), stream_ptr())
-    ufr = frame_desc(y.n, y.c, y.d, y.h, y.w)
-    ws = WS.get(_lib.load().vpx_conv3d_workspace_bytes(x.c, y.c, 3, ctypes.addressof(ufr)))
-    with region(f"{tag}.wgrad", 2 * 27 * x.c * y.c * nvox, 4 * (x.voxels() * x.c + nvox * y.c + out.numel())):
+    with region(f"{tag}.wgrad", flops, 4 * (x.voxels() * x.c + nvox * y.c + out.numel())):
         _lib.call("vpx_conv3d_bwd_filter_c4", x.ptr, x.desc, gb.data_ptr(), ctypes.addressof(ufr), out.data_ptr(),
                   0, ws.data_ptr(), ws.numel() * 4, stream_ptr())
     return out

@@ -95,6 +95,14 @@ def test_first_block_fused_backward_and_c4_wgrad(shape, margins):
               W.data_ptr(), W.numel() * 4, stream_ptr())
     wg_ref = O.conv3d_bwd_filter(xf.to_ncdhw().cpu().numpy(), got, (3, 3, 3), (1, 1, 1))
     assert rel(wg.cpu().numpy(), wg_ref) < TF32_RTOL
+    # one-kernel variant: pooled gradient -> u in TMEM -> filter gradient; the
+    # pooled gradient arrives with the same D/H margins as x here
+    upf = Frame(n, 16, d // 2, h // 2, w // 2, margins, zero=True).load_ncdhw(uf.to_ncdhw())
+    wg2 = torch.zeros(16, 4, 3, 3, 3, device="cuda")
+    _lib.call("vpx_conv3d_bwd_filter_c4_pooled", xf.ptr, xf.desc, yf.ptr, yf.desc, upf.ptr, upf.desc, 0.3, 0,
+              wg2.data_ptr(), 0, W.data_ptr(), W.numel() * 4, stream_ptr())
+    assert rel(wg2.cpu().numpy(), wg_ref) < TF32_RTOL
+    assert rel(wg2.cpu().numpy(), wg.cpu().numpy()) < 1e-5  # same rounded operands, other summation order
 
 
 def test_tapbox_dgrad_all_margins():

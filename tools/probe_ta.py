@@ -62,10 +62,35 @@ def t_correct():
     check("ta_col_offset4", D[:, :64], A[:, 4:12] @ Bm[:, :8].T)
 
 
+def swz32b(addr):
+    return addr ^ (((addr >> 7) & 3) << 5)
+
+
+def t_mn_rows():
+    """A (u) in TMEM, B = x rows of 128 B (8 voxels x 4 ch) MN-major SW128_BASE32B,
+    N = 48: block 0 = chunk k, block 1 = chunk k+1 (LBO = one 128-byte row)."""
+    nch = 40
+    X = tf32(rng.standard_normal((nch, 32)))
+    img = Img(65536)
+    flat = X.reshape(-1)
+    for i in range(flat.size):
+        img.put_f32(swz32b(i * 4), flat[i])
+    for N in (48, 64):
+        for s in (0, 1, 3):
+            A = tf32(rng.standard_normal((128, 16)))
+            Bm = np.zeros((N, 8), np.float32)
+            for n in range(N):
+                for k in range(8):
+                    Bm[n, k] = X[8 * s + k + n // 32, n % 32]
+            ops = [(256, sdesc(8 * s * 128, 128, 512, 1), idesc(128, N, False, True), 2)]
+            D = run_ta(img.b, ops, A, N)
+            check(f"ta_mnrows_N{N}_s{s}", D[:, :N], A[:, :8] @ Bm.T)
+
+
 def t_rate():
     cyc = torch.zeros(1, dtype=torch.int64, device="cuda")
     res = {}
-    for N, n_acc in ((16, 8), (32, 8), (64, 4), (128, 2), (256, 1)):
+    for N, n_acc in ((16, 8), (32, 8), (48, 8), (64, 4), (96, 2), (128, 2), (256, 1)):
         for mode in (0, 2):
             _lib.call("vpx_probe_mma_rate2", N, n_acc, mode, 4096, cyc.data_ptr(),
                       torch.cuda.current_stream().cuda_stream)
@@ -78,6 +103,7 @@ def t_rate():
 
 if __name__ == "__main__":
     t_correct()
+    t_mn_rows()
     t_rate()
     out = sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/probe_ta.json"
     json.dump(RESULTS, open(out, "w"), indent=1)
