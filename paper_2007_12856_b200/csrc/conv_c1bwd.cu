@@ -19,8 +19,8 @@
 // shared-memory A operand.
 //
 // Warp roles: w0 TMA (x rows into a 4-row ring per depth tap, y and pooled
-// gradient rows), w1 MMA issuer, w2 TMEM owner, w4..w7 u producers and
-// epilogue (fold D into wg, split-K partial per CTA, fixed-order reduction
+// gradient rows), w1 MMA issuer, w2 TMEM owner, w4..w11 u producers (w4..w7 also the
+// epilogue: fold D into wg, split-K partial per CTA, fixed-order reduction
 // afterwards -> deterministic).
 // Reference semantics: reference pkg/src/voxpar/kernels/_hot.pyx:70-93 (filter
 // gradient), layers/reference.py:170-173 (avg pool bwd), :231-236 (leaky bwd).
@@ -40,7 +40,6 @@ struct C1Params {
   int y_off_d, y_off_h;     // y frame margins
   int up_off_d, up_off_h;   // pooled-gradient frame margins
   float slope;
-  int rnd;                  // round u to nearest TF32
   float* part;              // [P][16][4][27]
 };
 
@@ -62,7 +61,7 @@ struct C1Cfg {
 };
 
 template <int W>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
     c1_pooled_wgrad_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap ymap,
                            const __grid_constant__ CUtensorMap upmap, const C1Params p) {
   using Cfg = C1Cfg<W>;
@@ -83,7 +82,7 @@ __global__ void __launch_bounds__(256, 1)
     for (int i = 0; i < 2; ++i) {
       vpx::mbar_init(&xfull[i], 1);
       vpx::mbar_init(&yfull[i], 1);
-      vpx::mbar_init(&yempty[i], 4);
+      vpx::mbar_init(&yempty[i], 8);
       vpx::mbar_init(&rowdone[i], 1);
     }
     for (int i = 0; i < kASlots; ++i) {
@@ -168,29 +167,49 @@ __global__ void __launch_bounds__(256, 1)
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------- u producers
-    const int q = warp - 4, m = q * 32 + lane, dd = m >> 4, co = m & 15;
+    // two producer warps per TMEM lane quarter (warps 4..7 and 8..11) take
+    // alternate K-step slots; each computes its next slot while the previous
+    // tcgen05.st drains
+    const int q = warp & 3, h = (warp - 4) >> 2, m = q * 32 + lane, dd = m >> 4, co = m & 15;
     const uint32_t lane_addr = tbase + (static_cast<uint32_t>(q * 32) << 16) + kACol;
+    const float slope = p.slope;
+    auto make_u = [&](int s, uint32_t ya0, uint32_t ua0, float (&v)[8]) {
+      // u voxel of column kk: 8k + d + 1 with k = 8s + kk - 1  ->  b + 8 kk
+      const int b = 64 * s - 7 + dd;
+      const uint32_t ya = ya0 + b * 64, ua = ua0 + (b >> 1) * 64;
+      if (s > 0 && 64 * s + 56 < W) {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const float gp = vpx::lds_f32(ua + kk * 256) * 0.125f;
+          const float yv = vpx::lds_f32(ya + kk * 512);
+          v[kk] = vpx::tf32_rn(yv >= 0.f ? gp : slope * gp);
+        }
+      } else {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          v[kk] = 0.f;
+          if (static_cast<unsigned>(b + 8 * kk) < static_cast<unsigned>(W)) {
+            const float gp = vpx::lds_f32(ua + kk * 256) * 0.125f;
+            const float yv = vpx::lds_f32(ya + kk * 512);
+            v[kk] = vpx::tf32_rn(yv >= 0.f ? gp : slope * gp);
+          }
+        }
+      }
+    };
     for (long long r = r0; r < r1; ++r) {
       const int i = static_cast<int>(r - r0);
       vpx::mbar_wait(&yfull[i & 1], (i >> 1) & 1);
-      const float* yrow = reinterpret_cast<const float*>(ys + (i & 1) * Cfg::YB);
-      const float* urow = reinterpret_cast<const float*>(us + (i & 1) * Cfg::UB);
-      for (int s = 0; s < KS; ++s) {
+      const uint32_t ya0 = vpx::smem_u32(ys + (i & 1) * Cfg::YB) + co * 4;
+      const uint32_t ua0 = vpx::smem_u32(us + (i & 1) * Cfg::UB) + co * 4;
+      int s = ((i * KS) & 1) == h ? 0 : 1;  // first K-step of this row in my slot parity
+      float v[8];
+      if (s < KS) make_u(s, ya0, ua0, v);
+#pragma unroll 1
+      for (; s < KS; s += 2) {
         const int g = i * KS + s, slot = g & (kASlots - 1);
-        float v[8];
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const int vox = 64 * s + 8 * kk - 7 + dd;  // u voxel 8k + d + 1, k = 8s + kk - 1
-          float val = 0.f;
-          if (vox >= 0 && vox < W) {
-            const float gp = urow[(vox >> 1) * 16 + co] / 8.0f;
-            val = yrow[vox * 16 + co] >= 0.f ? gp : p.slope * gp;
-            if (p.rnd) val = vpx::tf32_rn(val);
-          }
-          v[kk] = val;
-        }
         vpx::mbar_wait(&emptyA[slot], ((g >> 3) & 1) ^ 1);
         vpx::tmem_st8(lane_addr + slot * 8, v);
+        if (s + 2 < KS) make_u(s + 2, ya0, ua0, v);  // overlaps the store
         vpx::tmem_st_wait();
         vpx::tc_fence_before();
         __syncwarp();
@@ -203,13 +222,13 @@ __global__ void __launch_bounds__(256, 1)
 
   // ---------------------------------------------------------------- epilogue
   const bool have = r1 > r0;
-  if (warp >= 4 && have) {
+  if (warp >= 4 && warp < 8 && have) {
     vpx::mbar_wait(&tfull, 0);
     vpx::tc_fence_after();
   }
   __syncthreads();  // all TMA landed and consumed, all MMAs retired: reuse the x ring
   float* red = reinterpret_cast<float*>(smem);  // [d][co][ci][27]
-  if (warp >= 4) {
+  if (warp >= 4 && warp < 8) {
     const int q = warp - 4, m = q * 32 + lane, dd = m >> 4;
 #pragma unroll 1
     for (int ab = 0; ab < 9; ++ab) {
@@ -226,12 +245,15 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
         for (int j = 0; j < kNA; ++j) v[j] = 0.f;
       }
+      // x voxel offset t = e (+8 for chunk k+1) = d + c; compile-time column
+      // indices keep v[] in registers
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const int t = dd + c;  // x voxel offset e (+8 for chunk k+1) = d + c
-        const int nb = (t >> 3) * 32 + (t & 7) * 4;
+      for (int t = 0; t < 10; ++t) {
+        const int c = t - dd;
+        if (c >= 0 && c <= 2) {
 #pragma unroll
-        for (int ci = 0; ci < 4; ++ci) red[(m * 4 + ci) * 27 + ab * 3 + c] = v[nb + ci];
+          for (int ci = 0; ci < 4; ++ci) red[(m * 4 + ci) * 27 + ab * 3 + c] = v[(t >> 3) * 32 + (t & 7) * 4 + ci];
+        }
       }
     }
   }
@@ -256,7 +278,7 @@ int launch_c1(const CUtensorMap& xm, const CUtensorMap& ym, const CUtensorMap& u
   static_assert(smem <= 227 * 1024, "smem");
   auto kern = c1_pooled_wgrad_kernel<W>;
   VPX_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  kern<<<p.P, 256, smem, st>>>(xm, ym, um, p);
+  kern<<<p.P, 384, smem, st>>>(xm, ym, um, p);
   VPX_LAUNCH_CHECK();
   return VPX_OK;
 }
@@ -297,7 +319,6 @@ int conv_wgrad_c1_pooled(const float* x, const Frame& xf, const float* y, const 
   p.up_off_d = uf.md;
   p.up_off_h = uf.mh;
   p.slope = slope;
-  p.rnd = 1;
   p.part = part;
   const int W = yf.w;
   int xch = 0;
