@@ -24,6 +24,8 @@
 // afterwards -> deterministic).
 // Reference semantics: reference pkg/src/voxpar/kernels/_hot.pyx:70-93 (filter
 // gradient), layers/reference.py:170-173 (avg pool bwd), :231-236 (leaky bwd).
+#include <cstdlib>
+
 #include "conv_common.h"
 #include "conv_simt.h"
 #include "vpx_host.h"
@@ -31,6 +33,12 @@
 #include "vpx_round.cuh"
 
 namespace {
+
+__device__ __forceinline__ long long globaltimer_ns() {
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 struct C1Params {
   int n, d, h;              // u (= y) interior extents, W is the template parameter
@@ -40,6 +48,7 @@ struct C1Params {
   int y_off_d, y_off_h;     // y frame margins
   int up_off_d, up_off_h;   // pooled-gradient frame margins
   float slope;
+  int dbg;                  // profiling switch (VPX_C1_DEBUG): 1 skip u math, 2 skip TMEM stores
   float* part;              // [P][16][4][27]
 };
 
@@ -103,7 +112,7 @@ __global__ void __launch_bounds__(384, 1)
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
-    if (vpx::elect_one()) {
+    if (p.dbg < 4 && vpx::elect_one()) {
       for (long long r = r0; r < r1; ++r) {
         const int i = static_cast<int>(r - r0);
         long long t = r;
@@ -112,10 +121,14 @@ __global__ void __launch_bounds__(384, 1)
         const int z = t % p.d;
         const int n = static_cast<int>(t / p.d);
         const bool reset = (i == 0) || (y == 0);
+        // warm L2 with the x rows two steps ahead (the ring only holds one
+        // row of lookahead per depth tap)
+        if (r + 2 < r1 && y + 3 < p.h + p.x_off_h)
+          for (int a = 0; a < 3; ++a) vpx::tma_prefetch_5d(&xmap, 0, -1, y + 3 + p.x_off_h, z - 1 + a + p.x_off_d, n);
         // the x ring slot of row y+1 last served u row i-2; a reset reloads all
         // three rows per depth tap, so u row i-1 must be done
-        if (reset && i >= 1) vpx::mbar_wait(&rowdone[(i - 1) & 1], ((i - 1) >> 1) & 1);
-        else if (i >= 2) vpx::mbar_wait(&rowdone[i & 1], ((i - 2) >> 1) & 1);
+        if (reset && i >= 1) vpx::mbar_wait_sleep(&rowdone[(i - 1) & 1], ((i - 1) >> 1) & 1);
+        else if (i >= 2) vpx::mbar_wait_sleep(&rowdone[i & 1], ((i - 2) >> 1) & 1);
         const int nrow = reset ? 3 : 1;
         vpx::mbar_arrive_expect_tx(&xfull[i & 1], 3 * nrow * Cfg::XCH * 128);
 #pragma unroll 1
@@ -126,7 +139,19 @@ __global__ void __launch_bounds__(384, 1)
                              z - 1 + a + p.x_off_d, n);
           }
         }
-        vpx::mbar_wait(&yempty[i & 1], ((i >> 1) & 1) ^ 1);
+      }
+    }
+  } else if (warp == 3) {
+    // ------------------------------------- y / pooled-gradient rows (2 stages)
+    if (p.dbg < 4 && vpx::elect_one()) {
+      for (long long r = r0; r < r1; ++r) {
+        const int i = static_cast<int>(r - r0);
+        long long t = r;
+        const int y = t % p.h;
+        t /= p.h;
+        const int z = t % p.d;
+        const int n = static_cast<int>(t / p.d);
+        vpx::mbar_wait_sleep(&yempty[i & 1], ((i >> 1) & 1) ^ 1);
         vpx::mbar_arrive_expect_tx(&yfull[i & 1], Cfg::YB + Cfg::UB);
         vpx::tma_load_5d(ys + (i & 1) * Cfg::YB, &ymap, &yfull[i & 1], 0, 0, y + p.y_off_h, z + p.y_off_d, n);
         vpx::tma_load_5d(us + (i & 1) * Cfg::UB, &upmap, &yfull[i & 1], 0, 0, (y >> 1) + p.up_off_h,
@@ -135,35 +160,49 @@ __global__ void __launch_bounds__(384, 1)
     }
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA
+    // The issue loop must stay well under the ~25 cycles an N=48 MMA takes:
+    // descriptors are built once per row and advanced by one add per K-step,
+    // the K-step loop is fully unrolled (KS is a compile-time constant).
     constexpr uint32_t idesc = vpx::make_idesc(2, 128, kNA, false, true);
     const uint32_t xb = vpx::smem_u32(xs);
-    for (long long r = r0; r < r1; ++r) {
-      const int i = static_cast<int>(r - r0);
-      const int y = static_cast<int>(r % p.h);
-      vpx::mbar_wait(&xfull[i & 1], (i >> 1) & 1);
-      for (int s = 0; s < KS; ++s) {
-        const int g = i * KS + s, slot = g & (kASlots - 1);
-        vpx::mbar_wait(&fullA[slot], (g >> 3) & 1);
-        vpx::tc_fence_after();
-        if (vpx::elect_one()) {
+    const bool skip_waits = p.dbg >= 4;
+    const long long tclk0 = clock64();
+    const long long tgl0 = globaltimer_ns();
+    if (vpx::elect_one()) {  // one thread issues everything (no per-step warp sync)
+      int g = 0;
+      int y = static_cast<int>(r0 % p.h);
+      for (long long r = r0; r < r1; ++r) {
+        const int i = static_cast<int>(r - r0);
+        if (!skip_waits) vpx::mbar_wait(&xfull[i & 1], (i >> 1) & 1);
+        uint64_t bd[9];  // B descriptors of the 9 (depth, height) taps at K-step 0
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+          for (int b = 0; b < 3; ++b)
+            bd[a * 3 + b] = vpx::make_sdesc(xb + (a * 4 + ((y - 1 + b) & 3)) * XROW, 128, 512, 1);
+#pragma unroll
+        for (int s = 0; s < KS; ++s, ++g) {
+          const int slot = g & (kASlots - 1);
+          if (!skip_waits) vpx::mbar_wait(&fullA[slot], (g >> 3) & 1);
+          vpx::tc_fence_after();
           const uint32_t acol = tbase + kACol + slot * 8;
+          const uint32_t acc = (i > 0 || s > 0) ? 1u : 0u;
 #pragma unroll
-          for (int a = 0; a < 3; ++a) {
-#pragma unroll
-            for (int b = 0; b < 3; ++b) {
-              const uint32_t row = xb + (a * 4 + ((y - 1 + b) & 3)) * XROW + s * 8 * 128;
-              const uint64_t bdesc = vpx::make_sdesc(row, 128, 512, 1);
-              vpx::umma_tf32_ta(tbase + (a * 3 + b) * kNA, acol, bdesc, idesc, (i > 0 || s > 0) ? 1u : 0u);
-            }
-          }
+          for (int ab = 0; ab < 9; ++ab)  // K-step s starts 8 chunk rows (1024 B) further
+            vpx::umma_tf32_ta(tbase + ab * kNA, acol, bd[ab] + static_cast<uint64_t>(s * 64), idesc, acc);
           vpx::umma_commit(&emptyA[slot]);
-          if (s == KS - 1) {
-            vpx::umma_commit(&rowdone[i & 1]);
-            if (r == r1 - 1) vpx::umma_commit(&tfull);
-          }
         }
-        __syncwarp();
+        vpx::umma_commit(&rowdone[i & 1]);
+        if (r == r1 - 1) vpx::umma_commit(&tfull);
+        y = (y + 1 == p.h) ? 0 : y + 1;
       }
+    }
+    __syncwarp();
+    if (p.dbg && pidx == 0 && lane == 0) {
+      vpx::mbar_wait(&tfull, 0);
+      const long long c = clock64() - tclk0, ns = globaltimer_ns() - tgl0;
+      printf("c1 dbg %d: CTA0 %lld MMAs, %.1f cycles/MMA, %.2f GHz\n", p.dbg, (r1 - r0) * KS * 9,
+             double(c) / double((r1 - r0) * KS * 9), double(c) / double(ns));
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------- u producers
@@ -196,21 +235,28 @@ __global__ void __launch_bounds__(384, 1)
         }
       }
     };
-    for (long long r = r0; r < r1; ++r) {
+    for (long long r = r0; r < (p.dbg >= 4 ? r0 : r1); ++r) {
       const int i = static_cast<int>(r - r0);
-      vpx::mbar_wait(&yfull[i & 1], (i >> 1) & 1);
+      vpx::mbar_wait_sleep(&yfull[i & 1], (i >> 1) & 1, 64);
       const uint32_t ya0 = vpx::smem_u32(ys + (i & 1) * Cfg::YB) + co * 4;
       const uint32_t ua0 = vpx::smem_u32(us + (i & 1) * Cfg::UB) + co * 4;
       int s = ((i * KS) & 1) == h ? 0 : 1;  // first K-step of this row in my slot parity
       float v[8];
-      if (s < KS) make_u(s, ya0, ua0, v);
+      if (s < KS) {
+        if (p.dbg) {
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) v[kk] = 0.f;
+        } else {
+          make_u(s, ya0, ua0, v);
+        }
+      }
 #pragma unroll 1
       for (; s < KS; s += 2) {
         const int g = i * KS + s, slot = g & (kASlots - 1);
-        vpx::mbar_wait(&emptyA[slot], ((g >> 3) & 1) ^ 1);
-        vpx::tmem_st8(lane_addr + slot * 8, v);
-        if (s + 2 < KS) make_u(s + 2, ya0, ua0, v);  // overlaps the store
-        vpx::tmem_st_wait();
+        vpx::mbar_wait_sleep(&emptyA[slot], ((g >> 3) & 1) ^ 1);
+        if (p.dbg != 2) vpx::tmem_st8(lane_addr + slot * 8, v);
+        if (s + 2 < KS && !p.dbg) make_u(s + 2, ya0, ua0, v);  // overlaps the store
+        if (p.dbg != 2) vpx::tmem_st_wait();
         vpx::tc_fence_before();
         __syncwarp();
         if (lane == 0) vpx::mbar_arrive(&fullA[slot]);
@@ -223,7 +269,7 @@ __global__ void __launch_bounds__(384, 1)
   // ---------------------------------------------------------------- epilogue
   const bool have = r1 > r0;
   if (warp >= 4 && warp < 8 && have) {
-    vpx::mbar_wait(&tfull, 0);
+    vpx::mbar_wait_sleep(&tfull, 0, 256);
     vpx::tc_fence_after();
   }
   __syncthreads();  // all TMA landed and consumed, all MMAs retired: reuse the x ring
@@ -299,7 +345,7 @@ int c1_pooled_supported(const Frame& xf, const Frame& yf, const Frame& uf) {
 
 int c1_pooled_parts(const Frame& yf) {
   const long long rows = (long long)yf.n * yf.d * yf.h;
-  long long P = num_sms();
+  long long P = getenv("VPX_C1_P") ? atoi(getenv("VPX_C1_P")) : num_sms();
   if (P > rows) P = rows;
   return static_cast<int>(P < 1 ? 1 : P);
 }
@@ -319,6 +365,7 @@ int conv_wgrad_c1_pooled(const float* x, const Frame& xf, const float* y, const 
   p.up_off_d = uf.md;
   p.up_off_h = uf.mh;
   p.slope = slope;
+  p.dbg = getenv("VPX_C1_DEBUG") ? atoi(getenv("VPX_C1_DEBUG")) : 0;
   p.part = part;
   const int W = yf.w;
   int xch = 0;

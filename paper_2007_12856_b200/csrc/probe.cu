@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(128, 1)
   __shared__ uint64_t bar;
   __shared__ uint32_t tmem_base;
   const int tid = threadIdx.x, warp = tid >> 5;
-  for (int i = tid; i < 65536 / 4; i += blockDim.x) reinterpret_cast<float*>(smem)[i] = 1.0f;
+  for (int i = tid; i < 100 * 1024 / 4; i += blockDim.x) reinterpret_cast<float*>(smem)[i] = 1.0f;
   vpx::fence_proxy_async_smem();
   if (warp == 0) vpx::tmem_alloc<512>(&tmem_base);
   if (tid == 0) {
@@ -150,41 +150,69 @@ __global__ void __launch_bounds__(128, 1)
 
 // Same, with the issue loop in the canonical warp-uniform form (whole warp 1
 // iterates; one elected lane issues an unrolled burst of NACC MMAs).
-template <int N, int NACC, int MODE>  // MODE 0 tf32, 1 bf16, 2 tf32 with A in TMEM (cols 256..)
+// MODE 0 tf32, 1 bf16, 2 tf32 with A in TMEM (cols 256..), 3 = 2 with B MN-major
+// SWIZZLE_128B_BASE32B (LBO 128 B, SBO 512 B: the voxel-row operand of conv_c1bwd.cu)
+template <int N, int NACC, int MODE>
 __global__ void __launch_bounds__(128, 1) probe_rate2_kernel(int n_iter, long long* cycles) {
   constexpr bool BF16 = MODE == 1;
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t bar;
+  __shared__ uint64_t bar, bar2;
   __shared__ uint32_t tmem_base;
   const int tid = threadIdx.x, warp = tid >> 5;
-  for (int i = tid; i < 65536 / 4; i += blockDim.x) reinterpret_cast<float*>(smem)[i] = 1.0f;
+  // MODE 9 = MODE 8 with pseudo-random operands in smem and TMEM
+  for (int i = tid; i < 100 * 1024 / 4; i += blockDim.x)
+    reinterpret_cast<float*>(smem)[i] = MODE == 9 ? __uint_as_float((i * 2654435761u) & 0xbfffe000u | 0x3e000000u) : 1.0f;
   vpx::fence_proxy_async_smem();
   if (warp == 0) vpx::tmem_alloc<512>(&tmem_base);
   if (tid == 0) {
     vpx::mbar_init(&bar, 1);
+    vpx::mbar_init(&bar2, 1);
     vpx::fence_barrier_init();
   }
   vpx::tc_fence_before();
   __syncthreads();
   vpx::tc_fence_after();
+  if (MODE == 9) {
+    float v[16];
+    for (int c = 0; c < 512; c += 16) {
+      for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(((tid * 977 + c * 131 + j * 7919) * 2654435761u) & 0xbfffe000u | 0x3e000000u);
+      vpx::tmem_st16(tmem_base + (static_cast<uint32_t>(32 * warp) << 16) + c, v);
+    }
+    vpx::tmem_st_wait();
+    vpx::tc_fence_before();
+    __syncthreads();
+    vpx::tc_fence_after();
+  }
   const uint32_t tbase = tmem_base;
   if (warp == 1) {
     const uint32_t s0 = vpx::smem_u32(smem);
     const uint64_t a = vpx::make_sdesc(s0, 2048, 128, 0);
     const uint64_t b = vpx::make_sdesc(s0 + 32768, 4096, 128, 0);
     constexpr uint32_t idesc = vpx::make_idesc(BF16 ? 1 : 2, 128, N, false, false);
+    constexpr uint32_t idesc_mn = vpx::make_idesc(2, 128, N, false, true);
+    const uint64_t bmn = vpx::make_sdesc(s0 + 32768, 128, 512, 1);
+    const uint64_t bmn9 = vpx::make_sdesc(s0, 128, 512, 1);
     long long t0 = clock64();
     for (int i = 0; i < n_iter; i += NACC) {
+      if (MODE == 6) vpx::tc_fence_after();
       if (vpx::elect_one()) {
 #pragma unroll
         for (int j = 0; j < NACC; ++j) {
           if (MODE == 2)
             vpx::umma_tf32_ta(tbase + (j * N) % 256, tbase + 256 + 8 * (j & 7), b, idesc, i > 0);
+          else if (MODE == 7)
+            vpx::umma_tf32_ta(tbase + j * N, tbase + 432 + 8 * (j & 7), bmn + 64 * (j & 3), idesc_mn, i > 0);
+          else if (MODE == 8 || MODE == 9)  // 9 B rows 10 KB apart, as in conv_c1bwd.cu
+            vpx::umma_tf32_ta(tbase + j * N, tbase + 432 + 8 * (i & 7), bmn9 + 640 * j, idesc_mn, i > 0);
+          else if (MODE >= 3)
+            vpx::umma_tf32_ta(tbase + (j * N) % 256, tbase + 256 + 8 * (j & 7), bmn + 64 * (j & 3), idesc_mn,
+                              i > 0);
           else if (BF16)
             vpx::umma_f16(tbase + j * N, a + 2 * (j & 1), b, idesc, i > 0);
           else
             vpx::umma_tf32(tbase + j * N, a + 2 * (j & 1), b, idesc, i > 0);
         }
+        if (MODE == 5) vpx::umma_commit(&bar2);
       }
       __syncwarp();
     }
@@ -202,8 +230,8 @@ __global__ void __launch_bounds__(128, 1) probe_rate2_kernel(int n_iter, long lo
 template <int N, int NACC, int MODE>
 static int launch_rate2(int n_iter, long long* cycles, cudaStream_t st) {
   VPX_CHECK_CUDA(cudaFuncSetAttribute(probe_rate2_kernel<N, NACC, MODE>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 65536 + 1024));
-  probe_rate2_kernel<N, NACC, MODE><<<1, 128, 65536 + 1024, st>>>(n_iter, cycles);
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024 + 1024));
+  probe_rate2_kernel<N, NACC, MODE><<<1, 128, 100 * 1024 + 1024, st>>>(n_iter, cycles);
   VPX_LAUNCH_CHECK();
   return VPX_OK;
 }
@@ -215,11 +243,17 @@ extern "C" int vpx_probe_mma_rate2(int N, int n_acc, int bf16, int n_iter, long 
   cudaStream_t st = static_cast<cudaStream_t>(stream);
 #define RATE_CASE(n, a)                                                         \
   if (N == n && n_acc == a)                                                     \
-    return bf16 == 2 ? launch_rate2<n, a, 2>(n_iter, cycles, st)                \
+    return bf16 == 9 ? launch_rate2<n, a, 9>(n_iter, cycles, st)                \
+           : bf16 == 8 ? launch_rate2<n, a, 8>(n_iter, cycles, st)              \
+           : bf16 == 7 ? launch_rate2<n, a, 7>(n_iter, cycles, st)              \
+           : bf16 == 6 ? launch_rate2<n, a, 6>(n_iter, cycles, st)              \
+           : bf16 == 5 ? launch_rate2<n, a, 5>(n_iter, cycles, st)              \
+           : bf16 == 3 ? launch_rate2<n, a, 3>(n_iter, cycles, st)              \
+           : bf16 == 2 ? launch_rate2<n, a, 2>(n_iter, cycles, st)              \
            : bf16    ? launch_rate2<n, a, 1>(n_iter, cycles, st)                \
                      : launch_rate2<n, a, 0>(n_iter, cycles, st);
   RATE_CASE(16, 1) RATE_CASE(16, 4) RATE_CASE(16, 8) RATE_CASE(32, 1) RATE_CASE(32, 4)
-  RATE_CASE(32, 8) RATE_CASE(48, 8) RATE_CASE(96, 2) RATE_CASE(64, 1) RATE_CASE(64, 4) RATE_CASE(64, 8) RATE_CASE(128, 1)
+  RATE_CASE(32, 8) RATE_CASE(48, 8) RATE_CASE(48, 9) RATE_CASE(96, 2) RATE_CASE(64, 1) RATE_CASE(64, 4) RATE_CASE(64, 8) RATE_CASE(128, 1)
   RATE_CASE(128, 2) RATE_CASE(256, 1) RATE_CASE(256, 2)
 #undef RATE_CASE
   VPX_FAIL(VPX_ERR_UNSUPPORTED, "rate2 case");
@@ -228,8 +262,8 @@ extern "C" int vpx_probe_mma_rate2(int N, int n_acc, int bf16, int n_iter, long 
 extern "C" int vpx_probe_mma_rate(int N, int n_iter, int a_layout, int n_acc, int bf16,
                                   long long* cycles, void* stream) {
   VPX_CHECK_CUDA(cudaFuncSetAttribute(probe_rate_kernel,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 65536 + 1024));
-  probe_rate_kernel<<<1, 128, 65536 + 1024, static_cast<cudaStream_t>(stream)>>>(N, n_iter, a_layout,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024 + 1024));
+  probe_rate_kernel<<<1, 128, 100 * 1024 + 1024, static_cast<cudaStream_t>(stream)>>>(N, n_iter, a_layout,
                                                                                n_acc, bf16, cycles);
   VPX_LAUNCH_CHECK();
   return VPX_OK;

@@ -90,14 +90,16 @@ def t_mn_rows():
 def t_rate():
     cyc = torch.zeros(1, dtype=torch.int64, device="cuda")
     res = {}
-    for N, n_acc in ((16, 8), (32, 8), (48, 8), (64, 4), (96, 2), (128, 2), (256, 1)):
-        for mode in (0, 2):
+    for N, n_acc in ((16, 8), (32, 8), (48, 8), (48, 9), (64, 4), (96, 2), (128, 2), (256, 1)):
+        for mode in ((0, 2, 3, 5, 6, 7, 8, 9) if (N, n_acc) == (48, 9) else (0, 2, 3)):
             _lib.call("vpx_probe_mma_rate2", N, n_acc, mode, 4096, cyc.data_ptr(),
                       torch.cuda.current_stream().cuda_stream)
             torch.cuda.synchronize()
             c = int(cyc.item()) / 4096
-            res[f"N{N}_{'tmemA' if mode == 2 else 'smemA'}"] = c
-            print(f"N={N:3d} A={'tmem' if mode == 2 else 'smem'}: {c:.1f} cycles/MMA")
+            tag = {0: "smemA", 2: "tmemA", 3: "tmemA_mnB", 5: "tmemA_mnB_commit", 6: "tmemA_mnB_fence",
+                   7: "tmemA_mnB_acc0-431", 8: "tmemA_mnB_9rows", 9: "tmemA_mnB_9rows_random"}[mode]
+            res[f"N{N}_acc{n_acc}_{tag}"] = c
+            print(f"N={N:3d} acc={n_acc} {tag}: {c:.1f} cycles/MMA")
     RESULTS["rate"] = res
 
 
