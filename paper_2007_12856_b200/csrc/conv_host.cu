@@ -5,6 +5,8 @@
 // bwd_data,bwd_filter} (reference pkg/src/voxpar/kernels/__init__.py:63-72,
 // cyext.py:20-45): same math, device-resident NDHWC halo frames instead of
 // host NCDHW arrays, explicit workspace instead of internal allocation.
+#include <cstdlib>
+
 #include "conv_common.h"
 #include "conv_simt.h"
 #include "ops_vec.h"
@@ -126,6 +128,59 @@ static int rowwin_run(const float* in, const Frame& inf, const float* wpack, int
   return launch_rowwin_any(map, p, cin_eff, cout_eff, st);
 }
 
+// Same launch for the height-taps-in-N kernel (conv_rowh.cu): bands of RB
+// output rows, each streaming RB + 2 input rows.
+static int rowh_run(const float* in, const Frame& inf, const float* wpack, int cin_eff, int cout_eff, float* out,
+                    const Frame& of, int zlo, int zhi, int ylo, int yhi, int wout, cudaStream_t st, int act = 0,
+                    float slope = 0.f) {
+  CUtensorMap map;
+  {
+    const uint64_t Wf = inf.w + 2 * inf.mw, Hf = inf.h + 2 * inf.mh, Df = inf.d + 2 * inf.md;
+    uint64_t dims[5] = {(uint64_t)inf.c, Wf, Hf, Df, (uint64_t)inf.n};
+    uint64_t strides[4] = {(uint64_t)inf.c * 4, Wf * inf.c * 4, Hf * Wf * inf.c * 4, Df * Hf * Wf * inf.c * 4};
+    uint32_t box[5] = {4, 130, 1, 3, 1};
+    if (int rc = encode_tiled(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float*>(in), dims, strides, box,
+                              CU_TENSOR_MAP_SWIZZLE_NONE))
+      return rc;
+  }
+  ConvRowParams p{};
+  p.zlo = zlo;
+  p.zhi = zhi;
+  p.ylo = ylo;
+  p.yhi = yhi;
+  p.nxseg = wout / 128;
+  const long long cols = (long long)inf.n * (zhi - zlo) * p.nxseg;
+  const int H = yhi - ylo;
+  int rb = 64;  // band height: long bands (edge rows cost 2/(rb+2)) but >= 8 tasks per SM
+  while (rb > 16 && cols * ((H + rb - 1) / rb) < 8LL * num_sms()) rb /= 2;
+  if (rb > H) rb = H;
+  p.ngy = rb;
+  p.num_tiles = static_cast<int>(cols * ((H + rb - 1) / rb));
+  p.in_off_d = inf.md;
+  p.in_off_h = inf.mh;
+  p.in_off_w = inf.mw;
+  p.wpack = wpack;
+  p.out = out;
+  const long long Wf = of.w + 2 * of.mw, Hf = of.h + 2 * of.mh, Df = of.d + 2 * of.md;
+  p.out_sw = of.c;
+  p.out_sh = Wf * of.c;
+  p.out_sd = Hf * Wf * of.c;
+  p.out_sn = Df * Hf * Wf * of.c;
+  p.out_off_d = of.md;
+  p.out_off_h = of.mh;
+  p.out_off_w = of.mw;
+  p.act = act;
+  p.slope = slope;
+  p.rnd = of.rnd;
+  return launch_rowh_any(map, p, cin_eff, cout_eff, st);
+}
+
+static bool rowh_off() {
+  static int v = -1;
+  if (v < 0) v = getenv("VPX_NO_ROWH") != nullptr;
+  return v != 0;
+}
+
 static int pack(const float* w, int cout, int cin, int mode, float* dst, cudaStream_t st) {
   const int I = mode ? cout : cin, O = mode ? cin : cout;
   int R, CG;
@@ -152,6 +207,10 @@ extern "C" long long vpx_conv3d_workspace_bytes(int cin, int cout, int k, const 
   if (tc > parts) parts = tc;
   const long long tb = vpx::tapbox_workspace_bytes(cin, cout);
   if (tb > packed) packed = tb;
+  const long long rh = vpx::rowh_packed_bytes(cin, cout) > vpx::rowh_packed_bytes(cout, cin)
+                           ? vpx::rowh_packed_bytes(cin, cout)
+                           : vpx::rowh_packed_bytes(cout, cin);
+  if (rh > packed) packed = rh;
   return ((packed + 255) / 256) * 256 + ((parts + 255) / 256) * 256;
 }
 
@@ -171,6 +230,12 @@ extern "C" int vpx_conv3d_fwd_act(const float* x, const int* xfr, const float* w
   const int cin = xf.c, cout = yf.c;
   int R, CG;
   const bool tc = vpx::precision() == 0;
+  if (tc && k == 3 && stride == 1 && yf.w % 128 == 0 && vpx::rowh_supported(cin, cout) && !vpx::rowh_off()) {
+    if (ws_bytes < vpx::rowh_packed_bytes(cin, cout)) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "workspace too small");
+    float* wpack = static_cast<float*>(ws);
+    if (int rc = vpx::rowh_pack(w, cout, cin, 0, wpack, st)) return rc;
+    return vpx::rowh_run(x, xf, wpack, cin, cout, y, yf, 0, yf.d, 0, yf.h, yf.w, st, act, slope);
+  }
   if (tc && k == 3 && stride == 1 && yf.w % 128 == 0 && vpx::rowwin_config(cin, cout, &R, &CG)) {
     if (ws_bytes < vpx::packed_floats(cin, cout) * 4) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "workspace too small");
     float* wpack = static_cast<float*>(ws);
@@ -204,6 +269,13 @@ extern "C" int vpx_conv3d_bwd_data(const float* u, const int* ufr, const float* 
   const int cout = uf.c, cin = gf.c;
   int R, CG;
   const bool tc = vpx::precision() == 0;
+  if (tc && k == 3 && stride == 1 && gf.mw == 0 && gf.w % 128 == 0 && vpx::rowh_supported(cout, cin) &&
+      !vpx::rowh_off()) {
+    if (ws_bytes < vpx::rowh_packed_bytes(cout, cin)) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "workspace too small");
+    float* wpack = static_cast<float*>(ws);
+    if (int rc = vpx::rowh_pack(w, cout, cin, 1, wpack, st)) return rc;
+    return vpx::rowh_run(u, uf, wpack, cout, cin, xg, gf, -gf.md, gf.d + gf.md, -gf.mh, gf.h + gf.mh, gf.w, st);
+  }
   if (tc && k == 3 && stride == 1 && gf.mw == 0 && gf.w % 128 == 0 &&
       vpx::rowwin_config(cout, cin, &R, &CG)) {
     if (ws_bytes < vpx::packed_floats(cin, cout) * 4) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "workspace too small");

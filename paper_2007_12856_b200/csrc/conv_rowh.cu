@@ -1,0 +1,337 @@
+// Implicit-GEMM 3x3x3 convolution on tcgen05 for narrow outputs (16/32
+// channels): the three height taps go into the MMA's N dimension.
+//
+// The row-window kernel (conv_rowwin.cu) issues one M=128 x N=COUT MMA per
+// tap; with COUT = 16/32 every MMA still reads the whole 4 KB A tile from
+// shared memory, so it runs at the A-read rate (~40 cycles) for a small N.
+// Here the input row r is the unit of work: for each (depth tap a, width tap
+// c, channel chunk) ONE MMA multiplies the 128-voxel window of row r by the
+// weights of all three height taps at once,
+//     E_r[v][(b, co)] = sum_{a,c,ci} x[z+a-1][r][v+c-1][ci] * w[co][ci][a][b][c]
+// (N = 3*COUT), and output row y is assembled by the epilogue from three
+// consecutive input rows:  out[y] = E_{y-1}[b=0] + E_y[b=1] + E_{y+1}[b=2].
+// The E blocks live in a 4-slot TMEM ring (3 read by the epilogue while the
+// MMA fills the 4th).  Work unit: a band of RB output rows at (n, z, 128-voxel
+// W segment), i.e. RB+2 input rows.  All weights stay resident in shared
+// memory (<= 55 KB); the input rows stream through an S-stage TMA ring in the
+// same 16-byte-voxel-pitch layout as the row-window kernel (no im2col: every
+// width tap is the same window at a shifted start address).
+//
+// Warp roles (256 threads): w0 TMA producer, w1 MMA issuer (one elected
+// thread), w2 TMEM owner, w4..w7 epilogue (3 TMEM slices -> sum -> optional
+// LeakyReLU -> TF32 rounding -> coalesced NDHWC stores through padded smem).
+// Reference semantics: reference pkg/src/voxpar/kernels/_hot.pyx:19-41 (fwd),
+// :44-67 (bwd_data, computed as a gather conv with flipped/transposed weights).
+#include "conv_common.h"
+#include "vpx_host.h"
+#include "vpx_ptx.cuh"
+#include "vpx_round.cuh"
+
+namespace {
+
+using vpx::ConvRowParams;
+
+constexpr int kWinH = 130;                             // 128 outputs + 2 halo voxels
+constexpr int kPlane = (3 * kWinH * 16 + 127) / 128 * 128;  // 3 depth planes x 130 voxels x 16 B
+constexpr int kNB = 4;                                 // TMEM ring of E blocks
+
+template <int CIN, int C>
+struct RowH {
+  static constexpr bool PAIR = CIN == 4;                 // two (a,c) taps per K=8 step
+  static constexpr int NCH = CIN / 4;                    // 4-channel chunk planes per input row
+  static constexpr int KSTEPS = PAIR ? 5 : 9 * (CIN / 8);
+  static constexpr int N = 3 * C;
+  static constexpr int BSTEP = 2 * N * 16;               // bytes of B per K step
+  static constexpr int WBYTES = KSTEPS * BSTEP;
+  static constexpr int STAGE = NCH * kPlane;
+  static constexpr int EPI = 4 * 32 * (C + 4) * 4;
+  static constexpr int S0 = (226 * 1024 - 2048 - WBYTES - EPI) / STAGE;
+  static constexpr int S = S0 > 8 ? 8 : S0;
+  static constexpr int SMEM = (WBYTES + 1023) / 1024 * 1024 + S * STAGE + EPI + 1024;
+  static constexpr int TCOLS = kNB * N <= 256 ? 256 : 512;
+};
+
+template <int CIN, int C>
+__global__ void __launch_bounds__(256, 1)
+    conv_rowh_kernel(const __grid_constant__ CUtensorMap xmap, const ConvRowParams p) {
+  using K = RowH<CIN, C>;
+  constexpr int N = K::N, S = K::S;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sw = smem;                                                   // resident weights
+  uint8_t* sa = smem + (K::WBYTES + 1023) / 1024 * 1024;                // input-row stages
+  float* sepi = reinterpret_cast<float*>(sa + S * K::STAGE);            // epilogue staging
+  __shared__ __align__(8) uint64_t full[S], empty[S], bfull[kNB], bempty[kNB], wbar;
+  __shared__ uint32_t tmem_base;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rb = p.ngy;  // rows per band (ConvRowParams reuse: ngy = band height)
+  const int nbands = (p.yhi - p.ylo + rb - 1) / rb;
+  const int nz = p.zhi - p.zlo;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      vpx::mbar_init(&full[s], 1);
+      vpx::mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < kNB; ++s) {
+      vpx::mbar_init(&bfull[s], 1);
+      vpx::mbar_init(&bempty[s], 128);
+    }
+    vpx::mbar_init(&wbar, 1);
+    vpx::fence_barrier_init();
+    vpx::tma_prefetch_desc(&xmap);
+  }
+  if (warp == 2) vpx::tmem_alloc<K::TCOLS>(&tmem_base);
+  vpx::tc_fence_before();
+  __syncthreads();
+  vpx::tc_fence_after();
+  const uint32_t tbase = tmem_base;
+
+  auto decode = [&](int task, int& n, int& z, int& x0, int& y0, int& rows) {
+    int t = task;
+    const int xs = t % p.nxseg;
+    t /= p.nxseg;
+    const int band = t % nbands;
+    t /= nbands;
+    z = p.zlo + t % nz;
+    n = t / nz;
+    x0 = xs * 128;
+    y0 = p.ylo + band * rb;
+    rows = min(rb, p.yhi - y0);
+  };
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    if (vpx::elect_one()) {
+      vpx::mbar_arrive_expect_tx(&wbar, K::WBYTES);
+      vpx::bulk_g2s(sw, p.wpack, K::WBYTES, &wbar);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int task = blockIdx.x; task < p.num_tiles; task += gridDim.x) {
+        int n, z, x0, y0, rows;
+        decode(task, n, z, x0, y0, rows);
+        for (int j = 0; j < rows + 2; ++j) {
+          const int r = y0 - 1 + j;
+          vpx::mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* dst = sa + stage * K::STAGE;
+          vpx::mbar_arrive_expect_tx(&full[stage], K::NCH * 3 * kWinH * 16);
+#pragma unroll
+          for (int c = 0; c < K::NCH; ++c)
+            vpx::tma_load_5d(dst + c * kPlane, &xmap, &full[stage], 4 * c, x0 - 1 + p.in_off_w, r + p.in_off_h,
+                             z - 1 + p.in_off_d, n);
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------------- MMA
+    constexpr uint32_t idesc = vpx::make_idesc(2, 128, N, false, false);
+    if (vpx::elect_one()) {
+      vpx::mbar_wait(&wbar, 0);
+      const uint32_t wb = vpx::smem_u32(sw);
+      const uint32_t ab0 = vpx::smem_u32(sa);
+      int stage = 0;
+      uint32_t phase = 0;
+      long long gr = 0;  // E blocks produced by this CTA
+      for (int task = blockIdx.x; task < p.num_tiles; task += gridDim.x) {
+        int n, z, x0, y0, rows;
+        decode(task, n, z, x0, y0, rows);
+        for (int j = 0; j < rows + 2; ++j, ++gr) {
+          const int slot = static_cast<int>(gr % kNB);
+          vpx::mbar_wait(&bempty[slot], static_cast<uint32_t>(((gr / kNB) & 1) ^ 1));
+          vpx::mbar_wait(&full[stage], phase);
+          vpx::tc_fence_after();
+          const uint32_t d = tbase + slot * N;
+          const uint32_t ab = ab0 + stage * K::STAGE;
+          if constexpr (K::PAIR) {
+#pragma unroll
+            for (int q = 0; q < 5; ++q) {
+              const int t0 = 2 * q, t1 = q < 4 ? 2 * q + 1 : 2 * q;  // (a, c) taps, t = 3a + c
+              const uint32_t lbo = ((t1 / 3 - t0 / 3) * kWinH + (t1 % 3 - t0 % 3)) * 16;
+              const uint64_t adesc = vpx::make_sdesc(ab + ((t0 / 3) * kWinH + t0 % 3) * 16, q < 4 ? lbo : 16, 128, 0);
+              const uint64_t bdesc = vpx::make_sdesc(wb + q * K::BSTEP, N * 16, 128, 0);
+              vpx::umma_tf32(d, adesc, bdesc, idesc, q > 0 ? 1u : 0u);
+            }
+          } else {
+#pragma unroll
+            for (int t = 0; t < 9; ++t) {
+#pragma unroll
+              for (int jp = 0; jp < CIN / 8; ++jp) {
+                const uint64_t adesc =
+                    vpx::make_sdesc(ab + 2 * jp * kPlane + ((t / 3) * kWinH + t % 3) * 16, kPlane, 128, 0);
+                const uint64_t bdesc = vpx::make_sdesc(wb + (t * (CIN / 8) + jp) * K::BSTEP, N * 16, 128, 0);
+                vpx::umma_tf32(d, adesc, bdesc, idesc, (t | jp) != 0 ? 1u : 0u);
+              }
+            }
+          }
+          vpx::umma_commit(&empty[stage]);
+          vpx::umma_commit(&bfull[slot]);
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ epilogue
+    const int q = warp - 4;  // TMEM lane quarter = voxels 32q .. 32q+31 of the segment
+    float* stg = sepi + q * 32 * (C + 4);
+    const uint32_t lane_base = tbase + (static_cast<uint32_t>(q * 32) << 16);
+    long long gr = 0;
+    for (int task = blockIdx.x; task < p.num_tiles; task += gridDim.x) {
+      int n, z, x0, y0, rows;
+      decode(task, n, z, x0, y0, rows);
+      // E blocks of this band: gr .. gr + rows + 1 (input rows y0-1 .. y0+rows)
+      float* orow_w = p.out + static_cast<long long>(n) * p.out_sn +
+                      static_cast<long long>(z + p.out_off_d) * p.out_sd +
+                      static_cast<long long>(x0 + q * 32 + p.out_off_w) * p.out_sw;
+      for (int k = 0; k < rows; ++k) {
+        const long long gm = gr + k, g0 = gm + 1, gp = gm + 2;  // E_{y-1}, E_y, E_{y+1}
+        if (k == 0) {
+          vpx::mbar_wait(&bfull[gm % kNB], static_cast<uint32_t>((gm / kNB) & 1));
+          vpx::mbar_wait(&bfull[g0 % kNB], static_cast<uint32_t>((g0 / kNB) & 1));
+        }
+        vpx::mbar_wait(&bfull[gp % kNB], static_cast<uint32_t>((gp / kNB) & 1));
+        vpx::tc_fence_after();
+        const int y = y0 + k;
+#pragma unroll
+        for (int cb = 0; cb < C / 16; ++cb) {
+          uint32_t v0[16], v1[16], v2[16];  // three loads in flight, one wait
+          vpx::tmem_ld16_nw(lane_base + static_cast<uint32_t>(gm % kNB) * N + 0 * C + cb * 16, v0);
+          vpx::tmem_ld16_nw(lane_base + static_cast<uint32_t>(g0 % kNB) * N + 1 * C + cb * 16, v1);
+          vpx::tmem_ld16_nw(lane_base + static_cast<uint32_t>(gp % kNB) * N + 2 * C + cb * 16, v2);
+          vpx::tmem_ld_wait();
+          float v[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            v[i] = (__uint_as_float(v0[i]) + __uint_as_float(v1[i])) + __uint_as_float(v2[i]);
+            if (p.act) v[i] = v[i] >= 0.f ? v[i] : p.slope * v[i];  // reference layers/reference.py:231-233
+            if (p.rnd) v[i] = vpx::tf32_rn(v[i]);
+          }
+          float4* s4 = reinterpret_cast<float4*>(stg + lane * (C + 4) + cb * 16);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) s4[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        }
+        // E_{y-1} is not needed by any later output row of this band
+        vpx::tc_fence_before();
+        vpx::mbar_arrive(&bempty[gm % kNB]);
+        __syncwarp();
+        float* ow = orow_w + static_cast<long long>(y + p.out_off_h) * p.out_sh;
+        constexpr int Q = C / 4;  // float4 chunks per voxel
+#pragma unroll
+        for (int kk = 0; kk < Q; ++kk) {
+          const int c = kk * 32 + lane, vx = c / Q, qq = c % Q;
+          const float4 val = *reinterpret_cast<const float4*>(stg + vx * (C + 4) + qq * 4);
+          *reinterpret_cast<float4*>(ow + static_cast<long long>(vx) * p.out_sw + qq * 4) = val;
+        }
+        __syncwarp();
+      }
+      // the band's last two E blocks (input rows y0+rows-1, y0+rows)
+      vpx::tc_fence_before();
+      vpx::mbar_arrive(&bempty[(gr + rows) % kNB]);
+      vpx::mbar_arrive(&bempty[(gr + rows + 1) % kNB]);
+      gr += rows + 2;
+    }
+  }
+  vpx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) vpx::tmem_dealloc<K::TCOLS>(tbase);
+}
+
+template <int CIN, int C>
+int launch_rowh(const CUtensorMap& xmap, const ConvRowParams& p, cudaStream_t st) {
+  using K = RowH<CIN, C>;
+  static_assert(K::S >= 2, "stages");
+  static_assert(K::SMEM <= 227 * 1024, "smem");
+  auto kern = conv_rowh_kernel<CIN, C>;
+  VPX_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM));
+  int grid = p.num_tiles < vpx::num_sms() ? p.num_tiles : vpx::num_sms();
+  if (grid <= 0) return VPX_OK;
+  kern<<<grid, 256, K::SMEM, st>>>(xmap, p);
+  VPX_LAUNCH_CHECK();
+  return VPX_OK;
+}
+
+// Pack OIDHW weights into the resident B layout:
+//   B[kstep][h][n = (b, o)][e]  (K-major, no swizzle: 8 rows x 16 B core matrices,
+//   the two 4-channel halves of a K=8 step LBO = N*16 apart)
+//   non-pair: kstep = t*(I/8) + jp, t = 3a + c, input channel i = 4(2jp + h) + e
+//   pair (I = 4): kstep = q, tap t = 2q + h (t = 9 -> zeros), i = e
+//   mode 0: Weff[o][i][a][b][c] = w[o][i][a][b][c]; mode 1: w[i][o][2-a][2-b][2-c]
+__global__ void pack_rowh_kernel(const float* __restrict__ w, int cout, int cin, int mode, int pair,
+                                 float* __restrict__ out) {
+  const int O = mode ? cin : cout, I = mode ? cout : cin;
+  const int N = 3 * O;
+  const int ksteps = pair ? 5 : 9 * (I / 8);
+  const long long total = (long long)ksteps * 2 * N * 4;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    long long t = idx;
+    const int e = t % 4;
+    t /= 4;
+    const int nn = t % N;
+    t /= N;
+    const int h = t % 2;
+    const int ks = static_cast<int>(t / 2);
+    const int b = nn / O, o = nn % O;
+    int tap, i;
+    if (pair) {
+      tap = 2 * ks + h;
+      i = e;
+    } else {
+      tap = ks / (I / 8);
+      i = 4 * (2 * (ks % (I / 8)) + h) + e;
+    }
+    float v = 0.f;
+    if (tap < 9) {
+      const int a = tap / 3, c = tap % 3;
+      if (mode == 0)
+        v = w[(((long long)o * cin + i) * 3 + a) * 9 + b * 3 + c];
+      else
+        v = w[(((long long)i * cin + o) * 3 + (2 - a)) * 9 + (2 - b) * 3 + (2 - c)];
+    }
+    out[idx] = vpx::tf32_rn(v);
+  }
+}
+
+}  // namespace
+
+namespace vpx {
+
+// Channel configurations with a rowh instance (cin_eff -> cout_eff).
+int rowh_supported(int cin, int cout) {
+  return (cin == 4 && cout == 16) || (cin == 8 && cout == 16) || (cin == 16 && cout == 16) ||
+         (cin == 32 && cout == 16) || (cin == 16 && cout == 32);
+}
+
+long long rowh_packed_bytes(int cin, int cout) {
+  const int ksteps = cin == 4 ? 5 : 9 * (cin / 8);
+  return (long long)ksteps * 2 * 3 * cout * 16;
+}
+
+int rowh_pack(const float* w, int cout, int cin, int mode, float* dst, cudaStream_t st) {
+  const int I = mode ? cout : cin, O = mode ? cin : cout;
+  if (!rowh_supported(I, O)) VPX_FAIL(VPX_ERR_UNSUPPORTED, "rowh pack");
+  const long long total = rowh_packed_bytes(I, O) / 4;
+  int grid = static_cast<int>((total + 255) / 256);
+  if (grid > 4096) grid = 4096;
+  pack_rowh_kernel<<<grid, 256, 0, st>>>(w, cout, cin, mode, I == 4, dst);
+  VPX_LAUNCH_CHECK();
+  return VPX_OK;
+}
+
+int launch_rowh_any(const CUtensorMap& xmap, const ConvRowParams& p, int cin, int cout, cudaStream_t st) {
+  if (cin == 4 && cout == 16) return launch_rowh<4, 16>(xmap, p, st);
+  if (cin == 8 && cout == 16) return launch_rowh<8, 16>(xmap, p, st);
+  if (cin == 16 && cout == 16) return launch_rowh<16, 16>(xmap, p, st);
+  if (cin == 32 && cout == 16) return launch_rowh<32, 16>(xmap, p, st);
+  if (cin == 16 && cout == 32) return launch_rowh<16, 32>(xmap, p, st);
+  VPX_FAIL(VPX_ERR_UNSUPPORTED, "rowh conv: no instance for cin=%d cout=%d", cin, cout);
+}
+
+}  // namespace vpx
