@@ -93,6 +93,12 @@ int vpx_conv3d_bwd_filter(const float* x, const int* xfr, const float* u, const 
  * ufr describes the logical (unblocked) gradient: {n, 16, d, h, w, 0, 0, 0}. */
 int vpx_pool_leaky_bwd_blocked(const float* y, const int* yf, const float* up, const int* upf, float* gb,
                                float slope, int is_max, void* stream);
+/* Fused 2^3 pool backward + LeakyReLU backward of a conv -> leaky -> pool block
+ * (reference layers/reference.py:170-182 then :234-236): g = leaky'(y) *
+ * pool_bwd(y, up), written into the frame gf; y is the LeakyReLU output (= pool
+ * input).  One pass instead of pool-bwd write + leaky-bwd read/write. */
+int vpx_pool_leaky_bwd(const float* y, const int* yf, const float* up, const int* upf, float* g, const int* gf,
+                       float slope, int is_max, void* stream);
 int vpx_conv3d_bwd_filter_c4(const float* x, const int* xfr, const float* ub, const int* ufr, float* wg,
                              int accumulate, void* ws, long long ws_bytes, void* stream);
 /* The same filter gradient computed straight from the POOLED gradient `up`

@@ -322,6 +322,15 @@ extern "C" int vpx_pool_leaky_bwd_blocked(const float* y, const int* yfr, const 
   return vpx::pool_leaky_bwd_blocked(y, yf, up, uf, gb, slope, is_max, static_cast<cudaStream_t>(stream));
 }
 
+extern "C" int vpx_pool_leaky_bwd(const float* y, const int* yfr, const float* up, const int* upfr, float* g,
+                                  const int* gfr, float slope, int is_max, void* stream) {
+  Frame yf = vpx::to_frame(yfr), uf = vpx::to_frame(upfr), gf = vpx::to_frame(gfr);
+  if (yf.c % 4 || uf.c != yf.c || gf.c != yf.c || uf.d * 2 != yf.d || uf.h * 2 != yf.h || uf.w * 2 != yf.w ||
+      gf.d != yf.d || gf.h != yf.h || gf.w != yf.w || gf.n != yf.n || uf.n != yf.n)
+    VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "pool/leaky backward: extents");
+  return vpx::pool_leaky_bwd(y, yf, up, uf, g, gf, slope, is_max, static_cast<cudaStream_t>(stream));
+}
+
 extern "C" int vpx_conv3d_bwd_filter_c4(const float* x, const int* xfr, const float* ub, const int* ufr,
                                         float* wg, int accumulate, void* ws, long long ws_bytes,
                                         void* stream) {

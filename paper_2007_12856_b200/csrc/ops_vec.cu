@@ -273,7 +273,60 @@ __global__ void pool_leaky_bwd_blocked_v(const float* __restrict__ y, Frame yf, 
     }
   }
 }
+
+// Same fused pool + LeakyReLU backward, writing the gradient frame gf (NDHWC,
+// any margins): replaces the pool-backward write + leaky-backward read/write.
+__global__ void pool_leaky_bwd_v(const float* __restrict__ y, Frame yf, const float* __restrict__ up, Frame uf,
+                                 float* __restrict__ g, Frame gf, float s, int is_max) {
+  const int C = uf.c;
+  ROW_LOOP(uf) {
+    const long long orow = i / per_row, off = i % per_row;
+    const int xo = static_cast<int>(off / (C / 4)), c4 = static_cast<int>(off % (C / 4));
+    long long t = orow;
+    const int yo = t % uf.h;
+    t /= uf.h;
+    const int zo = t % uf.d;
+    const int n = static_cast<int>(t / uf.d);
+    auto foff = [&](const Frame& f, int a, int b, int cc) {
+      return ((((long long)n * (f.d + 2 * f.md) + (2 * zo + a + f.md)) * (f.h + 2 * f.mh) + (2 * yo + b + f.mh)) *
+                  (f.w + 2 * f.mw) + (2 * xo + cc + f.mw)) * C + 4 * c4;
+    };
+    const float4 uv = ld4(up + row_base(uf, orow) + 4 * off);
+    float4 vals[8];
+#pragma unroll
+    for (int w8 = 0; w8 < 8; ++w8) vals[w8] = ld4(y + foff(yf, w8 >> 2, (w8 >> 1) & 1, w8 & 1));
+    int ax = 0, ay = 0, az = 0, aw = 0;
+    if (is_max) {
+      float4 best = vals[0];
+#pragma unroll
+      for (int w8 = 1; w8 < 8; ++w8) {
+        if (vals[w8].x > best.x) { best.x = vals[w8].x; ax = w8; }
+        if (vals[w8].y > best.y) { best.y = vals[w8].y; ay = w8; }
+        if (vals[w8].z > best.z) { best.z = vals[w8].z; az = w8; }
+        if (vals[w8].w > best.w) { best.w = vals[w8].w; aw = w8; }
+      }
+    }
+    const float4 avg = make_float4(uv.x / 8.0f, uv.y / 8.0f, uv.z / 8.0f, uv.w / 8.0f);
+#pragma unroll
+    for (int w8 = 0; w8 < 8; ++w8) {
+      float4 gg = is_max ? make_float4(w8 == ax ? uv.x : 0.f, w8 == ay ? uv.y : 0.f, w8 == az ? uv.z : 0.f,
+                                       w8 == aw ? uv.w : 0.f)
+                         : avg;
+      const float4 v = vals[w8];
+      gg = make_float4(v.x >= 0.f ? gg.x : s * gg.x, v.y >= 0.f ? gg.y : s * gg.y, v.z >= 0.f ? gg.z : s * gg.z,
+                       v.w >= 0.f ? gg.w : s * gg.w);
+      st4(gf, g + foff(gf, w8 >> 2, (w8 >> 1) & 1, w8 & 1), gg);
+    }
+  }
+}
 }  // namespace
+
+int pool_leaky_bwd(const float* y, const Frame& yf, const float* up, const Frame& uf, float* g, const Frame& gf,
+                   float s, int is_max, cudaStream_t st) {
+  pool_leaky_bwd_v<<<grid_v(uf), 256, 0, st>>>(y, yf, up, uf, g, gf, s, is_max);
+  VPX_LAUNCH_CHECK();
+  return VPX_OK;
+}
 
 int pool_leaky_bwd_blocked(const float* y, const Frame& yf, const float* up, const Frame& uf, float* gb,
                            float s, int is_max, cudaStream_t st) {

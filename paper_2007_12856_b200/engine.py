@@ -418,6 +418,7 @@ def backward(ctx: RankCtx, plan: Plan, state: RankState, stash, dpred, trace: di
     u = dpred
     extra = {}
     skip_below = None
+    skip_one = None
     for i in range(len(net.layers) - 1, -1, -1):
         layer = net.layers[i]
         kept = stash[i]
@@ -432,6 +433,18 @@ def backward(ctx: RankCtx, plan: Plan, state: RankState, stash, dpred, trace: di
                                 G[f"{net.layers[0].name}.w"], tag=net.layers[0].name)
             u = None
             skip_below = 0
+            continue
+        if (trace is None and u is not None and layer.kind == "pool" and i >= 1
+                and net.layers[i - 1].kind == "leaky" and stash[i - 1] is kept and kept.c % 4 == 0
+                and layer.name not in extra and net.layers[i - 1].name not in extra
+                and plan.redist_idx not in (i, i - 1) and plan.placement[i] != "flat"):
+            # leaky -> pool backward fused into one pass over the block
+            act = net.layers[i - 1]
+            u = D.dist_pool_leaky_bwd(kept, u, act.slope, layer.pool_kind, plan.in_meta[i - 1], tag=act.name)
+            skip_below = None
+            skip_one = i - 1
+            continue
+        if skip_one == i:
             continue
         if plan.placement[i] == "flat":
             if layer.kind == "flatten":

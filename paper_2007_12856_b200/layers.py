@@ -280,6 +280,18 @@ def dist_leaky_relu_bwd(x: DistTensor, u: DistTensor, slope: float, in_meta, tag
     return g
 
 
+def dist_pool_leaky_bwd(y: DistTensor, u: DistTensor, slope: float, kind: str, in_meta,
+                        tag: str = "leaky") -> DistTensor:
+    """Backward of leaky -> pool in one pass: g = leaky'(y) * pool_bwd(y, u)
+    (reference layers/distributed.py:141-147 then :211-214); y is the LeakyReLU
+    output, which is also the pool input."""
+    g = DistTensor(in_meta, u.grid_rank, zero=False)
+    with region(f"{tag}.bwd", 0, 4 * (u.voxels() * u.c + 2 * y.voxels() * y.c)):
+        _lib.call("vpx_pool_leaky_bwd", y.ptr, y.desc, u.ptr, u.desc, g.ptr, g.desc, float(slope),
+                  int(kind == "max"), stream_ptr())
+    return g
+
+
 def dist_concat_channels(a: DistTensor, b: DistTensor, out_radii=NO_HALO) -> DistTensor:
     if a.meta.grid != b.meta.grid or a.meta.rank_map != b.meta.rank_map:
         raise ShapeMismatch("concat operands must share a partition layout")
