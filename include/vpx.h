@@ -111,6 +111,19 @@ int vpx_conv3d_bwd_filter_c4_pooled(const float* x, const int* xfr, const float*
                                     const float* up, const int* upfr, float slope, int is_max, float* wg,
                                     int accumulate, void* ws, long long ws_bytes, void* stream);
 
+/* Fused first-block forward (conv 4 -> 16, LeakyReLU, 2^3 average pool, TF32
+ * mode, conv_c1fwd.cu): writes only the pooled frame pout (pfr: half extents)
+ * and the sign mask[n][d][h][w] (bit co set when the stored activation is
+ * >= 0); the full-resolution activation never reaches memory.  ws holds the
+ * packed weights (vpx_conv3d_workspace_bytes(4, 16, 3, .) suffices). */
+int vpx_conv3d_fwd_leaky_pool_c4(const float* x, const int* xfr, const float* w, float slope, float* pout,
+                                 const int* pfr, uint16_t* mask, void* ws, long long ws_bytes, void* stream);
+/* Its backward: the c1 filter gradient from the pooled gradient and the sign
+ * mask (mfr = {n, 16, d, h, w, 0, 0, 0} describes the mask's voxel grid). */
+int vpx_conv3d_bwd_filter_c4_pooled_mask(const float* x, const int* xfr, const uint16_t* mask, const int* mfr,
+                                         const float* up, const int* upfr, float slope, float* wg, int accumulate,
+                                         void* ws, long long ws_bytes, void* stream);
+
 /* ------------------------------------------------------- pointwise / pool --
  * reference layers/reference.py:149-236, layers/distributed.py:132-214.
  * All read/write frame interiors; is_max selects max (ties -> lowest index in

@@ -56,24 +56,24 @@ constexpr int kNA = 48;          // N per tap (x chunks k, k+1: 64 > 48 used col
 constexpr int kACol = 9 * kNA;   // first A column (432)
 constexpr int kASlots = 8;       // A ring: 8 slots x 8 columns
 
-template <int W>
+template <int W, bool MASK = false>
 struct C1Cfg {
   static constexpr int KS = (W / 8 + 1 + 7) / 8;           // K-steps per row (k = -1 .. 8KS-2)
   static constexpr int XCH = 8 * KS + 1;                   // x chunks per row (-1 .. 8KS-1)
   static constexpr int XROW = (XCH * 128 + 1023) / 1024 * 1024;
   static constexpr int XS = 12 * XROW;                     // 3 depth taps x 4-row ring
-  static constexpr int YB = W * 16 * 4;                    // y row
+  static constexpr int YB = MASK ? W * 2 : W * 16 * 4;     // y row, or its 16-bit sign-mask row
   static constexpr int UB = W / 2 * 16 * 4;                // pooled-gradient row
   static constexpr int PIPE = XS + 2 * YB + 2 * UB;
   static constexpr int SCRATCH = 128 * 108 * 4;            // epilogue fold, reuses the pipeline buffers
   static constexpr int SMEM = PIPE > SCRATCH ? PIPE : SCRATCH;
 };
 
-template <int W>
+template <int W, bool MASK>
 __global__ void __launch_bounds__(384, 1)
     c1_pooled_wgrad_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap ymap,
                            const __grid_constant__ CUtensorMap upmap, const C1Params p) {
-  using Cfg = C1Cfg<W>;
+  using Cfg = C1Cfg<W, MASK>;
   constexpr int KS = Cfg::KS, XROW = Cfg::XROW;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -153,7 +153,10 @@ __global__ void __launch_bounds__(384, 1)
         const int n = static_cast<int>(t / p.d);
         vpx::mbar_wait_sleep(&yempty[i & 1], ((i >> 1) & 1) ^ 1);
         vpx::mbar_arrive_expect_tx(&yfull[i & 1], Cfg::YB + Cfg::UB);
-        vpx::tma_load_5d(ys + (i & 1) * Cfg::YB, &ymap, &yfull[i & 1], 0, 0, y + p.y_off_h, z + p.y_off_d, n);
+        if (MASK)
+          vpx::tma_load_5d(ys + (i & 1) * Cfg::YB, &ymap, &yfull[i & 1], 0, y, z, n, 0);
+        else
+          vpx::tma_load_5d(ys + (i & 1) * Cfg::YB, &ymap, &yfull[i & 1], 0, 0, y + p.y_off_h, z + p.y_off_d, n);
         vpx::tma_load_5d(us + (i & 1) * Cfg::UB, &upmap, &yfull[i & 1], 0, 0, (y >> 1) + p.up_off_h,
                          (z >> 1) + p.up_off_d, n);
       }
@@ -212,16 +215,22 @@ __global__ void __launch_bounds__(384, 1)
     const int q = warp & 3, h = (warp - 4) >> 2, m = q * 32 + lane, dd = m >> 4, co = m & 15;
     const uint32_t lane_addr = tbase + (static_cast<uint32_t>(q * 32) << 16) + kACol;
     const float slope = p.slope;
+    // sign of the stored activation at u voxel b + 8 kk: from y, or one bit of the mask
+    auto pos = [&](uint32_t ya, int kk) -> bool {
+      if constexpr (MASK)
+        return (vpx::lds_u16(ya + kk * 16) >> co) & 1u;
+      else
+        return vpx::lds_f32(ya + kk * 512) >= 0.f;
+    };
     auto make_u = [&](int s, uint32_t ya0, uint32_t ua0, float (&v)[8]) {
       // u voxel of column kk: 8k + d + 1 with k = 8s + kk - 1  ->  b + 8 kk
       const int b = 64 * s - 7 + dd;
-      const uint32_t ya = ya0 + b * 64, ua = ua0 + (b >> 1) * 64;
+      const uint32_t ya = ya0 + b * (MASK ? 2 : 64), ua = ua0 + (b >> 1) * 64;
       if (s > 0 && 64 * s + 56 < W) {
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           const float gp = vpx::lds_f32(ua + kk * 256) * 0.125f;
-          const float yv = vpx::lds_f32(ya + kk * 512);
-          v[kk] = vpx::tf32_rn(yv >= 0.f ? gp : slope * gp);
+          v[kk] = vpx::tf32_rn(pos(ya, kk) ? gp : slope * gp);
         }
       } else {
 #pragma unroll
@@ -229,8 +238,7 @@ __global__ void __launch_bounds__(384, 1)
           v[kk] = 0.f;
           if (static_cast<unsigned>(b + 8 * kk) < static_cast<unsigned>(W)) {
             const float gp = vpx::lds_f32(ua + kk * 256) * 0.125f;
-            const float yv = vpx::lds_f32(ya + kk * 512);
-            v[kk] = vpx::tf32_rn(yv >= 0.f ? gp : slope * gp);
+            v[kk] = vpx::tf32_rn(pos(ya, kk) ? gp : slope * gp);
           }
         }
       }
@@ -238,7 +246,7 @@ __global__ void __launch_bounds__(384, 1)
     for (long long r = r0; r < (p.dbg >= 4 ? r0 : r1); ++r) {
       const int i = static_cast<int>(r - r0);
       vpx::mbar_wait_sleep(&yfull[i & 1], (i >> 1) & 1, 64);
-      const uint32_t ya0 = vpx::smem_u32(ys + (i & 1) * Cfg::YB) + co * 4;
+      const uint32_t ya0 = vpx::smem_u32(ys + (i & 1) * Cfg::YB) + (MASK ? 0 : co * 4);
       const uint32_t ua0 = vpx::smem_u32(us + (i & 1) * Cfg::UB) + co * 4;
       int s = ((i * KS) & 1) == h ? 0 : 1;  // first K-step of this row in my slot parity
       float v[8];
@@ -317,12 +325,12 @@ __global__ void __launch_bounds__(384, 1)
   if (warp == 2) vpx::tmem_dealloc<512>(tbase);
 }
 
-template <int W>
+template <int W, bool MASK>
 int launch_c1(const CUtensorMap& xm, const CUtensorMap& ym, const CUtensorMap& um, const C1Params& p,
               cudaStream_t st) {
-  constexpr int smem = C1Cfg<W>::SMEM + 1024;
+  constexpr int smem = C1Cfg<W, MASK>::SMEM + 1024;
   static_assert(smem <= 227 * 1024, "smem");
-  auto kern = c1_pooled_wgrad_kernel<W>;
+  auto kern = c1_pooled_wgrad_kernel<W, MASK>;
   VPX_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   kern<<<p.P, 384, smem, st>>>(xm, ym, um, p);
   VPX_LAUNCH_CHECK();
@@ -351,7 +359,7 @@ int c1_pooled_parts(const Frame& yf) {
 }
 
 int conv_wgrad_c1_pooled(const float* x, const Frame& xf, const float* y, const Frame& yf, const float* up,
-                         const Frame& uf, float slope, float* part, cudaStream_t st) {
+                         const Frame& uf, float slope, float* part, cudaStream_t st, const uint16_t* mask) {
   C1Params p{};
   p.n = yf.n;
   p.d = yf.d;
@@ -370,10 +378,10 @@ int conv_wgrad_c1_pooled(const float* x, const Frame& xf, const float* y, const 
   const int W = yf.w;
   int xch = 0;
   switch (W) {
-    case 512: xch = C1Cfg<512>::XCH; break;
-    case 256: xch = C1Cfg<256>::XCH; break;
-    case 128: xch = C1Cfg<128>::XCH; break;
-    case 64: xch = C1Cfg<64>::XCH; break;
+    case 512: xch = C1Cfg<512, false>::XCH; break;
+    case 256: xch = C1Cfg<256, false>::XCH; break;
+    case 128: xch = C1Cfg<128, false>::XCH; break;
+    case 64: xch = C1Cfg<64, false>::XCH; break;
   }
   CUtensorMap xm, ym, um;
   {
@@ -385,7 +393,16 @@ int conv_wgrad_c1_pooled(const float* x, const Frame& xf, const float* y, const 
                               CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
       return rc;
   }
-  {
+  if (mask) {
+    // [n][d][h][w] 16-bit signs viewed as 32-bit pairs: one row per box
+    uint64_t dims[5] = {(uint64_t)W / 2, (uint64_t)yf.h, (uint64_t)yf.d, (uint64_t)yf.n, 1};
+    uint64_t strides[4] = {(uint64_t)W * 2, (uint64_t)yf.h * W * 2, (uint64_t)yf.d * yf.h * W * 2,
+                           (uint64_t)yf.n * yf.d * yf.h * W * 2};
+    uint32_t box[5] = {(uint32_t)(W / 2), 1, 1, 1, 1};
+    if (int rc = encode_tiled(&ym, CU_TENSOR_MAP_DATA_TYPE_UINT32, 5, const_cast<uint16_t*>(mask), dims, strides,
+                              box, CU_TENSOR_MAP_SWIZZLE_NONE))
+      return rc;
+  } else {
     const uint64_t Hf = yf.h + 2 * yf.mh, Df = yf.d + 2 * yf.md;
     uint64_t dims[5] = {64, (uint64_t)W / 4, Hf, Df, (uint64_t)yf.n};
     uint64_t strides[4] = {256, (uint64_t)W * 64, Hf * W * 64, Df * Hf * W * 64};
@@ -403,11 +420,19 @@ int conv_wgrad_c1_pooled(const float* x, const Frame& xf, const float* y, const 
                               CU_TENSOR_MAP_SWIZZLE_NONE))
       return rc;
   }
+  if (mask) {
+    switch (W) {
+      case 512: return launch_c1<512, true>(xm, ym, um, p, st);
+      case 256: return launch_c1<256, true>(xm, ym, um, p, st);
+      case 128: return launch_c1<128, true>(xm, ym, um, p, st);
+      case 64: return launch_c1<64, true>(xm, ym, um, p, st);
+    }
+  }
   switch (W) {
-    case 512: return launch_c1<512>(xm, ym, um, p, st);
-    case 256: return launch_c1<256>(xm, ym, um, p, st);
-    case 128: return launch_c1<128>(xm, ym, um, p, st);
-    case 64: return launch_c1<64>(xm, ym, um, p, st);
+    case 512: return launch_c1<512, false>(xm, ym, um, p, st);
+    case 256: return launch_c1<256, false>(xm, ym, um, p, st);
+    case 128: return launch_c1<128, false>(xm, ym, um, p, st);
+    case 64: return launch_c1<64, false>(xm, ym, um, p, st);
   }
   VPX_FAIL(VPX_ERR_UNSUPPORTED, "c1 pooled filter gradient: W=%d", W);
 }

@@ -322,6 +322,36 @@ extern "C" int vpx_pool_leaky_bwd_blocked(const float* y, const int* yfr, const 
   return vpx::pool_leaky_bwd_blocked(y, yf, up, uf, gb, slope, is_max, static_cast<cudaStream_t>(stream));
 }
 
+extern "C" int vpx_conv3d_fwd_leaky_pool_c4(const float* x, const int* xfr, const float* w, float slope,
+                                            float* pout, const int* pfr, uint16_t* mask, void* ws, long long ws_bytes,
+                                            void* stream) {
+  if (int rc = vpx::check_frame(xfr, "first block input")) return rc;
+  if (int rc = vpx::check_frame(pfr, "first block pooled output")) return rc;
+  Frame xf = vpx::to_frame(xfr), pf = vpx::to_frame(pfr);
+  if (!vpx::c1_fwd_pool_supported(xf, pf.c, pf)) VPX_FAIL(VPX_ERR_UNSUPPORTED, "fused first block: shape/mode");
+  if (ws_bytes < vpx::rowh_packed_bytes(4, 16)) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "workspace too small");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  float* wpack = static_cast<float*>(ws);
+  if (int rc = vpx::rowh_pack(w, 16, 4, 0, wpack, st)) return rc;
+  return vpx::conv_c1_fwd_pool(x, xf, wpack, slope, pout, pf, mask, st);
+}
+
+extern "C" int vpx_conv3d_bwd_filter_c4_pooled_mask(const float* x, const int* xfr, const uint16_t* mask,
+                                                    const int* mfr, const float* up, const int* upfr, float slope,
+                                                    float* wg, int accumulate, void* ws, long long ws_bytes,
+                                                    void* stream) {
+  Frame xf = vpx::to_frame(xfr), mf = vpx::to_frame(mfr), uf = vpx::to_frame(upfr);
+  if (mf.md || mf.mh || mf.mw || !vpx::c1_pooled_supported(xf, mf, uf))
+    VPX_FAIL(VPX_ERR_UNSUPPORTED, "pooled c1 filter gradient (mask): shape/mode");
+  const int P = vpx::c1_pooled_parts(mf);
+  const long long need = (long long)P * 16 * 4 * 27 * 4;
+  if (ws_bytes < need) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "workspace too small");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  float* part = static_cast<float*>(ws);
+  if (int rc = vpx::conv_wgrad_c1_pooled(x, xf, nullptr, mf, up, uf, slope, part, st, mask)) return rc;
+  return vpx::reduce_partials(part, P, 16 * 4 * 27, wg, accumulate, st);
+}
+
 extern "C" int vpx_pool_leaky_bwd(const float* y, const int* yfr, const float* up, const int* upfr, float* g,
                                   const int* gfr, float slope, int is_max, void* stream) {
   Frame yf = vpx::to_frame(yfr), uf = vpx::to_frame(upfr), gf = vpx::to_frame(gfr);

@@ -17,9 +17,12 @@
 // same 16-byte-voxel-pitch layout as the row-window kernel (no im2col: every
 // width tap is the same window at a shifted start address).
 //
-// Warp roles (256 threads): w0 TMA producer, w1 MMA issuer (one elected
-// thread), w2 TMEM owner, w4..w7 epilogue (3 TMEM slices -> sum -> optional
-// LeakyReLU -> TF32 rounding -> coalesced NDHWC stores through padded smem).
+// Warp roles (384 threads): w0 TMA producer, w1 MMA issuer (one elected
+// thread), w2 TMEM owner, w4..w11 epilogue in two sets of four (one per TMEM
+// lane quarter) taking alternate output rows: 3 TMEM slices -> sum ->
+// optional LeakyReLU -> TF32 rounding -> coalesced NDHWC stores through
+// padded smem.  (With 16 output channels a row is only 5 MMAs, so the
+// epilogue, not the tensor pipe, sets the pace unless it is doubled.)
 // Reference semantics: reference pkg/src/voxpar/kernels/_hot.pyx:19-41 (fwd),
 // :44-67 (bwd_data, computed as a gather conv with flipped/transposed weights).
 #include "conv_common.h"
@@ -44,7 +47,7 @@ struct RowH {
   static constexpr int BSTEP = 2 * N * 16;               // bytes of B per K step
   static constexpr int WBYTES = KSTEPS * BSTEP;
   static constexpr int STAGE = NCH * kPlane;
-  static constexpr int EPI = 4 * 32 * (C + 4) * 4;
+  static constexpr int EPI = 8 * 32 * (C + 4) * 4;       // 8 epilogue warps
   static constexpr int S0 = (226 * 1024 - 2048 - WBYTES - EPI) / STAGE;
   static constexpr int S = S0 > 8 ? 8 : S0;
   static constexpr int SMEM = (WBYTES + 1023) / 1024 * 1024 + S * STAGE + EPI + 1024;
@@ -52,7 +55,7 @@ struct RowH {
 };
 
 template <int CIN, int C>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
     conv_rowh_kernel(const __grid_constant__ CUtensorMap xmap, const ConvRowParams p) {
   using K = RowH<CIN, C>;
   constexpr int N = K::N, S = K::S;
@@ -179,8 +182,9 @@ __global__ void __launch_bounds__(256, 1)
     __syncwarp();
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
-    const int q = warp - 4;  // TMEM lane quarter = voxels 32q .. 32q+31 of the segment
-    float* stg = sepi + q * 32 * (C + 4);
+    const int q = warp & 3;          // TMEM lane quarter = voxels 32q .. 32q+31 of the segment
+    const int hset = (warp - 4) >> 2;  // output rows k with k % 2 == hset
+    float* stg = sepi + (warp - 4) * 32 * (C + 4);
     const uint32_t lane_base = tbase + (static_cast<uint32_t>(q * 32) << 16);
     long long gr = 0;
     for (int task = blockIdx.x; task < p.num_tiles; task += gridDim.x) {
@@ -190,12 +194,12 @@ __global__ void __launch_bounds__(256, 1)
       float* orow_w = p.out + static_cast<long long>(n) * p.out_sn +
                       static_cast<long long>(z + p.out_off_d) * p.out_sd +
                       static_cast<long long>(x0 + q * 32 + p.out_off_w) * p.out_sw;
-      for (int k = 0; k < rows; ++k) {
+      for (int k = hset; k < rows; k += 2) {
         const long long gm = gr + k, g0 = gm + 1, gp = gm + 2;  // E_{y-1}, E_y, E_{y+1}
-        if (k == 0) {
-          vpx::mbar_wait(&bfull[gm % kNB], static_cast<uint32_t>((gm / kNB) & 1));
-          vpx::mbar_wait(&bfull[g0 % kNB], static_cast<uint32_t>((g0 / kNB) & 1));
-        }
+        // none of the three can be recycled before this row frees E_{y-1} and
+        // the other set finishes row k+1, so the parity waits are unambiguous
+        vpx::mbar_wait(&bfull[gm % kNB], static_cast<uint32_t>((gm / kNB) & 1));
+        vpx::mbar_wait(&bfull[g0 % kNB], static_cast<uint32_t>((g0 / kNB) & 1));
         vpx::mbar_wait(&bfull[gp % kNB], static_cast<uint32_t>((gp / kNB) & 1));
         vpx::tc_fence_after();
         const int y = y0 + k;
@@ -217,9 +221,14 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
           for (int i = 0; i < 4; ++i) s4[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
         }
-        // E_{y-1} is not needed by any later output row of this band
+        // E_{y-1} is not needed by any later output row of this band; the last
+        // row also releases the band's final two blocks
         vpx::tc_fence_before();
         vpx::mbar_arrive(&bempty[gm % kNB]);
+        if (k == rows - 1) {
+          vpx::mbar_arrive(&bempty[(gm + 1) % kNB]);
+          vpx::mbar_arrive(&bempty[(gm + 2) % kNB]);
+        }
         __syncwarp();
         float* ow = orow_w + static_cast<long long>(y + p.out_off_h) * p.out_sh;
         constexpr int Q = C / 4;  // float4 chunks per voxel
@@ -231,10 +240,6 @@ __global__ void __launch_bounds__(256, 1)
         }
         __syncwarp();
       }
-      // the band's last two E blocks (input rows y0+rows-1, y0+rows)
-      vpx::tc_fence_before();
-      vpx::mbar_arrive(&bempty[(gr + rows) % kNB]);
-      vpx::mbar_arrive(&bempty[(gr + rows + 1) % kNB]);
       gr += rows + 2;
     }
   }
@@ -252,7 +257,7 @@ int launch_rowh(const CUtensorMap& xmap, const ConvRowParams& p, cudaStream_t st
   VPX_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM));
   int grid = p.num_tiles < vpx::num_sms() ? p.num_tiles : vpx::num_sms();
   if (grid <= 0) return VPX_OK;
-  kern<<<grid, 256, K::SMEM, st>>>(xmap, p);
+  kern<<<grid, 384, K::SMEM, st>>>(xmap, p);
   VPX_LAUNCH_CHECK();
   return VPX_OK;
 }

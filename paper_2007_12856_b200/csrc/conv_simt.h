@@ -2,6 +2,8 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <cstdint>
+
 namespace vpx {
 
 // NDHWC halo frame: interior extents (n,c,d,h,w) and margins (md,mh,mw).
@@ -31,7 +33,11 @@ int conv_wgrad_tc(const float* x, const Frame& xf, const float* u, const Frame& 
 int c1_pooled_supported(const Frame& xf, const Frame& yf, const Frame& uf);
 int c1_pooled_parts(const Frame& yf);
 int conv_wgrad_c1_pooled(const float* x, const Frame& xf, const float* y, const Frame& yf, const float* up,
-                         const Frame& uf, float slope, float* part, cudaStream_t st);
+                         const Frame& uf, float slope, float* part, cudaStream_t st,
+                         const uint16_t* mask = nullptr);
+int c1_fwd_pool_supported(const Frame& xf, int cout, const Frame& pf);
+int conv_c1_fwd_pool(const float* x, const Frame& xf, const float* wpack, float slope, float* pout,
+                     const Frame& pf, uint16_t* mask, cudaStream_t st);
 int conv_wgrad_simt(const float* x, const Frame& xf, const float* u, const Frame& uf, int k, int s,
                     float* wg, int accumulate, float* part, cudaStream_t st);
 

@@ -319,7 +319,26 @@ def forward(ctx: RankCtx, plan: Plan, state: RankState, batch: Batch, mode: str,
             DistTensor(plan.input_meta, gr0, batch.x_block)
     outputs, stash = {}, []
     fused_act = False
+    skip_to = -1
     for i, layer in enumerate(net.layers):
+        if i < skip_to:
+            continue
+        if (trace is None and cur is not None and layer.kind == "conv" and i == 0 and len(net.layers) > 3
+                and net.layers[i + 1].kind == "leaky" and net.layers[i + 2].kind == "pool"
+                and len({plan.placement[i], plan.placement[i + 1], plan.placement[i + 2]}) == 1
+                and plan.placement[i] != "flat" and plan.redist_idx not in (i, i + 1, i + 2)
+                and not any(getattr(l, "skip", None) in (layer.name, net.layers[i + 1].name)
+                            for l in net.layers)
+                and D.first_block_fwd_supported(cur, layer.params, net.layers[i + 2].pool_kind)):
+            # conv -> leaky -> avg pool in one kernel: pooled output + sign mask
+            pooled, mask = D.first_block_fwd(ctx, cur, P[f"{layer.name}.w"], layer.params,
+                                             net.layers[i + 1].slope, plan.out_radii[i + 2], tag=layer.name)
+            stash.extend([cur, mask, mask])
+            outputs[layer.name] = outputs[net.layers[i + 1].name] = None
+            outputs[net.layers[i + 2].name] = pooled
+            cur = pooled
+            skip_to = i + 3
+            continue
         if i == plan.redist_idx and plan.placement[i] != "flat":
             cur = D.redistribute(ctx, cur, plan.redist_src_meta, plan.in_meta[i])
         if plan.placement[i] == "flat":

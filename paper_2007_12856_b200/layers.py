@@ -409,6 +409,58 @@ def redistribute(ctx: RankCtx, x, src_meta: DistTensorMeta, dst_meta: DistTensor
 
 # ------------------------------------------------- first-block fast path
 
+class MaskFrame:
+    """Sign mask of the first block's LeakyReLU output: int16 [n][d][h][w],
+    bit co set where the stored activation is >= 0 (the backward needs only
+    the sign because slope > 0).  Stands in for the activation frame in the
+    stash when the forward ran fused (vpx_conv3d_fwd_leaky_pool_c4)."""
+
+    def __init__(self, n, c, d, h, w):
+        self.n, self.c, self.d, self.h, self.w = n, c, d, h, w
+        self.t = torch.empty((n, d, h, w), dtype=torch.int16, device="cuda")
+        self._desc = frame_desc(n, c, d, h, w)
+
+    @property
+    def ptr(self):
+        return self.t.data_ptr()
+
+    @property
+    def desc(self):
+        return ctypes.addressof(self._desc)
+
+    def voxels(self):
+        return self.n * self.d * self.h * self.w
+
+
+def first_block_fwd_supported(x: DistTensor, conv_params, pool_kind: str) -> bool:
+    """conv(4 -> 16, k3 s1) -> leaky -> average pool in one kernel (TF32 mode)."""
+    if pool_kind != "average" or _lib.load().vpx_get_precision() != 0:
+        return False
+    if conv_params.cin != 4 or conv_params.cout != 16:
+        return False
+    if tuple(conv_params.kernel) != (3, 3, 3) or tuple(conv_params.stride) != (1, 1, 1):
+        return False
+    # the backward (first_block_wgrad with the mask) covers W in 128..512 per rank
+    return x.m[2] == 0 and x.w in (128, 256, 512) and x.d % 2 == 0 and x.h % 2 == 0
+
+
+def first_block_fwd(ctx: RankCtx, x: DistTensor, w: torch.Tensor, conv_params, slope: float, out_radii,
+                    tag: str = "c1"):
+    """Pooled output + sign mask of conv -> leaky -> avg pool (conv_c1fwd.cu)."""
+    halo_exchange(ctx, x)
+    gs = x.meta.global_shape
+    pooled = _out(x.meta, Shape5D(gs.n, conv_params.cout, gs.d // 2, gs.h // 2, gs.w // 2), out_radii,
+                  x.grid_rank)
+    mask = MaskFrame(x.n, conv_params.cout, x.d, x.h, x.w)
+    yfr = frame_desc(x.n, conv_params.cout, x.d, x.h, x.w)
+    ws = WS.get(_lib.load().vpx_conv3d_workspace_bytes(x.c, conv_params.cout, 3, ctypes.addressof(yfr)))
+    nvox = x.voxels()
+    with region(f"{tag}.fwd", _conv_flops(conv_params, nvox),
+                4 * (x.voxels() * x.c + pooled.voxels() * pooled.c) + 2 * nvox):
+        _lib.call("vpx_conv3d_fwd_leaky_pool_c4", x.ptr, x.desc, w.data_ptr(), float(slope), pooled.ptr,
+                  pooled.desc, mask.ptr, ws.data_ptr(), ws.numel() * 4, stream_ptr())
+    return pooled, mask
+
 def first_block_fast_path(conv, act, y: DistTensor, u: DistTensor, x_meta) -> bool:
     """True when the first conv block (Cin=4 -> 16, LeakyReLU, 2^3 pool) can
     take the fused backward: blocked pool/leaky backward + dense c1 wgrad."""
@@ -429,6 +481,12 @@ def first_block_wgrad(ctx: RankCtx, x: DistTensor, y: DistTensor, u_pool: DistTe
     ufr = frame_desc(y.n, y.c, y.d, y.h, y.w)
     ws = WS.get(_lib.load().vpx_conv3d_workspace_bytes(x.c, y.c, 3, ctypes.addressof(ufr)))
     flops = 2 * 27 * x.c * y.c * nvox
+    if isinstance(y, MaskFrame):
+        # forward ran fused: the LeakyReLU signs come from the mask
+        with region(f"{tag}.wgrad", flops, 4 * (x.voxels() * x.c + u_pool.voxels() * u_pool.c) + 2 * nvox):
+            _lib.call("vpx_conv3d_bwd_filter_c4_pooled_mask", x.ptr, x.desc, y.ptr, y.desc, u_pool.ptr,
+                      u_pool.desc, float(slope), out.data_ptr(), 0, ws.data_ptr(), ws.numel() * 4, stream_ptr())
+        return out
     if pool_kind != "max" and _lib.load().vpx_get_precision() == 0:
         # one kernel: pooled gradient -> u (in TMEM) -> filter gradient
         with region(f"{tag}.wgrad", flops, 4 * (x.voxels() * x.c + nvox * y.c + u_pool.voxels() * u_pool.c)):

@@ -105,6 +105,48 @@ def test_first_block_fused_backward_and_c4_wgrad(shape, margins):
     assert rel(wg2.cpu().numpy(), wg.cpu().numpy()) < 1e-5  # same rounded operands, other summation order
 
 
+@pytest.mark.parametrize("shape,margins", [((1, 4, 6, 128), (0, 0, 0)), ((2, 2, 4, 256), (1, 1, 0))])
+def test_first_block_fused_forward_and_mask_backward(shape, margins):
+    """conv(4->16)+leaky+avg-pool in one kernel (pooled output + sign mask)
+    equals the unfused conv/pool kernels bit for bit, and the mask-driven
+    filter gradient equals the y-driven one bit for bit."""
+    n, d, h, w = shape
+    rng = np.random.default_rng(5)
+    x = rng.uniform(-1, 1, (n, 4, d, h, w)).astype(np.float32)
+    wt = torch.from_numpy((rng.uniform(-1, 1, (16, 4, 3, 3, 3)) / 5).astype(np.float32)).cuda()
+    xf = Frame(n, 4, d, h, w, margins, zero=True).load_ncdhw(x)
+    W = ws(4, 16, 3, Frame(n, 16, d, h, w))
+    # unfused reference path: conv + fused leaky epilogue, then pool
+    yf = Frame(n, 16, d, h, w)
+    _lib.call("vpx_conv3d_fwd_act", xf.ptr, xf.desc, wt.data_ptr(), 3, 1, yf.ptr, yf.desc, 1, 0.3, W.data_ptr(),
+              W.numel() * 4, stream_ptr())
+    pref = Frame(n, 16, d // 2, h // 2, w // 2, margins, zero=True)
+    _lib.call("vpx_pool_fwd", yf.ptr, yf.desc, pref.ptr, pref.desc, 0, stream_ptr())
+    # fused
+    pf = Frame(n, 16, d // 2, h // 2, w // 2, margins, zero=True)
+    mask = torch.zeros((n, d, h, w), dtype=torch.int16, device="cuda")
+    _lib.call("vpx_conv3d_fwd_leaky_pool_c4", xf.ptr, xf.desc, wt.data_ptr(), 0.3, pf.ptr, pf.desc,
+              mask.data_ptr(), W.data_ptr(), W.numel() * 4, stream_ptr())
+    torch.cuda.synchronize()
+    assert torch.equal(pf.t, pref.t)
+    ybits = (yf.t >= 0).to(torch.int32) * (2 ** torch.arange(16, device="cuda", dtype=torch.int32))
+    assert torch.equal(mask.to(torch.int32) & 0xFFFF, ybits.sum(-1) & 0xFFFF)
+    # backward from a pooled gradient
+    up = rng.uniform(-1, 1, (n, 16, d // 2, h // 2, w // 2)).astype(np.float32)
+    upf = Frame(n, 16, d // 2, h // 2, w // 2, margins, zero=True).load_ncdhw(up)
+    wg_y = torch.zeros(16, 4, 3, 3, 3, device="cuda")
+    wg_m = torch.zeros(16, 4, 3, 3, 3, device="cuda")
+    _lib.call("vpx_conv3d_bwd_filter_c4_pooled", xf.ptr, xf.desc, yf.ptr, yf.desc, upf.ptr, upf.desc, 0.3, 0,
+              wg_y.data_ptr(), 0, W.data_ptr(), W.numel() * 4, stream_ptr())
+    from paper_2007_12856_b200.frames import frame_desc
+
+    mfr = frame_desc(n, 16, d, h, w)
+    _lib.call("vpx_conv3d_bwd_filter_c4_pooled_mask", xf.ptr, xf.desc, mask.data_ptr(), ctypes.addressof(mfr),
+              upf.ptr, upf.desc, 0.3, wg_m.data_ptr(), 0, W.data_ptr(), W.numel() * 4, stream_ptr())
+    torch.cuda.synchronize()
+    assert torch.equal(wg_y, wg_m)
+
+
 def test_tapbox_dgrad_all_margins():
     """W-partitioned frames (margins in all three dims) go through the tap-box
     kernel for both passes."""
