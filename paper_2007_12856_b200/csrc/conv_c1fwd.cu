@@ -41,7 +41,7 @@ struct C1FwdParams {
 constexpr int kWin = 130;
 constexpr int kPlane = (3 * kWin * 16 + 127) / 128 * 128;
 constexpr int kN = 48;           // 3 height taps x 16 channels
-constexpr int kNB = 4;           // E-block ring
+constexpr int kNB = 8;           // E-block ring (8 x 48 TMEM columns)
 constexpr int kKSteps = 5;       // (a, c) tap pairs, 4 input channels
 constexpr int kBStep = 2 * kN * 16;
 constexpr int kWBytes = kKSteps * kBStep;
@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(384, 1)
     vpx::fence_barrier_init();
     vpx::tma_prefetch_desc(&xmap);
   }
-  if (warp == 2) vpx::tmem_alloc<256>(&tmem_base);
+  if (warp == 2) vpx::tmem_alloc<512>(&tmem_base);
   vpx::tc_fence_before();
   __syncthreads();
   vpx::tc_fence_after();
@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(384, 1)
         decode(task, n, z0, x0, y0, rows);
         for (int pz = 0; pz < 2; ++pz)
           for (int j = 0; j < rows + 2; ++j) {
-            vpx::mbar_wait(&empty[stage], phase ^ 1);
+            vpx::mbar_wait_sleep(&empty[stage], phase ^ 1, 20);
             vpx::mbar_arrive_expect_tx(&full[stage], 3 * kWin * 16);
             vpx::tma_load_5d(sa + stage * kPlane, &xmap, &full[stage], 0, x0 - 1 + p.x_off_w,
                              y0 - 1 + j + p.x_off_h, z0 + pz - 1 + p.x_off_d, n);
@@ -125,14 +125,14 @@ __global__ void __launch_bounds__(384, 1)
       const uint32_t ab0 = vpx::smem_u32(sa);
       int stage = 0;
       uint32_t phase = 0;
-      long long gr = 0;
+      uint32_t gr = 0;
       for (int task = blockIdx.x; task < p.num_tasks; task += gridDim.x) {
         int n, z0, x0, y0, rows;
         decode(task, n, z0, x0, y0, rows);
         for (int pz = 0; pz < 2; ++pz)
           for (int j = 0; j < rows + 2; ++j, ++gr) {
-            const int slot = static_cast<int>(gr % kNB);
-            vpx::mbar_wait(&bempty[slot], static_cast<uint32_t>(((gr / kNB) & 1) ^ 1));
+            const int slot = static_cast<int>(gr & (kNB - 1));
+            vpx::mbar_wait_sleep(&bempty[slot], ((gr / kNB) & 1) ^ 1, 20);
             vpx::mbar_wait(&full[stage], phase);
             vpx::tc_fence_after();
             const uint32_t d = tbase + slot * kN;
@@ -157,88 +157,100 @@ __global__ void __launch_bounds__(384, 1)
     __syncwarp();
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
-    const int q = warp & 3;            // TMEM lane quarter: voxels 32q .. 32q+31
+    // Row pairs (y, y+1) per iteration; 32-bit bookkeeping, pointers advanced
+    // incrementally (the per-row overhead, not the math, used to dominate).
+    const int q = warp & 3;                // TMEM lane quarter: voxels 32q .. 32q+31
     const int ch = ((warp - 4) >> 2) * 8;  // this set's 8 channels
-    const uint32_t lane_base = tbase + (static_cast<uint32_t>(q * 32) << 16);
+    const uint32_t lane_base = tbase + (static_cast<uint32_t>(q * 32) << 16) + ch;
     const float slope = p.slope;
-    long long gr = 0;
+    const bool rnd = p.rnd != 0;
+    const bool even = (lane & 1) == 0;
+    uint32_t gr = 0;
+    // one output row: sum of the three E slices -> leaky -> TF32 -> sign bits
+    auto row = [&](uint32_t g, float (&v)[8]) -> uint32_t {
+      uint32_t a0[8], a1[8], a2[8];
+      vpx::tmem_ld8_nw(lane_base + (g & (kNB - 1)) * kN + 0 * 16, a0);
+      vpx::tmem_ld8_nw(lane_base + ((g + 1) & (kNB - 1)) * kN + 1 * 16, a1);
+      vpx::tmem_ld8_nw(lane_base + ((g + 2) & (kNB - 1)) * kN + 2 * 16, a2);
+      vpx::tmem_ld_wait();
+      uint32_t bits = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        float s = (__uint_as_float(a0[i]) + __uint_as_float(a1[i])) + __uint_as_float(a2[i]);
+        s = fmaxf(s, slope * s);  // LeakyReLU, 0 < slope <= 1 (reference layers/reference.py:231-233)
+        if (rnd) s = vpx::tf32_rn(s);
+        v[i] = s;
+        bits |= (s >= 0.f ? 1u : 0u) << i;
+      }
+      return bits;
+    };
+    auto wait_full = [&](uint32_t g) { vpx::mbar_wait(&bfull[g & (kNB - 1)], (g / kNB) & 1); };
     for (int task = blockIdx.x; task < p.num_tasks; task += gridDim.x) {
       int n, z0, x0, y0, rows;
       decode(task, n, z0, x0, y0, rows);
       const int x = x0 + q * 32 + lane;
+      float* dst = p.pout + static_cast<long long>(n) * p.p_sn + static_cast<long long>((z0 >> 1) + p.p_off_d) * p.p_sd +
+                   static_cast<long long>((y0 >> 1) + p.p_off_h) * p.p_sh +
+                   static_cast<long long>((x >> 1) + p.p_off_w) * p.p_sw + ch;
       for (int pz = 0; pz < 2; ++pz) {
-        const int z = z0 + pz;
-        float prev[8];  // row y-1 of the pair (even row), this voxel
-        for (int k = 0; k < rows; ++k) {
-          const long long gm = gr + k, g0 = gm + 1, gp = gm + 2;
-          if (k == 0) {
-            vpx::mbar_wait(&bfull[gm % kNB], static_cast<uint32_t>((gm / kNB) & 1));
-            vpx::mbar_wait(&bfull[g0 % kNB], static_cast<uint32_t>((g0 / kNB) & 1));
-          }
-          vpx::mbar_wait(&bfull[gp % kNB], static_cast<uint32_t>((gp / kNB) & 1));
+        uint8_t* mrow = reinterpret_cast<uint8_t*>(p.mask) +
+                        ((((long long)n * p.d + z0 + pz) * p.h + y0) * p.w + x) * 2 + (ch >> 3);
+        const long long mstep = static_cast<long long>(p.w) * 2;
+        float* pb = pbuf + ((q * 16 + (lane >> 1)) * 16 + ch);
+        float* dp = dst;
+        wait_full(gr);
+        wait_full(gr + 1);
+        for (int k = 0; k < rows; k += 2, mrow += 2 * mstep, pb += 64 * 16, dp += p.p_sh) {
+          const uint32_t g = gr + k;
+          float v0[8], v1[8];
+          wait_full(g + 2);
           vpx::tc_fence_after();
-          uint32_t a0[8], a1[8], a2[8];
-          vpx::tmem_ld8_nw(lane_base + static_cast<uint32_t>(gm % kNB) * kN + 0 * 16 + ch, a0);
-          vpx::tmem_ld8_nw(lane_base + static_cast<uint32_t>(g0 % kNB) * kN + 1 * 16 + ch, a1);
-          vpx::tmem_ld8_nw(lane_base + static_cast<uint32_t>(gp % kNB) * kN + 2 * 16 + ch, a2);
-          vpx::tmem_ld_wait();
+          const uint32_t b0 = row(g, v0);
+          wait_full(g + 3);
+          vpx::tc_fence_after();
+          const uint32_t b1 = row(g + 1, v1);
+          // E_{y-1}, E_y are not needed by later rows of this pass
           vpx::tc_fence_before();
-          vpx::mbar_arrive(&bempty[gm % kNB]);  // E_{y-1}: no later row of this pass needs it
-          if (k == rows - 1) {
-            vpx::mbar_arrive(&bempty[g0 % kNB]);
-            vpx::mbar_arrive(&bempty[gp % kNB]);
+          vpx::mbar_arrive(&bempty[g & (kNB - 1)]);
+          vpx::mbar_arrive(&bempty[(g + 1) & (kNB - 1)]);
+          if (k + 2 >= rows) {
+            vpx::mbar_arrive(&bempty[(g + 2) & (kNB - 1)]);
+            vpx::mbar_arrive(&bempty[(g + 3) & (kNB - 1)]);
           }
-          const int y = y0 + k;
-          float v[8];
-          uint32_t bits = 0;
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            float s = (__uint_as_float(a0[i]) + __uint_as_float(a1[i])) + __uint_as_float(a2[i]);
-            s = s >= 0.f ? s : slope * s;  // LeakyReLU (reference layers/reference.py:231-233)
-            if (p.rnd) s = vpx::tf32_rn(s);
-            v[i] = s;
-            bits |= (s >= 0.f ? 1u : 0u) << i;
-          }
-          // sign mask byte of this channel half
-          reinterpret_cast<uint8_t*>(p.mask)[((((long long)n * p.d + z) * p.h + y) * p.w + x) * 2 + (ch >> 3)] =
-              static_cast<uint8_t>(bits);
-          if ((k & 1) == 0) {
-#pragma unroll
-            for (int i = 0; i < 8; ++i) prev[i] = v[i];
-            continue;
-          }
+          mrow[0] = static_cast<uint8_t>(b0);
+          mrow[mstep] = static_cast<uint8_t>(b1);
           // vpx_pool_fwd sums the window as (z,y,x) (z,y,x+1) (z,y+1,x) (z,y+1,x+1),
           // then the same four at z+1, sequentially; the even lane of each x
           // pair owns the pooled voxel and keeps that exact order
-          float pn[8], vn[8];
+          float n0[8], n1[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            pn[i] = __shfl_down_sync(0xffffffffu, prev[i], 1);
-            vn[i] = __shfl_down_sync(0xffffffffu, v[i], 1);
+            n0[i] = __shfl_down_sync(0xffffffffu, v0[i], 1);
+            n1[i] = __shfl_down_sync(0xffffffffu, v1[i], 1);
           }
-          if ((lane & 1) == 0) {
-            float* pb = pbuf + ((((k >> 1) * 64) + (q * 16 + (lane >> 1))) * 16 + ch);
+          if (even) {
             if (pz == 0) {
+              float4* pb4 = reinterpret_cast<float4*>(pb);
 #pragma unroll
-              for (int i = 0; i < 8; ++i) pb[i] = ((prev[i] + pn[i]) + v[i]) + vn[i];
+              for (int i = 0; i < 2; ++i)
+                pb4[i] = make_float4(((v0[4 * i] + n0[4 * i]) + v1[4 * i]) + n1[4 * i],
+                                     ((v0[4 * i + 1] + n0[4 * i + 1]) + v1[4 * i + 1]) + n1[4 * i + 1],
+                                     ((v0[4 * i + 2] + n0[4 * i + 2]) + v1[4 * i + 2]) + n1[4 * i + 2],
+                                     ((v0[4 * i + 3] + n0[4 * i + 3]) + v1[4 * i + 3]) + n1[4 * i + 3]);
             } else {
               float fin[8];
 #pragma unroll
               for (int i = 0; i < 8; ++i) {
                 float t = pb[i];
-                t = t + prev[i];
-                t = t + pn[i];
-                t = t + v[i];
-                t = t + vn[i];
+                t = t + v0[i];
+                t = t + n0[i];
+                t = t + v1[i];
+                t = t + n1[i];
                 t = t / 8.0f;
-                fin[i] = p.rnd ? vpx::tf32_rn(t) : t;
+                fin[i] = rnd ? vpx::tf32_rn(t) : t;
               }
-              const int yo = y >> 1, xo = x >> 1, zo = z0 >> 1;
-              float* dst = p.pout + static_cast<long long>(n) * p.p_sn + static_cast<long long>(zo + p.p_off_d) * p.p_sd +
-                           static_cast<long long>(yo + p.p_off_h) * p.p_sh +
-                           static_cast<long long>(xo + p.p_off_w) * p.p_sw + ch;
-              reinterpret_cast<float4*>(dst)[0] = make_float4(fin[0], fin[1], fin[2], fin[3]);
-              reinterpret_cast<float4*>(dst)[1] = make_float4(fin[4], fin[5], fin[6], fin[7]);
+              reinterpret_cast<float4*>(dp)[0] = make_float4(fin[0], fin[1], fin[2], fin[3]);
+              reinterpret_cast<float4*>(dp)[1] = make_float4(fin[4], fin[5], fin[6], fin[7]);
             }
           }
         }
@@ -248,7 +260,7 @@ __global__ void __launch_bounds__(384, 1)
   }
   vpx::tc_fence_before();
   __syncthreads();
-  if (warp == 2) vpx::tmem_dealloc<256>(tbase);
+  if (warp == 2) vpx::tmem_dealloc<512>(tbase);
 }
 
 }  // namespace

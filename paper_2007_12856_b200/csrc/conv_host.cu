@@ -329,6 +329,7 @@ extern "C" int vpx_conv3d_fwd_leaky_pool_c4(const float* x, const int* xfr, cons
   if (int rc = vpx::check_frame(pfr, "first block pooled output")) return rc;
   Frame xf = vpx::to_frame(xfr), pf = vpx::to_frame(pfr);
   if (!vpx::c1_fwd_pool_supported(xf, pf.c, pf)) VPX_FAIL(VPX_ERR_UNSUPPORTED, "fused first block: shape/mode");
+  if (!(slope > 0.f && slope <= 1.f)) VPX_FAIL(VPX_ERR_UNSUPPORTED, "fused first block: slope must be in (0, 1]");
   if (ws_bytes < vpx::rowh_packed_bytes(4, 16)) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "workspace too small");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   float* wpack = static_cast<float*>(ws);

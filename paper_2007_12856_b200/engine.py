@@ -329,7 +329,8 @@ def forward(ctx: RankCtx, plan: Plan, state: RankState, batch: Batch, mode: str,
                 and plan.placement[i] != "flat" and plan.redist_idx not in (i, i + 1, i + 2)
                 and not any(getattr(l, "skip", None) in (layer.name, net.layers[i + 1].name)
                             for l in net.layers)
-                and D.first_block_fwd_supported(cur, layer.params, net.layers[i + 2].pool_kind)):
+                and D.first_block_fwd_supported(cur, layer.params, net.layers[i + 2].pool_kind,
+                                                net.layers[i + 1].slope)):
             # conv -> leaky -> avg pool in one kernel: pooled output + sign mask
             pooled, mask = D.first_block_fwd(ctx, cur, P[f"{layer.name}.w"], layer.params,
                                              net.layers[i + 1].slope, plan.out_radii[i + 2], tag=layer.name)

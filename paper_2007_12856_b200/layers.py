@@ -432,9 +432,10 @@ class MaskFrame:
         return self.n * self.d * self.h * self.w
 
 
-def first_block_fwd_supported(x: DistTensor, conv_params, pool_kind: str) -> bool:
-    """conv(4 -> 16, k3 s1) -> leaky -> average pool in one kernel (TF32 mode)."""
-    if pool_kind != "average" or _lib.load().vpx_get_precision() != 0:
+def first_block_fwd_supported(x: DistTensor, conv_params, pool_kind: str, slope: float) -> bool:
+    """conv(4 -> 16, k3 s1) -> leaky(0 < slope <= 1) -> average pool in one
+    kernel (TF32 mode)."""
+    if pool_kind != "average" or _lib.load().vpx_get_precision() != 0 or not 0.0 < slope <= 1.0:
         return False
     if conv_params.cin != 4 or conv_params.cout != 16:
         return False
