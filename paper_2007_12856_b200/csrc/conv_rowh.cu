@@ -36,7 +36,6 @@ using vpx::ConvRowParams;
 
 constexpr int kWinH = 130;                             // 128 outputs + 2 halo voxels
 constexpr int kPlane = (3 * kWinH * 16 + 127) / 128 * 128;  // 3 depth planes x 130 voxels x 16 B
-constexpr int kNB = 4;                                 // TMEM ring of E blocks
 
 template <int CIN, int C>
 struct RowH {
@@ -51,14 +50,15 @@ struct RowH {
   static constexpr int S0 = (226 * 1024 - 2048 - WBYTES - EPI) / STAGE;
   static constexpr int S = S0 > 8 ? 8 : S0;
   static constexpr int SMEM = (WBYTES + 1023) / 1024 * 1024 + S * STAGE + EPI + 1024;
-  static constexpr int TCOLS = kNB * N <= 256 ? 256 : 512;
+  static constexpr int NB = 512 / N >= 8 ? 8 : 4;       // TMEM ring of E blocks (power of 2)
+  static constexpr int TCOLS = NB * N <= 256 ? 256 : 512;
 };
 
 template <int CIN, int C>
 __global__ void __launch_bounds__(384, 1)
     conv_rowh_kernel(const __grid_constant__ CUtensorMap xmap, const ConvRowParams p) {
   using K = RowH<CIN, C>;
-  constexpr int N = K::N, S = K::S;
+  constexpr int N = K::N, S = K::S, kNB = K::NB;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sw = smem;                                                   // resident weights
@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(384, 1)
         decode(task, n, z, x0, y0, rows);
         for (int j = 0; j < rows + 2; ++j) {
           const int r = y0 - 1 + j;
-          vpx::mbar_wait(&empty[stage], phase ^ 1);
+          vpx::mbar_wait_sleep(&empty[stage], phase ^ 1, 20);
           uint8_t* dst = sa + stage * K::STAGE;
           vpx::mbar_arrive_expect_tx(&full[stage], K::NCH * 3 * kWinH * 16);
 #pragma unroll
@@ -138,13 +138,13 @@ __global__ void __launch_bounds__(384, 1)
       const uint32_t ab0 = vpx::smem_u32(sa);
       int stage = 0;
       uint32_t phase = 0;
-      long long gr = 0;  // E blocks produced by this CTA
+      uint32_t gr = 0;  // E blocks produced by this CTA
       for (int task = blockIdx.x; task < p.num_tiles; task += gridDim.x) {
         int n, z, x0, y0, rows;
         decode(task, n, z, x0, y0, rows);
         for (int j = 0; j < rows + 2; ++j, ++gr) {
-          const int slot = static_cast<int>(gr % kNB);
-          vpx::mbar_wait(&bempty[slot], static_cast<uint32_t>(((gr / kNB) & 1) ^ 1));
+          const int slot = static_cast<int>(gr & (kNB - 1));
+          vpx::mbar_wait_sleep(&bempty[slot], ((gr / kNB) & 1) ^ 1, 20);
           vpx::mbar_wait(&full[stage], phase);
           vpx::tc_fence_after();
           const uint32_t d = tbase + slot * N;
@@ -182,40 +182,44 @@ __global__ void __launch_bounds__(384, 1)
     __syncwarp();
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
-    const int q = warp & 3;          // TMEM lane quarter = voxels 32q .. 32q+31 of the segment
+    const int q = warp & 3;            // TMEM lane quarter = voxels 32q .. 32q+31 of the segment
     const int hset = (warp - 4) >> 2;  // output rows k with k % 2 == hset
     float* stg = sepi + (warp - 4) * 32 * (C + 4);
     const uint32_t lane_base = tbase + (static_cast<uint32_t>(q * 32) << 16);
-    long long gr = 0;
+    const bool act = p.act != 0, rnd = p.rnd != 0;
+    const float slope = p.slope;
+    uint32_t gr = 0;
     for (int task = blockIdx.x; task < p.num_tiles; task += gridDim.x) {
       int n, z, x0, y0, rows;
       decode(task, n, z, x0, y0, rows);
       // E blocks of this band: gr .. gr + rows + 1 (input rows y0-1 .. y0+rows)
-      float* orow_w = p.out + static_cast<long long>(n) * p.out_sn +
-                      static_cast<long long>(z + p.out_off_d) * p.out_sd +
-                      static_cast<long long>(x0 + q * 32 + p.out_off_w) * p.out_sw;
-      for (int k = hset; k < rows; k += 2) {
-        const long long gm = gr + k, g0 = gm + 1, gp = gm + 2;  // E_{y-1}, E_y, E_{y+1}
+      float* ow = p.out + static_cast<long long>(n) * p.out_sn + static_cast<long long>(z + p.out_off_d) * p.out_sd +
+                  static_cast<long long>(x0 + q * 32 + p.out_off_w) * p.out_sw +
+                  static_cast<long long>(y0 + hset + p.out_off_h) * p.out_sh;
+      const long long ostep = 2 * p.out_sh;
+      for (int k = hset; k < rows; k += 2, ow += ostep) {
+        const uint32_t gm = gr + k;  // E_{y-1}, E_y, E_{y+1} = gm, gm+1, gm+2
         // none of the three can be recycled before this row frees E_{y-1} and
         // the other set finishes row k+1, so the parity waits are unambiguous
-        vpx::mbar_wait(&bfull[gm % kNB], static_cast<uint32_t>((gm / kNB) & 1));
-        vpx::mbar_wait(&bfull[g0 % kNB], static_cast<uint32_t>((g0 / kNB) & 1));
-        vpx::mbar_wait(&bfull[gp % kNB], static_cast<uint32_t>((gp / kNB) & 1));
+        vpx::mbar_wait(&bfull[gm & (kNB - 1)], (gm / kNB) & 1);
+        vpx::mbar_wait(&bfull[(gm + 1) & (kNB - 1)], ((gm + 1) / kNB) & 1);
+        vpx::mbar_wait(&bfull[(gm + 2) & (kNB - 1)], ((gm + 2) / kNB) & 1);
         vpx::tc_fence_after();
-        const int y = y0 + k;
+        const uint32_t s0 = lane_base + (gm & (kNB - 1)) * N, s1 = lane_base + ((gm + 1) & (kNB - 1)) * N + C,
+                       s2 = lane_base + ((gm + 2) & (kNB - 1)) * N + 2 * C;
 #pragma unroll
         for (int cb = 0; cb < C / 16; ++cb) {
           uint32_t v0[16], v1[16], v2[16];  // three loads in flight, one wait
-          vpx::tmem_ld16_nw(lane_base + static_cast<uint32_t>(gm % kNB) * N + 0 * C + cb * 16, v0);
-          vpx::tmem_ld16_nw(lane_base + static_cast<uint32_t>(g0 % kNB) * N + 1 * C + cb * 16, v1);
-          vpx::tmem_ld16_nw(lane_base + static_cast<uint32_t>(gp % kNB) * N + 2 * C + cb * 16, v2);
+          vpx::tmem_ld16_nw(s0 + cb * 16, v0);
+          vpx::tmem_ld16_nw(s1 + cb * 16, v1);
+          vpx::tmem_ld16_nw(s2 + cb * 16, v2);
           vpx::tmem_ld_wait();
           float v[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             v[i] = (__uint_as_float(v0[i]) + __uint_as_float(v1[i])) + __uint_as_float(v2[i]);
-            if (p.act) v[i] = v[i] >= 0.f ? v[i] : p.slope * v[i];  // reference layers/reference.py:231-233
-            if (p.rnd) v[i] = vpx::tf32_rn(v[i]);
+            if (act) v[i] = v[i] >= 0.f ? v[i] : slope * v[i];  // reference layers/reference.py:231-233
+            if (rnd) v[i] = vpx::tf32_rn(v[i]);
           }
           float4* s4 = reinterpret_cast<float4*>(stg + lane * (C + 4) + cb * 16);
 #pragma unroll
@@ -224,13 +228,12 @@ __global__ void __launch_bounds__(384, 1)
         // E_{y-1} is not needed by any later output row of this band; the last
         // row also releases the band's final two blocks
         vpx::tc_fence_before();
-        vpx::mbar_arrive(&bempty[gm % kNB]);
+        vpx::mbar_arrive(&bempty[gm & (kNB - 1)]);
         if (k == rows - 1) {
-          vpx::mbar_arrive(&bempty[(gm + 1) % kNB]);
-          vpx::mbar_arrive(&bempty[(gm + 2) % kNB]);
+          vpx::mbar_arrive(&bempty[(gm + 1) & (kNB - 1)]);
+          vpx::mbar_arrive(&bempty[(gm + 2) & (kNB - 1)]);
         }
         __syncwarp();
-        float* ow = orow_w + static_cast<long long>(y + p.out_off_h) * p.out_sh;
         constexpr int Q = C / 4;  // float4 chunks per voxel
 #pragma unroll
         for (int kk = 0; kk < Q; ++kk) {
