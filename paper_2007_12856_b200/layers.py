@@ -469,6 +469,8 @@ def first_block_fast_path(conv, act, y: DistTensor, u: DistTensor, x_meta) -> bo
         return False
     if tuple(conv.params.kernel) != (3, 3, 3) or tuple(conv.params.stride) != (1, 1, 1):
         return False
+    if not isinstance(y, MaskFrame) and _lib.load().vpx_get_precision() != 0:
+        return False  # the fast-path kernels are tcgen05 (TF32); FP32 mode takes the CUDA-core path
     # frames may carry D/H halo margins (the pooled gradient arrives in the
     # next conv's dgrad frame); the dense x view needs no W margin
     return y.w in (64, 128, 256, 512) and x_meta.margins()[2] == 0
