@@ -191,6 +191,11 @@ int vpx_prng_volume(unsigned long long key, const int* ff, long long counter_bas
 int vpx_adam(float* p, const float* g, float* m, float* v, long long n, float lr, float b1, float b2,
              float c1, float c2, float eps, void* stream);
 int vpx_sgd(float* p, const float* g, long long n, float lr, void* stream);
+/* Graph-replayable variants: per-step scalars read from device memory
+ * (hyper = {lr, 1-b1^t, 1-b2^t}; key = the folded dropout key). */
+int vpx_adam_dev(float* p, const float* g, float* m, float* v, long long n, const float* hyper, float b1,
+                 float b2, float eps, void* stream);
+int vpx_prng_mask_dev(const unsigned long long* key, long long n, double keep, unsigned char* out, void* stream);
 
 /* ----------------------------------------------------------------- losses --
  * Per-voxel softmax cross entropy (reference layers/reference.py:282-307):

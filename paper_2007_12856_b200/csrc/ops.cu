@@ -421,6 +421,33 @@ __global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ g, 
     p[i] = p[i] - lr * (mi / c1) / (sqrtf(vi / c2) + eps);
   }
 }
+// Same update with lr, 1-b1^t, 1-b2^t read from device memory (hyper = {lr, c1,
+// c2}): the step can be captured once in a CUDA graph and replayed with the
+// per-step scalars rewritten in place.
+__global__ void adam_dev_kernel(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
+                                float* __restrict__ v, long long n, const float* __restrict__ hyper, float b1,
+                                float b2, float eps) {
+  const float lr = hyper[0], c1 = hyper[1], c2 = hyper[2];
+  GRID_STRIDE(i, n) {
+    const float gi = g[i];
+    float mi = m[i] * b1;
+    mi = mi + (1.f - b1) * gi;
+    float vi = v[i] * b2;
+    vi = vi + (1.f - b2) * (gi * gi);
+    m[i] = mi;
+    v[i] = vi;
+    p[i] = p[i] - lr * (mi / c1) / (sqrtf(vi / c2) + eps);
+  }
+}
+__global__ void prng_mask_dev_kernel(const uint64_t* __restrict__ keyp, long long n, double keep,
+                                     uint8_t* __restrict__ out) {
+  const uint64_t key = *keyp;
+  GRID_STRIDE(i, n) {
+    const uint64_t r = sm_mix(key + (static_cast<uint64_t>(i) + 1ULL) * 0x9E3779B97F4A7C15ULL);
+    const double u01 = __dmul_rn(static_cast<double>(r >> 11), 1.1102230246251565e-16);
+    out[i] = u01 < keep ? 1 : 0;
+  }
+}
 __global__ void sgd_kernel(float* __restrict__ p, const float* __restrict__ g, long long n, float lr) {
   GRID_STRIDE(i, n) p[i] = p[i] - lr * g[i];
 }
@@ -655,6 +682,16 @@ extern "C" int vpx_prng_volume(unsigned long long key, const int* ff, long long 
 extern "C" int vpx_adam(float* p, const float* g, float* m, float* v, long long n, float lr,
                         float b1, float b2, float c1, float c2, float eps, void* st) {
   adam_kernel<<<grid1d(n), 256, 0, S(st)>>>(p, g, m, v, n, lr, b1, b2, c1, c2, eps);
+  LAUNCH_TAIL;
+}
+extern "C" int vpx_adam_dev(float* p, const float* g, float* m, float* v, long long n, const float* hyper,
+                            float b1, float b2, float eps, void* st) {
+  adam_dev_kernel<<<grid1d(n), 256, 0, S(st)>>>(p, g, m, v, n, hyper, b1, b2, eps);
+  LAUNCH_TAIL;
+}
+extern "C" int vpx_prng_mask_dev(const unsigned long long* key, long long n, double keep, unsigned char* out,
+                                 void* st) {
+  prng_mask_dev_kernel<<<grid1d(n), 256, 0, S(st)>>>(reinterpret_cast<const uint64_t*>(key), n, keep, out);
   LAUNCH_TAIL;
 }
 extern "C" int vpx_sgd(float* p, const float* g, long long n, float lr, void* st) {

@@ -270,12 +270,19 @@ def lr_at(lr0: float, epoch: int, horizon: int = 100, terminal: float = 0.01) ->
     return lr0 * (1.0 - (1.0 - terminal) * e / horizon)
 
 
-def optimizer_step(state: RankState, lr: float):
+def optimizer_step(state: RankState, lr: float, scalars: "StepScalars" = None):
     """Adam (bias corrected, sqrt(v_hat)+eps) or SGD over the flat buffers
-    (reference optim.py:63-93)."""
+    (reference optim.py:63-93).  With `scalars` the step count, lr and bias
+    corrections come from device memory (graph replay; StepScalars owns t)."""
     p, opt = state.params, state.opt
-    opt.t += 1
     st = stream_ptr()
+    if scalars is not None:
+        if opt.kind != "adam":
+            raise ShapeMismatch("graph-captured steps support Adam only")
+        _lib.call("vpx_adam_dev", p.flat.data_ptr(), p.grad.data_ptr(), opt.m.data_ptr(), opt.v.data_ptr(),
+                  p.numel, scalars.hyper_ptr, opt.beta1, opt.beta2, opt.eps, st)
+        return
+    opt.t += 1
     if opt.kind == "adam":
         c1 = 1.0 - opt.beta1 ** opt.t
         c2 = 1.0 - opt.beta2 ** opt.t
@@ -287,9 +294,17 @@ def optimizer_step(state: RankState, lr: float):
 
 # ------------------------------------------------------------------ forward
 
-def _flat_mask(layer_idx, step_key, sample_ids, features, keep):
+def _flat_mask(layer_idx, step_key, sample_ids, features, keep, scalars=None):
     seed, epoch, it = step_key
-    rows = [prng.keep_mask_device([seed, epoch, it, int(s), layer_idx], features, keep) for s in sample_ids]
+    if scalars is not None:  # keys live in device memory, rewritten per replay
+        rows = []
+        for s in sample_ids:
+            out = torch.empty(features, dtype=torch.uint8, device="cuda")
+            _lib.call("vpx_prng_mask_dev", scalars.key_ptr(layer_idx, int(s)), features, float(keep),
+                      out.data_ptr(), stream_ptr())
+            rows.append(out)
+    else:
+        rows = [prng.keep_mask_device([seed, epoch, it, int(s), layer_idx], features, keep) for s in sample_ids]
     if not rows:
         return torch.zeros((0, features), dtype=torch.uint8, device="cuda")
     return torch.stack(rows)
@@ -305,7 +320,7 @@ def _flatten(t: DistTensor):
 
 
 def forward(ctx: RankCtx, plan: Plan, state: RankState, batch: Batch, mode: str, seed: int = 0,
-            trace: dict = None):
+            trace: dict = None, scalars: "StepScalars" = None):
     net = plan.net
     P, bn = state.params.views, state.bn_states
     me = ctx.rank
@@ -359,7 +374,7 @@ def forward(ctx: RankCtx, plan: Plan, state: RankState, batch: Batch, mode: str,
                 cur = torch.where(cur >= 0, cur, cur * layer.slope)
             elif layer.kind == "dropout":
                 if mode == "train":
-                    m = _flat_mask(i, step_key, batch.sample_ids, cur.shape[1], layer.keep)
+                    m = _flat_mask(i, step_key, batch.sample_ids, cur.shape[1], layer.keep, scalars)
                     cur = _apply_mask(cur, m, layer.keep)
                     stash.append(m)
                 else:
@@ -545,16 +560,86 @@ def gradient_allreduce(ctx: RankCtx, state: RankState):
     ctx.allreduce_sum_(state.params.grad, None)
 
 
-def train_step(ctx: RankCtx, plan: Plan, state: RankState, batch: Batch, lr: float, seed: int = 0):
+def train_step(ctx: RankCtx, plan: Plan, state: RankState, batch: Batch, lr: float, seed: int = 0,
+               scalars: "StepScalars" = None):
     """One hybrid-parallel training step; returns the loss as a 1-element
     fp64 CUDA tensor (identical on every rank).  No host synchronisation."""
     state.params.grad.zero_()
-    pred, stash = forward(ctx, plan, state, batch, "train", seed)
+    pred, stash = forward(ctx, plan, state, batch, "train", seed, scalars=scalars)
     loss, dpred = loss_and_grad(ctx, plan, pred, batch)
     backward(ctx, plan, state, stash, dpred)
     gradient_allreduce(ctx, state)
-    optimizer_step(state, lr)
+    optimizer_step(state, lr, scalars)
     return loss
+
+
+class StepScalars:
+    """Per-step scalars that a captured step reads from device memory: Adam's
+    {lr, 1-b1^t, 1-b2^t} and one folded dropout key per (dropout layer,
+    sample).  `set(...)` recomputes them on the host (same formulas as the
+    eager step: reference optim.py:71-88, engine.py:314-320) and queues one
+    pinned host->device copy on the current stream."""
+
+    def __init__(self, net: NetworkSpec, sample_ids):
+        self.slots = {}
+        for i, layer in enumerate(net.layers):
+            if layer.kind == "dropout":
+                for s in sample_ids:
+                    self.slots[(i, int(s))] = len(self.slots)
+        self.dev = torch.zeros(4 + 2 * max(1, len(self.slots)), dtype=torch.float32, device="cuda")
+        self.host = torch.zeros_like(self.dev, device="cpu").pin_memory()
+        self.hyper_ptr = self.dev.data_ptr()
+        self._keys = self.host[4:].view(torch.int64)
+
+    def key_ptr(self, layer_idx: int, sample_id: int) -> int:
+        return self.dev.data_ptr() + 16 + 8 * self.slots[(layer_idx, sample_id)]
+
+    def set(self, state: RankState, lr: float, step_key):
+        opt = state.opt
+        opt.t += 1
+        self.host[0] = float(lr)
+        self.host[1] = float(1.0 - opt.beta1 ** opt.t)
+        self.host[2] = float(1.0 - opt.beta2 ** opt.t)
+        seed, epoch, it = step_key
+        for (i, s), k in self.slots.items():
+            v = prng.key_fold([seed, epoch, it, s, i])
+            self._keys[k] = v - (1 << 64) if v >= (1 << 63) else v
+        self.dev.copy_(self.host, non_blocking=True)
+
+
+class CapturedStep:
+    """train_step captured once in a CUDA graph and replayed (no per-kernel
+    launch cost, no Python on the hot path).  Shapes, buffers and the batch's
+    device frames are fixed at capture; per-step scalars (lr, Adam bias
+    corrections, dropout keys) go through StepScalars, the input block is
+    refreshed in place (e.g. HostInputPipeline.load) before each call.  The
+    loss tensor returned is the graph's static output."""
+
+    def __init__(self, ctx: RankCtx, plan: Plan, state: RankState, batch: Batch, lr: float, seed: int = 0,
+                 warmup: int = 2):
+        self.ctx, self.plan, self.state, self.batch, self.seed = ctx, plan, state, batch, seed
+        self.scalars = StepScalars(plan.net, batch.sample_ids)
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            for _ in range(warmup):  # real steps: settles workspaces and allocator state
+                self.scalars.set(state, lr, (seed, batch.epoch, batch.iteration))
+                train_step(ctx, plan, state, batch, lr, seed, scalars=self.scalars)
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.loss = train_step(ctx, plan, state, batch, lr, seed, scalars=self.scalars)
+
+    def __call__(self, lr: float, epoch: int = None, iteration: int = None):
+        b = self.batch
+        if epoch is not None:
+            b.epoch = epoch
+        if iteration is not None:
+            b.iteration = iteration
+        self.scalars.set(self.state, lr, (self.seed, b.epoch, b.iteration))
+        self.graph.replay()
+        return self.loss
 
 
 # ------------------------------------------------------------------ batches
