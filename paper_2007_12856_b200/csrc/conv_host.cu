@@ -306,6 +306,10 @@ extern "C" int vpx_conv3d_bwd_filter(const float* x, const int* xfr, const float
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   float* part = reinterpret_cast<float*>(static_cast<char*>(ws) +
                                          ((vpx::packed_floats(xf.c, uf.c) * 4 + 255) / 256) * 256);
+  if (k == 3 && vpx::wgrad_ut_supported(xf, uf, stride) && !getenv("VPX_NO_WGRAD_UT")) {
+    if (int rc = vpx::conv_wgrad_ut(x, xf, u, uf, part, st)) return rc;
+    return vpx::reduce_partials(part, vpx::wgrad_ut_parts(uf), (long long)uf.c * xf.c * 27, wg, accumulate, st);
+  }
   if (vpx::precision() == 0 && k == 3 && vpx::wgrad_tc_supported(xf, uf, stride)) {
     if (int rc = vpx::conv_wgrad_tc(x, xf, u, uf, stride, part, st)) return rc;
     return vpx::reduce_partials(part, vpx::wgrad_tc_parts(xf, uf), (long long)uf.c * xf.c * 27, wg,

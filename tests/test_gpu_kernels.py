@@ -46,6 +46,7 @@ CASES = [
     (1, 4, 16, 4, 6, 128, 3, 1),
     (2, 4, 16, 3, 5, 256, 3, 1),
     (1, 16, 32, 4, 4, 128, 3, 1),
+    (2, 16, 32, 3, 6, 256, 3, 1),      # u-in-TMEM filter gradient (W = 256)
     (1, 32, 64, 3, 3, 128, 3, 1),
     (1, 64, 128, 8, 8, 8, 3, 2),
     (1, 128, 256, 4, 4, 4, 3, 1),
