@@ -36,16 +36,16 @@ struct UtParams {
 
 constexpr int kAcc = 64;          // N per accumulator
 constexpr int kACol = 4 * kAcc;   // A ring starts at TMEM column 256
-constexpr int kSlots = 8;         // A slots in TMEM
-constexpr int kUSt = 16;          // u stages in shared memory (TMA lookahead)
+constexpr int kSlots = 8;         // A slots in TMEM, 16 columns (two K=8 steps) each
+constexpr int kUSt = 8;           // u stages in shared memory (TMA lookahead)
 
 template <int W>
 struct UtCfg {
-  static constexpr int KS = (W / 2 + 1 + 7) / 8;          // K steps per row pair (k = -1 .. 8KS-2)
-  static constexpr int XCH = 8 * KS + 1;                  // x chunks -1 .. 8KS-1
+  static constexpr int KS = (W / 2 + 1 + 15) / 16;        // 16-row slots per row pair (k = -1 .. 16KS-2)
+  static constexpr int XCH = 16 * KS + 1;                 // x chunks -1 .. 16KS-1
   static constexpr int XROW = (XCH * 128 + 1023) / 1024 * 1024;
   static constexpr int XS = 8 * XROW;                     // 8-row ring of input rows
-  static constexpr int UST = 2 * 16 * 32 * 4;             // u box: 2 rows x 16 voxels x 32 ch (4 KB)
+  static constexpr int UST = 2 * 32 * 32 * 4;             // u box: 2 rows x 32 voxels x 32 ch (8 KB)
   static constexpr int PIPE = XS + kUSt * UST;
   static constexpr int SCRATCH = 4 * 32 * 16 * 9 * 4;    // epilogue fold
   static constexpr int SMEM = PIPE > SCRATCH ? PIPE : SCRATCH;
@@ -133,37 +133,41 @@ __global__ void __launch_bounds__(384, 1)
           const int st = g & (kUSt - 1);
           vpx::mbar_wait_sleep(&uempty[st], ((g / kUSt) & 1) ^ 1, 20);
           vpx::mbar_arrive_expect_tx(&ufull[st], Cfg::UST);
-          vpx::tma_load_5d(us + st * Cfg::UST, &umap, &ufull[st], 0, 16 * s - 1, y, z, n);
+          vpx::tma_load_5d(us + st * Cfg::UST, &umap, &ufull[st], 0, 32 * s - 1, y, z, n);
         }
       }
     }
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA
     constexpr uint32_t idesc = vpx::make_idesc(2, 128, kAcc, false, true);
-    if (vpx::elect_one()) {
+    if (vpx::elect_one()) {  // one thread issues everything
       const uint32_t xb = vpx::smem_u32(xs);
       uint32_t g = 0;
+      int y = 2 * static_cast<int>(r0 % hp);
       for (long long pr = r0; pr < r1; ++pr) {
         const int i = static_cast<int>(pr - r0);
-        const int y = 2 * static_cast<int>(pr % hp);
         vpx::mbar_wait(&xfull[i & 3], (i >> 2) & 1);
         uint64_t bd[4];  // input rows y-1 .. y+2 at K step 0
 #pragma unroll
         for (int X = 0; X < 4; ++X) bd[X] = vpx::make_sdesc(xb + ((y - 1 + X) & 7) * XROW, 128, 512, 1);
-#pragma unroll 1
         for (int s = 0; s < KS; ++s, ++g) {
           const int slot = g & (kSlots - 1);
           vpx::mbar_wait(&fullA[slot], (g / kSlots) & 1);
           vpx::tc_fence_after();
-          const uint32_t acol = tbase + kACol + slot * 8;
-          const uint32_t acc = (i > 0 || s > 0) ? 1u : 0u;
+          const uint32_t acol = tbase + kACol + slot * 16;
 #pragma unroll
-          for (int X = 0; X < 4; ++X)  // K step s starts 8 chunk rows (1024 B) further
-            vpx::umma_tf32_ta(tbase + X * kAcc, acol, bd[X] + static_cast<uint64_t>(s * 64), idesc, acc);
+          for (int hh = 0; hh < 2; ++hh) {  // two K=8 steps per slot; 8 chunk rows (1024 B) each
+            const uint32_t acc = (i > 0 || s > 0 || hh > 0) ? 1u : 0u;
+#pragma unroll
+            for (int X = 0; X < 4; ++X)
+              vpx::umma_tf32_ta(tbase + X * kAcc, acol + 8 * hh, bd[X] + static_cast<uint64_t>((2 * s + hh) * 64),
+                                idesc, acc);
+          }
           vpx::umma_commit(&emptyA[slot]);
         }
         vpx::umma_commit(&rowdone[i & 3]);
         if (pr == r1 - 1) vpx::umma_commit(&tfull);
+        y = (y + 2 == p.h) ? 0 : y + 2;
       }
     }
     __syncwarp();
@@ -174,24 +178,24 @@ __global__ void __launch_bounds__(384, 1)
     const int q = warp & 3, h = (warp - 4) >> 2;  // lane quarter = (r, d) = (q >> 1, q & 1); lane = co
     const int r = q >> 1, dsh = q & 1;
     const uint32_t lane_addr = tbase + (static_cast<uint32_t>(q * 32) << 16) + kACol;
-    const uint32_t ub = vpx::smem_u32(us) + (r * 16 + dsh) * 128 + lane * 4;
+    const uint32_t ub = vpx::smem_u32(us) + (r * 32 + dsh) * 128 + lane * 4;
     const uint32_t total = static_cast<uint32_t>((r1 - r0) * KS);
-    auto load = [&](uint32_t g, float (&v)[8]) {
+    auto load = [&](uint32_t g, float (&v)[16]) {
       const int st = g & (kUSt - 1);
       vpx::mbar_wait(&ufull[st], (g / kUSt) & 1);
       const uint32_t base = ub + st * Cfg::UST;  // column kk: box voxel 2kk + d
 #pragma unroll
-      for (int kk = 0; kk < 8; ++kk) v[kk] = vpx::lds_f32(base + kk * 256);
+      for (int kk = 0; kk < 16; ++kk) v[kk] = vpx::lds_f32(base + kk * 256);
       __syncwarp();
       if (lane == 0) vpx::mbar_arrive(&uempty[st]);
     };
-    float v[8];
+    float v[16];
     uint32_t g = h;
     if (g < total) load(g, v);
     for (; g < total; g += 2) {
       const int st = g & (kSlots - 1);
       vpx::mbar_wait(&emptyA[st], ((g / kSlots) & 1) ^ 1);
-      vpx::tmem_st8(lane_addr + st * 8, v);
+      vpx::tmem_st16(lane_addr + st * 16, v);
       if (g + 2 < total) load(g + 2, v);  // overlaps the store
       vpx::tmem_st_wait();
       vpx::tc_fence_before();
@@ -308,7 +312,7 @@ int conv_wgrad_ut(const float* x, const Frame& xf, const float* u, const Frame& 
   {
     uint64_t dims[5] = {32, (uint64_t)W, (uint64_t)uf.h, (uint64_t)uf.d, (uint64_t)uf.n};
     uint64_t strides[4] = {128, (uint64_t)W * 128, (uint64_t)uf.h * W * 128, (uint64_t)uf.d * uf.h * W * 128};
-    uint32_t box[5] = {32, 16, 2, 1, 1};
+    uint32_t box[5] = {32, 32, 2, 1, 1};
     if (int rc = encode_tiled(&um, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float*>(u), dims, strides, box,
                               CU_TENSOR_MAP_SWIZZLE_NONE))
       return rc;
