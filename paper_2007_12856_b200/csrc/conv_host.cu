@@ -138,9 +138,16 @@ static int rowh_run(const float* in, const Frame& inf, const float* wpack, int c
     const uint64_t Wf = inf.w + 2 * inf.mw, Hf = inf.h + 2 * inf.mh, Df = inf.d + 2 * inf.md;
     uint64_t dims[5] = {(uint64_t)inf.c, Wf, Hf, Df, (uint64_t)inf.n};
     uint64_t strides[4] = {(uint64_t)inf.c * 4, Wf * inf.c * 4, Hf * Wf * inf.c * 4, Df * Hf * Wf * inf.c * 4};
-    uint32_t box[5] = {4, 130, 1, 3, 1};
+    // cin 4: one 16-byte voxel row per box row (interleaved layout); cin 8/16/32:
+    // whole voxel rows in the K-major swizzle of matching width (conv_rowh.cu)
+    const uint32_t ci = static_cast<uint32_t>(cin_eff);
+    uint32_t box[5] = {ci, 130, 1, 3, 1};
+    const CUtensorMapSwizzle sw = ci == 32   ? CU_TENSOR_MAP_SWIZZLE_128B
+                                  : ci == 16 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                  : ci == 8  ? CU_TENSOR_MAP_SWIZZLE_32B
+                                             : CU_TENSOR_MAP_SWIZZLE_NONE;
     if (int rc = encode_tiled(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float*>(in), dims, strides, box,
-                              CU_TENSOR_MAP_SWIZZLE_NONE))
+                              sw))
       return rc;
   }
   ConvRowParams p{};

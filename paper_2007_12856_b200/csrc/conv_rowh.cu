@@ -40,12 +40,16 @@ constexpr int kPlane = (3 * kWinH * 16 + 127) / 128 * 128;  // 3 depth planes x 
 template <int CIN, int C>
 struct RowH {
   static constexpr bool PAIR = CIN == 4;                 // two (a,c) taps per K=8 step
-  static constexpr int NCH = CIN / 4;                    // 4-channel chunk planes per input row
+  static constexpr int NCH = CIN / 4;                    // 4-channel chunk planes per input row (PAIR)
+  // CIN >= 8: the window is stored as whole voxel rows (CIN*4 bytes) in the
+  // matching K-major swizzle (one wide TMA box; a width tap is a row shift)
+  static constexpr int RB = CIN * 4;
+  static constexpr uint32_t LAYOUT = RB == 128 ? 2 : RB == 64 ? 4 : 6;  // SW128 / SW64 / SW32
   static constexpr int KSTEPS = PAIR ? 5 : 9 * (CIN / 8);
   static constexpr int N = 3 * C;
   static constexpr int BSTEP = 2 * N * 16;               // bytes of B per K step
   static constexpr int WBYTES = KSTEPS * BSTEP;
-  static constexpr int STAGE = NCH * kPlane;
+  static constexpr int STAGE = PAIR ? NCH * kPlane : (3 * kWinH * RB + 1023) / 1024 * 1024;
   static constexpr int EPI = 8 * 32 * (C + 4) * 4;       // 8 epilogue warps
   static constexpr int S0 = (226 * 1024 - 2048 - WBYTES - EPI) / STAGE;
   static constexpr int S = S0 > 8 ? 8 : S0;
@@ -117,11 +121,14 @@ __global__ void __launch_bounds__(384, 1)
           const int r = y0 - 1 + j;
           vpx::mbar_wait_sleep(&empty[stage], phase ^ 1, 20);
           uint8_t* dst = sa + stage * K::STAGE;
-          vpx::mbar_arrive_expect_tx(&full[stage], K::NCH * 3 * kWinH * 16);
-#pragma unroll
-          for (int c = 0; c < K::NCH; ++c)
-            vpx::tma_load_5d(dst + c * kPlane, &xmap, &full[stage], 4 * c, x0 - 1 + p.in_off_w, r + p.in_off_h,
-                             z - 1 + p.in_off_d, n);
+          vpx::mbar_arrive_expect_tx(&full[stage], 3 * kWinH * CIN * 4);
+          if constexpr (K::PAIR) {
+            vpx::tma_load_5d(dst, &xmap, &full[stage], 0, x0 - 1 + p.in_off_w, r + p.in_off_h, z - 1 + p.in_off_d,
+                             n);
+          } else {
+            vpx::tma_load_5d(dst, &xmap, &full[stage], 0, x0 - 1 + p.in_off_w, r + p.in_off_h, z - 1 + p.in_off_d,
+                             n);
+          }
           if (++stage == S) {
             stage = 0;
             phase ^= 1;
@@ -163,8 +170,9 @@ __global__ void __launch_bounds__(384, 1)
             for (int t = 0; t < 9; ++t) {
 #pragma unroll
               for (int jp = 0; jp < CIN / 8; ++jp) {
-                const uint64_t adesc =
-                    vpx::make_sdesc(ab + 2 * jp * kPlane + ((t / 3) * kWinH + t % 3) * 16, kPlane, 128, 0);
+                // row (plane a, voxel c) of the swizzled window, K step jp = 8 channels (32 B)
+                const uint64_t adesc = vpx::make_sdesc(ab + ((t / 3) * kWinH + t % 3) * K::RB + jp * 32, 16,
+                                                       8 * K::RB, K::LAYOUT);
                 const uint64_t bdesc = vpx::make_sdesc(wb + (t * (CIN / 8) + jp) * K::BSTEP, N * 16, 128, 0);
                 vpx::umma_tf32(d, adesc, bdesc, idesc, (t | jp) != 0 ? 1u : 0u);
               }
