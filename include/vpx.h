@@ -48,6 +48,9 @@ long long vpx_launch_count(void);
  * 1 = FP32: every conv pass on CUDA-core direct kernels in fp32, no rounding
  * (the reference's own fp32 verify tolerance, rel 1e-5, reference cli.py:186). */
 int vpx_set_precision(int mode);
+/* Persistent-kernel grid budget for subsequent launches (0 = every SM): lets
+ * NCCL kernels run beside an overlapped convolution. */
+int vpx_set_sm_limit(int n);
 int vpx_get_precision(void);
 
 /* ------------------------------------------------------------ convolution --
@@ -72,11 +75,22 @@ int vpx_conv3d_fwd_act(const float* x, const int* xfr, const float* w, int k, in
                        const int* yfr, int act, float slope, void* ws, long long ws_bytes,
                        void* stream);
 
+/* Same on output planes [zlo, zhi) only (row kernels; VPX_ERR_UNSUPPORTED
+ * otherwise): lets the caller overlap a halo exchange with the planes that do
+ * not read the halo. */
+int vpx_conv3d_fwd_act_range(const float* x, const int* xfr, const float* w, int k, int stride, float* y,
+                             const int* yfr, int act, float slope, int zlo, int zhi, void* ws, long long ws_bytes,
+                             void* stream);
+
 /* xg = adjoint scatter of u through w, over EVERY position of the xg frame
  * (interior and margins): replaces voxpar.kernels.conv3d_bwd_data(u, w,
  * stride, pad_spatial) (reference kernels/__init__.py:67, _hot.pyx:44-67). */
 int vpx_conv3d_bwd_data(const float* u, const int* ufr, const float* w, int k, int stride,
                         float* xg, const int* gfr, void* ws, long long ws_bytes, void* stream);
+
+/* bwd_data on gradient-frame planes [zlo, zhi), margins included (-md .. d+md). */
+int vpx_conv3d_bwd_data_range(const float* u, const int* ufr, const float* w, int k, int stride, float* xg,
+                              const int* gfr, int zlo, int zhi, void* ws, long long ws_bytes, void* stream);
 
 /* wg (=|+=) sum over voxels of u (x) x-patches; x frame margins must hold the
  * exchanged halos.  Replaces voxpar.kernels.conv3d_bwd_filter(xpad, u, stride,

@@ -123,6 +123,13 @@ class RankCtx:
         if self.size > 1:
             dist.barrier()
 
+    def comm_stream(self):
+        """Side stream for exchanges overlapped with compute (one per process)."""
+        st = getattr(self, "_comm_stream", None)
+        if st is None:
+            st = self._comm_stream = torch.cuda.Stream()
+        return st
+
     def buffer(self, key, numel, device):
         b = self._bufs.get(key)
         if b is None or b.numel() < numel:

@@ -5,6 +5,7 @@
 // bwd_data,bwd_filter} (reference pkg/src/voxpar/kernels/__init__.py:63-72,
 // cyext.py:20-45): same math, device-resident NDHWC halo frames instead of
 // host NCDHW arrays, explicit workspace instead of internal allocation.
+#include <climits>
 #include <cstdlib>
 
 #include "conv_common.h"
@@ -15,6 +16,8 @@
 
 namespace vpx {
 
+static int g_sm_limit = 0;  // vpx_set_sm_limit: 0 = every SM
+
 int num_sms() {
   static int n = 0;
   if (!n) {
@@ -23,7 +26,7 @@ int num_sms() {
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     if (n <= 0) n = 148;
   }
-  return n;
+  return g_sm_limit > 0 && g_sm_limit < n ? g_sm_limit : n;
 }
 
 // Pack OIDHW weights into the row-window B layout.
@@ -205,6 +208,14 @@ static int pack(const float* w, int cout, int cin, int mode, float* dst, cudaStr
 
 using vpx::Frame;
 
+// Grid budget of the persistent kernels launched after this call (0 = all
+// SMs).  Leaving a few SMs free lets communication kernels (NCCL) run next to
+// a convolution instead of after it.
+extern "C" int vpx_set_sm_limit(int n) {
+  vpx::g_sm_limit = n < 0 ? 0 : n;
+  return VPX_OK;
+}
+
 extern "C" long long vpx_conv3d_workspace_bytes(int cin, int cout, int k, const int* ufr) {
   Frame uf = vpx::to_frame(ufr);
   const long long k3 = (long long)k * k * k;
@@ -221,9 +232,12 @@ extern "C" long long vpx_conv3d_workspace_bytes(int cin, int cout, int k, const 
   return ((packed + 255) / 256) * 256 + ((parts + 255) / 256) * 256;
 }
 
-extern "C" int vpx_conv3d_fwd_act(const float* x, const int* xfr, const float* w, int k, int stride,
-                                  float* y, const int* yfr, int act, float slope, void* ws,
-                                  long long ws_bytes, void* stream) {
+// Output planes [zlo, zhi) only (zlo = INT_MIN: all).  Partial ranges are
+// implemented by the row kernels; other paths report VPX_ERR_UNSUPPORTED so
+// the caller runs the whole layer instead (halo overlap, layers.py).
+static int conv_fwd_impl(const float* x, const int* xfr, const float* w, int k, int stride, float* y,
+                         const int* yfr, int act, float slope, int zlo, int zhi, void* ws, long long ws_bytes,
+                         void* stream) {
   if (int rc = vpx::check_frame(xfr, "conv fwd input")) return rc;
   if (int rc = vpx::check_frame(yfr, "conv fwd output")) return rc;
   Frame xf = vpx::to_frame(xfr), yf = vpx::to_frame(yfr);
@@ -237,23 +251,43 @@ extern "C" int vpx_conv3d_fwd_act(const float* x, const int* xfr, const float* w
   const int cin = xf.c, cout = yf.c;
   int R, CG;
   const bool tc = vpx::precision() == 0;
+  const bool full = zlo == INT_MIN;
+  if (full) {
+    zlo = 0;
+    zhi = yf.d;
+  } else if (zlo < 0 || zhi > yf.d || zlo >= zhi) {
+    VPX_FAIL(VPX_ERR_OUT_OF_BOUNDS, "conv fwd: plane range [%d, %d) outside [0, %d)", zlo, zhi, yf.d);
+  }
   if (tc && k == 3 && stride == 1 && yf.w % 128 == 0 && vpx::rowh_supported(cin, cout) && !vpx::rowh_off()) {
     if (ws_bytes < vpx::rowh_packed_bytes(cin, cout)) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "workspace too small");
     float* wpack = static_cast<float*>(ws);
     if (int rc = vpx::rowh_pack(w, cout, cin, 0, wpack, st)) return rc;
-    return vpx::rowh_run(x, xf, wpack, cin, cout, y, yf, 0, yf.d, 0, yf.h, yf.w, st, act, slope);
+    return vpx::rowh_run(x, xf, wpack, cin, cout, y, yf, zlo, zhi, 0, yf.h, yf.w, st, act, slope);
   }
   if (tc && k == 3 && stride == 1 && yf.w % 128 == 0 && vpx::rowwin_config(cin, cout, &R, &CG)) {
     if (ws_bytes < vpx::packed_floats(cin, cout) * 4) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "workspace too small");
     float* wpack = static_cast<float*>(ws);
     if (int rc = vpx::pack(w, cout, cin, 0, wpack, st)) return rc;
-    return vpx::rowwin_run(x, xf, wpack, cin, cout, y, yf, 0, yf.d, 0, yf.h, yf.w, st, act, slope);
+    return vpx::rowwin_run(x, xf, wpack, cin, cout, y, yf, zlo, zhi, 0, yf.h, yf.w, st, act, slope);
   }
+  if (!full && (zlo != 0 || zhi != yf.d)) VPX_FAIL(VPX_ERR_UNSUPPORTED, "conv fwd: plane ranges need a row kernel");
   if (tc && k == 3 && cin % 4 == 0 && vpx::tapbox_supported(cin, cout, 0)) {
     if (ws_bytes < vpx::tapbox_workspace_bytes(cin, cout)) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "workspace too small");
     return vpx::conv_tapbox(0, x, xf, w, cin, cout, stride, y, yf, act, slope, ws, st);
   }
   return vpx::conv_fwd_simt(x, xf, w, k, stride, y, yf, st, act, slope);
+}
+
+extern "C" int vpx_conv3d_fwd_act(const float* x, const int* xfr, const float* w, int k, int stride,
+                                  float* y, const int* yfr, int act, float slope, void* ws,
+                                  long long ws_bytes, void* stream) {
+  return conv_fwd_impl(x, xfr, w, k, stride, y, yfr, act, slope, INT_MIN, 0, ws, ws_bytes, stream);
+}
+
+extern "C" int vpx_conv3d_fwd_act_range(const float* x, const int* xfr, const float* w, int k, int stride,
+                                        float* y, const int* yfr, int act, float slope, int zlo, int zhi,
+                                        void* ws, long long ws_bytes, void* stream) {
+  return conv_fwd_impl(x, xfr, w, k, stride, y, yfr, act, slope, zlo, zhi, ws, ws_bytes, stream);
 }
 
 extern "C" int vpx_conv3d_fwd(const float* x, const int* xfr, const float* w, int k, int stride,
@@ -262,9 +296,8 @@ extern "C" int vpx_conv3d_fwd(const float* x, const int* xfr, const float* w, in
   return vpx_conv3d_fwd_act(x, xfr, w, k, stride, y, yfr, 0, 0.f, ws, ws_bytes, stream);
 }
 
-extern "C" int vpx_conv3d_bwd_data(const float* u, const int* ufr, const float* w, int k,
-                                   int stride, float* xg, const int* gfr, void* ws,
-                                   long long ws_bytes, void* stream) {
+static int conv_bwd_data_impl(const float* u, const int* ufr, const float* w, int k, int stride, float* xg,
+                              const int* gfr, int zlo, int zhi, void* ws, long long ws_bytes, void* stream) {
   if (int rc = vpx::check_frame(ufr, "conv bwd_data upstream")) return rc;
   if (int rc = vpx::check_frame(gfr, "conv bwd_data output")) return rc;
   Frame uf = vpx::to_frame(ufr), gf = vpx::to_frame(gfr);
@@ -276,21 +309,29 @@ extern "C" int vpx_conv3d_bwd_data(const float* u, const int* ufr, const float* 
   const int cout = uf.c, cin = gf.c;
   int R, CG;
   const bool tc = vpx::precision() == 0;
+  // output planes of the gradient frame, margins included: [-md, d + md)
+  const bool full = zlo == INT_MIN;
+  if (full) {
+    zlo = -gf.md;
+    zhi = gf.d + gf.md;
+  } else if (zlo < -gf.md || zhi > gf.d + gf.md || zlo >= zhi) {
+    VPX_FAIL(VPX_ERR_OUT_OF_BOUNDS, "conv bwd_data: plane range [%d, %d) outside the frame", zlo, zhi);
+  }
   if (tc && k == 3 && stride == 1 && gf.mw == 0 && gf.w % 128 == 0 && vpx::rowh_supported(cout, cin) &&
       !vpx::rowh_off()) {
     if (ws_bytes < vpx::rowh_packed_bytes(cout, cin)) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "workspace too small");
     float* wpack = static_cast<float*>(ws);
     if (int rc = vpx::rowh_pack(w, cout, cin, 1, wpack, st)) return rc;
-    return vpx::rowh_run(u, uf, wpack, cout, cin, xg, gf, -gf.md, gf.d + gf.md, -gf.mh, gf.h + gf.mh, gf.w, st);
+    return vpx::rowh_run(u, uf, wpack, cout, cin, xg, gf, zlo, zhi, -gf.mh, gf.h + gf.mh, gf.w, st);
   }
   if (tc && k == 3 && stride == 1 && gf.mw == 0 && gf.w % 128 == 0 &&
       vpx::rowwin_config(cout, cin, &R, &CG)) {
     if (ws_bytes < vpx::packed_floats(cin, cout) * 4) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "workspace too small");
     float* wpack = static_cast<float*>(ws);
     if (int rc = vpx::pack(w, cout, cin, 1, wpack, st)) return rc;
-    return vpx::rowwin_run(u, uf, wpack, cout, cin, xg, gf, -gf.md, gf.d + gf.md, -gf.mh,
-                           gf.h + gf.mh, gf.w, st);
+    return vpx::rowwin_run(u, uf, wpack, cout, cin, xg, gf, zlo, zhi, -gf.mh, gf.h + gf.mh, gf.w, st);
   }
+  if (!full) VPX_FAIL(VPX_ERR_UNSUPPORTED, "conv bwd_data: plane ranges need a row kernel");
   if (tc && k == 3 && cout % 4 == 0 && vpx::tapbox_supported(cin, cout, 1)) {
     if (ws_bytes < vpx::tapbox_workspace_bytes(cin, cout)) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "workspace too small");
     return vpx::conv_tapbox(1, u, uf, w, cin, cout, stride, xg, gf, 0, 0.f, ws, st);
@@ -323,6 +364,17 @@ extern "C" int vpx_conv3d_bwd_filter(const float* x, const int* xfr, const float
                                 accumulate, st);
   }
   return vpx::conv_wgrad_simt(x, xf, u, uf, k, stride, wg, accumulate, part, st);
+}
+
+extern "C" int vpx_conv3d_bwd_data(const float* u, const int* ufr, const float* w, int k, int stride, float* xg,
+                                   const int* gfr, void* ws, long long ws_bytes, void* stream) {
+  return conv_bwd_data_impl(u, ufr, w, k, stride, xg, gfr, INT_MIN, 0, ws, ws_bytes, stream);
+}
+
+extern "C" int vpx_conv3d_bwd_data_range(const float* u, const int* ufr, const float* w, int k, int stride,
+                                         float* xg, const int* gfr, int zlo, int zhi, void* ws, long long ws_bytes,
+                                         void* stream) {
+  return conv_bwd_data_impl(u, ufr, w, k, stride, xg, gfr, zlo, zhi, ws, ws_bytes, stream);
 }
 
 extern "C" int vpx_pool_leaky_bwd_blocked(const float* y, const int* yfr, const float* up, const int* upfr,

@@ -16,12 +16,13 @@ buffers (views of the flat gradient-allreduce bucket) when `out` is given.
 from __future__ import annotations
 
 import ctypes
+import os
 
 import torch
 
 from . import _lib
 from .comm import RankCtx, halo_exchange, reverse_halo_exchange, copy_box
-from .errors import NonDivisible, ShapeMismatch
+from .errors import NonDivisible, ShapeMismatch, Unsupported
 from .frames import DistTensor, frame_desc, stream_ptr
 from .geometry import DistTensorMeta, Shape5D, make_partition
 from .timing import region
@@ -72,6 +73,32 @@ def _conv_flops(params, out_vox):
     return 2 * k ** 3 * params.cin * params.cout * out_vox
 
 
+def _overlap_d(ctx: RankCtx, meta: DistTensorMeta) -> bool:
+    """Depth-only spatial split on several GPUs: the halo exchange can run on
+    the communication stream while the planes that do not touch it compute."""
+    # Off by default: measured on 4 B200s (graph replay) it does not pay --
+    # the exchanges are latency-bound NCCL calls that the step has to wait for
+    # either way.  VPX_OVERLAP=1 enables it.
+    parts = meta.grid.spatial_parts
+    return (ctx.size > 1 and parts[0] > 1 and parts[1] == 1 and parts[2] == 1
+            and os.environ.get("VPX_OVERLAP") == "1" and torch.cuda.is_available())
+
+
+OVERLAP_FREE_SMS = int(os.environ.get("VPX_OVERLAP_FREE_SMS", "16"))
+
+
+class _sm_budget:
+    """Leave OVERLAP_FREE_SMS SMs to the communication kernels while a
+    convolution overlaps an exchange (vpx_set_sm_limit)."""
+
+    def __enter__(self):
+        n = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+        _lib.call("vpx_set_sm_limit", max(1, n - OVERLAP_FREE_SMS))
+
+    def __exit__(self, *exc):
+        _lib.call("vpx_set_sm_limit", 0)
+
+
 def dist_conv3d(ctx: RankCtx, x: DistTensor, w: torch.Tensor, params, out_radii=NO_HALO,
                 tag: str = "conv", leaky_slope: float = None) -> DistTensor:
     """Halo exchange, then the local tcgen05 implicit-GEMM conv on the frame
@@ -86,17 +113,43 @@ def dist_conv3d(ctx: RankCtx, x: DistTensor, w: torch.Tensor, params, out_radii=
     for name, e, p, s in zip("dhw", x.spatial, meta.grid.spatial_parts, params.stride):
         if p > 1 and e % s:
             raise NonDivisible(f"local extent {name}={e} not divisible by stride {s}")
-    halo_exchange(ctx, x)
     k, s = _cubic(params.kernel), _cubic(params.stride)
     gs = meta.global_shape
     y = _out(meta, Shape5D(gs.n, params.cout, *(-(-e // s) for e in gs.spatial)), out_radii, x.grid_rank)
     nb = _lib.load().vpx_conv3d_workspace_bytes(params.cin, params.cout, k, y.desc)
     ws = WS.get(nb)
-    with region(f"{tag}.fwd", _conv_flops(params, y.voxels()),
-                4 * (x.voxels() * x.c + y.voxels() * y.c + w.numel())):
-        _lib.call("vpx_conv3d_fwd_act", x.ptr, x.desc, w.data_ptr(), k, s, y.ptr, y.desc,
-                  int(leaky_slope is not None), float(leaky_slope or 0.0), ws.data_ptr(), ws.numel() * 4,
-                  stream_ptr())
+    act, slope = int(leaky_slope is not None), float(leaky_slope or 0.0)
+
+    def conv(zlo=None, zhi=None):
+        if zlo is None:
+            _lib.call("vpx_conv3d_fwd_act", x.ptr, x.desc, w.data_ptr(), k, s, y.ptr, y.desc, act, slope,
+                      ws.data_ptr(), ws.numel() * 4, stream_ptr())
+        else:
+            _lib.call("vpx_conv3d_fwd_act_range", x.ptr, x.desc, w.data_ptr(), k, s, y.ptr, y.desc, act, slope,
+                      zlo, zhi, ws.data_ptr(), ws.numel() * 4, stream_ptr())
+
+    flops, nbytes = _conv_flops(params, y.voxels()), 4 * (x.voxels() * x.c + y.voxels() * y.c + w.numel())
+    if _overlap_d(ctx, meta) and s == 1 and y.d >= 3:
+        # exchange on the communication stream; output planes 1 .. d-2 read no
+        # halo and run meanwhile, the two boundary planes after the join
+        main, comm = torch.cuda.current_stream(), ctx.comm_stream()
+        comm.wait_stream(main)
+        with torch.cuda.stream(comm):
+            halo_exchange(ctx, x)
+        with region(f"{tag}.fwd", flops, nbytes):
+            try:
+                with _sm_budget():
+                    conv(1, y.d - 1)
+                main.wait_stream(comm)
+                conv(0, 1)
+                conv(y.d - 1, y.d)
+            except Unsupported:
+                main.wait_stream(comm)
+                conv()
+        return y
+    halo_exchange(ctx, x)
+    with region(f"{tag}.fwd", flops, nbytes):
+        conv()
     return y
 
 
@@ -109,10 +162,38 @@ def dist_conv3d_bwd_data(ctx: RankCtx, u: DistTensor, w: torch.Tensor, params,
     g = DistTensor(in_meta, u.grid_rank, zero=False)
     nb = _lib.load().vpx_conv3d_workspace_bytes(params.cin, params.cout, k, u.desc)
     ws = WS.get(nb)
-    with region(f"{tag}.dgrad", _conv_flops(params, u.voxels()),
-                4 * (u.voxels() * u.c + g.t.numel() + w.numel())):
-        _lib.call("vpx_conv3d_bwd_data", u.ptr, u.desc, w.data_ptr(), k, s, g.ptr, g.desc, ws.data_ptr(),
-                  ws.numel() * 4, stream_ptr())
+
+    def dgrad(zlo=None, zhi=None):
+        if zlo is None:
+            _lib.call("vpx_conv3d_bwd_data", u.ptr, u.desc, w.data_ptr(), k, s, g.ptr, g.desc, ws.data_ptr(),
+                      ws.numel() * 4, stream_ptr())
+        else:
+            _lib.call("vpx_conv3d_bwd_data_range", u.ptr, u.desc, w.data_ptr(), k, s, g.ptr, g.desc, zlo, zhi,
+                      ws.data_ptr(), ws.numel() * 4, stream_ptr())
+
+    flops, nbytes = _conv_flops(params, u.voxels()), 4 * (u.voxels() * u.c + g.t.numel() + w.numel())
+    md = g.m[0]
+    if _overlap_d(ctx, in_meta) and s == 1 and md == 1 and g.d >= 3:
+        # boundary planes (and the margin planes that go to the neighbours)
+        # first; the adjoint exchange then overlaps the interior planes
+        main, comm = torch.cuda.current_stream(), ctx.comm_stream()
+        with region(f"{tag}.dgrad", flops, nbytes):
+            try:
+                dgrad(-1, 1)
+                dgrad(g.d - 1, g.d + 1)
+            except Unsupported:
+                dgrad()
+                reverse_halo_exchange(ctx, in_meta, u.grid_rank, g)
+                return g
+            comm.wait_stream(main)
+            with torch.cuda.stream(comm):
+                reverse_halo_exchange(ctx, in_meta, u.grid_rank, g)
+            with _sm_budget():
+                dgrad(1, g.d - 1)
+            main.wait_stream(comm)
+        return g
+    with region(f"{tag}.dgrad", flops, nbytes):
+        dgrad()
     reverse_halo_exchange(ctx, in_meta, u.grid_rank, g)
     return g
 
