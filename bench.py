@@ -408,7 +408,7 @@ def run_ours(args):
                    "global_batch": n_global, "width": W, "grid": f"{grid.groups}x{grid.pd}x{grid.ph}x{grid.pw}",
                    "parallelism": f"dp{grid.groups}xspatial{grid.spatial_size}",
                    "l2": "inputs larger than L2 (no flush needed)",
-                   "storage": "fp32 NDHWC, TF32 tensor-core math"},
+                   "storage": "fp32 NDHWC, TF32 tensor-core math", "halo": ctx.halo_path},
         "roofline": roof,
         "cpu_baseline": cpu,
         "e2e": e2e,

@@ -189,6 +189,16 @@ int vpx_deconv_bwd_filter(const float* x, const int* xf, const float* u, const i
  * the block moves of redistribute (reference layers/distributed.py:298-368). */
 int vpx_halo_copy(float* frame, const int* ff, const int* box8, float* buf, int mode, void* stream);
 
+/* Peer-memory halo mailboxes (CUDA IPC over NVLink, comm.py PeerHalo): after
+ * packing a face into the neighbour's mailbox with vpx_halo_copy(peer ptr),
+ * vpx_peer_signal bumps the neighbour's arrival counter (system-scope
+ * atomic); vpx_peer_wait blocks the stream until the local counter exceeds
+ * *expected, then increments *expected (device-side, graph-replayable).  A
+ * neighbour that never arrives within timeout_ns sets *error and traps. */
+int vpx_peer_signal(unsigned long long* peer_flag, void* stream);
+int vpx_peer_wait(const unsigned long long* flag, unsigned long long* expected, long long timeout_ns, int* error,
+                  void* stream);
+
 /* ------------------------------------------------------------------- prng --
  * Pinned splitmix64 streams (reference prng.py:28-90), bit-exact with numpy:
  * value i = lo + (hi-lo) * ((mix(key + (i+1)*golden) >> 11) * 2^-53). */

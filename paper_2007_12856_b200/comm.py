@@ -36,6 +36,11 @@ from .geometry import round_boxes
 from .timing import region
 
 
+# Profiling switch only (results are wrong with it): VPX_SKIP_HALO=1 skips the
+# halo exchanges to measure what they cost inside a step.
+_SKIP_HALO = os.environ.get("VPX_SKIP_HALO") == "1"
+
+
 class RankCtx:
     """Per-process handle (reference fabric.py:111-128 API)."""
 
@@ -45,6 +50,7 @@ class RankCtx:
         self.device = device
         self._groups = {}
         self._bufs = {}
+        self.peer = None
 
     # -------------------------------------------------------------- setup
     @classmethod
@@ -123,6 +129,33 @@ class RankCtx:
         if self.size > 1:
             dist.barrier()
 
+    def ensure_peer_halo(self, plan):
+        """Set up CUDA-IPC halo mailboxes (PeerHalo) once per plan; collective.
+        Falls back to NCCL P2P when IPC is unavailable or VPX_NCCL_HALO=1."""
+        if self.size == 1 or getattr(self, "_peer_plan", None) is plan:
+            return
+        self._peer_plan = plan
+        self.peer = None
+        if os.environ.get("VPX_NCCL_HALO") == "1" or not torch.cuda.is_available():
+            return
+        ok = 1
+        try:
+            peer = PeerHalo(self, plan)
+        except Exception as exc:  # pragma: no cover - reported through halo_path
+            peer, ok = None, 0
+            self.halo_error = f"{type(exc).__name__}: {exc}"
+        flag = torch.tensor([ok], dtype=torch.int32, device="cuda")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        self.peer = peer if int(flag.item()) == 1 else None
+
+    @property
+    def halo_path(self) -> str:
+        if self.size == 1:
+            return "none (single rank)"
+        if self.peer is not None:
+            return "CUDA-IPC mailboxes over NVLink (PeerHalo)"
+        return "NCCL send/recv" + (f" (IPC setup failed: {self.halo_error})" if getattr(self, "halo_error", None) else "")
+
     def comm_stream(self):
         """Side stream for exchanges overlapped with compute (one per process)."""
         st = getattr(self, "_comm_stream", None)
@@ -136,6 +169,108 @@ class RankCtx:
             b = torch.empty(numel, dtype=torch.float32, device=device)
             self._bufs[key] = b
         return b[:numel]
+
+
+class PeerHalo:
+    """Halo faces through CUDA-IPC mailboxes over NVLink instead of NCCL P2P.
+
+    Every rank allocates, once, two mailboxes per (dim, side) it receives
+    from plus an arrival counter, and opens its neighbours' allocations via
+    CUDA IPC.  A face is packed by vpx_halo_copy straight into the
+    neighbour's mailbox (peer stores), vpx_peer_signal bumps the neighbour's
+    counter; the receiver's vpx_peer_wait holds its stream until the face has
+    arrived and unpacks locally.  No NCCL kernel, no rendezvous: each round is
+    a pack kernel, a one-thread signal and a one-thread wait.  Mailboxes
+    alternate per exchange; a rank writes mailbox p again only after it has
+    received the neighbour's next face, which the neighbour sends after
+    unpacking p (exchanges with a neighbour are always two-way), and steps are
+    separated by the gradient all-reduce.  Counters live in device memory, so
+    the exchange replays inside a CUDA graph.
+    """
+
+    TIMEOUT_NS = 10_000_000_000
+
+    def __init__(self, ctx: "RankCtx", plan):
+        from cuda.bindings import runtime as rt
+
+        self.rt = rt
+        metas = [m for m in plan.in_meta if m is not None and any(p > 1 for p in m.grid.spatial_parts)]
+        if not metas:
+            raise OutOfBounds("no spatially partitioned tensors")
+        meta = metas[0]
+        gr = meta.grid_rank_of(ctx.rank)
+        # largest face any round can carry: whole frame cross-section, all channels
+        slab = 0
+        for m in metas:
+            try:
+                g = m.grid_rank_of(ctx.rank)
+            except OutOfBounds:
+                continue
+            ls, mg = m.local_shape(g), m.margins()
+            ext = (ls.d + 2 * mg[0], ls.h + 2 * mg[1], ls.w + 2 * mg[2])
+            for dim in range(3):
+                slab = max(slab, ls.n * ls.c * ext[(dim + 1) % 3] * ext[(dim + 2) % 3] * max(1, m.radii[dim]) * 4)
+        self.slab = (slab + 4095) // 4096 * 4096
+        self.flags_off = 12 * self.slab
+        total = self.flags_off + 4096
+        err, ptr = rt.cudaMalloc(total)
+        if err != rt.cudaError_t.cudaSuccess:
+            raise OutOfBounds(f"peer mailbox allocation failed: {err}")
+        rt.cudaMemset(ptr, 0, total)
+        rt.cudaDeviceSynchronize()
+        self.base = int(ptr)
+        err, handle = rt.cudaIpcGetMemHandle(ptr)
+        if err != rt.cudaError_t.cudaSuccess:
+            raise OutOfBounds(f"cudaIpcGetMemHandle failed: {err}")
+        handles = [None] * ctx.size
+        dist.all_gather_object(handles, bytes(handle.reserved))
+        self.peer_base, opened = {}, {}
+        for dim in range(3):
+            for side in (-1, 1):
+                nbr = meta.neighbor(gr, dim, side)
+                if nbr is None:
+                    continue
+                peer = meta.fabric_rank(nbr)
+                if peer not in opened:  # one mapping per peer process
+                    h = rt.cudaIpcMemHandle_t()
+                    h.reserved = handles[peer]
+                    err, pptr = rt.cudaIpcOpenMemHandle(h, rt.cudaIpcMemLazyEnablePeerAccess)
+                    if err != rt.cudaError_t.cudaSuccess:
+                        raise OutOfBounds(f"cudaIpcOpenMemHandle({peer}) failed: {err}")
+                    opened[peer] = int(pptr)
+                self.peer_base[(dim, side)] = opened[peer]
+        self.count = {}
+        ctx.barrier()
+
+    @staticmethod
+    def _chan(dim, side):
+        return 2 * dim + (side + 1) // 2
+
+    def _parity(self, key):
+        c = self.count.get(key, 0)
+        self.count[key] = c + 1
+        return c & 1
+
+    def send(self, dim, side, frame, box, mode):
+        """Face `box` of `frame` -> the neighbour on `side` (its channel (dim, -side))."""
+        ch = self._chan(dim, -side)
+        par = self._parity(("s", dim, side))
+        dst = self.peer_base[(dim, side)] + (2 * ch + par) * self.slab
+        if _box_numel(frame, box) * 4 > self.slab:
+            raise OutOfBounds("halo face larger than the mailbox")
+        st = torch.cuda.current_stream().cuda_stream
+        _lib.call("vpx_halo_copy", frame.ptr, frame.desc, _box_arg(_box8(frame, box)), dst, mode, st)
+        _lib.call("vpx_peer_signal", self.peer_base[(dim, side)] + self.flags_off + 8 * ch, st)
+
+    def recv(self, dim, side, frame, box, mode):
+        """Face from the neighbour on `side` (my channel (dim, side)) -> `box` of `frame`."""
+        ch = self._chan(dim, side)
+        par = self._parity(("r", dim, side))
+        st = torch.cuda.current_stream().cuda_stream
+        _lib.call("vpx_peer_wait", self.base + self.flags_off + 8 * ch, self.base + self.flags_off + 64 + 8 * ch,
+                  self.TIMEOUT_NS, self.base + self.flags_off + 128, st)
+        src = self.base + (2 * ch + par) * self.slab
+        _lib.call("vpx_halo_copy", frame.ptr, frame.desc, _box_arg(_box8(frame, box)), src, mode, st)
 
 
 def _box_numel(frame, box):
@@ -182,11 +317,22 @@ def halo_exchange(ctx: RankCtx, tensor, pack=_cuda_pack, unpack=_cuda_unpack):
     """Fill the frame margins of `tensor` (a DistTensor) with neighbour
     boundary data, one round per partitioned dim in ascending order.  Outer
     walls keep their zeros.  Collective over the tensor's rank map."""
+    if _SKIP_HALO:
+        return tensor
     meta, gr = tensor.meta, tensor.grid_rank
     if meta.fabric_rank(gr) != ctx.rank:
         raise OutOfBounds(f"rank {ctx.rank} exchanging a tensor owned by {meta.fabric_rank(gr)}")
+    peer = ctx.peer if (pack is _cuda_pack and getattr(ctx, "peer", None) is not None) else None
     for dim in range(3):
         if meta.radii[dim] == 0 or meta.grid.spatial_parts[dim] == 1:
+            continue
+        if peer is not None:
+            sides = [s for s in (-1, 1) if meta.neighbor(gr, dim, s) is not None]
+            with region("comm.p2p", 0, 0):
+                for side in sides:
+                    peer.send(dim, side, tensor, round_boxes(meta, gr, dim, side)[0], 0)
+                for side in sides:
+                    peer.recv(dim, side, tensor, round_boxes(meta, gr, dim, side)[1], 1)
             continue
         ops, unpacks = [], []
         for side in (-1, 1):
@@ -198,9 +344,9 @@ def halo_exchange(ctx: RankCtx, tensor, pack=_cuda_pack, unpack=_cuda_unpack):
             sbuf = ctx.buffer(("hs", dim, side), n, tensor.t.device)
             rbuf = ctx.buffer(("hr", dim, side), n, tensor.t.device)
             pack(tensor, bbox, sbuf)
-            peer = meta.fabric_rank(nbr)
-            ops.append(("send", peer, sbuf))
-            ops.append(("recv", peer, rbuf))
+            other = meta.fabric_rank(nbr)
+            ops.append(("send", other, sbuf))
+            ops.append(("recv", other, rbuf))
             unpacks.append((mbox, rbuf))
         ctx.exchange(ops)
         for mbox, rbuf in unpacks:
@@ -213,10 +359,21 @@ def reverse_halo_exchange(ctx: RankCtx, meta, grid_rank: int, frame, pack=_cuda_
     """Adjoint of halo_exchange on a gradient frame: descending dims, send
     the margin slab, accumulate what arrives into the boundary; wall margins
     are dropped (reference fabric.py:414-443)."""
+    if _SKIP_HALO:
+        return frame
     if meta.fabric_rank(grid_rank) != ctx.rank:
         raise OutOfBounds(f"rank {ctx.rank} exchanging a frame owned by {meta.fabric_rank(grid_rank)}")
+    peer = ctx.peer if (pack is _cuda_pack and getattr(ctx, "peer", None) is not None) else None
     for dim in (2, 1, 0):
         if meta.radii[dim] == 0 or meta.grid.spatial_parts[dim] == 1:
+            continue
+        if peer is not None:
+            sides = [s for s in (-1, 1) if meta.neighbor(grid_rank, dim, s) is not None]
+            with region("comm.p2p", 0, 0):
+                for side in sides:
+                    peer.send(dim, side, frame, round_boxes(meta, grid_rank, dim, side)[1], 0)
+                for side in sides:
+                    peer.recv(dim, side, frame, round_boxes(meta, grid_rank, dim, side)[0], 2)
             continue
         ops, unpacks = [], []
         for side in (-1, 1):
@@ -228,9 +385,9 @@ def reverse_halo_exchange(ctx: RankCtx, meta, grid_rank: int, frame, pack=_cuda_
             sbuf = ctx.buffer(("rs", dim, side), n, frame.t.device)
             rbuf = ctx.buffer(("rr", dim, side), n, frame.t.device)
             pack(frame, mbox, sbuf)
-            peer = meta.fabric_rank(nbr)
-            ops.append(("send", peer, sbuf))
-            ops.append(("recv", peer, rbuf))
+            other = meta.fabric_rank(nbr)
+            ops.append(("send", other, sbuf))
+            ops.append(("recv", other, rbuf))
             unpacks.append((bbox, rbuf))
         ctx.exchange(ops)
         for bbox, rbuf in unpacks:

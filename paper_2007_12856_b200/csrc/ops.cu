@@ -448,6 +448,34 @@ __global__ void prng_mask_dev_kernel(const uint64_t* __restrict__ keyp, long lon
     out[i] = u01 < keep ? 1 : 0;
   }
 }
+// ---- peer-memory halo mailboxes (comm.py PeerHalo) -------------------------
+// The sender packs its face straight into the neighbour's mailbox over NVLink
+// (vpx_halo_copy with a peer pointer), then bumps the neighbour's arrival
+// counter; the receiver waits for its counter and unpacks from local memory.
+__global__ void peer_signal_kernel(unsigned long long* peer_flag) {
+  __threadfence_system();
+  atomicAdd_system(peer_flag, 1ULL);
+}
+__global__ void peer_wait_kernel(const unsigned long long* flag, unsigned long long* expected,
+                                 long long timeout_ns, int* error) {
+  const unsigned long long want = *expected + 1ULL;
+  long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
+    if (v >= want) break;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > timeout_ns) {  // the neighbour never arrived: fail loudly instead of hanging
+      *error = 1;
+      __threadfence_system();
+      asm volatile("trap;");
+    }
+    __nanosleep(64);
+  }
+  *expected = want;
+  __threadfence_system();
+}
 __global__ void sgd_kernel(float* __restrict__ p, const float* __restrict__ g, long long n, float lr) {
   GRID_STRIDE(i, n) p[i] = p[i] - lr * g[i];
 }
@@ -692,6 +720,15 @@ extern "C" int vpx_adam_dev(float* p, const float* g, float* m, float* v, long l
 extern "C" int vpx_prng_mask_dev(const unsigned long long* key, long long n, double keep, unsigned char* out,
                                  void* st) {
   prng_mask_dev_kernel<<<grid1d(n), 256, 0, S(st)>>>(reinterpret_cast<const uint64_t*>(key), n, keep, out);
+  LAUNCH_TAIL;
+}
+extern "C" int vpx_peer_signal(unsigned long long* peer_flag, void* st) {
+  peer_signal_kernel<<<1, 1, 0, S(st)>>>(peer_flag);
+  LAUNCH_TAIL;
+}
+extern "C" int vpx_peer_wait(const unsigned long long* flag, unsigned long long* expected, long long timeout_ns,
+                             int* error, void* st) {
+  peer_wait_kernel<<<1, 1, 0, S(st)>>>(flag, expected, timeout_ns, error);
   LAUNCH_TAIL;
 }
 extern "C" int vpx_sgd(float* p, const float* g, long long n, float lr, void* st) {

@@ -563,7 +563,9 @@ def gradient_allreduce(ctx: RankCtx, state: RankState):
 def train_step(ctx: RankCtx, plan: Plan, state: RankState, batch: Batch, lr: float, seed: int = 0,
                scalars: "StepScalars" = None):
     """One hybrid-parallel training step; returns the loss as a 1-element
-    fp64 CUDA tensor (identical on every rank).  No host synchronisation."""
+    fp64 CUDA tensor (identical on every rank).  No host synchronisation
+    (except once per plan, when the halo mailboxes are set up)."""
+    ctx.ensure_peer_halo(plan)
     state.params.grad.zero_()
     pred, stash = forward(ctx, plan, state, batch, "train", seed, scalars=scalars)
     loss, dpred = loss_and_grad(ctx, plan, pred, batch)

@@ -39,6 +39,7 @@ def main():
     state = engine.make_state(net, 0)
     batch = engine.scatter_batch(plan, x, y, ids, ctx.rank)
     lr = 1e-3
+    ctx.ensure_peer_halo(plan)  # CUDA-IPC mailboxes unless VPX_NCCL_HALO=1
     state.params.grad.zero_()
     pred, stash = engine.forward(ctx, plan, state, batch, "train", 0)
     loss, dpred = engine.loss_and_grad(ctx, plan, pred, batch)
@@ -77,6 +78,7 @@ def main():
                 ok = False
         le = abs(float(loss.item()) - loss_o) / abs(loss_o)
         ok = ok and le < (1e-5 if prec == "fp32" else 1e-3) and replicated
+        print(f"[check_dist] halo path: {ctx.halo_path}")
         print(f"[check_dist] grid {sys.argv[1]} W={W} n={n} {prec}{' bn' if bn else ''}: loss {float(loss.item())!r} "
               f"oracle {loss_o!r} (rel {le:.2e}); worst grad err {worst:.2e}; replicated={replicated}; "
               f"{'PASS' if ok else 'FAIL'}", flush=True)

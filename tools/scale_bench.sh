@@ -6,6 +6,6 @@ for N in "$@"; do
   python - <<PY
 import json
 l=json.loads(open('gpurun_out/bench_${N}gpu.json').read().strip().splitlines()[-1])
-print("N=$N", round(l['value'],2), round(l['ms_per_step'],3), "e2e", round((l.get('e2e') or {}).get('value') or 0,2), l['step_mode'][:40])
+print("N=$N", round(l['value'],2), round(l['ms_per_step'],3), "e2e", round((l.get('e2e') or {}).get('value') or 0,2), l['step_mode'][:40], l['config'].get('halo'))
 PY
 done
