@@ -33,7 +33,7 @@ struct Frame;
 long long tapbox_workspace_bytes(int cin, int cout);
 int tapbox_supported(int cin, int cout, int mode);
 int conv_tapbox(int mode, const float* in, const Frame& inf, const float* w, int cin, int cout, int stride,
-                float* out, const Frame& of, int act, float slope, void* ws, cudaStream_t st);
+                float* out, const Frame& of, int act, float slope, void* ws, cudaStream_t st, long long ws_bytes);
 int rowh_supported(int cin, int cout);
 long long rowh_packed_bytes(int cin, int cout);
 int rowh_pack(const float* w, int cout, int cin, int mode, float* dst, cudaStream_t st);

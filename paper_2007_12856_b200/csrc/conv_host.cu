@@ -273,7 +273,7 @@ static int conv_fwd_impl(const float* x, const int* xfr, const float* w, int k, 
   if (!full && (zlo != 0 || zhi != yf.d)) VPX_FAIL(VPX_ERR_UNSUPPORTED, "conv fwd: plane ranges need a row kernel");
   if (tc && k == 3 && cin % 4 == 0 && vpx::tapbox_supported(cin, cout, 0)) {
     if (ws_bytes < vpx::tapbox_workspace_bytes(cin, cout)) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "workspace too small");
-    return vpx::conv_tapbox(0, x, xf, w, cin, cout, stride, y, yf, act, slope, ws, st);
+    return vpx::conv_tapbox(0, x, xf, w, cin, cout, stride, y, yf, act, slope, ws, st, ws_bytes);
   }
   return vpx::conv_fwd_simt(x, xf, w, k, stride, y, yf, st, act, slope);
 }
@@ -334,7 +334,7 @@ static int conv_bwd_data_impl(const float* u, const int* ufr, const float* w, in
   if (!full) VPX_FAIL(VPX_ERR_UNSUPPORTED, "conv bwd_data: plane ranges need a row kernel");
   if (tc && k == 3 && cout % 4 == 0 && vpx::tapbox_supported(cin, cout, 1)) {
     if (ws_bytes < vpx::tapbox_workspace_bytes(cin, cout)) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "workspace too small");
-    return vpx::conv_tapbox(1, u, uf, w, cin, cout, stride, xg, gf, 0, 0.f, ws, st);
+    return vpx::conv_tapbox(1, u, uf, w, cin, cout, stride, xg, gf, 0, 0.f, ws, st, ws_bytes);
   }
   return vpx::conv_bwd_data_simt(u, uf, w, k, stride, xg, gf, st);
 }

@@ -12,6 +12,8 @@
 // stride-1 gather over u with its own list of taps (ConvTapParams.cls_*).
 // B = packed weights [entry][N_total][32] by 2D TMA, N tile <= 256.
 // Reference semantics: reference pkg/src/voxpar/kernels/_hot.pyx:19-67.
+#include <cstdlib>
+
 #include "conv_common.h"
 #include "conv_simt.h"
 #include "vpx_host.h"
@@ -45,6 +47,9 @@ struct ConvTapParams {
   int act;
   float slope;
   int rnd;
+  int ksplit;                   // split of each tile's K entries across CTAs (1 = none)
+  int base_tiles;               // tiles without the split
+  float* part;                  // ksplit > 1: raw partial tiles [ks][base_tiles][128][NT]
 };
 
 }  // namespace vpx
@@ -87,8 +92,9 @@ __global__ void __launch_bounds__(256, 1)
   vpx::tc_fence_after();
   const uint32_t tbase = tmem_base;
 
-  // tile -> (n-tile, class, n, zt, yt, xt)
+  // tile -> (k split, n-tile, class, n, zt, yt, xt)
   auto decode = [&](int tile, int& nt, int& cls, int& n, int& zt, int& yt, int& xt) {
+    tile %= p.base_tiles;
     nt = tile % p.ntn;
     tile /= p.ntn;
     cls = tile % p.ncls;
@@ -100,6 +106,12 @@ __global__ void __launch_bounds__(256, 1)
     zt = tile % p.td;
     n = tile / p.td;
   };
+  // K entries of this tile's class, restricted to its split
+  auto krange = [&](int tile, int cls, int& e0, int& e1) {
+    const int c0 = p.cls_start[cls], len = p.cls_start[cls + 1] - c0, ks = tile / p.base_tiles;
+    e0 = c0 + len * ks / p.ksplit;
+    e1 = c0 + len * (ks + 1) / p.ksplit;
+  };
 
   if (warp == 0) {
     if (vpx::elect_one()) {
@@ -110,7 +122,8 @@ __global__ void __launch_bounds__(256, 1)
         int nt, cls, n, zt, yt, xt;
         decode(tile, nt, cls, n, zt, yt, xt);
         const int qz = p.qd + zt * p.Db, qy = p.qh + yt * p.Hb, qx = p.qw + xt * p.Wb;
-        const int e0 = p.cls_start[cls], e1 = p.cls_start[cls + 1];
+        int e0, e1;
+        krange(tile, cls, e0, e1);
         for (int e = e0; e < e1; ++e) {
           const int ent = p.entries[e];
           const int od = (ent & 3) - 1, oh = ((ent >> 2) & 3) - 1, ow = ((ent >> 4) & 3) - 1;
@@ -135,7 +148,8 @@ __global__ void __launch_bounds__(256, 1)
     for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
       int nt, cls, n, zt, yt, xt;
       decode(tile, nt, cls, n, zt, yt, xt);
-      const int e0 = p.cls_start[cls], e1 = p.cls_start[cls + 1];
+      int e0, e1;
+      krange(tile, cls, e0, e1);
       vpx::mbar_wait(&tempty[acc], aphase ^ 1);
       vpx::tc_fence_after();
       const uint32_t d = tbase + acc * TCOLS;
@@ -171,7 +185,9 @@ __global__ void __launch_bounds__(256, 1)
     for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
       int nt, cls, n, zt, yt, xt;
       decode(tile, nt, cls, n, zt, yt, xt);
-      const bool empty_cls = p.cls_start[cls + 1] == p.cls_start[cls];
+      int e0, e1;
+      krange(tile, cls, e0, e1);
+      const bool empty_cls = e1 == e0;
       vpx::mbar_wait(&tfull[acc], aphase);
       vpx::tc_fence_after();
       const int dx = r % p.Wb, dy = (r / p.Wb) % p.Hb, dz = r / (p.Wb * p.Hb);
@@ -184,11 +200,19 @@ __global__ void __launch_bounds__(256, 1)
       float* o = p.out + static_cast<long long>(n) * p.out_sn + static_cast<long long>(pz + p.out_off_d) * p.out_sd +
                  static_cast<long long>(py + p.out_off_h) * p.out_sh + static_cast<long long>(px + p.out_off_w) * p.out_sw +
                  nt * NT;
+      // split K: raw partial accumulators, summed in order by tapbox_reduce_kernel
+      float* prow = p.part + (static_cast<long long>(tile) * 128 + r) * NT;
 #pragma unroll 1
       for (int cb = 0; cb < NT; cb += 16) {
         float v[16];
         vpx::tmem_ld16(tbase + (static_cast<uint32_t>(q * 32) << 16) + acc * TCOLS + cb, v);
-        if (valid) {
+        if (p.ksplit > 1) {
+          float4* o4 = reinterpret_cast<float4*>(prow + cb);
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            o4[i] = empty_cls ? make_float4(0.f, 0.f, 0.f, 0.f)
+                              : make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        } else if (valid) {
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             if (empty_cls) v[i] = 0.f;
@@ -211,6 +235,56 @@ __global__ void __launch_bounds__(256, 1)
   if (warp == 2) vpx::tmem_dealloc<2 * TCOLS>(tbase);
 }
 
+// Fixed-order sum of the split-K partial tiles, then the epilogue (LeakyReLU,
+// TF32 rounding, frame store) the single-pass kernel would have applied.
+template <int NT>
+__global__ void tapbox_reduce_kernel(const __grid_constant__ ConvTapParams p) {
+  const long long total = (long long)p.base_tiles * 128 * (NT / 4);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int c4 = static_cast<int>(i % (NT / 4));
+    const int r = static_cast<int>((i / (NT / 4)) % 128);
+    int tile = static_cast<int>(i / (NT / 4) / 128);
+    const int tb = tile;
+    const int nt = tile % p.ntn;
+    tile /= p.ntn;
+    const int cls = tile % p.ncls;
+    tile /= p.ncls;
+    const int xt = tile % p.tw;
+    tile /= p.tw;
+    const int yt = tile % p.th;
+    tile /= p.th;
+    const int zt = tile % p.td;
+    const int n = tile / p.td;
+    const int dx = r % p.Wb, dy = (r / p.Wb) % p.Hb, dz = r / (p.Wb * p.Hb);
+    const int qz = p.qd + zt * p.Db + dz, qy = p.qh + yt * p.Hb + dy, qx = p.qw + xt * p.Wb + dx;
+    const int Pd = (cls >> 2) & 1, Ph = (cls >> 1) & 1, Pw = cls & 1;
+    const int pz = p.out_stride * qz + Pd, py = p.out_stride * qy + Ph, px = p.out_stride * qx + Pw;
+    const bool valid = dz < p.Db && qz < p.qd + p.QD && qy < p.qh + p.QH && qx < p.qw + p.QW && pz >= p.pd_lo &&
+                       pz < p.pd_hi && py >= p.ph_lo && py < p.ph_hi && px >= p.pw_lo && px < p.pw_hi;
+    if (!valid) continue;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int ks = 0; ks < p.ksplit; ++ks) {
+      const float4 v = reinterpret_cast<const float4*>(
+          p.part + ((static_cast<long long>(ks) * p.base_tiles + tb) * 128 + r) * NT)[c4];
+      acc.x += v.x;
+      acc.y += v.y;
+      acc.z += v.z;
+      acc.w += v.w;
+    }
+    float o[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (p.act) o[j] = o[j] >= 0.f ? o[j] : p.slope * o[j];
+      if (p.rnd) o[j] = vpx::tf32_rn(o[j]);
+    }
+    float* dst = p.out + static_cast<long long>(n) * p.out_sn + static_cast<long long>(pz + p.out_off_d) * p.out_sd +
+                 static_cast<long long>(py + p.out_off_h) * p.out_sh + static_cast<long long>(px + p.out_off_w) * p.out_sw +
+                 nt * NT + 4 * c4;
+    *reinterpret_cast<float4*>(dst) = make_float4(o[0], o[1], o[2], o[3]);
+  }
+}
+
 template <int NT>
 int launch_tapbox(const CUtensorMap& xm, const CUtensorMap& wm, const ConvTapParams& p, cudaStream_t st) {
   constexpr int STAGE = 128 * 128 + NT * 128;
@@ -221,6 +295,12 @@ int launch_tapbox(const CUtensorMap& xm, const CUtensorMap& wm, const ConvTapPar
   const int grid = p.num_tiles < vpx::num_sms() ? p.num_tiles : vpx::num_sms();
   kern<<<grid, 256, smem, st>>>(xm, wm, p);
   VPX_LAUNCH_CHECK();
+  if (p.ksplit > 1) {
+    const long long total = (long long)p.base_tiles * 128 * (NT / 4);
+    const int rg = static_cast<int>((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);
+    tapbox_reduce_kernel<NT><<<rg, 256, 0, st>>>(p);
+    VPX_LAUNCH_CHECK();
+  }
   return VPX_OK;
 }
 
@@ -292,7 +372,7 @@ int tapbox_supported(int cin, int cout, int mode) {
 // mode 0: forward (stride 1 or 2); mode 1: backward-data (stride 1 or 2).
 // in: input frame (x for fwd, u for dgrad); out: output frame.
 int conv_tapbox(int mode, const float* in, const Frame& inf, const float* w, int cin, int cout, int stride,
-                float* out, const Frame& of, int act, float slope, void* ws, cudaStream_t st) {
+                float* out, const Frame& of, int act, float slope, void* ws, cudaStream_t st, long long ws_bytes) {
   const int ntot = mode == 0 ? cout : cin;
   const int kchan = mode == 0 ? cin : cout;  // channels along K
   const int nchunks = (kchan + 31) / 32;
@@ -380,7 +460,26 @@ int conv_tapbox(int mode, const float* in, const Frame& inf, const float* w, int
   p.ncls = ncls;
   const int NT = ntot <= 256 ? ntot : 256;
   p.ntn = ntot / NT;
-  p.num_tiles = of.n * p.td * p.th * p.tw * ncls * p.ntn;
+  p.base_tiles = of.n * p.td * p.th * p.tw * ncls * p.ntn;
+  // few tiles (deep layers): split each tile's K entries over otherwise idle
+  // SMs; partial tiles go after the packed weights in the workspace
+  p.ksplit = 1;
+  p.part = nullptr;
+  {
+    const long long wbytes = (tapbox_workspace_bytes(cin, cout) + 255) / 256 * 256;
+    int ks = 2 * p.base_tiles <= num_sms() ? num_sms() / p.base_tiles : 1;
+    const int min_entries = ne / ncls;
+    if (ks > min_entries / 2) ks = min_entries / 2 > 1 ? min_entries / 2 : 1;
+    if (ks > 64) ks = 64;
+    const int NTc = ntot <= 256 ? ntot : 256;
+    while (ks > 1 && wbytes + (long long)ks * p.base_tiles * 128 * NTc * 4 > ws_bytes) --ks;
+    if (getenv("VPX_NO_KSPLIT")) ks = 1;
+    if (ks > 1) {
+      p.ksplit = ks;
+      p.part = reinterpret_cast<float*>(static_cast<char*>(ws) + wbytes);
+    }
+  }
+  p.num_tiles = p.base_tiles * p.ksplit;
   p.in_stride = s_in;
   p.in_off_d = inf.md;
   p.in_off_h = inf.mh;
