@@ -10,7 +10,7 @@ TAG=${1:-r1}
 shift || true
 OUT=gpurun_out
 mkdir -p $OUT
-BENCH="python bench.py --steps 3 --warmup 3 --no-cpu --no-e2e $*"
+BENCH="python bench.py --steps 3 --warmup 3 --no-cpu --no-e2e --no-graph $*"
 
 timeout 900 python bench.py "$@" > $OUT/${TAG}_bench.json 2> $OUT/${TAG}_bench.err || { echo "bench failed"; tail -5 $OUT/${TAG}_bench.err; exit 1; }
 timeout 300 $BENCH > $OUT/${TAG}_plain.json 2> $OUT/${TAG}_plain.err || { echo "plain bench failed"; exit 1; }
@@ -19,7 +19,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file $OUT/${TAG}_launches.csv $BENCH > $OUT/${TAG}_ncu_list.log 2>&1 || echo "launch list failed"
 
 export VPX_NVTX=1
-for grp in "c2.wgrad c1.wgrad" "c1.fwd c2.dgrad c1_act.bwd p1.fwd"; do
+for grp in "c1.wgrad c1.fwd c2.wgrad" "c2.dgrad c2.fwd c3.dgrad c2_act.bwd"; do
   inc=""
   name=""
   for t in $grp; do inc="$inc --nvtx-include $t/"; name="${name}_${t//./}"; done
