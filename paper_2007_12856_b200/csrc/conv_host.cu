@@ -84,13 +84,14 @@ static long long packed_floats(int cin, int cout) {
   return a > b ? a : b;
 }
 
-static int encode_frame_map(CUtensorMap* map, const float* base, const Frame& f, int R) {
+static int encode_frame_map(CUtensorMap* map, const float* base, const Frame& f, int R, bool pair) {
   const uint64_t Wf = f.w + 2 * f.mw, Hf = f.h + 2 * f.mh, Df = f.d + 2 * f.md;
   uint64_t dims[5] = {(uint64_t)f.c, Wf, Hf, Df, (uint64_t)f.n};
   uint64_t strides[4] = {(uint64_t)f.c * 4, Wf * f.c * 4, Hf * Wf * f.c * 4, Df * Hf * Wf * f.c * 4};
-  uint32_t box[5] = {4, 130, (uint32_t)(R + 2), 3, 1};
+  // pair (cin 4): 16-byte voxel rows; otherwise 8 channels as 32-byte SW32 rows
+  uint32_t box[5] = {pair ? 4u : 8u, 130, (uint32_t)(R + 2), 3, 1};
   return encode_tiled(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float*>(base), dims,
-                      strides, box, CU_TENSOR_MAP_SWIZZLE_NONE);
+                      strides, box, pair ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_32B);
 }
 
 // One row-window launch: output frame region z in [zlo,zhi), y in [ylo,yhi),
@@ -101,7 +102,7 @@ static int rowwin_run(const float* in, const Frame& inf, const float* wpack, int
   int R, CG;
   if (!rowwin_config(cin_eff, cout_eff, &R, &CG)) VPX_FAIL(VPX_ERR_UNSUPPORTED, "rowwin config");
   CUtensorMap map;
-  int rc = encode_frame_map(&map, in, inf, R);
+  int rc = encode_frame_map(&map, in, inf, R, cin_eff == 4);
   if (rc) return rc;
   ConvRowParams p{};
   p.zlo = zlo;

@@ -37,13 +37,20 @@ template <int R>
 __host__ __device__ constexpr int plane_bytes() {
   return (plane_raw<R>() + 127) / 128 * 128;
 }
+// non-pair instances: 8-channel planes stored as 32-byte voxel rows in the
+// K-major SWIZZLE_32B layout (one TMA box per plane instead of two 16-byte ones)
+template <int R>
+__host__ __device__ constexpr int plane8_bytes() {
+  return (2 * plane_raw<R>() + 1023) / 1024 * 1024;
+}
 template <int COUT, int CG, bool PAIR>
 __host__ __device__ constexpr int b_bytes() {
   return (PAIR ? 28 : 27 * CG) * COUT * 16;
 }
 template <int COUT, int R, int CG, bool PAIR>
 __host__ __device__ constexpr int stage_bytes() {
-  return (CG * plane_bytes<R>() + b_bytes<COUT, CG, PAIR>() + 1023) / 1024 * 1024;
+  return ((PAIR ? CG * plane_bytes<R>() : (CG / 2) * plane8_bytes<R>()) + b_bytes<COUT, CG, PAIR>() + 1023) /
+         1024 * 1024;
 }
 __host__ __device__ constexpr int pow2_cols(int c) {
   return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512;
@@ -60,8 +67,8 @@ template <int COUT, int R, int CG, bool PAIR, int S>
 __global__ void __launch_bounds__(256, 1)
     conv_rowwin_kernel(const __grid_constant__ CUtensorMap xmap, const ConvRowParams p) {
   constexpr bool kStaged = epi_bytes<COUT>() > 0;
-  constexpr int PLANE = plane_bytes<R>();
-  constexpr int ABYTES = CG * PLANE;
+  constexpr int PLANE = PAIR ? plane_bytes<R>() : plane8_bytes<R>();
+  constexpr int ABYTES = PAIR ? CG * PLANE : (CG / 2) * PLANE;
   constexpr int BBYTES = b_bytes<COUT, CG, PAIR>();
   constexpr int STAGE = stage_bytes<COUT, R, CG, PAIR>();
   constexpr int ACC = R * COUT;
@@ -115,10 +122,17 @@ __global__ void __launch_bounds__(256, 1)
           vpx::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sA = smem + stage * STAGE;
           vpx::mbar_arrive_expect_tx(&full[stage], TX);
+          if constexpr (PAIR) {
 #pragma unroll
-          for (int c = 0; c < CG; ++c)
-            vpx::tma_load_5d(sA + c * PLANE, &xmap, &full[stage], 4 * (g * CG + c),
-                             x0 - 1 + p.in_off_w, y0 - 1 + p.in_off_h, z - 1 + p.in_off_d, n);
+            for (int c = 0; c < CG; ++c)
+              vpx::tma_load_5d(sA + c * PLANE, &xmap, &full[stage], 4 * (g * CG + c), x0 - 1 + p.in_off_w,
+                               y0 - 1 + p.in_off_h, z - 1 + p.in_off_d, n);
+          } else {
+#pragma unroll
+            for (int c = 0; c < CG / 2; ++c)
+              vpx::tma_load_5d(sA + c * PLANE, &xmap, &full[stage], 4 * (g * CG + 2 * c), x0 - 1 + p.in_off_w,
+                               y0 - 1 + p.in_off_h, z - 1 + p.in_off_d, n);
+          }
           vpx::bulk_g2s(sA + ABYTES, p.wpack + static_cast<size_t>(g) * (BBYTES / 4), BBYTES,
                         &full[stage]);
           if (++stage == S) {
@@ -174,9 +188,9 @@ __global__ void __launch_bounds__(256, 1)
                     vpx::make_sdesc(bBase + (t * CG + 2 * jp) * COUT * 16, COUT * 16, 128, 0);
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
-                  const uint32_t as =
-                      aBase + 2 * jp * PLANE + ((a * (R + 2) + r + b) * kWin + c) * 16;
-                  vpx::umma_tf32(dacc + r * COUT, vpx::make_sdesc(as, PLANE, 128, 0), bdesc, idesc,
+                  // 8-channel plane jp, voxel row (a, r+b, c): 32-byte SW32 rows, 8-row atoms
+                  const uint32_t as = aBase + jp * PLANE + ((a * (R + 2) + r + b) * kWin + c) * 32;
+                  vpx::umma_tf32(dacc + r * COUT, vpx::make_sdesc(as, 16, 256, 6), bdesc, idesc,
                                  (g | t | jp) != 0);
                 }
               }
