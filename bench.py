@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--width", type=int, default=WIDTH)
     ap.add_argument("--grid", default=None, help="GxPDxPHxPW override (default 1xNx1x1)")
     ap.add_argument("--bn", action="store_true")
+    ap.add_argument("--net", default="cosmoflow", choices=["cosmoflow", "unet"],
+                    help="unet = the U-Net-mini config (BASELINE configs[4]); default width 256 then")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of the CUDA graph")
@@ -243,7 +245,7 @@ def run_ours(args):
     from paper_2007_12856_b200.comm import RankCtx
     from paper_2007_12856_b200.frames import DistTensor
     from paper_2007_12856_b200.geometry import ProcessGrid
-    from paper_2007_12856_b200.networks import build_cosmoflow
+    from paper_2007_12856_b200.networks import build_cosmoflow, build_unet_mini
     from paper_2007_12856_b200.timing import Recorder
     from paper_2007_12856_b200.accounting import train_step_flops
 
@@ -256,7 +258,11 @@ def run_ours(args):
         raise SystemExit(f"grid {grid} needs {grid.size} ranks, have {world}")
     n_global = N_PER_GROUP * grid.groups
     W = args.width
-    net = build_cosmoflow(W, with_bn=args.bn)
+    if args.net == "unet":
+        W = W if W != WIDTH else 256
+        net = build_unet_mini(W)
+    else:
+        net = build_cosmoflow(W, with_bn=args.bn)
     plan = engine.make_plan(net, grid, n_global, W)
     ctx.prepare_groups([plan.leads])
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
@@ -385,7 +391,7 @@ def run_ours(args):
                     "kernel": top_tag, "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"}
         roof["share_of_step"] = top["ms"] / ms_eager
         roof["traffic"] = ncu_traffic(top_tag)
-    fl = train_step_flops(net, (n_global, 4, W, W, W))
+    fl = train_step_flops(net, (n_global, net.in_channels, W, W, W))
     breakdown = {k: {"ms_per_step": v["ms"] / nprof,
                      "tflops": (v["flops"] / (v["ms"] / v["launches"] * 1e-3) / 1e12) if v["flops"] else None,
                      "gbs": v["bytes"] / (v["ms"] / v["launches"] * 1e-3) / 1e9}
@@ -400,10 +406,11 @@ def run_ours(args):
         cpu = {"value": v, "unit": "samples/s", "cores": threads, "kind": "reference" if use_ref else "port",
                "sample": desc}
     line = {
-        "metric": f"CosmoFlow {W}^3 samples/sec", "value": value, "unit": "samples/s", "n_gpus": world,
+        "metric": (f"U-Net-mini {W}^3 samples/sec" if args.net == "unet" else f"CosmoFlow {W}^3 samples/sec"),
+        "value": value, "unit": "samples/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "tf32", "data": "synthetic",
-        "config": {"workload": f"cosmoflow{W}{'_bn' if args.bn else ''} train step (fwd+bwd+allreduce+adam), "
+        "config": {"workload": f"{net.name}{'_bn' if args.bn else ''} train step (fwd+bwd+allreduce+adam), "
                                f"batch {n_global}, grid {grid.groups}x{grid.pd}x{grid.ph}x{grid.pw}",
                    "global_batch": n_global, "width": W, "grid": f"{grid.groups}x{grid.pd}x{grid.ph}x{grid.pw}",
                    "parallelism": f"dp{grid.groups}xspatial{grid.spatial_size}",

@@ -56,24 +56,28 @@ constexpr int kNA = 48;          // N per tap (x chunks k, k+1: 64 > 48 used col
 constexpr int kACol = 9 * kNA;   // first A column (432)
 constexpr int kASlots = 8;       // A ring: 8 slots x 8 columns
 
-template <int W, bool MASK = false>
+// SRC: 0 = u from the LeakyReLU output y and the pooled gradient, 1 = from the
+// sign mask and the pooled gradient, 2 = u itself (any conv 4 -> 16 whose
+// upstream gradient is already materialised, e.g. after BatchNorm)
+template <int W, int SRC = 0>
 struct C1Cfg {
   static constexpr int KS = (W / 8 + 1 + 7) / 8;           // K-steps per row (k = -1 .. 8KS-2)
   static constexpr int XCH = 8 * KS + 1;                   // x chunks per row (-1 .. 8KS-1)
   static constexpr int XROW = (XCH * 128 + 1023) / 1024 * 1024;
   static constexpr int XS = 12 * XROW;                     // 3 depth taps x 4-row ring
-  static constexpr int YB = MASK ? W * 2 : W * 16 * 4;     // y row, or its 16-bit sign-mask row
-  static constexpr int UB = W / 2 * 16 * 4;                // pooled-gradient row
+  static constexpr int YB = SRC == 1 ? W * 2 : W * 16 * 4; // y / u row, or its 16-bit sign-mask row
+  static constexpr int UB = SRC == 2 ? 0 : W / 2 * 16 * 4;  // pooled-gradient row
   static constexpr int PIPE = XS + 2 * YB + 2 * UB;
   static constexpr int SCRATCH = 128 * 108 * 4;            // epilogue fold, reuses the pipeline buffers
   static constexpr int SMEM = PIPE > SCRATCH ? PIPE : SCRATCH;
 };
 
-template <int W, bool MASK>
+template <int W, int SRC>
 __global__ void __launch_bounds__(384, 1)
     c1_pooled_wgrad_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap ymap,
                            const __grid_constant__ CUtensorMap upmap, const C1Params p) {
-  using Cfg = C1Cfg<W, MASK>;
+  using Cfg = C1Cfg<W, SRC>;
+  constexpr bool MASK = SRC == 1;
   constexpr int KS = Cfg::KS, XROW = Cfg::XROW;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -157,8 +161,9 @@ __global__ void __launch_bounds__(384, 1)
           vpx::tma_load_5d(ys + (i & 1) * Cfg::YB, &ymap, &yfull[i & 1], 0, y, z, n, 0);
         else
           vpx::tma_load_5d(ys + (i & 1) * Cfg::YB, &ymap, &yfull[i & 1], 0, 0, y + p.y_off_h, z + p.y_off_d, n);
-        vpx::tma_load_5d(us + (i & 1) * Cfg::UB, &upmap, &yfull[i & 1], 0, 0, (y >> 1) + p.up_off_h,
-                         (z >> 1) + p.up_off_d, n);
+        if (SRC != 2)
+          vpx::tma_load_5d(us + (i & 1) * Cfg::UB, &upmap, &yfull[i & 1], 0, 0, (y >> 1) + p.up_off_h,
+                           (z >> 1) + p.up_off_d, n);
       }
     }
   } else if (warp == 1) {
@@ -226,20 +231,22 @@ __global__ void __launch_bounds__(384, 1)
       // u voxel of column kk: 8k + d + 1 with k = 8s + kk - 1  ->  b + 8 kk
       const int b = 64 * s - 7 + dd;
       const uint32_t ya = ya0 + b * (MASK ? 2 : 64), ua = ua0 + (b >> 1) * 64;
+      auto val = [&](int kk) -> float {
+        if constexpr (SRC == 2) {
+          return vpx::lds_f32(ya + kk * 512);  // u as stored (already TF32)
+        } else {
+          const float gp = vpx::lds_f32(ua + kk * 256) * 0.125f;
+          return vpx::tf32_rn(pos(ya, kk) ? gp : slope * gp);
+        }
+      };
       if (s > 0 && 64 * s + 56 < W) {
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const float gp = vpx::lds_f32(ua + kk * 256) * 0.125f;
-          v[kk] = vpx::tf32_rn(pos(ya, kk) ? gp : slope * gp);
-        }
+        for (int kk = 0; kk < 8; ++kk) v[kk] = val(kk);
       } else {
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           v[kk] = 0.f;
-          if (static_cast<unsigned>(b + 8 * kk) < static_cast<unsigned>(W)) {
-            const float gp = vpx::lds_f32(ua + kk * 256) * 0.125f;
-            v[kk] = vpx::tf32_rn(pos(ya, kk) ? gp : slope * gp);
-          }
+          if (static_cast<unsigned>(b + 8 * kk) < static_cast<unsigned>(W)) v[kk] = val(kk);
         }
       }
     };
@@ -325,12 +332,12 @@ __global__ void __launch_bounds__(384, 1)
   if (warp == 2) vpx::tmem_dealloc<512>(tbase);
 }
 
-template <int W, bool MASK>
+template <int W, int SRC>
 int launch_c1(const CUtensorMap& xm, const CUtensorMap& ym, const CUtensorMap& um, const C1Params& p,
               cudaStream_t st) {
-  constexpr int smem = C1Cfg<W, MASK>::SMEM + 1024;
+  constexpr int smem = C1Cfg<W, SRC>::SMEM + 1024;
   static_assert(smem <= 227 * 1024, "smem");
-  auto kern = c1_pooled_wgrad_kernel<W, MASK>;
+  auto kern = c1_pooled_wgrad_kernel<W, SRC>;
   VPX_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   kern<<<p.P, 384, smem, st>>>(xm, ym, um, p);
   VPX_LAUNCH_CHECK();
@@ -351,6 +358,13 @@ int c1_pooled_supported(const Frame& xf, const Frame& yf, const Frame& uf) {
   return 1;
 }
 
+// c1 filter gradient from a materialised u (conv 4 -> 16, stride 1, TF32)
+int c1_direct_supported(const Frame& xf, const Frame& uf) {
+  if (precision() != 0 || xf.c != 4 || uf.c != 16 || xf.mw || uf.md || uf.mh || uf.mw) return 0;
+  if (!(uf.w == 64 || uf.w == 128 || uf.w == 256 || uf.w == 512)) return 0;
+  return xf.n == uf.n && xf.d == uf.d && xf.h == uf.h && xf.w == uf.w;
+}
+
 int c1_pooled_parts(const Frame& yf) {
   const long long rows = (long long)yf.n * yf.d * yf.h;
   long long P = getenv("VPX_C1_P") ? atoi(getenv("VPX_C1_P")) : num_sms();
@@ -359,7 +373,8 @@ int c1_pooled_parts(const Frame& yf) {
 }
 
 int conv_wgrad_c1_pooled(const float* x, const Frame& xf, const float* y, const Frame& yf, const float* up,
-                         const Frame& uf, float slope, float* part, cudaStream_t st, const uint16_t* mask) {
+                         const Frame& uf, float slope, float* part, cudaStream_t st, const uint16_t* mask,
+                         bool u_direct) {
   C1Params p{};
   p.n = yf.n;
   p.d = yf.d;
@@ -378,10 +393,10 @@ int conv_wgrad_c1_pooled(const float* x, const Frame& xf, const float* y, const 
   const int W = yf.w;
   int xch = 0;
   switch (W) {
-    case 512: xch = C1Cfg<512, false>::XCH; break;
-    case 256: xch = C1Cfg<256, false>::XCH; break;
-    case 128: xch = C1Cfg<128, false>::XCH; break;
-    case 64: xch = C1Cfg<64, false>::XCH; break;
+    case 512: xch = C1Cfg<512, 0>::XCH; break;
+    case 256: xch = C1Cfg<256, 0>::XCH; break;
+    case 128: xch = C1Cfg<128, 0>::XCH; break;
+    case 64: xch = C1Cfg<64, 0>::XCH; break;
   }
   CUtensorMap xm, ym, um;
   {
@@ -411,7 +426,9 @@ int conv_wgrad_c1_pooled(const float* x, const Frame& xf, const float* y, const 
                               CU_TENSOR_MAP_SWIZZLE_NONE))
       return rc;
   }
-  {
+  if (u_direct) {
+    um = ym;  // unused
+  } else {
     const uint64_t Wu = uf.w, Hf = uf.h + 2 * uf.mh, Df = uf.d + 2 * uf.md;
     uint64_t dims[5] = {64, Wu / 4, Hf, Df, (uint64_t)uf.n};
     uint64_t strides[4] = {256, Wu * 64, Hf * Wu * 64, Df * Hf * Wu * 64};
@@ -420,19 +437,27 @@ int conv_wgrad_c1_pooled(const float* x, const Frame& xf, const float* y, const 
                               CU_TENSOR_MAP_SWIZZLE_NONE))
       return rc;
   }
+  if (u_direct) {
+    switch (W) {
+      case 512: return launch_c1<512, 2>(xm, ym, um, p, st);
+      case 256: return launch_c1<256, 2>(xm, ym, um, p, st);
+      case 128: return launch_c1<128, 2>(xm, ym, um, p, st);
+      case 64: return launch_c1<64, 2>(xm, ym, um, p, st);
+    }
+  }
   if (mask) {
     switch (W) {
-      case 512: return launch_c1<512, true>(xm, ym, um, p, st);
-      case 256: return launch_c1<256, true>(xm, ym, um, p, st);
-      case 128: return launch_c1<128, true>(xm, ym, um, p, st);
-      case 64: return launch_c1<64, true>(xm, ym, um, p, st);
+      case 512: return launch_c1<512, 1>(xm, ym, um, p, st);
+      case 256: return launch_c1<256, 1>(xm, ym, um, p, st);
+      case 128: return launch_c1<128, 1>(xm, ym, um, p, st);
+      case 64: return launch_c1<64, 1>(xm, ym, um, p, st);
     }
   }
   switch (W) {
-    case 512: return launch_c1<512, false>(xm, ym, um, p, st);
-    case 256: return launch_c1<256, false>(xm, ym, um, p, st);
-    case 128: return launch_c1<128, false>(xm, ym, um, p, st);
-    case 64: return launch_c1<64, false>(xm, ym, um, p, st);
+    case 512: return launch_c1<512, 0>(xm, ym, um, p, st);
+    case 256: return launch_c1<256, 0>(xm, ym, um, p, st);
+    case 128: return launch_c1<128, 0>(xm, ym, um, p, st);
+    case 64: return launch_c1<64, 0>(xm, ym, um, p, st);
   }
   VPX_FAIL(VPX_ERR_UNSUPPORTED, "c1 pooled filter gradient: W=%d", W);
 }

@@ -355,6 +355,11 @@ extern "C" int vpx_conv3d_bwd_filter(const float* x, const int* xfr, const float
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   float* part = reinterpret_cast<float*>(static_cast<char*>(ws) +
                                          ((vpx::packed_floats(xf.c, uf.c) * 4 + 255) / 256) * 256);
+  if (k == 3 && stride == 1 && vpx::c1_direct_supported(xf, uf)) {
+    // 4 -> 16 channels: u in TMEM, x as dense 8-voxel rows (conv_c1bwd.cu, SRC 2)
+    if (int rc = vpx::conv_wgrad_c1_pooled(x, xf, u, uf, u, uf, 0.f, part, st, nullptr, true)) return rc;
+    return vpx::reduce_partials(part, vpx::c1_pooled_parts(uf), (long long)uf.c * xf.c * 27, wg, accumulate, st);
+  }
   if (k == 3 && vpx::wgrad_ut_supported(xf, uf, stride) && !getenv("VPX_NO_WGRAD_UT")) {
     if (int rc = vpx::conv_wgrad_ut(x, xf, u, uf, part, st)) return rc;
     return vpx::reduce_partials(part, vpx::wgrad_ut_parts(uf), (long long)uf.c * xf.c * 27, wg, accumulate, st);

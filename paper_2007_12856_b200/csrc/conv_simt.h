@@ -37,7 +37,8 @@ int c1_pooled_supported(const Frame& xf, const Frame& yf, const Frame& uf);
 int c1_pooled_parts(const Frame& yf);
 int conv_wgrad_c1_pooled(const float* x, const Frame& xf, const float* y, const Frame& yf, const float* up,
                          const Frame& uf, float slope, float* part, cudaStream_t st,
-                         const uint16_t* mask = nullptr);
+                         const uint16_t* mask = nullptr, bool u_direct = false);
+int c1_direct_supported(const Frame& xf, const Frame& uf);
 int c1_fwd_pool_supported(const Frame& xf, int cout, const Frame& pf);
 int conv_c1_fwd_pool(const float* x, const Frame& xf, const float* wpack, float slope, float* pout,
                      const Frame& pf, uint16_t* mask, cudaStream_t st);

@@ -126,7 +126,7 @@ __global__ void pool_bwd_kernel(const float* __restrict__ x, Frame xf, const flo
 // -------------------------------------------------------------- batchnorm
 // Per-channel partial sums over a fixed voxel partition (deterministic).
 // mode 0: (sum x, sum x^2); mode 1: (sum u, sum u*xhat) with xhat=(x-mean)*inv.
-constexpr int kBnParts = 512;
+constexpr int kBnParts = 1184;  // 8 blocks per SM: enough loads in flight for HBM
 
 __global__ void bn_partial_kernel(const float* __restrict__ x, Frame xf, const float* __restrict__ u,
                                   Frame uf, const float* __restrict__ mean,
@@ -597,6 +597,12 @@ extern "C" int vpx_bn_sums(const float* x, const int* xf, const float* u, const 
                            const float* mean, const float* inv, int mode, float* out2c, void* ws,
                            void* st) {
   Frame a = F(xf), b = uf ? F(uf) : F(xf);
+  if (a.c % 4 == 0 && a.c / 4 <= 256 && 256 % (a.c / 4) == 0) {
+    if (int rc = bn_sums_vec(x, a, u ? u : x, b, mean, inv, mode, static_cast<double*>(ws), kBnParts, S(st)))
+      return rc;
+    bn_finish_kernel<<<1, 256, 0, S(st)>>>(static_cast<double*>(ws), kBnParts, a.c, out2c);
+    LAUNCH_TAIL;
+  }
   const int threads = a.c >= 256 ? a.c : (256 / a.c) * a.c;
   if (threads > 1024) VPX_FAIL(VPX_ERR_UNSUPPORTED, "bn channels %d", a.c);
   bn_partial_kernel<<<kBnParts, threads, 2 * threads * sizeof(double), S(st)>>>(

@@ -35,9 +35,18 @@ __device__ __forceinline__ float lk(float v, float s) { return v >= 0.f ? v : s 
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;          \
        i += (long long)gridDim.x * blockDim.x)
 
+// Two-level loop for one-to-one pointwise kernels: blocks stride over the
+// interior rows (n, z, y), threads over a row's float4s -- no 64-bit divide per
+// element (which otherwise costs more than the memory traffic).
+#define ROWS2_LOOP(f)                                                                     \
+  const int per_row = (f).w * (f).c / 4;                                                  \
+  const long long nrows = (long long)(f).n * (f).d * (f).h;                               \
+  for (long long row = blockIdx.x; row < nrows; row += gridDim.x)                         \
+    for (int jj = threadIdx.x; jj < per_row; jj += blockDim.x)
+
 __global__ void leaky_fwd_v(const float* __restrict__ x, Frame xf, float* __restrict__ y, Frame yf, float s) {
-  ROW_LOOP(xf) {
-    const long long row = i / per_row, off = 4 * (i % per_row);
+  ROWS2_LOOP(xf) {
+    const int off = 4 * jj;
     float4 v = ld4(x + row_base(xf, row) + off);
     v = make_float4(lk(v.x, s), lk(v.y, s), lk(v.z, s), lk(v.w, s));
     st4(yf, y + row_base(yf, row) + off, v);
@@ -46,8 +55,8 @@ __global__ void leaky_fwd_v(const float* __restrict__ x, Frame xf, float* __rest
 
 __global__ void leaky_bwd_v(const float* __restrict__ x, Frame xf, const float* __restrict__ u, Frame uf,
                             float* __restrict__ g, Frame gf, float s) {
-  ROW_LOOP(xf) {
-    const long long row = i / per_row, off = 4 * (i % per_row);
+  ROWS2_LOOP(xf) {
+    const int off = 4 * jj;
     const float4 a = ld4(x + row_base(xf, row) + off);
     const float4 b = ld4(u + row_base(uf, row) + off);
     st4(gf, g + row_base(gf, row) + off, make_float4(a.x >= 0.f ? b.x : s * b.x, a.y >= 0.f ? b.y : s * b.y,
@@ -140,9 +149,9 @@ __global__ void bn_apply_v(const float* __restrict__ x, Frame xf, const float* _
                            const float* __restrict__ inv, const float* __restrict__ gamma,
                            const float* __restrict__ beta, float* __restrict__ y, Frame yf) {
   const int C = xf.c;
-  ROW_LOOP(xf) {
-    const long long row = i / per_row, off = 4 * (i % per_row);
-    const int c = static_cast<int>(off % C);
+  ROWS2_LOOP(xf) {
+    const int off = 4 * jj;
+    const int c = off % C;
     const float4 v = ld4(x + row_base(xf, row) + off);
     float r[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
@@ -156,9 +165,9 @@ __global__ void bn_bwd_apply_v(const float* __restrict__ x, Frame xf, const floa
                                const float* __restrict__ gamma, const float* __restrict__ sums,
                                float inv_count, float* __restrict__ g, Frame gf) {
   const int C = xf.c;
-  ROW_LOOP(xf) {
-    const long long row = i / per_row, off = 4 * (i % per_row);
-    const int c = static_cast<int>(off % C);
+  ROWS2_LOOP(xf) {
+    const int off = 4 * jj;
+    const int c = off % C;
     const float4 a = ld4(x + row_base(xf, row) + off);
     const float4 b = ld4(u + row_base(uf, row) + off);
     const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
@@ -178,17 +187,23 @@ int grid_v(const Frame& f) {
   const long long cap = (long long)num_sms() * 16;
   return static_cast<int>(g < 1 ? 1 : (g > cap ? cap : g));
 }
+// grid for ROWS2_LOOP kernels: one block per row, capped
+int grid_rows(const Frame& f) {
+  const long long rows = (long long)f.n * f.d * f.h;
+  const long long cap = (long long)num_sms() * 16;
+  return static_cast<int>(rows < 1 ? 1 : (rows > cap ? cap : rows));
+}
 
 }  // namespace
 
 int leaky_fwd_vec(const float* x, const Frame& xf, float* y, const Frame& yf, float s, cudaStream_t st) {
-  leaky_fwd_v<<<grid_v(xf), 256, 0, st>>>(x, xf, y, yf, s);
+  leaky_fwd_v<<<grid_rows(xf), 256, 0, st>>>(x, xf, y, yf, s);
   VPX_LAUNCH_CHECK();
   return VPX_OK;
 }
 int leaky_bwd_vec(const float* x, const Frame& xf, const float* u, const Frame& uf, float* g, const Frame& gf,
                   float s, cudaStream_t st) {
-  leaky_bwd_v<<<grid_v(xf), 256, 0, st>>>(x, xf, u, uf, g, gf, s);
+  leaky_bwd_v<<<grid_rows(xf), 256, 0, st>>>(x, xf, u, uf, g, gf, s);
   VPX_LAUNCH_CHECK();
   return VPX_OK;
 }
@@ -205,14 +220,14 @@ int pool_bwd_vec(const float* x, const Frame& xf, const float* u, const Frame& u
 }
 int bn_apply_vec(const float* x, const Frame& xf, const float* mean, const float* inv, const float* gamma,
                  const float* beta, float* y, const Frame& yf, cudaStream_t st) {
-  bn_apply_v<<<grid_v(xf), 256, 0, st>>>(x, xf, mean, inv, gamma, beta, y, yf);
+  bn_apply_v<<<grid_rows(xf), 256, 0, st>>>(x, xf, mean, inv, gamma, beta, y, yf);
   VPX_LAUNCH_CHECK();
   return VPX_OK;
 }
 int bn_bwd_apply_vec(const float* x, const Frame& xf, const float* u, const Frame& uf, const float* mean,
                      const float* inv, const float* gamma, const float* sums, float inv_count, float* g,
                      const Frame& gf, cudaStream_t st) {
-  bn_bwd_apply_v<<<grid_v(xf), 256, 0, st>>>(x, xf, u, uf, mean, inv, gamma, sums, inv_count, g, gf);
+  bn_bwd_apply_v<<<grid_rows(xf), 256, 0, st>>>(x, xf, u, uf, mean, inv, gamma, sums, inv_count, g, gf);
   VPX_LAUNCH_CHECK();
   return VPX_OK;
 }
@@ -320,6 +335,81 @@ __global__ void pool_leaky_bwd_v(const float* __restrict__ y, Frame yf, const fl
   }
 }
 }  // namespace
+
+// BatchNorm per-channel sums, float4 over channels and whole interior rows
+// per block (no per-voxel index decode).  Block p owns rows
+// [rows*p/P, rows*(p+1)/P); lanes with the same channel quad are combined in
+// a fixed order, so the fp64 partials are deterministic.
+// mode 0: (sum x, sum x^2); mode 1: (sum u, sum u*xhat), xhat = (x-mean)*inv.
+template <int MODE>
+__global__ void bn_sums_v(const float* __restrict__ x, Frame xf, const float* __restrict__ u, Frame uf,
+                          const float* __restrict__ mean, const float* __restrict__ inv, double* __restrict__ part) {
+  extern __shared__ double shd[];  // [8][blockDim.x]
+  const int C = xf.c, C4 = C / 4;
+  const int lanes = blockDim.x / C4, c4 = threadIdx.x % C4, lane = threadIdx.x / C4;
+  const long long rows = (long long)xf.n * xf.d * xf.h;
+  const long long r0 = rows * blockIdx.x / gridDim.x, r1 = rows * (blockIdx.x + 1) / gridDim.x;
+  double s1[4] = {0.0, 0.0, 0.0, 0.0}, s2[4] = {0.0, 0.0, 0.0, 0.0};
+  float4 mu = make_float4(0.f, 0.f, 0.f, 0.f), iv = mu;
+  if (MODE == 1) {
+    mu = ld4(mean + 4 * c4);
+    iv = ld4(inv + 4 * c4);
+  }
+  if (lane < lanes) {
+    for (long long row = r0; row < r1; ++row) {
+      const float* xb = x + row_base(xf, row) + 4 * c4;
+      const float* ub = MODE == 1 ? u + row_base(uf, row) + 4 * c4 : nullptr;
+      for (int v = lane; v < xf.w; v += lanes) {
+        const float4 a = ld4(xb + (long long)v * C);
+        if (MODE == 0) {
+          s1[0] += a.x; s1[1] += a.y; s1[2] += a.z; s1[3] += a.w;
+          s2[0] += (double)a.x * a.x; s2[1] += (double)a.y * a.y;
+          s2[2] += (double)a.z * a.z; s2[3] += (double)a.w * a.w;
+        } else {
+          const float4 b = ld4(ub + (long long)v * uf.c);
+          s1[0] += b.x; s1[1] += b.y; s1[2] += b.z; s1[3] += b.w;
+          s2[0] += (double)b.x * ((a.x - mu.x) * iv.x);
+          s2[1] += (double)b.y * ((a.y - mu.y) * iv.y);
+          s2[2] += (double)b.z * ((a.z - mu.z) * iv.z);
+          s2[3] += (double)b.w * ((a.w - mu.w) * iv.w);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    shd[j * blockDim.x + threadIdx.x] = s1[j];
+    shd[(4 + j) * blockDim.x + threadIdx.x] = s2[j];
+  }
+  __syncthreads();
+  if (threadIdx.x < C4) {  // lane 0 of every channel quad folds the lanes in order
+    double t1[4] = {0.0, 0.0, 0.0, 0.0}, t2[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int l = 0; l < lanes; ++l)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        t1[j] += shd[j * blockDim.x + l * C4 + threadIdx.x];
+        t2[j] += shd[(4 + j) * blockDim.x + l * C4 + threadIdx.x];
+      }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      part[(long long)blockIdx.x * 2 * C + 4 * threadIdx.x + j] = t1[j];
+      part[(long long)blockIdx.x * 2 * C + C + 4 * threadIdx.x + j] = t2[j];
+    }
+  }
+}
+
+int bn_sums_vec(const float* x, const Frame& xf, const float* u, const Frame& uf, const float* mean,
+                const float* inv, int mode, double* part, int P, cudaStream_t st) {
+  const int C4 = xf.c / 4;
+  if (xf.c % 4 || C4 > 256 || 256 % C4) return VPX_ERR_UNSUPPORTED;
+  const size_t sh = 8 * 256 * sizeof(double);
+  if (mode == 0)
+    bn_sums_v<0><<<P, 256, sh, st>>>(x, xf, x, xf, mean, inv, part);
+  else
+    bn_sums_v<1><<<P, 256, sh, st>>>(x, xf, u, uf, mean, inv, part);
+  VPX_LAUNCH_CHECK();
+  return VPX_OK;
+}
 
 int pool_leaky_bwd(const float* y, const Frame& yf, const float* up, const Frame& uf, float* g, const Frame& gf,
                    float s, int is_max, cudaStream_t st) {

@@ -16,6 +16,8 @@ int bn_apply_vec(const float* x, const Frame& xf, const float* mean, const float
 int bn_bwd_apply_vec(const float* x, const Frame& xf, const float* u, const Frame& uf, const float* mean,
                      const float* inv, const float* gamma, const float* sums, float inv_count, float* g,
                      const Frame& gf, cudaStream_t st);
+int bn_sums_vec(const float* x, const Frame& xf, const float* u, const Frame& uf, const float* mean,
+                const float* inv, int mode, double* part, int P, cudaStream_t st);
 int pool_leaky_bwd(const float* y, const Frame& yf, const float* up, const Frame& uf, float* g, const Frame& gf,
                    float s, int is_max, cudaStream_t st);
 int pool_leaky_bwd_blocked(const float* y, const Frame& yf, const float* up, const Frame& uf, float* gb,

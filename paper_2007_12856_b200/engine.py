@@ -410,7 +410,7 @@ def forward(ctx: RankCtx, plan: Plan, state: RankState, batch: Batch, mode: str,
             stash.append(cur)
             cur = D.dist_pool3d(ctx, cur, layer.pool_kind, radii, tag=layer.name)
         elif layer.kind == "bn":
-            cur, cache = D.dist_batchnorm(ctx, cur, bn[layer.name], mode, radii)
+            cur, cache = D.dist_batchnorm(ctx, cur, bn[layer.name], mode, radii, tag=layer.name)
             stash.append(cache)
         elif layer.kind == "leaky":
             stash.append(cur)
@@ -528,7 +528,7 @@ def backward(ctx: RankCtx, plan: Plan, state: RankState, stash, dpred, trace: di
         elif layer.kind == "pool":
             u = D.dist_pool3d_bwd(ctx, kept, u, layer.pool_kind, in_meta, tag=layer.name)
         elif layer.kind == "bn":
-            u, _, _ = D.dist_batchnorm_bwd(ctx, u, bn[layer.name], kept, in_meta,
+            u, _, _ = D.dist_batchnorm_bwd(ctx, u, bn[layer.name], kept, in_meta, tag=layer.name,
                                            dgamma=G[f"{layer.name}.gamma"], dbeta=G[f"{layer.name}.beta"])
         elif layer.kind == "leaky":
             u = D.dist_leaky_relu_bwd(kept, u, layer.slope, in_meta, tag=layer.name)

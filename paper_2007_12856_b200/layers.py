@@ -297,7 +297,7 @@ def _bn_sums(x, u, mean, inv, mode):
 
 
 def dist_batchnorm(ctx: RankCtx, x: DistTensor, state: BNState, mode: str = "train",
-                   out_radii=NO_HALO):
+                   out_radii=NO_HALO, tag: str = "bn"):
     """Local (sum x, sum x^2) -> allreduce(2C) over the tensor's whole rank
     group -> normalise (reference layers/distributed.py:152-180).  Returns
     (y, cache); the cache keeps x and the batch statistics (xhat is recomputed)."""
@@ -307,7 +307,8 @@ def dist_batchnorm(ctx: RankCtx, x: DistTensor, state: BNState, mode: str = "tra
     inv = torch.empty(c, dtype=torch.float32, device="cuda")
     if mode == "train":
         count = gs.n * gs.d * gs.h * gs.w
-        sums = _bn_sums(x, None, None, None, 0)
+        with region(f"{tag}.stats", 0, 4 * x.voxels() * c):
+            sums = _bn_sums(x, None, None, None, 0)
         ctx.allreduce_sum_(sums, _group(x.meta))
         _lib.call("vpx_bn_stats", sums.data_ptr(), c, float(count), float(state.eps), float(state.momentum),
                   mean.data_ptr(), inv.data_ptr(), state.running_mean.data_ptr(),
@@ -319,19 +320,21 @@ def dist_batchnorm(ctx: RankCtx, x: DistTensor, state: BNState, mode: str = "tra
     else:
         raise ShapeMismatch(f"unknown bn mode {mode!r}")
     y = _out(x.meta, gs, out_radii, x.grid_rank)
-    _lib.call("vpx_bn_apply", x.ptr, x.desc, mean.data_ptr(), inv.data_ptr(), state.gamma.data_ptr(),
-              state.beta.data_ptr(), y.ptr, y.desc, stream_ptr())
+    with region(f"{tag}.fwd", 0, 8 * x.voxels() * c):
+        _lib.call("vpx_bn_apply", x.ptr, x.desc, mean.data_ptr(), inv.data_ptr(), state.gamma.data_ptr(),
+                  state.beta.data_ptr(), y.ptr, y.desc, stream_ptr())
     return y, (x, mean, inv, count)
 
 
 def dist_batchnorm_bwd(ctx: RankCtx, u: DistTensor, state: BNState, cache, in_meta,
-                       dgamma: torch.Tensor = None, dbeta: torch.Tensor = None):
+                       dgamma: torch.Tensor = None, dbeta: torch.Tensor = None, tag: str = "bn"):
     """(dx, dgamma partial, dbeta partial); the two reduction terms are
     allreduced for dx, the parameter gradients stay rank-local partials
     (reference layers/distributed.py:183-201)."""
     x, mean, inv, count = cache
     c = x.c
-    local = _bn_sums(x, u, mean, inv, 1)  # [sum u, sum u*xhat]
+    with region(f"{tag}.bwd_stats", 0, 8 * x.voxels() * c):
+        local = _bn_sums(x, u, mean, inv, 1)  # [sum u, sum u*xhat]
     if dgamma is None:
         dgamma = torch.empty(c, dtype=torch.float32, device="cuda")
     if dbeta is None:
@@ -340,8 +343,9 @@ def dist_batchnorm_bwd(ctx: RankCtx, u: DistTensor, state: BNState, cache, in_me
     dgamma.copy_(local[c:])
     ctx.allreduce_sum_(local, _group(u.meta))
     g = DistTensor(in_meta, u.grid_rank, zero=False)
-    _lib.call("vpx_bn_bwd_apply", x.ptr, x.desc, u.ptr, u.desc, mean.data_ptr(), inv.data_ptr(),
-              state.gamma.data_ptr(), local.data_ptr(), float(count), g.ptr, g.desc, stream_ptr())
+    with region(f"{tag}.bwd", 0, 12 * x.voxels() * c):
+        _lib.call("vpx_bn_bwd_apply", x.ptr, x.desc, u.ptr, u.desc, mean.data_ptr(), inv.data_ptr(),
+                  state.gamma.data_ptr(), local.data_ptr(), float(count), g.ptr, g.desc, stream_ptr())
     return g, dgamma, dbeta
 
 
