@@ -46,7 +46,7 @@ struct RowH {
   static constexpr int RB = CIN * 4;
   static constexpr uint32_t LAYOUT = RB == 128 ? 2 : RB == 64 ? 4 : 6;  // SW128 / SW64 / SW32
   static constexpr int KSTEPS = PAIR ? 5 : 9 * (CIN / 8);
-  static constexpr int N = 3 * C;
+  static constexpr int N = (3 * C + 15) / 16 * 16;        // 3 height taps x C, padded to a multiple of 16
   static constexpr int BSTEP = 2 * N * 16;               // bytes of B per K step
   static constexpr int WBYTES = KSTEPS * BSTEP;
   static constexpr int STAGE = PAIR ? NCH * kPlane : (3 * kWinH * RB + 1023) / 1024 * 1024;
@@ -215,23 +215,30 @@ __global__ void __launch_bounds__(384, 1)
         vpx::tc_fence_after();
         const uint32_t s0 = lane_base + (gm & (kNB - 1)) * N, s1 = lane_base + ((gm + 1) & (kNB - 1)) * N + C,
                        s2 = lane_base + ((gm + 2) & (kNB - 1)) * N + 2 * C;
+        constexpr int CW = C < 16 ? C : 16;  // TMEM columns per load
 #pragma unroll
-        for (int cb = 0; cb < C / 16; ++cb) {
-          uint32_t v0[16], v1[16], v2[16];  // three loads in flight, one wait
-          vpx::tmem_ld16_nw(s0 + cb * 16, v0);
-          vpx::tmem_ld16_nw(s1 + cb * 16, v1);
-          vpx::tmem_ld16_nw(s2 + cb * 16, v2);
+        for (int cb = 0; cb < C / CW; ++cb) {
+          uint32_t v0[CW], v1[CW], v2[CW];  // three loads in flight, one wait
+          if constexpr (CW == 16) {
+            vpx::tmem_ld16_nw(s0 + cb * 16, v0);
+            vpx::tmem_ld16_nw(s1 + cb * 16, v1);
+            vpx::tmem_ld16_nw(s2 + cb * 16, v2);
+          } else {
+            vpx::tmem_ld8_nw(s0, v0);
+            vpx::tmem_ld8_nw(s1, v1);
+            vpx::tmem_ld8_nw(s2, v2);
+          }
           vpx::tmem_ld_wait();
-          float v[16];
+          float v[CW];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
+          for (int i = 0; i < CW; ++i) {
             v[i] = (__uint_as_float(v0[i]) + __uint_as_float(v1[i])) + __uint_as_float(v2[i]);
             if (act) v[i] = v[i] >= 0.f ? v[i] : slope * v[i];  // reference layers/reference.py:231-233
             if (rnd) v[i] = vpx::tf32_rn(v[i]);
           }
-          float4* s4 = reinterpret_cast<float4*>(stg + lane * (C + 4) + cb * 16);
+          float4* s4 = reinterpret_cast<float4*>(stg + lane * (C + 4) + cb * CW);
 #pragma unroll
-          for (int i = 0; i < 4; ++i) s4[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+          for (int i = 0; i < CW / 4; ++i) s4[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
         }
         // E_{y-1} is not needed by any later output row of this band; the last
         // row also releases the band's final two blocks
@@ -282,7 +289,7 @@ int launch_rowh(const CUtensorMap& xmap, const ConvRowParams& p, cudaStream_t st
 __global__ void pack_rowh_kernel(const float* __restrict__ w, int cout, int cin, int mode, int pair,
                                  float* __restrict__ out) {
   const int O = mode ? cin : cout, I = mode ? cout : cin;
-  const int N = 3 * O;
+  const int N = (3 * O + 15) / 16 * 16;  // rows >= 3*O are zero padding
   const int ksteps = pair ? 5 : 9 * (I / 8);
   const long long total = (long long)ksteps * 2 * N * 4;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
@@ -304,7 +311,7 @@ __global__ void pack_rowh_kernel(const float* __restrict__ w, int cout, int cin,
       i = 4 * (2 * (ks % (I / 8)) + h) + e;
     }
     float v = 0.f;
-    if (tap < 9) {
+    if (tap < 9 && b < 3) {
       const int a = tap / 3, c = tap % 3;
       if (mode == 0)
         v = w[(((long long)o * cin + i) * 3 + a) * 9 + b * 3 + c];
@@ -322,12 +329,13 @@ namespace vpx {
 // Channel configurations with a rowh instance (cin_eff -> cout_eff).
 int rowh_supported(int cin, int cout) {
   return (cin == 4 && cout == 16) || (cin == 8 && cout == 16) || (cin == 16 && cout == 16) ||
-         (cin == 32 && cout == 16) || (cin == 16 && cout == 32);
+         (cin == 32 && cout == 16) || (cin == 16 && cout == 32) || (cin == 8 && cout == 8) ||
+         (cin == 16 && cout == 8) || (cin == 32 && cout == 8);
 }
 
 long long rowh_packed_bytes(int cin, int cout) {
   const int ksteps = cin == 4 ? 5 : 9 * (cin / 8);
-  return (long long)ksteps * 2 * 3 * cout * 16;
+  return (long long)ksteps * 2 * ((3 * cout + 15) / 16 * 16) * 16;
 }
 
 int rowh_pack(const float* w, int cout, int cin, int mode, float* dst, cudaStream_t st) {
@@ -347,6 +355,9 @@ int launch_rowh_any(const CUtensorMap& xmap, const ConvRowParams& p, int cin, in
   if (cin == 16 && cout == 16) return launch_rowh<16, 16>(xmap, p, st);
   if (cin == 32 && cout == 16) return launch_rowh<32, 16>(xmap, p, st);
   if (cin == 16 && cout == 32) return launch_rowh<16, 32>(xmap, p, st);
+  if (cin == 8 && cout == 8) return launch_rowh<8, 8>(xmap, p, st);
+  if (cin == 16 && cout == 8) return launch_rowh<16, 8>(xmap, p, st);
+  if (cin == 32 && cout == 8) return launch_rowh<32, 8>(xmap, p, st);
   VPX_FAIL(VPX_ERR_UNSUPPORTED, "rowh conv: no instance for cin=%d cout=%d", cin, cout);
 }
 

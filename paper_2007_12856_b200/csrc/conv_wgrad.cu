@@ -255,7 +255,7 @@ int wgrad_tc_supported(const Frame& xf, const Frame& uf, int stride) {
   if (uf.w % 8 || (uf.w > 128 && uf.w % 128)) return 0;
   if (uf.mw || uf.md || uf.mh) return 0;  // upstream gradients are margin-free
   const int cin = xf.c, cout = uf.c;
-  if (stride == 1 && cin <= 32 && cin % 4 == 0) return cout == 16 || cout == 32 || cout == 64;
+  if (stride == 1 && cin <= 32 && cin % 4 == 0) return cout == 8 || cout == 16 || cout == 32 || cout == 64;
   if (cin % 32 == 0 && cin >= 64 && uf.w <= 32 && (stride == 1 || stride == 2))
     return cout == 128 || cout % 256 == 0;
   return 0;
@@ -307,7 +307,8 @@ int conv_wgrad_tc(const float* x, const Frame& xf, const float* u, const Frame& 
   if (int rc = encode_ch32_map(&um, u, uf, p.wseg, 1)) return rc;
   if (modeA) {
     switch (uf.c) {
-      case 16:  // 32-wide N tile, upper 16 columns are TMA zero-fill
+      case 8:   // 32-wide N tile, channels beyond cout are TMA zero-fill
+      case 16:
       case 32: return launch_wgrad<true, 32>(xm, um, p, st);
       case 64: return launch_wgrad<true, 64>(xm, um, p, st);
     }

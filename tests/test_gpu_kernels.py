@@ -47,6 +47,8 @@ CASES = [
     (2, 4, 16, 3, 5, 256, 3, 1),
     (1, 16, 32, 4, 4, 128, 3, 1),
     (2, 16, 32, 3, 6, 256, 3, 1),      # u-in-TMEM filter gradient (W = 256)
+    (1, 8, 8, 4, 4, 128, 3, 1),        # U-Net 8-channel levels: rowh N padded 24 -> 32
+    (1, 16, 8, 3, 4, 256, 3, 1),
     (1, 32, 64, 3, 3, 128, 3, 1),
     (1, 64, 128, 8, 8, 8, 3, 2),
     (1, 128, 256, 4, 4, 4, 3, 1),
