@@ -224,6 +224,10 @@ extern "C" long long vpx_conv3d_workspace_bytes(int cin, int cout, int k, const 
   long long parts = vpx::wgrad_simt_parts(uf) * cout * cin * k3 * 4;
   const long long tc = (long long)vpx::num_sms() * cout * cin * 27 * 4;
   if (tc > parts) parts = tc;
+  if (k == 1 || cin == 1) {  // conv_small.cu partials
+    const long long sm = 4LL * vpx::num_sms() * cout * cin * k3 * 4;
+    if (sm > parts) parts = sm;
+  }
   const long long tb = vpx::tapbox_workspace_bytes(cin, cout);
   if (tb > packed) packed = tb;
   const long long rh = vpx::rowh_packed_bytes(cin, cout) > vpx::rowh_packed_bytes(cout, cin)
@@ -276,6 +280,8 @@ static int conv_fwd_impl(const float* x, const int* xfr, const float* w, int k, 
     if (ws_bytes < vpx::tapbox_workspace_bytes(cin, cout)) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "workspace too small");
     return vpx::conv_tapbox(0, x, xf, w, cin, cout, stride, y, yf, act, slope, ws, st, ws_bytes);
   }
+  if (vpx::small_conv_supported(0, xf, yf, k, stride) && !getenv("VPX_NO_SMALL"))
+    return vpx::small_conv_fwd(x, xf, w, k, y, yf, act, slope, st);
   return vpx::conv_fwd_simt(x, xf, w, k, stride, y, yf, st, act, slope);
 }
 
@@ -337,6 +343,8 @@ static int conv_bwd_data_impl(const float* u, const int* ufr, const float* w, in
     if (ws_bytes < vpx::tapbox_workspace_bytes(cin, cout)) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "workspace too small");
     return vpx::conv_tapbox(1, u, uf, w, cin, cout, stride, xg, gf, 0, 0.f, ws, st, ws_bytes);
   }
+  if (k == 1 && vpx::small_conv_supported(1, uf, gf, k, stride) && !getenv("VPX_NO_SMALL"))
+    return vpx::small_conv_bwd_data(u, uf, w, xg, gf, st);
   return vpx::conv_bwd_data_simt(u, uf, w, k, stride, xg, gf, st);
 }
 
@@ -367,6 +375,11 @@ extern "C" int vpx_conv3d_bwd_filter(const float* x, const int* xfr, const float
   if (vpx::precision() == 0 && k == 3 && vpx::wgrad_tc_supported(xf, uf, stride)) {
     if (int rc = vpx::conv_wgrad_tc(x, xf, u, uf, stride, part, st)) return rc;
     return vpx::reduce_partials(part, vpx::wgrad_tc_parts(xf, uf), (long long)uf.c * xf.c * 27, wg,
+                                accumulate, st);
+  }
+  if (vpx::small_conv_supported(2, xf, uf, k, stride) && !getenv("VPX_NO_SMALL")) {
+    if (int rc = vpx::small_conv_wgrad(x, xf, u, uf, k, part, st)) return rc;
+    return vpx::reduce_partials(part, vpx::small_wgrad_parts(uf, k), (long long)uf.c * xf.c * k * k * k, wg,
                                 accumulate, st);
   }
   return vpx::conv_wgrad_simt(x, xf, u, uf, k, stride, wg, accumulate, part, st);

@@ -42,6 +42,15 @@ int c1_direct_supported(const Frame& xf, const Frame& uf);
 int c1_fwd_pool_supported(const Frame& xf, int cout, const Frame& pf);
 int conv_c1_fwd_pool(const float* x, const Frame& xf, const float* wpack, float slope, float* pout,
                      const Frame& pf, uint16_t* mask, cudaStream_t st);
+// conv_small.cu: 1x1x1 convs and 3x3x3 convs on 1 input channel (U-Net edges)
+int small_conv_supported(int which, const Frame& xf, const Frame& of, int k, int s);
+int small_wgrad_parts(const Frame& uf, int k);
+int small_conv_fwd(const float* x, const Frame& xf, const float* w, int k, float* y, const Frame& yf, int act,
+                   float slope, cudaStream_t st);
+int small_conv_bwd_data(const float* u, const Frame& uf, const float* w, float* g, const Frame& gf,
+                        cudaStream_t st);
+int small_conv_wgrad(const float* x, const Frame& xf, const float* u, const Frame& uf, int k, float* part,
+                     cudaStream_t st);
 int conv_wgrad_simt(const float* x, const Frame& xf, const float* u, const Frame& uf, int k, int s,
                     float* wg, int accumulate, float* part, cudaStream_t st);
 

@@ -1,0 +1,388 @@
+// CUDA-core convolutions for the two U-Net layers whose channel counts are too
+// small for a tensor-core tile (reference networks.py U-Net-mini):
+//   * the 1x1x1 head (8 -> 2 channels): forward, input gradient, filter gradient;
+//   * the first 3x3x3 layer on the 1-channel input (1 -> 8): forward (+ fused
+//     LeakyReLU) and filter gradient.
+// Both are HBM- or LSU-bound; what matters is one index decode per row (not per
+// element), float4 channel loads, weights broadcast from shared memory, and for
+// the filter gradients a persistent grid whose per-block partials are summed in
+// fixed order by reduce_partials (deterministic).
+// Arithmetic order of the forward / input-gradient kernels equals the generic
+// direct kernels in conv_simt.cu (taps ascending, channels ascending, fmaf), so
+// swapping paths does not change a single bit of those outputs.
+#include "conv_simt.h"
+#include "vpx_host.h"
+#include "vpx_round.cuh"
+
+namespace vpx {
+
+namespace {
+
+__device__ __forceinline__ long long fidx(const Frame& f, int n, int z, int y, int x) {
+  return ((((long long)n * (f.d + 2 * f.md) + (z + f.md)) * (f.h + 2 * f.mh) + (y + f.mh)) *
+              (f.w + 2 * f.mw) +
+          (x + f.mw)) *
+         f.c;
+}
+// first interior voxel of interior row `row` = (n, z, y)
+__device__ __forceinline__ long long frow(const Frame& f, long long row) {
+  const int y = static_cast<int>(row % f.h);
+  row /= f.h;
+  const int z = static_cast<int>(row % f.d);
+  const int n = static_cast<int>(row / f.d);
+  return fidx(f, n, z, y, 0);
+}
+__device__ __forceinline__ bool finside(const Frame& f, int z, int y, int x) {
+  return z >= -f.md && z < f.d + f.md && y >= -f.mh && y < f.h + f.mh && x >= -f.mw && x < f.w + f.mw;
+}
+
+template <int C>
+__device__ __forceinline__ void load_c(const float* p, float (&v)[C]) {
+  if constexpr (C % 4 == 0) {
+#pragma unroll
+    for (int i = 0; i < C / 4; ++i) {
+      const float4 t = *reinterpret_cast<const float4*>(p + 4 * i);
+      v[4 * i] = t.x;
+      v[4 * i + 1] = t.y;
+      v[4 * i + 2] = t.z;
+      v[4 * i + 3] = t.w;
+    }
+  } else if constexpr (C % 2 == 0) {
+#pragma unroll
+    for (int i = 0; i < C / 2; ++i) {
+      const float2 t = *reinterpret_cast<const float2*>(p + 2 * i);
+      v[2 * i] = t.x;
+      v[2 * i + 1] = t.y;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < C; ++i) v[i] = p[i];
+  }
+}
+
+// ------------------------------------------------------------ 1x1x1 conv
+// y[v][co] = sum_ci x[v][ci] w[co][ci]; blocks stride over interior rows.
+template <int CI, int CO>
+__global__ void __launch_bounds__(256) pw_fwd_kernel(const float* __restrict__ x, Frame xf,
+                                                     const float* __restrict__ w, float* __restrict__ y,
+                                                     Frame yf, int act, float slope) {
+  __shared__ float ws[CO * CI];
+  for (int i = threadIdx.x; i < CO * CI; i += blockDim.x) ws[i] = w[i];
+  __syncthreads();
+  const long long nrows = (long long)xf.n * xf.d * xf.h;
+  for (long long row = blockIdx.x; row < nrows; row += gridDim.x) {
+    const float* xr = x + frow(xf, row);
+    float* yr = y + frow(yf, row);
+    for (int i = threadIdx.x; i < xf.w; i += blockDim.x) {
+      float xv[CI];
+      load_c<CI>(xr + (long long)i * CI, xv);
+#pragma unroll
+      for (int co = 0; co < CO; ++co) {
+        float acc = 0.f;
+#pragma unroll
+        for (int ci = 0; ci < CI; ++ci) acc = fmaf(xv[ci], ws[co * CI + ci], acc);
+        yr[(long long)i * CO + co] = rnd(yf, (act && acc < 0.f) ? slope * acc : acc);
+      }
+    }
+  }
+}
+
+// g[v][ci] = sum_co u[v][co] w[co][ci] (gradient frame without margins)
+template <int CI, int CO>
+__global__ void __launch_bounds__(256) pw_dgrad_kernel(const float* __restrict__ u, Frame uf,
+                                                       const float* __restrict__ w, float* __restrict__ g,
+                                                       Frame gf) {
+  __shared__ float ws[CO * CI];
+  for (int i = threadIdx.x; i < CO * CI; i += blockDim.x) ws[i] = w[i];
+  __syncthreads();
+  const long long nrows = (long long)uf.n * uf.d * uf.h;
+  for (long long row = blockIdx.x; row < nrows; row += gridDim.x) {
+    const float* ur = u + frow(uf, row);
+    float* gr = g + frow(gf, row);
+    for (int i = threadIdx.x; i < uf.w; i += blockDim.x) {
+      float uv[CO];
+      load_c<CO>(ur + (long long)i * CO, uv);
+      float acc[CI];
+#pragma unroll
+      for (int ci = 0; ci < CI; ++ci) acc[ci] = 0.f;
+#pragma unroll
+      for (int co = 0; co < CO; ++co)
+#pragma unroll
+        for (int ci = 0; ci < CI; ++ci) acc[ci] = fmaf(uv[co], ws[co * CI + ci], acc[ci]);
+      float* gp = gr + (long long)i * CI;
+      if constexpr (CI % 4 == 0) {
+#pragma unroll
+        for (int q = 0; q < CI / 4; ++q)
+          *reinterpret_cast<float4*>(gp + 4 * q) =
+              rnd4(gf, make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]));
+      } else {
+#pragma unroll
+        for (int ci = 0; ci < CI; ++ci) gp[ci] = rnd(gf, acc[ci]);
+      }
+    }
+  }
+}
+
+// Block-level fixed-order reduction of NV per-thread values into out[0..NV).
+template <int NV>
+__device__ __forceinline__ void block_reduce_store(float (&acc)[NV], float* red, float* out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    float v = acc[j];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (lane == 0) red[warp * NV + j] = v;
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < NV; j += blockDim.x) {
+    float s = 0.f;
+    for (int q = 0; q < nw; ++q) s += red[q * NV + j];
+    out[j] = s;
+  }
+}
+
+// part[block][co][ci] = sum over the block's rows of u[v][co] x[v][ci]
+template <int CI, int CO>
+__global__ void __launch_bounds__(256) pw_wgrad_kernel(const float* __restrict__ x, Frame xf,
+                                                       const float* __restrict__ u, Frame uf,
+                                                       float* __restrict__ part) {
+  __shared__ float red[8 * CO * CI];
+  float acc[CO * CI];
+#pragma unroll
+  for (int j = 0; j < CO * CI; ++j) acc[j] = 0.f;
+  const long long nrows = (long long)uf.n * uf.d * uf.h;
+  for (long long row = blockIdx.x; row < nrows; row += gridDim.x) {
+    const float* xr = x + frow(xf, row);
+    const float* ur = u + frow(uf, row);
+    for (int i = threadIdx.x; i < uf.w; i += blockDim.x) {
+      float xv[CI], uv[CO];
+      load_c<CI>(xr + (long long)i * CI, xv);
+      load_c<CO>(ur + (long long)i * CO, uv);
+#pragma unroll
+      for (int co = 0; co < CO; ++co)
+#pragma unroll
+        for (int ci = 0; ci < CI; ++ci) acc[co * CI + ci] = fmaf(uv[co], xv[ci], acc[co * CI + ci]);
+    }
+  }
+  block_reduce_store<CO * CI>(acc, red, part + (long long)blockIdx.x * CO * CI);
+}
+
+// ------------------------------------------------ 3x3x3 conv, 1 input channel
+constexpr int kTX = 64, kTY = 4;  // output tile: 4 rows x 64 voxels of one plane
+
+struct C1Tile {
+  int n, z, y0, x0;
+};
+__device__ __forceinline__ C1Tile c1_tile(const Frame& of, long long t) {
+  const int tx = (of.w + kTX - 1) / kTX, ty = (of.h + kTY - 1) / kTY;
+  C1Tile r;
+  r.x0 = static_cast<int>(t % tx) * kTX;
+  t /= tx;
+  r.y0 = static_cast<int>(t % ty) * kTY;
+  t /= ty;
+  r.z = static_cast<int>(t % of.d);
+  r.n = static_cast<int>(t / of.d);
+  return r;
+}
+// xs[a][yy][xx] = x[z + a - 1][y0 + yy - 1][x0 + xx - 1] (0 outside the frame)
+__device__ __forceinline__ void c1_load_x(const float* __restrict__ x, const Frame& xf, const C1Tile& t,
+                                          float* xs) {
+  constexpr int PY = kTY + 2, PX = kTX + 2;
+  for (int i = threadIdx.x; i < 3 * PY * PX; i += blockDim.x) {
+    const int xx = i % PX, yy = (i / PX) % PY, a = i / (PX * PY);
+    const int iz = t.z + a - 1, iy = t.y0 + yy - 1, ix = t.x0 + xx - 1;
+    xs[i] = finside(xf, iz, iy, ix) ? __ldg(x + fidx(xf, t.n, iz, iy, ix)) : 0.f;
+  }
+}
+
+template <int CO>
+__global__ void __launch_bounds__(256) c1k3_fwd_kernel(const float* __restrict__ x, Frame xf,
+                                                       const float* __restrict__ w, float* __restrict__ y,
+                                                       Frame yf, int act, float slope) {
+  constexpr int PY = kTY + 2, PX = kTX + 2;
+  __shared__ float xs[3 * PY * PX];
+  __shared__ __align__(16) float ws[27 * CO];  // ws[tap][co] = w[co][0][tap]
+  for (int i = threadIdx.x; i < 27 * CO; i += blockDim.x) ws[i] = w[(i % CO) * 27 + i / CO];
+  const C1Tile t = c1_tile(yf, blockIdx.x);
+  c1_load_x(x, xf, t, xs);
+  __syncthreads();
+  const int tx = threadIdx.x % kTX, ty = threadIdx.x / kTX;
+  const int ox = t.x0 + tx, oy = t.y0 + ty;
+  if (ox >= yf.w || oy >= yf.h) return;
+  float acc[CO];
+#pragma unroll
+  for (int co = 0; co < CO; ++co) acc[co] = 0.f;
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const float xv = xs[(a * PY + ty + b) * PX + tx + c];
+        const float* wt = ws + ((a * 3 + b) * 3 + c) * CO;
+#pragma unroll
+        for (int co = 0; co < CO; ++co) acc[co] = fmaf(xv, wt[co], acc[co]);
+      }
+  float* yp = y + fidx(yf, t.n, t.z, oy, ox);
+#pragma unroll
+  for (int j = 0; j < CO; ++j) acc[j] = (act && acc[j] < 0.f) ? slope * acc[j] : acc[j];
+#pragma unroll
+  for (int q = 0; q < CO / 4; ++q)
+    *reinterpret_cast<float4*>(yp + 4 * q) =
+        rnd4(yf, make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]));
+}
+
+// part[block][co][tap] = sum over the block's tiles of u[v][co] x[v + tap - 1].
+// Thread roles: (tap, 4-channel group q) x VG voxel groups.
+template <int CO>
+__global__ void __launch_bounds__(256) c1k3_wgrad_kernel(const float* __restrict__ x, Frame xf,
+                                                         const float* __restrict__ u, Frame uf,
+                                                         long long ntiles, float* __restrict__ part) {
+  constexpr int PY = kTY + 2, PX = kTX + 2, NQ = CO / 4, ROLES = 27 * NQ, VG = 216 / ROLES;
+  static_assert(ROLES * VG == 216, "role split");
+  __shared__ float xs[3 * PY * PX];
+  __shared__ __align__(16) float us[kTX * kTY * CO];
+  __shared__ __align__(16) float red[VG * 27 * CO];
+  const int role = threadIdx.x % ROLES, vg = threadIdx.x / ROLES;
+  const int tap = role / NQ, q = role % NQ;
+  const int a = tap / 9, b = (tap / 3) % 3, c = tap % 3;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  for (long long ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+    const C1Tile t = c1_tile(uf, ti);
+    c1_load_x(x, xf, t, xs);
+    for (int i = threadIdx.x; i < kTX * kTY * NQ; i += blockDim.x) {
+      const int v = i / NQ, qq = i % NQ;
+      const int oy = t.y0 + v / kTX, ox = t.x0 + v % kTX;
+      float4 val = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (oy < uf.h && ox < uf.w) val = *reinterpret_cast<const float4*>(u + fidx(uf, t.n, t.z, oy, ox) + 4 * qq);
+      *reinterpret_cast<float4*>(us + v * CO + 4 * qq) = val;
+    }
+    __syncthreads();
+    if (vg < VG) {
+      const float* xb = xs + (a * PY + b) * PX + c;
+      for (int v = vg; v < kTX * kTY; v += VG) {
+        const float xv = xb[(v / kTX) * PX + (v % kTX)];
+        const float4 uv = *reinterpret_cast<const float4*>(us + v * CO + 4 * q);
+        acc[0] = fmaf(uv.x, xv, acc[0]);
+        acc[1] = fmaf(uv.y, xv, acc[1]);
+        acc[2] = fmaf(uv.z, xv, acc[2]);
+        acc[3] = fmaf(uv.w, xv, acc[3]);
+      }
+    }
+    __syncthreads();
+  }
+  if (vg < VG) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) red[(vg * CO + 4 * q + j) * 27 + tap] = acc[j];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 27 * CO; i += blockDim.x) {
+    float s = 0.f;
+    for (int g = 0; g < VG; ++g) s += red[g * 27 * CO + i];
+    part[(long long)blockIdx.x * 27 * CO + i] = s;  // [co][ci = 0][tap]
+  }
+}
+
+int rows_grid(const Frame& f, int cap_per_sm) {
+  const long long rows = (long long)f.n * f.d * f.h;
+  const long long cap = (long long)num_sms() * cap_per_sm;
+  return static_cast<int>(rows < 1 ? 1 : (rows > cap ? cap : rows));
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------- host
+#define PW_CASES(X) X(4, 1) X(4, 2) X(4, 4) X(8, 1) X(8, 2) X(8, 4) X(16, 1) X(16, 2) X(16, 4) X(32, 1) X(32, 2)
+
+int small_conv_supported(int which, const Frame& xf, const Frame& of, int k, int s) {
+  // which: 0 fwd (xf input, of output), 1 bwd-data (xf = upstream, of = gradient), 2 bwd-filter
+  if (s != 1) return 0;
+  if (k == 1) {
+    const int ci = which == 1 ? of.c : xf.c, co = which == 1 ? xf.c : of.c;
+#define PW_OK(a, b) if (ci == a && co == b) return which != 1 || (of.md == 0 && of.mh == 0 && of.mw == 0);
+    PW_CASES(PW_OK)
+#undef PW_OK
+    return 0;
+  }
+  if (k == 3 && which != 1) {
+    const int co = of.c;
+    return xf.c == 1 && (co == 4 || co == 8 || co == 16);
+  }
+  return 0;
+}
+
+int small_wgrad_parts(const Frame& uf, int k) {
+  if (k == 1) return rows_grid(uf, 4);
+  const long long ntiles = (long long)uf.n * uf.d * ((uf.h + kTY - 1) / kTY) * ((uf.w + kTX - 1) / kTX);
+  const long long cap = 4LL * num_sms();
+  return static_cast<int>(ntiles < cap ? ntiles : cap);
+}
+
+int small_conv_fwd(const float* x, const Frame& xf, const float* w, int k, float* y, const Frame& yf, int act,
+                   float slope, cudaStream_t st) {
+  if (k == 1) {
+#define PW_F(a, b)                                                                           \
+  if (xf.c == a && yf.c == b) {                                                              \
+    pw_fwd_kernel<a, b><<<rows_grid(xf, 16), 256, 0, st>>>(x, xf, w, y, yf, act, slope);     \
+    VPX_LAUNCH_CHECK();                                                                      \
+    return VPX_OK;                                                                           \
+  }
+    PW_CASES(PW_F)
+#undef PW_F
+  } else {
+    const long long ntiles = (long long)yf.n * yf.d * ((yf.h + kTY - 1) / kTY) * ((yf.w + kTX - 1) / kTX);
+    if (ntiles > 0x7fffffffLL) VPX_FAIL(VPX_ERR_UNSUPPORTED, "too many tiles");
+    const int g = static_cast<int>(ntiles);
+    switch (yf.c) {
+      case 4: c1k3_fwd_kernel<4><<<g, 256, 0, st>>>(x, xf, w, y, yf, act, slope); break;
+      case 8: c1k3_fwd_kernel<8><<<g, 256, 0, st>>>(x, xf, w, y, yf, act, slope); break;
+      case 16: c1k3_fwd_kernel<16><<<g, 256, 0, st>>>(x, xf, w, y, yf, act, slope); break;
+      default: VPX_FAIL(VPX_ERR_UNSUPPORTED, "small conv fwd: %d channels", yf.c);
+    }
+    VPX_LAUNCH_CHECK();
+    return VPX_OK;
+  }
+  VPX_FAIL(VPX_ERR_UNSUPPORTED, "small conv fwd: %d -> %d channels", xf.c, yf.c);
+}
+
+int small_conv_bwd_data(const float* u, const Frame& uf, const float* w, float* g, const Frame& gf,
+                        cudaStream_t st) {
+#define PW_D(a, b)                                                                   \
+  if (gf.c == a && uf.c == b) {                                                      \
+    pw_dgrad_kernel<a, b><<<rows_grid(uf, 16), 256, 0, st>>>(u, uf, w, g, gf);       \
+    VPX_LAUNCH_CHECK();                                                              \
+    return VPX_OK;                                                                   \
+  }
+  PW_CASES(PW_D)
+#undef PW_D
+  VPX_FAIL(VPX_ERR_UNSUPPORTED, "small conv bwd_data: %d -> %d channels", gf.c, uf.c);
+}
+
+// Partials only: part[P][cout][cin][k^3], P = small_wgrad_parts(uf, k).
+int small_conv_wgrad(const float* x, const Frame& xf, const float* u, const Frame& uf, int k, float* part,
+                     cudaStream_t st) {
+  const int P = small_wgrad_parts(uf, k);
+  if (k == 1) {
+#define PW_W(a, b)                                                              \
+  if (xf.c == a && uf.c == b) {                                                 \
+    pw_wgrad_kernel<a, b><<<P, 256, 0, st>>>(x, xf, u, uf, part);               \
+    VPX_LAUNCH_CHECK();                                                         \
+    return VPX_OK;                                                              \
+  }
+    PW_CASES(PW_W)
+#undef PW_W
+    VPX_FAIL(VPX_ERR_UNSUPPORTED, "small conv wgrad: %d -> %d channels", xf.c, uf.c);
+  }
+  const long long ntiles = (long long)uf.n * uf.d * ((uf.h + kTY - 1) / kTY) * ((uf.w + kTX - 1) / kTX);
+  switch (uf.c) {
+    case 4: c1k3_wgrad_kernel<4><<<P, 256, 0, st>>>(x, xf, u, uf, ntiles, part); break;
+    case 8: c1k3_wgrad_kernel<8><<<P, 256, 0, st>>>(x, xf, u, uf, ntiles, part); break;
+    case 16: c1k3_wgrad_kernel<16><<<P, 256, 0, st>>>(x, xf, u, uf, ntiles, part); break;
+    default: VPX_FAIL(VPX_ERR_UNSUPPORTED, "small conv wgrad: %d channels", uf.c);
+  }
+  VPX_LAUNCH_CHECK();
+  return VPX_OK;
+}
+
+}  // namespace vpx

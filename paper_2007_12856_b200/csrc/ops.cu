@@ -637,12 +637,15 @@ extern "C" int vpx_concat(const float* a, const int* af, const float* b, const i
                           const int* yf, void* st) {
   Frame A = F(af), B = F(bf), Y = F(yf);
   if (A.c + B.c != Y.c) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "concat channels");
+  if (A.c % 4 == 0 && B.c % 4 == 0) return vpx::concat_vec(a, A, b, B, y, Y, S(st));
   concat_kernel<<<grid1d(VC(Y) * Y.c), 256, 0, S(st)>>>(a, A, b, B, y, Y);
   LAUNCH_TAIL;
 }
 extern "C" int vpx_split(const float* u, const int* uf, float* ga, const int* gaf, float* gb,
                          const int* gbf, int acc_b, void* st) {
   Frame U = F(uf), A = F(gaf), B = F(gbf);
+  if (A.c + B.c != U.c) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "split channels");
+  if (A.c % 4 == 0 && B.c % 4 == 0) return vpx::split_vec(u, U, ga, A, gb, B, acc_b, S(st));
   split_kernel<<<grid1d(VC(U) * U.c), 256, 0, S(st)>>>(u, U, ga, A, gb, B, acc_b);
   LAUNCH_TAIL;
 }
@@ -659,12 +662,14 @@ extern "C" int vpx_copy(const float* x, const int* xf, float* y, const int* yf, 
 extern "C" int vpx_deconv_fwd(const float* x, const int* xf, const float* w, float* y, const int* yf,
                               void* st) {
   Frame A = F(xf), B = F(yf);
+  if (vpx::deconv_vec_supported(A.c, B.c)) return vpx::deconv_fwd_vec(x, A, w, y, B, S(st));
   deconv_fwd_kernel<<<grid1d(VC(B) * B.c), 256, 0, S(st)>>>(x, A, w, y, B);
   LAUNCH_TAIL;
 }
 extern "C" int vpx_deconv_bwd_data(const float* u, const int* uf, const float* w, float* g,
                                    const int* gf, void* st) {
   Frame A = F(uf), B = F(gf);
+  if (vpx::deconv_vec_supported(B.c, A.c)) return vpx::deconv_dgrad_vec(u, A, w, g, B, S(st));
   deconv_bwd_data_kernel<<<grid1d(VC(B) * B.c), 256, 0, S(st)>>>(u, A, w, g, B);
   LAUNCH_TAIL;
 }
@@ -678,6 +683,12 @@ extern "C" int vpx_deconv_bwd_filter(const float* x, const int* xf, const float*
   const int P = static_cast<int>(nv < 256 ? nv : 256);
   const long long chunk = (nv + P - 1) / P;
   const int len = A.c * B.c * 8;
+  if (vpx::deconv_vec_supported(A.c, B.c)) {
+    int Pv = 0;
+    if (int rc = vpx::deconv_wgrad_vec(x, A, u, B, static_cast<float*>(ws), 256, &Pv, S(st))) return rc;
+    reduce_parts_kernel<<<grid1d(len), 256, 0, S(st)>>>(static_cast<float*>(ws), Pv, len, wg, accumulate);
+    LAUNCH_TAIL;
+  }
   dim3 grid((len + 255) / 256, P);
   deconv_wgrad_kernel<<<grid, 256, 0, S(st)>>>(x, A, u, B, chunk, static_cast<float*>(ws));
   VPX_LAUNCH_CHECK();

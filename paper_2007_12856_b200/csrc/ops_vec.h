@@ -26,4 +26,14 @@ int wgrad_c4_supported(const Frame& xf, const Frame& uf);
 int wgrad_c4_parts(const Frame& uf);
 int conv_wgrad_c4(const float* x, const Frame& xf, const float* ub, const Frame& uf, float* part,
                   cudaStream_t st);
+// ops_unet.cu
+int deconv_vec_supported(int cin, int cout);
+int deconv_fwd_vec(const float* x, const Frame& xf, const float* w, float* y, const Frame& yf, cudaStream_t st);
+int deconv_dgrad_vec(const float* u, const Frame& uf, const float* w, float* g, const Frame& gf, cudaStream_t st);
+int deconv_wgrad_vec(const float* x, const Frame& xf, const float* u, const Frame& uf, float* part, int max_parts,
+                     int* parts, cudaStream_t st);
+int concat_vec(const float* a, const Frame& af, const float* b, const Frame& bf, float* y, const Frame& yf,
+               cudaStream_t st);
+int split_vec(const float* u, const Frame& uf, float* ga, const Frame& gaf, float* gb, const Frame& gbf, int acc_b,
+              cudaStream_t st);
 }  // namespace vpx

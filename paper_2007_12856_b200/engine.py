@@ -405,7 +405,7 @@ def forward(ctx: RankCtx, plan: Plan, state: RankState, batch: Batch, mode: str,
                                 leaky_slope=nxt.slope if fused_act else None)
         elif layer.kind == "deconv":
             stash.append(cur)
-            cur = D.dist_deconv3d(ctx, cur, P[f"{layer.name}.w"], radii)
+            cur = D.dist_deconv3d(ctx, cur, P[f"{layer.name}.w"], radii, tag=layer.name)
         elif layer.kind == "pool":
             stash.append(cur)
             cur = D.dist_pool3d(ctx, cur, layer.pool_kind, radii, tag=layer.name)
@@ -418,7 +418,7 @@ def forward(ctx: RankCtx, plan: Plan, state: RankState, batch: Batch, mode: str,
         elif layer.kind == "concat":
             skip = outputs[layer.skip]
             stash.append((cur.c, skip.c))
-            cur = D.dist_concat_channels(cur, skip, radii)
+            cur = D.dist_concat_channels(cur, skip, radii, tag=layer.name)
         elif layer.kind == "dropout":
             raise ShapeMismatch("spatial dropout is not part of either network")
         else:
@@ -523,8 +523,8 @@ def backward(ctx: RankCtx, plan: Plan, state: RankState, stash, dpred, trace: di
             else:
                 u = D.dist_conv3d_bwd_data(ctx, u, P[f"{layer.name}.w"], layer.params, in_meta, tag=layer.name)
         elif layer.kind == "deconv":
-            D.dist_deconv3d_bwd_filter(ctx, kept, u, reduce=False, out=G[f"{layer.name}.w"])
-            u = D.dist_deconv3d_bwd_data(ctx, u, P[f"{layer.name}.w"], in_meta)
+            D.dist_deconv3d_bwd_filter(ctx, kept, u, reduce=False, out=G[f"{layer.name}.w"], tag=layer.name)
+            u = D.dist_deconv3d_bwd_data(ctx, u, P[f"{layer.name}.w"], in_meta, tag=layer.name)
         elif layer.kind == "pool":
             u = D.dist_pool3d_bwd(ctx, kept, u, layer.pool_kind, in_meta, tag=layer.name)
         elif layer.kind == "bn":
@@ -535,7 +535,7 @@ def backward(ctx: RankCtx, plan: Plan, state: RankState, stash, dpred, trace: di
         elif layer.kind == "concat":
             c_main, _ = kept
             main, sk = D.dist_concat_bwd(u, c_main, _meta_like(in_meta),
-                                         _skip_meta(plan, layer), extra.get(layer.skip))
+                                         _skip_meta(plan, layer), extra.get(layer.skip), tag=layer.name)
             extra[layer.skip] = sk
             u = main
         if u is not None and i == plan.redist_idx:

@@ -218,29 +218,32 @@ def dist_conv3d_bwd_filter(ctx: RankCtx, x: DistTensor, u: DistTensor, params, r
 
 # ------------------------------------------------------------------- deconv
 
-def dist_deconv3d(ctx: RankCtx, x: DistTensor, w: torch.Tensor, out_radii=NO_HALO) -> DistTensor:
+def dist_deconv3d(ctx: RankCtx, x: DistTensor, w: torch.Tensor, out_radii=NO_HALO, tag: str = "deconv") -> DistTensor:
     """k2s2 transposed conv: purely local (reference layers/distributed.py:103-112)."""
     if tuple(x.meta.radii) != NO_HALO:
         raise ShapeMismatch("deconv input must carry no halos")
     gs = x.meta.global_shape
     y = _out(x.meta, Shape5D(gs.n, w.shape[1], 2 * gs.d, 2 * gs.h, 2 * gs.w), out_radii, x.grid_rank)
-    _lib.call("vpx_deconv_fwd", x.ptr, x.desc, w.data_ptr(), y.ptr, y.desc, stream_ptr())
+    with region(f"{tag}.fwd", 2 * 8 * x.voxels() * x.c * y.c, 4 * (x.voxels() * x.c + y.voxels() * y.c)):
+        _lib.call("vpx_deconv_fwd", x.ptr, x.desc, w.data_ptr(), y.ptr, y.desc, stream_ptr())
     return y
 
 
-def dist_deconv3d_bwd_data(ctx: RankCtx, u: DistTensor, w: torch.Tensor, in_meta) -> DistTensor:
+def dist_deconv3d_bwd_data(ctx: RankCtx, u: DistTensor, w: torch.Tensor, in_meta, tag: str = "deconv") -> DistTensor:
     g = DistTensor(in_meta, u.grid_rank, zero=False)
-    _lib.call("vpx_deconv_bwd_data", u.ptr, u.desc, w.data_ptr(), g.ptr, g.desc, stream_ptr())
+    with region(f"{tag}.dgrad", 2 * u.voxels() * u.c * g.c, 4 * (u.voxels() * u.c + g.voxels() * g.c)):
+        _lib.call("vpx_deconv_bwd_data", u.ptr, u.desc, w.data_ptr(), g.ptr, g.desc, stream_ptr())
     return g
 
 
 def dist_deconv3d_bwd_filter(ctx: RankCtx, x: DistTensor, u: DistTensor, reduce: bool = True,
-                             out: torch.Tensor = None) -> torch.Tensor:
+                             out: torch.Tensor = None, tag: str = "deconv") -> torch.Tensor:
     if out is None:
         out = torch.empty((x.c, u.c, 2, 2, 2), dtype=torch.float32, device="cuda")
     ws = WS.get(_lib.load().vpx_deconv_workspace_bytes(x.c, u.c))
-    _lib.call("vpx_deconv_bwd_filter", x.ptr, x.desc, u.ptr, u.desc, out.data_ptr(), 0, ws.data_ptr(),
-              stream_ptr())
+    with region(f"{tag}.wgrad", 2 * u.voxels() * u.c * x.c, 4 * (u.voxels() * u.c + x.voxels() * x.c)):
+        _lib.call("vpx_deconv_bwd_filter", x.ptr, x.desc, u.ptr, u.desc, out.data_ptr(), 0, ws.data_ptr(),
+                  stream_ptr())
     if reduce:
         ctx.allreduce_sum_(out.view(-1), _group(x.meta))
     return out
@@ -377,24 +380,27 @@ def dist_pool_leaky_bwd(y: DistTensor, u: DistTensor, slope: float, kind: str, i
     return g
 
 
-def dist_concat_channels(a: DistTensor, b: DistTensor, out_radii=NO_HALO) -> DistTensor:
+def dist_concat_channels(a: DistTensor, b: DistTensor, out_radii=NO_HALO, tag: str = "concat") -> DistTensor:
     if a.meta.grid != b.meta.grid or a.meta.rank_map != b.meta.rank_map:
         raise ShapeMismatch("concat operands must share a partition layout")
     ga, gb = a.meta.global_shape, b.meta.global_shape
     if (ga.n, ga.d, ga.h, ga.w) != (gb.n, gb.d, gb.h, gb.w):
         raise ShapeMismatch(f"concat shapes {ga} vs {gb}")
     y = _out(a.meta, Shape5D(ga.n, ga.c + gb.c, ga.d, ga.h, ga.w), out_radii, a.grid_rank)
-    _lib.call("vpx_concat", a.ptr, a.desc, b.ptr, b.desc, y.ptr, y.desc, stream_ptr())
+    with region(f"{tag}.fwd", 0, 8 * y.voxels() * y.c):
+        _lib.call("vpx_concat", a.ptr, a.desc, b.ptr, b.desc, y.ptr, y.desc, stream_ptr())
     return y
 
 
-def dist_concat_bwd(u: DistTensor, c_main: int, main_meta, skip_meta, skip_grad: DistTensor = None):
+def dist_concat_bwd(u: DistTensor, c_main: int, main_meta, skip_meta, skip_grad: DistTensor = None,
+                    tag: str = "concat"):
     """Split a concat's gradient into (main part, skip part); the skip part is
     accumulated into skip_grad when given (reference engine.py:432-438)."""
     ga = DistTensor(main_meta, u.grid_rank, zero=False)
     acc = skip_grad is not None
     gb = skip_grad if acc else DistTensor(skip_meta, u.grid_rank, zero=False)
-    _lib.call("vpx_split", u.ptr, u.desc, ga.ptr, ga.desc, gb.ptr, gb.desc, int(acc), stream_ptr())
+    with region(f"{tag}.bwd", 0, 4 * u.voxels() * u.c * (3 if acc else 2)):
+        _lib.call("vpx_split", u.ptr, u.desc, ga.ptr, ga.desc, gb.ptr, gb.desc, int(acc), stream_ptr())
     return ga, gb
 
 
@@ -428,9 +434,10 @@ def dist_cross_entropy(ctx: RankCtx, pred: DistTensor, labels: torch.Tensor, cou
     g = DistTensor(make_partition(pred.meta.global_shape, pred.meta.grid, NO_HALO, pred.meta.rank_map),
                    pred.grid_rank, zero=False)
     part = torch.empty(nparts, dtype=torch.float64, device="cuda")
-    _lib.call("vpx_xent", pred.ptr, pred.desc, labels.data_ptr(), float(count), g.ptr, g.desc,
-              part.data_ptr(), nparts, stream_ptr())
-    local = part.sum().reshape(1)
+    with region("loss.xent", 0, 4 * pred.voxels() * pred.c * 2 + 8 * pred.voxels()):
+        _lib.call("vpx_xent", pred.ptr, pred.desc, labels.data_ptr(), float(count), g.ptr, g.desc,
+                  part.data_ptr(), nparts, stream_ptr())
+        local = part.sum().reshape(1)
     ctx.allreduce_sum_(local, group)
     return local / count, g
 

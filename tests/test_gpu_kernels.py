@@ -4,6 +4,7 @@ tolerance rtol 1e-3 in the reference's metric max|got-ref| / max|ref|
 
 import ctypes
 import json
+import os
 
 import numpy as np
 import pytest
@@ -53,6 +54,12 @@ CASES = [
     (1, 64, 128, 8, 8, 8, 3, 2),
     (1, 128, 256, 4, 4, 4, 3, 1),
     (2, 8, 2, 6, 6, 6, 1, 1),
+    # U-Net edges on CUDA cores (conv_small.cu): 1x1x1 head, 1-channel first layer
+    (1, 8, 2, 3, 4, 256, 1, 1),
+    (1, 16, 4, 2, 3, 40, 1, 1),
+    (1, 1, 8, 3, 5, 100, 3, 1),
+    (2, 1, 8, 4, 6, 64, 3, 1),
+    (1, 1, 16, 2, 9, 70, 3, 1),
     # tcgen05 filter gradient: mode A (Cin <= 32, W taps folded into M) ...
     (1, 4, 16, 3, 4, 32, 3, 1),
     (2, 16, 32, 3, 3, 16, 3, 1),
@@ -313,3 +320,72 @@ def test_halo_copy_round_trip():
     before = t.t.clone()
     copy_box(t, box, buf, 2)
     assert torch.equal(t.t[1:2, 0:4, 1:4, 2:7, :], 2 * before[1:2, 0:4, 1:4, 2:7, :])
+
+
+@pytest.mark.parametrize("cin,cout,spatial", [(16, 8, (3, 4, 40)), (32, 16, (2, 3, 64)), (32, 8, (2, 2, 33))])
+def test_deconv_vectorised_vs_oracle(cin, cout, spatial, fp32_mode):
+    """Transposed conv fwd / dgrad / wgrad on the float4 row kernels (ops_unet.cu),
+    partial 32-voxel tiles included; fp32 CUDA-core arithmetic."""
+    rng = np.random.default_rng(11)
+    x = rng.standard_normal((2, cin) + spatial).astype(np.float32)
+    w = (rng.standard_normal((cin, cout, 2, 2, 2)) / np.sqrt(8 * cin)).astype(np.float32)
+    xf = _frame_of(x)
+    yf = Frame(2, cout, *(2 * e for e in spatial))
+    wdev = torch.from_numpy(w).cuda()
+    _lib.call("vpx_deconv_fwd", xf.ptr, xf.desc, wdev.data_ptr(), yf.ptr, yf.desc, stream_ptr())
+    assert rel(yf.to_ncdhw().cpu().numpy(), O.deconv3d(x, w)) < 1e-5
+    u = rng.standard_normal((2, cout) + tuple(2 * e for e in spatial)).astype(np.float32)
+    uf = _frame_of(u)
+    gf = Frame(2, cin, *spatial, (1, 1, 1), zero=True)
+    _lib.call("vpx_deconv_bwd_data", uf.ptr, uf.desc, wdev.data_ptr(), gf.ptr, gf.desc, stream_ptr())
+    assert rel(gf.to_ncdhw().cpu().numpy(), O.deconv3d_bwd_data(u, w)) < 1e-5
+    assert float(gf.t.abs().sum()) > 0 and gf.t[:, 0].abs().max().item() == 0.0  # margins untouched
+    wg = torch.full_like(wdev, 0.5)
+    W = torch.empty(_lib.load().vpx_deconv_workspace_bytes(cin, cout) // 4, device="cuda")
+    _lib.call("vpx_deconv_bwd_filter", xf.ptr, xf.desc, uf.ptr, uf.desc, wg.data_ptr(), 1, W.data_ptr(),
+              stream_ptr())
+    assert rel(wg.cpu().numpy() - 0.5, O.deconv3d_bwd_filter(x, u)) < 1e-5
+
+
+@pytest.mark.parametrize("ca,cb", [(8, 8), (16, 16), (3, 5)])
+def test_concat_split_exact(ca, cb, fp32_mode):
+    rng = np.random.default_rng(5)
+    a = rng.standard_normal((2, ca, 3, 4, 20)).astype(np.float32)
+    b = rng.standard_normal((2, cb, 3, 4, 20)).astype(np.float32)
+    af, bf = _frame_of(a), _frame_of(b)
+    yf = Frame(2, ca + cb, 3, 4, 20, (1, 1, 1), zero=True)
+    _lib.call("vpx_concat", af.ptr, af.desc, bf.ptr, bf.desc, yf.ptr, yf.desc, stream_ptr())
+    assert np.array_equal(yf.to_ncdhw().cpu().numpy(), np.concatenate([a, b], axis=1))
+    u = rng.standard_normal((2, ca + cb, 3, 4, 20)).astype(np.float32)
+    uf = _frame_of(u)
+    ga = Frame(2, ca, 3, 4, 20)
+    gb = _frame_of(b)
+    _lib.call("vpx_split", uf.ptr, uf.desc, ga.ptr, ga.desc, gb.ptr, gb.desc, 1, stream_ptr())
+    assert np.array_equal(ga.to_ncdhw().cpu().numpy(), u[:, :ca])
+    assert np.array_equal(gb.to_ncdhw().cpu().numpy(), b + u[:, ca:])
+
+
+def test_first_layer_one_channel_fused_leaky_margins():
+    """1 -> 8 channel 3x3x3 conv with fused LeakyReLU reading halo margins
+    (conv_small.cu), bit-identical to the generic direct kernel."""
+    rng = np.random.default_rng(8)
+    n, d, h, w = 1, 3, 5, 70
+    full = rng.uniform(-1, 1, (n, 1, d + 2, h + 2, w + 2)).astype(np.float32)
+    wt = (rng.uniform(-1, 1, (8, 1, 3, 3, 3)) / 5).astype(np.float32)
+    xf = Frame(n, 1, d, h, w, (1, 1, 1), zero=True)
+    xf.t.copy_(torch.from_numpy(full.transpose(0, 2, 3, 4, 1).copy()).cuda())
+    wdev = torch.from_numpy(wt).cuda()
+    outs = []
+    for env in ("", "1"):
+        os.environ["VPX_NO_SMALL"] = env
+        if not env:
+            del os.environ["VPX_NO_SMALL"]
+        yf = Frame(n, 8, d, h, w)
+        W = ws(1, 8, 3, yf)
+        _lib.call("vpx_conv3d_fwd_act", xf.ptr, xf.desc, wdev.data_ptr(), 3, 1, yf.ptr, yf.desc, 1, 0.3,
+                  W.data_ptr(), W.numel() * 4, stream_ptr())
+        outs.append(yf.to_ncdhw().cpu().numpy())
+    os.environ.pop("VPX_NO_SMALL", None)
+    y_ref = O.leaky(O.k_conv3d_fwd(full, wt, (1, 1, 1)), 0.3)
+    assert rel(outs[0], y_ref) < TF32_RTOL
+    assert np.array_equal(outs[0].view(np.uint32), outs[1].view(np.uint32))
