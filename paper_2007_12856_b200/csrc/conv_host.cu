@@ -372,6 +372,10 @@ extern "C" int vpx_conv3d_bwd_filter(const float* x, const int* xfr, const float
     if (int rc = vpx::conv_wgrad_ut(x, xf, u, uf, part, st)) return rc;
     return vpx::reduce_partials(part, vpx::wgrad_ut_parts(uf), (long long)uf.c * xf.c * 27, wg, accumulate, st);
   }
+  if (vpx::precision() == 0 && k == 3 && vpx::wgrad_g_supported(xf, uf, stride) && !getenv("VPX_NO_WGRAD_G")) {
+    if (int rc = vpx::conv_wgrad_g(x, xf, u, uf, part, st)) return rc;
+    return vpx::reduce_partials(part, vpx::wgrad_g_parts(uf), (long long)uf.c * xf.c * 27, wg, accumulate, st);
+  }
   if (vpx::precision() == 0 && k == 3 && vpx::wgrad_tc_supported(xf, uf, stride)) {
     if (int rc = vpx::conv_wgrad_tc(x, xf, u, uf, stride, part, st)) return rc;
     return vpx::reduce_partials(part, vpx::wgrad_tc_parts(xf, uf), (long long)uf.c * xf.c * 27, wg,

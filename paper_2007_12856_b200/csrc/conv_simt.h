@@ -33,6 +33,9 @@ int conv_wgrad_tc(const float* x, const Frame& xf, const float* u, const Frame& 
 int wgrad_ut_supported(const Frame& xf, const Frame& uf, int stride);
 int wgrad_ut_parts(const Frame& uf);
 int conv_wgrad_ut(const float* x, const Frame& xf, const float* u, const Frame& uf, float* part, cudaStream_t st);
+int wgrad_g_supported(const Frame& xf, const Frame& uf, int stride);
+int wgrad_g_parts(const Frame& uf);
+int conv_wgrad_g(const float* x, const Frame& xf, const float* u, const Frame& uf, float* part, cudaStream_t st);
 int c1_pooled_supported(const Frame& xf, const Frame& yf, const Frame& uf);
 int c1_pooled_parts(const Frame& yf);
 int conv_wgrad_c1_pooled(const float* x, const Frame& xf, const float* y, const Frame& yf, const float* up,

@@ -50,6 +50,11 @@ CASES = [
     (2, 16, 32, 3, 6, 256, 3, 1),      # u-in-TMEM filter gradient (W = 256)
     (1, 8, 8, 4, 4, 128, 3, 1),        # U-Net 8-channel levels: rowh N padded 24 -> 32
     (1, 16, 8, 3, 4, 256, 3, 1),
+    # grouped-voxel filter gradient (Cin = Cout <= 32, conv_wgrad_g.cu)
+    (2, 8, 8, 3, 5, 256, 3, 1),
+    (1, 8, 8, 3, 3, 32, 3, 1),
+    (1, 16, 16, 3, 4, 128, 3, 1),
+    (1, 32, 32, 2, 3, 64, 3, 1),
     (1, 32, 64, 3, 3, 128, 3, 1),
     (1, 64, 128, 8, 8, 8, 3, 2),
     (1, 128, 256, 4, 4, 4, 3, 1),
@@ -389,3 +394,23 @@ def test_first_layer_one_channel_fused_leaky_margins():
     y_ref = O.leaky(O.k_conv3d_fwd(full, wt, (1, 1, 1)), 0.3)
     assert rel(outs[0], y_ref) < TF32_RTOL
     assert np.array_equal(outs[0].view(np.uint32), outs[1].view(np.uint32))
+
+
+@pytest.mark.parametrize("ch,w", [(8, 256), (16, 128)])
+def test_grouped_wgrad_reads_x_margins(ch, w):
+    """Filter gradient with an input frame carrying D/H halo margins (as in a
+    D/H-partitioned layer): the grouped-voxel kernel must read the margin rows."""
+    rng = np.random.default_rng(4)
+    n, d, h = 1, 3, 4
+    full = rng.uniform(-1, 1, (n, ch, d + 2, h + 2, w)).astype(np.float32)
+    xf = Frame(n, ch, d, h, w, (1, 1, 0), zero=True)
+    xf.t.copy_(torch.from_numpy(full.transpose(0, 2, 3, 4, 1).copy()).cuda())
+    u = rng.uniform(-1, 1, (n, ch, d, h, w)).astype(np.float32)
+    uf = Frame(n, ch, d, h, w).load_ncdhw(u)
+    W = ws(ch, ch, 3, uf)
+    wg = torch.zeros((ch, ch, 3, 3, 3), device="cuda")
+    _lib.call("vpx_conv3d_bwd_filter", xf.ptr, xf.desc, uf.ptr, uf.desc, 3, 1, wg.data_ptr(), 0, W.data_ptr(),
+              W.numel() * 4, stream_ptr())
+    xpad = np.pad(full, ((0, 0), (0, 0), (0, 0), (0, 0), (1, 1)))
+    ref = O.k_conv3d_bwd_filter(xpad, u, (1, 1, 1), (3, 3, 3))
+    assert rel(wg.cpu().numpy(), ref) < TF32_RTOL
