@@ -99,6 +99,15 @@ int vpx_conv3d_bwd_filter(const float* x, const int* xfr, const float* u, const 
                           int stride, float* wg, int accumulate, void* ws, long long ws_bytes,
                           void* stream);
 
+/* The filter gradient of input channels [ci0, ci0 + xf.c) of a weight tensor
+ * (cout, cin_total, k, k, k): x is one operand of a channel concat (reference
+ * engine.py:432-438 concatenates the U-Net skip before the conv), so the conv
+ * after a concat can take its filter gradient from the concat's sources
+ * instead of the concatenated frame.  Only that slice of wg is written. */
+int vpx_conv3d_bwd_filter_cslice(const float* x, const int* xfr, const float* u, const int* ufr, int k,
+                                 int stride, float* wg, int ci0, int cin_total, int accumulate, void* ws,
+                                 long long ws_bytes, void* stream);
+
 /* First-layer fast path (Cin = 4, Cout = 16, the CosmoFlow c1 block):
  * vpx_pool_leaky_bwd_blocked fuses the 2^3 pool backward and the LeakyReLU
  * backward (y = LeakyReLU output = pool input) and writes the conv-output
@@ -132,6 +141,16 @@ int vpx_conv3d_bwd_filter_c4_pooled(const float* x, const int* xfr, const float*
  * packed weights (vpx_conv3d_workspace_bytes(4, 16, 3, .) suffices). */
 int vpx_conv3d_fwd_leaky_pool_c4(const float* x, const int* xfr, const float* w, float slope, float* pout,
                                  const int* pfr, uint16_t* mask, void* ws, long long ws_bytes, void* stream);
+/* The same fusion for every conv -> LeakyReLU -> average-pool block with an
+ * instance (Cin 4 -> 16 as above; 16 -> 32 and 16 -> 16 on the height-taps-in-N
+ * kernel, e.g. CosmoFlow c2): pooled output + sign mask (cout/8 bytes per
+ * voxel, [n][d][h][w]).  TF32 mode, 0 < slope <= 1, even D/H, W % 128 == 0. */
+int vpx_conv3d_fwd_leaky_pool(const float* x, const int* xfr, const float* w, float slope, float* pout,
+                              const int* pfr, void* mask, void* ws, long long ws_bytes, void* stream);
+/* Average-pool + LeakyReLU backward from that mask (reference
+ * layers/reference.py:170-173 then :234-236): g = leaky'(mask) * up / 8. */
+int vpx_pool_leaky_bwd_mask(const void* mask, const int* mfr, const float* up, const int* upfr, float* g,
+                            const int* gfr, float slope, void* stream);
 /* Its backward: the c1 filter gradient from the pooled gradient and the sign
  * mask (mfr = {n, 16, d, h, w, 0, 0, 0} describes the mask's voxel grid). */
 int vpx_conv3d_bwd_filter_c4_pooled_mask(const float* x, const int* xfr, const uint16_t* mask, const int* mfr,

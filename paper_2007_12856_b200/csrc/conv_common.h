@@ -27,6 +27,23 @@ struct ConvRowParams {
   int rnd;                                   // 1: round stores to nearest TF32
 };
 
+// Fused conv -> LeakyReLU -> 2^3 average pool on the height-taps-in-N kernel
+// (conv_rowh.cu, conv_rowh_pool_kernel): pooled output + per-voxel sign mask.
+struct RowhPoolParams {
+  int n, d, h, w;            // conv output (= input interior) extents
+  int nxseg, rb, nbands, zpairs, num_tasks;
+  int in_off_d, in_off_h, in_off_w;
+  const float* wpack;        // rowh B layout (rowh_pack mode 0)
+  float slope;               // 0 < slope <= 1
+  float* pout;               // pooled frame storage
+  long long p_sn, p_sd, p_sh, p_sw;
+  int p_off_d, p_off_h, p_off_w;
+  int rnd;
+  uint8_t* mask;             // [n][d][h][w] x cout/8 bytes, bit co = stored activation >= 0
+};
+int rowh_pool_instance(int cin, int cout);
+int launch_rowh_pool_any(const CUtensorMap& xmap, const RowhPoolParams& p, int cin, int cout, cudaStream_t st);
+
 int num_sms();
 int rowwin_config(int cin, int cout, int* R, int* CG);
 struct Frame;

@@ -348,9 +348,12 @@ static int conv_bwd_data_impl(const float* u, const int* ufr, const float* w, in
   return vpx::conv_bwd_data_simt(u, uf, w, k, stride, xg, gf, st);
 }
 
-extern "C" int vpx_conv3d_bwd_filter(const float* x, const int* xfr, const float* u,
-                                     const int* ufr, int k, int stride, float* wg, int accumulate,
-                                     void* ws, long long ws_bytes, void* stream) {
+// Filter gradient; cin_total > 0 selects slice mode: x holds input channels
+// [ci0, ci0 + xf.c) of a weight tensor with cin_total input channels and only
+// that slice of wg is written (a conv whose input is a channel concat).
+static int conv_bwd_filter_impl(const float* x, const int* xfr, const float* u, const int* ufr, int k, int stride,
+                                float* wg, int accumulate, int ci0, int cin_total, void* ws, long long ws_bytes,
+                                void* stream) {
   if (int rc = vpx::check_frame(xfr, "conv bwd_filter input")) return rc;
   if (int rc = vpx::check_frame(ufr, "conv bwd_filter upstream")) return rc;
   Frame xf = vpx::to_frame(xfr), uf = vpx::to_frame(ufr);
@@ -358,35 +361,57 @@ extern "C" int vpx_conv3d_bwd_filter(const float* x, const int* xfr, const float
   if (uf.n != xf.n || uf.d != (xf.d + stride - 1) / stride || uf.h != (xf.h + stride - 1) / stride ||
       uf.w != (xf.w + stride - 1) / stride)
     VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "conv bwd_filter: upstream does not match input extents");
+  const bool slice = cin_total > 0;
+  if (slice && (ci0 < 0 || ci0 + xf.c > cin_total))
+    VPX_FAIL(VPX_ERR_OUT_OF_BOUNDS, "conv bwd_filter: channel slice [%d, %d) outside %d", ci0, ci0 + xf.c, cin_total);
   long long need = vpx_conv3d_workspace_bytes(xf.c, uf.c, k, ufr);
   if (ws_bytes < need) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "workspace too small (%lld < %lld)", ws_bytes, need);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   float* part = reinterpret_cast<float*>(static_cast<char*>(ws) +
                                          ((vpx::packed_floats(xf.c, uf.c) * 4 + 255) / 256) * 256);
+  const int k3 = k * k * k;
+  const long long len = (long long)uf.c * xf.c * k3;
+  auto finish = [&](int P) {
+    if (!slice) return vpx::reduce_partials(part, P, len, wg, accumulate, st);
+    return vpx::reduce_partials_slice(part, P, len, xf.c * k3, (long long)cin_total * k3, (long long)ci0 * k3, wg,
+                                      accumulate, st);
+  };
   if (k == 3 && stride == 1 && vpx::c1_direct_supported(xf, uf)) {
     // 4 -> 16 channels: u in TMEM, x as dense 8-voxel rows (conv_c1bwd.cu, SRC 2)
     if (int rc = vpx::conv_wgrad_c1_pooled(x, xf, u, uf, u, uf, 0.f, part, st, nullptr, true)) return rc;
-    return vpx::reduce_partials(part, vpx::c1_pooled_parts(uf), (long long)uf.c * xf.c * 27, wg, accumulate, st);
+    return finish(vpx::c1_pooled_parts(uf));
   }
   if (k == 3 && vpx::wgrad_ut_supported(xf, uf, stride) && !getenv("VPX_NO_WGRAD_UT")) {
     if (int rc = vpx::conv_wgrad_ut(x, xf, u, uf, part, st)) return rc;
-    return vpx::reduce_partials(part, vpx::wgrad_ut_parts(uf), (long long)uf.c * xf.c * 27, wg, accumulate, st);
+    return finish(vpx::wgrad_ut_parts(uf));
   }
   if (vpx::precision() == 0 && k == 3 && vpx::wgrad_g_supported(xf, uf, stride) && !getenv("VPX_NO_WGRAD_G")) {
     if (int rc = vpx::conv_wgrad_g(x, xf, u, uf, part, st)) return rc;
-    return vpx::reduce_partials(part, vpx::wgrad_g_parts(uf), (long long)uf.c * xf.c * 27, wg, accumulate, st);
+    return finish(vpx::wgrad_g_parts(uf));
   }
   if (vpx::precision() == 0 && k == 3 && vpx::wgrad_tc_supported(xf, uf, stride)) {
     if (int rc = vpx::conv_wgrad_tc(x, xf, u, uf, stride, part, st)) return rc;
-    return vpx::reduce_partials(part, vpx::wgrad_tc_parts(xf, uf), (long long)uf.c * xf.c * 27, wg,
-                                accumulate, st);
+    return finish(vpx::wgrad_tc_parts(xf, uf));
   }
   if (vpx::small_conv_supported(2, xf, uf, k, stride) && !getenv("VPX_NO_SMALL")) {
     if (int rc = vpx::small_conv_wgrad(x, xf, u, uf, k, part, st)) return rc;
-    return vpx::reduce_partials(part, vpx::small_wgrad_parts(uf, k), (long long)uf.c * xf.c * k * k * k, wg,
-                                accumulate, st);
+    return finish(vpx::small_wgrad_parts(uf, k));
   }
+  if (slice) VPX_FAIL(VPX_ERR_UNSUPPORTED, "conv bwd_filter: channel slices need a partial-sum kernel");
   return vpx::conv_wgrad_simt(x, xf, u, uf, k, stride, wg, accumulate, part, st);
+}
+
+extern "C" int vpx_conv3d_bwd_filter(const float* x, const int* xfr, const float* u,
+                                     const int* ufr, int k, int stride, float* wg, int accumulate,
+                                     void* ws, long long ws_bytes, void* stream) {
+  return conv_bwd_filter_impl(x, xfr, u, ufr, k, stride, wg, accumulate, 0, 0, ws, ws_bytes, stream);
+}
+
+extern "C" int vpx_conv3d_bwd_filter_cslice(const float* x, const int* xfr, const float* u, const int* ufr, int k,
+                                            int stride, float* wg, int ci0, int cin_total, int accumulate,
+                                            void* ws, long long ws_bytes, void* stream) {
+  if (cin_total < 1) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "cin_total %d", cin_total);
+  return conv_bwd_filter_impl(x, xfr, u, ufr, k, stride, wg, accumulate, ci0, cin_total, ws, ws_bytes, stream);
 }
 
 extern "C" int vpx_conv3d_bwd_data(const float* u, const int* ufr, const float* w, int k, int stride, float* xg,
@@ -423,6 +448,70 @@ extern "C" int vpx_conv3d_fwd_leaky_pool_c4(const float* x, const int* xfr, cons
   return vpx::conv_c1_fwd_pool(x, xf, wpack, slope, pout, pf, mask, st);
 }
 
+// conv(k3 s1) -> LeakyReLU -> 2^3 average pool in one kernel for any layer
+// with a fused instance: Cin 4 -> 16 (conv_c1fwd.cu) or the height-taps-in-N
+// instances (conv_rowh.cu: 16 -> 32, 16 -> 16).  mask: cout/8 bytes per voxel.
+extern "C" int vpx_conv3d_fwd_leaky_pool(const float* x, const int* xfr, const float* w, float slope, float* pout,
+                                         const int* pfr, void* mask, void* ws, long long ws_bytes, void* stream) {
+  if (int rc = vpx::check_frame(xfr, "fused conv+pool input")) return rc;
+  if (int rc = vpx::check_frame(pfr, "fused conv+pool output")) return rc;
+  Frame xf = vpx::to_frame(xfr), pf = vpx::to_frame(pfr);
+  const int cin = xf.c, cout = pf.c;
+  if (cin == 4 && cout == 16)
+    return vpx_conv3d_fwd_leaky_pool_c4(x, xfr, w, slope, pout, pfr, static_cast<uint16_t*>(mask), ws, ws_bytes,
+                                        stream);
+  if (vpx::precision() != 0 || !vpx::rowh_pool_instance(cin, cout))
+    VPX_FAIL(VPX_ERR_UNSUPPORTED, "fused conv+pool: %d -> %d channels / mode", cin, cout);
+  if (xf.w % 128 || xf.d % 2 || xf.h % 2 || xf.mw || pf.n != xf.n || pf.d * 2 != xf.d || pf.h * 2 != xf.h ||
+      pf.w * 2 != xf.w)
+    VPX_FAIL(VPX_ERR_UNSUPPORTED, "fused conv+pool: extents");
+  if (!(slope > 0.f && slope <= 1.f)) VPX_FAIL(VPX_ERR_UNSUPPORTED, "fused conv+pool: slope must be in (0, 1]");
+  if (ws_bytes < vpx::rowh_packed_bytes(cin, cout)) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "workspace too small");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  float* wpack = static_cast<float*>(ws);
+  if (int rc = vpx::rowh_pack(w, cout, cin, 0, wpack, st)) return rc;
+  CUtensorMap map;
+  {
+    const uint64_t Wf = xf.w + 2 * xf.mw, Hf = xf.h + 2 * xf.mh, Df = xf.d + 2 * xf.md;
+    uint64_t dims[5] = {(uint64_t)cin, Wf, Hf, Df, (uint64_t)xf.n};
+    uint64_t strides[4] = {(uint64_t)cin * 4, Wf * cin * 4, Hf * Wf * cin * 4, Df * Hf * Wf * cin * 4};
+    uint32_t box[5] = {(uint32_t)cin, 130, 1, 3, 1};
+    const CUtensorMapSwizzle sw = cin == 32   ? CU_TENSOR_MAP_SWIZZLE_128B
+                                  : cin == 16 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                              : CU_TENSOR_MAP_SWIZZLE_32B;
+    if (int rc = vpx::encode_tiled(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float*>(x), dims, strides,
+                                   box, sw))
+      return rc;
+  }
+  vpx::RowhPoolParams p{};
+  p.n = xf.n;
+  p.d = xf.d;
+  p.h = xf.h;
+  p.w = xf.w;
+  p.nxseg = xf.w / 128;
+  p.rb = 16 < xf.h ? 16 : xf.h;
+  p.nbands = (xf.h + p.rb - 1) / p.rb;
+  p.zpairs = xf.d / 2;
+  p.num_tasks = xf.n * p.zpairs * p.nbands * p.nxseg;
+  p.in_off_d = xf.md;
+  p.in_off_h = xf.mh;
+  p.in_off_w = xf.mw;
+  p.wpack = wpack;
+  p.slope = slope;
+  p.pout = pout;
+  const long long Wf = pf.w + 2 * pf.mw, Hf = pf.h + 2 * pf.mh, Df = pf.d + 2 * pf.md;
+  p.p_sw = pf.c;
+  p.p_sh = Wf * pf.c;
+  p.p_sd = Hf * Wf * pf.c;
+  p.p_sn = Df * Hf * Wf * pf.c;
+  p.p_off_d = pf.md;
+  p.p_off_h = pf.mh;
+  p.p_off_w = pf.mw;
+  p.rnd = pf.rnd;
+  p.mask = static_cast<uint8_t*>(mask);
+  return vpx::launch_rowh_pool_any(map, p, cin, cout, st);
+}
+
 extern "C" int vpx_conv3d_bwd_filter_c4_pooled_mask(const float* x, const int* xfr, const uint16_t* mask,
                                                     const int* mfr, const float* up, const int* upfr, float slope,
                                                     float* wg, int accumulate, void* ws, long long ws_bytes,
@@ -446,6 +535,19 @@ extern "C" int vpx_pool_leaky_bwd(const float* y, const int* yfr, const float* u
       gf.d != yf.d || gf.h != yf.h || gf.w != yf.w || gf.n != yf.n || uf.n != yf.n)
     VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "pool/leaky backward: extents");
   return vpx::pool_leaky_bwd(y, yf, up, uf, g, gf, slope, is_max, static_cast<cudaStream_t>(stream));
+}
+
+// Same backward (average pool only) from the fused forward's sign mask
+// (mfr = {n, C, d, h, w, 0, 0, 0}: the mask's voxel grid, C/8 bytes per voxel).
+extern "C" int vpx_pool_leaky_bwd_mask(const void* mask, const int* mfr, const float* up, const int* upfr, float* g,
+                                       const int* gfr, float slope, void* stream) {
+  Frame mf = vpx::to_frame(mfr), uf = vpx::to_frame(upfr), gf = vpx::to_frame(gfr);
+  if (mf.md || mf.mh || mf.mw || uf.c != mf.c || gf.c != mf.c || uf.d * 2 != mf.d || uf.h * 2 != mf.h ||
+      uf.w * 2 != mf.w || gf.d != mf.d || gf.h != mf.h || gf.w != mf.w || gf.n != mf.n || uf.n != mf.n)
+    VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "pool/leaky backward (mask): extents");
+  if (mf.c != 8 && mf.c != 16 && mf.c != 32) VPX_FAIL(VPX_ERR_UNSUPPORTED, "mask of %d channels", mf.c);
+  return vpx::pool_leaky_bwd_mask(static_cast<const uint8_t*>(mask), up, uf, g, gf, slope,
+                                  static_cast<cudaStream_t>(stream));
 }
 
 extern "C" int vpx_conv3d_bwd_filter_c4(const float* x, const int* xfr, const float* ub, const int* ufr,

@@ -322,6 +322,277 @@ __global__ void pack_rowh_kernel(const float* __restrict__ w, int cout, int cin,
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// conv -> LeakyReLU -> 2^3 average pool fused into the height-taps-in-N
+// kernel (the conv_c1fwd.cu scheme for wider layers, e.g. CosmoFlow c2):
+// a task is (sample, depth pair, band of RB rows, 128-voxel segment); depth z0
+// leaves its row-and-width pooled partials in shared memory, depth z0+1
+// finishes them in vpx_pool_fwd's exact summation order.  Only the pooled
+// output and a sign mask (cout bits per voxel) reach HBM.  The 8 epilogue
+// warps split the channels in two halves; each thread takes output rows in
+// pairs (y, y+1), so the pool's row sum and (via a lane shuffle) its width
+// sum stay in registers.  The E-block ring needs only 3 + 1 slots per row,
+// so it is sized 512 / N (5 for N = 96, not a power of two).
+template <int CIN, int C>
+struct RowhPoolCfg {
+  using K = RowH<CIN, C>;
+  static constexpr int NB = 512 / K::N > 8 ? 8 : 512 / K::N;
+  static constexpr int RBAND = 16;
+  static constexpr int CH = C / 2;                         // channels per epilogue warp set
+  static constexpr int PBUF = RBAND / 2 * 64 * C * 4;
+  static constexpr int S0 = (226 * 1024 - 2048 - K::WBYTES - PBUF) / K::STAGE;
+  static constexpr int S = S0 > 8 ? 8 : S0;
+  static constexpr int SMEM = (K::WBYTES + 1023) / 1024 * 1024 + S * K::STAGE + PBUF + 1024;
+  static_assert(!K::PAIR && (CH == 8 || CH == 16), "channel split");
+};
+
+template <int CIN, int C>
+__global__ void __launch_bounds__(384, 1)
+    conv_rowh_pool_kernel(const __grid_constant__ CUtensorMap xmap, const vpx::RowhPoolParams p) {
+  using K = RowH<CIN, C>;
+  using Q = RowhPoolCfg<CIN, C>;
+  constexpr int N = K::N, S = Q::S, NB = Q::NB, CH = Q::CH;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sw = smem;
+  uint8_t* sa = smem + (K::WBYTES + 1023) / 1024 * 1024;
+  float* pbuf = reinterpret_cast<float*>(sa + S * K::STAGE);
+  __shared__ __align__(8) uint64_t full[S], empty[S], bfull[NB], bempty[NB], wbar;
+  __shared__ uint32_t tmem_base;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      vpx::mbar_init(&full[s], 1);
+      vpx::mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < NB; ++s) {
+      vpx::mbar_init(&bfull[s], 1);
+      vpx::mbar_init(&bempty[s], 256);
+    }
+    vpx::mbar_init(&wbar, 1);
+    vpx::fence_barrier_init();
+    vpx::tma_prefetch_desc(&xmap);
+  }
+  if (warp == 2) vpx::tmem_alloc<512>(&tmem_base);
+  vpx::tc_fence_before();
+  __syncthreads();
+  vpx::tc_fence_after();
+  const uint32_t tbase = tmem_base;
+
+  auto decode = [&](int task, int& n, int& z0, int& x0, int& y0, int& rows) {
+    int t = task;
+    const int xs = t % p.nxseg;
+    t /= p.nxseg;
+    const int band = t % p.nbands;
+    t /= p.nbands;
+    z0 = 2 * (t % p.zpairs);
+    n = t / p.zpairs;
+    x0 = xs * 128;
+    y0 = band * p.rb;
+    rows = min(p.rb, p.h - y0);
+  };
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    if (vpx::elect_one()) {
+      vpx::mbar_arrive_expect_tx(&wbar, K::WBYTES);
+      vpx::bulk_g2s(sw, p.wpack, K::WBYTES, &wbar);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int task = blockIdx.x; task < p.num_tasks; task += gridDim.x) {
+        int n, z0, x0, y0, rows;
+        decode(task, n, z0, x0, y0, rows);
+        for (int pz = 0; pz < 2; ++pz)
+          for (int j = 0; j < rows + 2; ++j) {
+            vpx::mbar_wait_sleep(&empty[stage], phase ^ 1, 20);
+            vpx::mbar_arrive_expect_tx(&full[stage], 3 * kWinH * CIN * 4);
+            vpx::tma_load_5d(sa + stage * K::STAGE, &xmap, &full[stage], 0, x0 - 1 + p.in_off_w,
+                             y0 - 1 + j + p.in_off_h, z0 + pz - 1 + p.in_off_d, n);
+            if (++stage == S) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------------- MMA
+    constexpr uint32_t idesc = vpx::make_idesc(2, 128, N, false, false);
+    if (vpx::elect_one()) {
+      vpx::mbar_wait(&wbar, 0);
+      const uint32_t wb = vpx::smem_u32(sw);
+      const uint32_t ab0 = vpx::smem_u32(sa);
+      int stage = 0;
+      uint32_t phase = 0;
+      uint32_t gr = 0;
+      for (int task = blockIdx.x; task < p.num_tasks; task += gridDim.x) {
+        int n, z0, x0, y0, rows;
+        decode(task, n, z0, x0, y0, rows);
+        for (int pz = 0; pz < 2; ++pz)
+          for (int j = 0; j < rows + 2; ++j, ++gr) {
+            const uint32_t slot = gr % NB;
+            vpx::mbar_wait_sleep(&bempty[slot], ((gr / NB) & 1) ^ 1, 20);
+            vpx::mbar_wait(&full[stage], phase);
+            vpx::tc_fence_after();
+            const uint32_t d = tbase + slot * N;
+            const uint32_t ab = ab0 + stage * K::STAGE;
+#pragma unroll
+            for (int t = 0; t < 9; ++t) {
+#pragma unroll
+              for (int jp = 0; jp < CIN / 8; ++jp) {
+                const uint64_t adesc = vpx::make_sdesc(ab + ((t / 3) * kWinH + t % 3) * K::RB + jp * 32, 16,
+                                                       8 * K::RB, K::LAYOUT);
+                const uint64_t bdesc = vpx::make_sdesc(wb + (t * (CIN / 8) + jp) * K::BSTEP, N * 16, 128, 0);
+                vpx::umma_tf32(d, adesc, bdesc, idesc, (t | jp) != 0 ? 1u : 0u);
+              }
+            }
+            vpx::umma_commit(&empty[stage]);
+            vpx::umma_commit(&bfull[slot]);
+            if (++stage == S) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ epilogue
+    const int q = warp & 3;                // TMEM lane quarter: voxels 32q .. 32q+31
+    const int hset = (warp - 4) >> 2;      // channel half
+    const int ch0 = hset * CH;
+    const uint32_t lane_base = tbase + (static_cast<uint32_t>(q * 32) << 16) + ch0;
+    const float slope = p.slope;
+    const bool rnd = p.rnd != 0;
+    const bool even = (lane & 1) == 0;
+    constexpr int MB = C / 8;              // mask bytes per voxel
+    uint32_t gr = 0;
+    // output row g: sum of three E slices -> leaky -> TF32 -> sign bits
+    auto row = [&](uint32_t g, float (&v)[CH]) -> uint32_t {
+      uint32_t a0[CH], a1[CH], a2[CH];
+      if constexpr (CH == 16) {
+        vpx::tmem_ld16_nw(lane_base + (g % NB) * N, a0);
+        vpx::tmem_ld16_nw(lane_base + ((g + 1) % NB) * N + C, a1);
+        vpx::tmem_ld16_nw(lane_base + ((g + 2) % NB) * N + 2 * C, a2);
+      } else {
+        vpx::tmem_ld8_nw(lane_base + (g % NB) * N, a0);
+        vpx::tmem_ld8_nw(lane_base + ((g + 1) % NB) * N + C, a1);
+        vpx::tmem_ld8_nw(lane_base + ((g + 2) % NB) * N + 2 * C, a2);
+      }
+      vpx::tmem_ld_wait();
+      uint32_t bits = 0;
+#pragma unroll
+      for (int i = 0; i < CH; ++i) {
+        float s = (__uint_as_float(a0[i]) + __uint_as_float(a1[i])) + __uint_as_float(a2[i]);
+        s = fmaxf(s, slope * s);  // LeakyReLU, 0 < slope <= 1 (reference layers/reference.py:231-233)
+        if (rnd) s = vpx::tf32_rn(s);
+        v[i] = s;
+        bits |= (s >= 0.f ? 1u : 0u) << i;
+      }
+      return bits;
+    };
+    auto wait_full = [&](uint32_t g) { vpx::mbar_wait(&bfull[g % NB], (g / NB) & 1); };
+    auto release = [&](uint32_t g) { vpx::mbar_arrive(&bempty[g % NB]); };
+    for (int task = blockIdx.x; task < p.num_tasks; task += gridDim.x) {
+      int n, z0, x0, y0, rows;
+      decode(task, n, z0, x0, y0, rows);
+      const int x = x0 + q * 32 + lane;
+      float* dst = p.pout + static_cast<long long>(n) * p.p_sn +
+                   static_cast<long long>((z0 >> 1) + p.p_off_d) * p.p_sd +
+                   static_cast<long long>((y0 >> 1) + p.p_off_h) * p.p_sh +
+                   static_cast<long long>((x >> 1) + p.p_off_w) * p.p_sw + ch0;
+      for (int pz = 0; pz < 2; ++pz) {
+        uint8_t* mrow = p.mask + ((((long long)n * p.d + z0 + pz) * p.h + y0) * p.w + x) * MB + hset * (CH / 8);
+        const long long mstep = static_cast<long long>(p.w) * MB;
+        float* pb = pbuf + ((q * 16 + (lane >> 1)) * C + ch0);
+        float* dp = dst;
+        for (int k = 0; k < rows; k += 2, mrow += 2 * mstep, pb += 64 * C, dp += p.p_sh) {
+          const uint32_t g = gr + k;
+          float v0[CH], v1[CH];
+          wait_full(g);
+          wait_full(g + 1);
+          wait_full(g + 2);
+          vpx::tc_fence_after();
+          const uint32_t b0 = row(g, v0);
+          vpx::tc_fence_before();
+          release(g);
+          wait_full(g + 3);
+          vpx::tc_fence_after();
+          const uint32_t b1 = row(g + 1, v1);
+          vpx::tc_fence_before();
+          release(g + 1);
+          if (k + 2 >= rows) {
+            release(g + 2);
+            release(g + 3);
+          }
+          if constexpr (CH == 16) {
+            *reinterpret_cast<uint16_t*>(mrow) = static_cast<uint16_t>(b0);
+            *reinterpret_cast<uint16_t*>(mrow + mstep) = static_cast<uint16_t>(b1);
+          } else {
+            mrow[0] = static_cast<uint8_t>(b0);
+            mrow[mstep] = static_cast<uint8_t>(b1);
+          }
+          // vpx_pool_fwd order: (z,y,x) (z,y,x+1) (z,y+1,x) (z,y+1,x+1), then z+1
+          float n0[CH], n1[CH];
+#pragma unroll
+          for (int i = 0; i < CH; ++i) {
+            n0[i] = __shfl_down_sync(0xffffffffu, v0[i], 1);
+            n1[i] = __shfl_down_sync(0xffffffffu, v1[i], 1);
+          }
+          if (even) {
+            float4* pb4 = reinterpret_cast<float4*>(pb);
+            if (pz == 0) {
+#pragma unroll
+              for (int i = 0; i < CH / 4; ++i)
+                pb4[i] = make_float4(((v0[4 * i] + n0[4 * i]) + v1[4 * i]) + n1[4 * i],
+                                     ((v0[4 * i + 1] + n0[4 * i + 1]) + v1[4 * i + 1]) + n1[4 * i + 1],
+                                     ((v0[4 * i + 2] + n0[4 * i + 2]) + v1[4 * i + 2]) + n1[4 * i + 2],
+                                     ((v0[4 * i + 3] + n0[4 * i + 3]) + v1[4 * i + 3]) + n1[4 * i + 3]);
+            } else {
+#pragma unroll
+              for (int i = 0; i < CH / 4; ++i) {
+                const float4 part = pb4[i];
+                const float pv[4] = {part.x, part.y, part.z, part.w};
+                float fin[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                  float t = pv[j];
+                  t = t + v0[4 * i + j];
+                  t = t + n0[4 * i + j];
+                  t = t + v1[4 * i + j];
+                  t = t + n1[4 * i + j];
+                  t = t / 8.0f;
+                  fin[j] = rnd ? vpx::tf32_rn(t) : t;
+                }
+                reinterpret_cast<float4*>(dp)[i] = make_float4(fin[0], fin[1], fin[2], fin[3]);
+              }
+            }
+          }
+        }
+        gr += rows + 2;
+      }
+    }
+  }
+  vpx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) vpx::tmem_dealloc<512>(tbase);
+}
+
+template <int CIN, int C>
+int launch_rowh_pool(const CUtensorMap& xmap, const vpx::RowhPoolParams& p, cudaStream_t st) {
+  using Q = RowhPoolCfg<CIN, C>;
+  static_assert(Q::S >= 3, "stages");
+  static_assert(Q::SMEM <= 227 * 1024, "smem");
+  auto kern = conv_rowh_pool_kernel<CIN, C>;
+  VPX_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Q::SMEM));
+  const int grid = p.num_tasks < vpx::num_sms() ? p.num_tasks : vpx::num_sms();
+  if (grid <= 0) return VPX_OK;
+  kern<<<grid, 384, Q::SMEM, st>>>(xmap, p);
+  VPX_LAUNCH_CHECK();
+  return VPX_OK;
+}
 }  // namespace
 
 namespace vpx {
@@ -359,6 +630,14 @@ int launch_rowh_any(const CUtensorMap& xmap, const ConvRowParams& p, int cin, in
   if (cin == 16 && cout == 8) return launch_rowh<16, 8>(xmap, p, st);
   if (cin == 32 && cout == 8) return launch_rowh<32, 8>(xmap, p, st);
   VPX_FAIL(VPX_ERR_UNSUPPORTED, "rowh conv: no instance for cin=%d cout=%d", cin, cout);
+}
+
+int rowh_pool_instance(int cin, int cout) { return (cin == 16 && cout == 32) || (cin == 16 && cout == 16); }
+
+int launch_rowh_pool_any(const CUtensorMap& xmap, const RowhPoolParams& p, int cin, int cout, cudaStream_t st) {
+  if (cin == 16 && cout == 32) return launch_rowh_pool<16, 32>(xmap, p, st);
+  if (cin == 16 && cout == 16) return launch_rowh_pool<16, 16>(xmap, p, st);
+  VPX_FAIL(VPX_ERR_UNSUPPORTED, "fused conv+pool: no instance for cin=%d cout=%d", cin, cout);
 }
 
 }  // namespace vpx

@@ -190,6 +190,20 @@ __global__ void reduce_partials_kernel(const float* __restrict__ part, int P, lo
   }
 }
 
+// Same, writing element (co, r) of the [cout][inner] sum to out[co * out_stride + out_off + r]:
+// the filter gradient of an input-channel slice of a larger weight tensor.
+__global__ void reduce_partials_slice_kernel(const float* __restrict__ part, int P, long long len, int inner,
+                                             long long out_stride, long long out_off, float* __restrict__ out,
+                                             int accumulate) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < len;
+       i += (long long)gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int p = 0; p < P; ++p) s += part[(long long)p * len + i];
+    float* o = out + (i / inner) * out_stride + out_off + i % inner;
+    *o = accumulate ? *o + s : s;
+  }
+}
+
 static int grid_for(long long total, int block) {
   long long g = (total + block - 1) / block;
   long long cap = (long long)num_sms() * 16;
@@ -227,6 +241,14 @@ long long wgrad_simt_parts(const Frame& uf) {
 int reduce_partials(const float* part, int P, long long len, float* out, int accumulate,
                     cudaStream_t st) {
   reduce_partials_kernel<<<grid_for(len, 256), 256, 0, st>>>(part, P, len, out, accumulate);
+  VPX_LAUNCH_CHECK();
+  return VPX_OK;
+}
+
+int reduce_partials_slice(const float* part, int P, long long len, int inner, long long out_stride,
+                          long long out_off, float* out, int accumulate, cudaStream_t st) {
+  reduce_partials_slice_kernel<<<grid_for(len, 256), 256, 0, st>>>(part, P, len, inner, out_stride, out_off, out,
+                                                                   accumulate);
   VPX_LAUNCH_CHECK();
   return VPX_OK;
 }

@@ -26,6 +26,8 @@ int conv_bwd_data_simt(const float* u, const Frame& uf, const float* w, int k, i
 long long wgrad_simt_parts(const Frame& uf);
 int reduce_partials(const float* part, int P, long long len, float* out, int accumulate,
                     cudaStream_t st);
+int reduce_partials_slice(const float* part, int P, long long len, int inner, long long out_stride,
+                          long long out_off, float* out, int accumulate, cudaStream_t st);
 int wgrad_tc_supported(const Frame& xf, const Frame& uf, int stride);
 int wgrad_tc_parts(const Frame& xf, const Frame& uf);
 int conv_wgrad_tc(const float* x, const Frame& xf, const float* u, const Frame& uf, int stride, float* part,

@@ -181,6 +181,81 @@ __global__ void bn_bwd_apply_v(const float* __restrict__ x, Frame xf, const floa
   }
 }
 
+// Margin-free frames: the interior is one contiguous NDHWC array, so the
+// pointwise kernels run a flat float4 loop with no index decode at all.  The
+// grid stride is a multiple of 256 float4s and C/4 divides 256, so a thread's
+// channel quad is fixed (per-channel constants live in registers).
+#define FLAT_LOOP(n4)                                                                       \
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (n4);          \
+       i += (long long)gridDim.x * blockDim.x)
+
+__global__ void leaky_fwd_flat(const float4* __restrict__ x, float4* __restrict__ y, long long n4, float s,
+                               Frame yf) {
+  FLAT_LOOP(n4) {
+    const float4 v = x[i];
+    y[i] = rnd4(yf, make_float4(lk(v.x, s), lk(v.y, s), lk(v.z, s), lk(v.w, s)));
+  }
+}
+__global__ void leaky_bwd_flat(const float4* __restrict__ x, const float4* __restrict__ u, float4* __restrict__ g,
+                               long long n4, float s, Frame gf) {
+  FLAT_LOOP(n4) {
+    const float4 a = x[i], b = u[i];
+    g[i] = rnd4(gf, make_float4(a.x >= 0.f ? b.x : s * b.x, a.y >= 0.f ? b.y : s * b.y,
+                                a.z >= 0.f ? b.z : s * b.z, a.w >= 0.f ? b.w : s * b.w));
+  }
+}
+__global__ void bn_apply_flat(const float4* __restrict__ x, const float* __restrict__ mean,
+                              const float* __restrict__ inv, const float* __restrict__ gamma,
+                              const float* __restrict__ beta, float4* __restrict__ y, long long n4, int C4,
+                              Frame yf) {
+  const int c = 4 * (threadIdx.x % C4);
+  float mu[4], iv[4], ga[4], be[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    mu[j] = mean[c + j];
+    iv[j] = inv[c + j];
+    ga[j] = gamma[c + j];
+    be[j] = beta[c + j];
+  }
+  FLAT_LOOP(n4) {
+    const float4 v = x[i];
+    const float r[4] = {v.x, v.y, v.z, v.w};
+    float o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) o[j] = ga[j] * ((r[j] - mu[j]) * iv[j]) + be[j];
+    y[i] = rnd4(yf, make_float4(o[0], o[1], o[2], o[3]));
+  }
+}
+__global__ void bn_bwd_apply_flat(const float4* __restrict__ x, const float4* __restrict__ u,
+                                  const float* __restrict__ mean, const float* __restrict__ inv,
+                                  const float* __restrict__ gamma, const float* __restrict__ sums, float inv_count,
+                                  float4* __restrict__ g, long long n4, int C4, Frame gf) {
+  const int C = 4 * C4, c = 4 * (threadIdx.x % C4);
+  float mu[4], iv[4], gi[4], s0[4], s1[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    mu[j] = mean[c + j];
+    iv[j] = inv[c + j];
+    gi[j] = gamma[c + j] * inv[c + j];
+    s0[j] = sums[c + j];
+    s1[j] = sums[C + c + j];
+  }
+  FLAT_LOOP(n4) {
+    const float4 a = x[i], b = u[i];
+    const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+    float r[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float xh = (av[j] - mu[j]) * iv[j];
+      r[j] = gi[j] * (bv[j] - (s0[j] + xh * s1[j]) * inv_count);
+    }
+    g[i] = rnd4(gf, make_float4(r[0], r[1], r[2], r[3]));
+  }
+}
+
+bool flat_ok(const Frame& f) { return f.md == 0 && f.mh == 0 && f.mw == 0 && f.c % 4 == 0 && 256 % (f.c / 4) == 0; }
+long long n4_of(const Frame& f) { return (long long)f.n * f.d * f.h * f.w * f.c / 4; }
+
 int grid_v(const Frame& f) {
   const long long total = (long long)f.n * f.d * f.h * f.w * f.c / 4;
   long long g = (total + 255) / 256;
@@ -197,12 +272,24 @@ int grid_rows(const Frame& f) {
 }  // namespace
 
 int leaky_fwd_vec(const float* x, const Frame& xf, float* y, const Frame& yf, float s, cudaStream_t st) {
+  if (flat_ok(xf) && flat_ok(yf)) {
+    leaky_fwd_flat<<<grid_v(xf), 256, 0, st>>>(reinterpret_cast<const float4*>(x), reinterpret_cast<float4*>(y),
+                                                n4_of(xf), s, yf);
+    VPX_LAUNCH_CHECK();
+    return VPX_OK;
+  }
   leaky_fwd_v<<<grid_rows(xf), 256, 0, st>>>(x, xf, y, yf, s);
   VPX_LAUNCH_CHECK();
   return VPX_OK;
 }
 int leaky_bwd_vec(const float* x, const Frame& xf, const float* u, const Frame& uf, float* g, const Frame& gf,
                   float s, cudaStream_t st) {
+  if (flat_ok(xf) && flat_ok(uf) && flat_ok(gf)) {
+    leaky_bwd_flat<<<grid_v(xf), 256, 0, st>>>(reinterpret_cast<const float4*>(x), reinterpret_cast<const float4*>(u),
+                                                reinterpret_cast<float4*>(g), n4_of(xf), s, gf);
+    VPX_LAUNCH_CHECK();
+    return VPX_OK;
+  }
   leaky_bwd_v<<<grid_rows(xf), 256, 0, st>>>(x, xf, u, uf, g, gf, s);
   VPX_LAUNCH_CHECK();
   return VPX_OK;
@@ -220,6 +307,12 @@ int pool_bwd_vec(const float* x, const Frame& xf, const float* u, const Frame& u
 }
 int bn_apply_vec(const float* x, const Frame& xf, const float* mean, const float* inv, const float* gamma,
                  const float* beta, float* y, const Frame& yf, cudaStream_t st) {
+  if (flat_ok(xf) && flat_ok(yf)) {
+    bn_apply_flat<<<grid_v(xf), 256, 0, st>>>(reinterpret_cast<const float4*>(x), mean, inv, gamma, beta,
+                                               reinterpret_cast<float4*>(y), n4_of(xf), xf.c / 4, yf);
+    VPX_LAUNCH_CHECK();
+    return VPX_OK;
+  }
   bn_apply_v<<<grid_rows(xf), 256, 0, st>>>(x, xf, mean, inv, gamma, beta, y, yf);
   VPX_LAUNCH_CHECK();
   return VPX_OK;
@@ -227,6 +320,13 @@ int bn_apply_vec(const float* x, const Frame& xf, const float* mean, const float
 int bn_bwd_apply_vec(const float* x, const Frame& xf, const float* u, const Frame& uf, const float* mean,
                      const float* inv, const float* gamma, const float* sums, float inv_count, float* g,
                      const Frame& gf, cudaStream_t st) {
+  if (flat_ok(xf) && flat_ok(uf) && flat_ok(gf)) {
+    bn_bwd_apply_flat<<<grid_v(xf), 256, 0, st>>>(reinterpret_cast<const float4*>(x),
+                                                   reinterpret_cast<const float4*>(u), mean, inv, gamma, sums,
+                                                   inv_count, reinterpret_cast<float4*>(g), n4_of(xf), xf.c / 4, gf);
+    VPX_LAUNCH_CHECK();
+    return VPX_OK;
+  }
   bn_bwd_apply_v<<<grid_rows(xf), 256, 0, st>>>(x, xf, u, uf, mean, inv, gamma, sums, inv_count, g, gf);
   VPX_LAUNCH_CHECK();
   return VPX_OK;
@@ -334,6 +434,42 @@ __global__ void pool_leaky_bwd_v(const float* __restrict__ y, Frame yf, const fl
     }
   }
 }
+// Average-pool + LeakyReLU backward from the forward's sign mask (the fused
+// conv+pool forward never stores the activation): g = (bit ? 1 : s) * up / 8,
+// the same operations in the same order as pool_leaky_bwd_v.  mask: MB bytes
+// per voxel, [n][d][h][w], no margins.
+template <int MB>
+__global__ void pool_leaky_bwd_mask_v(const uint8_t* __restrict__ mask, const float* __restrict__ up, Frame uf,
+                                      float* __restrict__ g, Frame gf, float s) {
+  const int C = uf.c;
+  const int Dm = 2 * uf.d, Hm = 2 * uf.h, Wm = 2 * uf.w;
+  ROW_LOOP(uf) {
+    const long long orow = i / per_row, off = i % per_row;
+    const int xo = static_cast<int>(off / (C / 4)), c4 = static_cast<int>(off % (C / 4));
+    long long t = orow;
+    const int yo = t % uf.h;
+    t /= uf.h;
+    const int zo = t % uf.d;
+    const int n = static_cast<int>(t / uf.d);
+    const float4 uv = ld4(up + row_base(uf, orow) + 4 * off);
+    const float4 avg = make_float4(uv.x / 8.0f, uv.y / 8.0f, uv.z / 8.0f, uv.w / 8.0f);
+#pragma unroll
+    for (int w8 = 0; w8 < 8; ++w8) {
+      const int a = w8 >> 2, b = (w8 >> 1) & 1, cc = w8 & 1;
+      const long long vox = (((long long)n * Dm + 2 * zo + a) * Hm + 2 * yo + b) * Wm + 2 * xo + cc;
+      uint32_t bits;
+      if constexpr (MB == 4) bits = reinterpret_cast<const uint32_t*>(mask)[vox];
+      else if constexpr (MB == 2) bits = reinterpret_cast<const uint16_t*>(mask)[vox];
+      else bits = mask[vox];
+      bits >>= 4 * c4;
+      const float4 gg = make_float4((bits & 1u) ? avg.x : s * avg.x, (bits & 2u) ? avg.y : s * avg.y,
+                                    (bits & 4u) ? avg.z : s * avg.z, (bits & 8u) ? avg.w : s * avg.w);
+      st4(gf, g + ((((long long)n * (gf.d + 2 * gf.md) + (2 * zo + a + gf.md)) * (gf.h + 2 * gf.mh) +
+                    (2 * yo + b + gf.mh)) * (gf.w + 2 * gf.mw) + (2 * xo + cc + gf.mw)) * C + 4 * c4,
+          gg);
+    }
+  }
+}
 }  // namespace
 
 // BatchNorm per-channel sums, float4 over channels and whole interior rows
@@ -343,7 +479,8 @@ __global__ void pool_leaky_bwd_v(const float* __restrict__ y, Frame yf, const fl
 // mode 0: (sum x, sum x^2); mode 1: (sum u, sum u*xhat), xhat = (x-mean)*inv.
 template <int MODE>
 __global__ void bn_sums_v(const float* __restrict__ x, Frame xf, const float* __restrict__ u, Frame uf,
-                          const float* __restrict__ mean, const float* __restrict__ inv, double* __restrict__ part) {
+                          const float* __restrict__ mean, const float* __restrict__ inv, double* __restrict__ part,
+                          int flat) {
   extern __shared__ double shd[];  // [8][blockDim.x]
   const int C = xf.c, C4 = C / 4;
   const int lanes = blockDim.x / C4, c4 = threadIdx.x % C4, lane = threadIdx.x / C4;
@@ -355,7 +492,29 @@ __global__ void bn_sums_v(const float* __restrict__ x, Frame xf, const float* __
     mu = ld4(mean + 4 * c4);
     iv = ld4(inv + 4 * c4);
   }
-  if (lane < lanes) {
+  if (flat) {
+    // contiguous interior: rows [r0, r1) are one float4 range; c4 = threadIdx.x % C4
+    const long long per_row4 = (long long)xf.w * C4;
+    const float4* xp = reinterpret_cast<const float4*>(x) + r0 * per_row4;
+    const float4* up = reinterpret_cast<const float4*>(u) + r0 * per_row4;
+    const long long n4 = (r1 - r0) * per_row4;
+#pragma unroll 4
+    for (long long i = threadIdx.x; i < n4; i += blockDim.x) {
+      const float4 a = xp[i];
+      if (MODE == 0) {
+        s1[0] += a.x; s1[1] += a.y; s1[2] += a.z; s1[3] += a.w;
+        s2[0] += (double)a.x * a.x; s2[1] += (double)a.y * a.y;
+        s2[2] += (double)a.z * a.z; s2[3] += (double)a.w * a.w;
+      } else {
+        const float4 b = up[i];
+        s1[0] += b.x; s1[1] += b.y; s1[2] += b.z; s1[3] += b.w;
+        s2[0] += (double)b.x * ((a.x - mu.x) * iv.x);
+        s2[1] += (double)b.y * ((a.y - mu.y) * iv.y);
+        s2[2] += (double)b.z * ((a.z - mu.z) * iv.z);
+        s2[3] += (double)b.w * ((a.w - mu.w) * iv.w);
+      }
+    }
+  } else if (lane < lanes) {
     for (long long row = r0; row < r1; ++row) {
       const float* xb = x + row_base(xf, row) + 4 * c4;
       const float* ub = MODE == 1 ? u + row_base(uf, row) + 4 * c4 : nullptr;
@@ -403,10 +562,11 @@ int bn_sums_vec(const float* x, const Frame& xf, const float* u, const Frame& uf
   const int C4 = xf.c / 4;
   if (xf.c % 4 || C4 > 256 || 256 % C4) return VPX_ERR_UNSUPPORTED;
   const size_t sh = 8 * 256 * sizeof(double);
+  const int flat = flat_ok(xf) && (mode == 0 || flat_ok(uf));
   if (mode == 0)
-    bn_sums_v<0><<<P, 256, sh, st>>>(x, xf, x, xf, mean, inv, part);
+    bn_sums_v<0><<<P, 256, sh, st>>>(x, xf, x, xf, mean, inv, part, flat);
   else
-    bn_sums_v<1><<<P, 256, sh, st>>>(x, xf, u, uf, mean, inv, part);
+    bn_sums_v<1><<<P, 256, sh, st>>>(x, xf, u, uf, mean, inv, part, flat);
   VPX_LAUNCH_CHECK();
   return VPX_OK;
 }
@@ -414,6 +574,18 @@ int bn_sums_vec(const float* x, const Frame& xf, const float* u, const Frame& uf
 int pool_leaky_bwd(const float* y, const Frame& yf, const float* up, const Frame& uf, float* g, const Frame& gf,
                    float s, int is_max, cudaStream_t st) {
   pool_leaky_bwd_v<<<grid_v(uf), 256, 0, st>>>(y, yf, up, uf, g, gf, s, is_max);
+  VPX_LAUNCH_CHECK();
+  return VPX_OK;
+}
+
+int pool_leaky_bwd_mask(const uint8_t* mask, const float* up, const Frame& uf, float* g, const Frame& gf, float s,
+                        cudaStream_t st) {
+  switch (uf.c / 8) {
+    case 1: pool_leaky_bwd_mask_v<1><<<grid_v(uf), 256, 0, st>>>(mask, up, uf, g, gf, s); break;
+    case 2: pool_leaky_bwd_mask_v<2><<<grid_v(uf), 256, 0, st>>>(mask, up, uf, g, gf, s); break;
+    case 4: pool_leaky_bwd_mask_v<4><<<grid_v(uf), 256, 0, st>>>(mask, up, uf, g, gf, s); break;
+    default: return VPX_ERR_UNSUPPORTED;
+  }
   VPX_LAUNCH_CHECK();
   return VPX_OK;
 }

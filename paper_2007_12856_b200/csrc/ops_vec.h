@@ -20,6 +20,8 @@ int bn_sums_vec(const float* x, const Frame& xf, const float* u, const Frame& uf
                 const float* inv, int mode, double* part, int P, cudaStream_t st);
 int pool_leaky_bwd(const float* y, const Frame& yf, const float* up, const Frame& uf, float* g, const Frame& gf,
                    float s, int is_max, cudaStream_t st);
+int pool_leaky_bwd_mask(const uint8_t* mask, const float* up, const Frame& uf, float* g, const Frame& gf, float s,
+                        cudaStream_t st);
 int pool_leaky_bwd_blocked(const float* y, const Frame& yf, const float* up, const Frame& uf, float* gb,
                            float s, int is_max, cudaStream_t st);
 int wgrad_c4_supported(const Frame& xf, const Frame& uf);

@@ -24,6 +24,7 @@ kernel over the flat parameter / moment buffers.
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass, field
 
 import torch
@@ -319,6 +320,10 @@ def _flatten(t: DistTensor):
     return t.to_ncdhw().reshape(t.n, -1)
 
 
+def _no_fused_pool() -> bool:
+    return os.environ.get("VPX_NO_FUSED_POOL", "") == "1"
+
+
 def forward(ctx: RankCtx, plan: Plan, state: RankState, batch: Batch, mode: str, seed: int = 0,
             trace: dict = None, scalars: "StepScalars" = None):
     net = plan.net
@@ -338,14 +343,17 @@ def forward(ctx: RankCtx, plan: Plan, state: RankState, batch: Batch, mode: str,
     for i, layer in enumerate(net.layers):
         if i < skip_to:
             continue
-        if (trace is None and cur is not None and layer.kind == "conv" and i == 0 and len(net.layers) > 3
+        if (trace is None and cur is not None and layer.kind == "conv" and i + 3 < len(net.layers)
                 and net.layers[i + 1].kind == "leaky" and net.layers[i + 2].kind == "pool"
                 and len({plan.placement[i], plan.placement[i + 1], plan.placement[i + 2]}) == 1
                 and plan.placement[i] != "flat" and plan.redist_idx not in (i, i + 1, i + 2)
                 and not any(getattr(l, "skip", None) in (layer.name, net.layers[i + 1].name)
                             for l in net.layers)
-                and D.first_block_fwd_supported(cur, layer.params, net.layers[i + 2].pool_kind,
-                                                net.layers[i + 1].slope)):
+                and (D.first_block_fwd_supported(cur, layer.params, net.layers[i + 2].pool_kind,
+                                                 net.layers[i + 1].slope) if i == 0 else
+                     D.block_fwd_pool_supported(cur, layer.params, net.layers[i + 2].pool_kind,
+                                                net.layers[i + 1].slope))
+                and not _no_fused_pool()):
             # conv -> leaky -> avg pool in one kernel: pooled output + sign mask
             pooled, mask = D.first_block_fwd(ctx, cur, P[f"{layer.name}.w"], layer.params,
                                              net.layers[i + 1].slope, plan.out_radii[i + 2], tag=layer.name)
@@ -417,7 +425,7 @@ def forward(ctx: RankCtx, plan: Plan, state: RankState, batch: Batch, mode: str,
             cur = D.dist_leaky_relu(cur, layer.slope, radii, tag=layer.name)
         elif layer.kind == "concat":
             skip = outputs[layer.skip]
-            stash.append((cur.c, skip.c))
+            stash.append((cur.c, skip.c, cur, skip))
             cur = D.dist_concat_channels(cur, skip, radii, tag=layer.name)
         elif layer.kind == "dropout":
             raise ShapeMismatch("spatial dropout is not part of either network")
@@ -516,8 +524,14 @@ def backward(ctx: RankCtx, plan: Plan, state: RankState, stash, dpred, trace: di
             continue
         in_meta = plan.in_meta[i]
         if layer.kind == "conv":
-            D.dist_conv3d_bwd_filter(ctx, kept, u, layer.params, reduce=False, out=G[f"{layer.name}.w"],
-                                     tag=layer.name)
+            srcs = None
+            if trace is None and i > 0 and net.layers[i - 1].kind == "concat":
+                srcs = D.concat_wgrad_sources(kept, stash[i - 1][2:], u, layer.params)
+            if srcs is not None:
+                D.dist_conv3d_bwd_filter_slices(ctx, srcs, u, layer.params, G[f"{layer.name}.w"], tag=layer.name)
+            else:
+                D.dist_conv3d_bwd_filter(ctx, kept, u, layer.params, reduce=False, out=G[f"{layer.name}.w"],
+                                         tag=layer.name)
             if i == 0 and trace is None:
                 u = None  # nothing consumes the network input's gradient
             else:
@@ -533,7 +547,7 @@ def backward(ctx: RankCtx, plan: Plan, state: RankState, stash, dpred, trace: di
         elif layer.kind == "leaky":
             u = D.dist_leaky_relu_bwd(kept, u, layer.slope, in_meta, tag=layer.name)
         elif layer.kind == "concat":
-            c_main, _ = kept
+            c_main = kept[0]
             main, sk = D.dist_concat_bwd(u, c_main, _meta_like(in_meta),
                                          _skip_meta(plan, layer), extra.get(layer.skip), tag=layer.name)
             extra[layer.skip] = sk

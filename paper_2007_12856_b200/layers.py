@@ -216,6 +216,41 @@ def dist_conv3d_bwd_filter(ctx: RankCtx, x: DistTensor, u: DistTensor, params, r
     return out
 
 
+def concat_wgrad_sources(x: DistTensor, sources, u: DistTensor, params):
+    """The (ci0, source) list for taking a conv's filter gradient from the
+    operands of the channel concat that produced its input x, or None.  Worth
+    it when each source's channel count equals the conv's Cout (the
+    grouped-voxel tcgen05 kernel then applies per source, while the concat as
+    a whole would not) and no frame carries halo margins (the sources' margins
+    are never exchanged)."""
+    if sources is None or _cubic(params.kernel) != 3 or _cubic(params.stride) != 1:
+        return None
+    if any(any(t.m) for t in (x, u) + tuple(sources)):
+        return None
+    if any(t.c != u.c for t in sources) or sum(t.c for t in sources) != x.c:
+        return None
+    out, c0 = [], 0
+    for t in sources:
+        out.append((c0, t))
+        c0 += t.c
+    return out
+
+
+def dist_conv3d_bwd_filter_slices(ctx: RankCtx, slices, u: DistTensor, params, out: torch.Tensor,
+                                  tag: str = "conv") -> torch.Tensor:
+    """Filter gradient of a conv whose input is a channel concat, one input
+    channel slice per concat source (vpx_conv3d_bwd_filter_cslice)."""
+    k, s = _cubic(params.kernel), _cubic(params.stride)
+    nvox = u.voxels()
+    with region(f"{tag}.wgrad", _conv_flops(params, nvox),
+                4 * (sum(t.t.numel() for _, t in slices) + nvox * u.c + out.numel())):
+        for ci0, t in slices:
+            ws = WS.get(_lib.load().vpx_conv3d_workspace_bytes(t.c, params.cout, k, u.desc))
+            _lib.call("vpx_conv3d_bwd_filter_cslice", t.ptr, t.desc, u.ptr, u.desc, k, s, out.data_ptr(), ci0,
+                      params.cin, 0, ws.data_ptr(), ws.numel() * 4, stream_ptr())
+    return out
+
+
 # ------------------------------------------------------------------- deconv
 
 def dist_deconv3d(ctx: RankCtx, x: DistTensor, w: torch.Tensor, out_radii=NO_HALO, tag: str = "deconv") -> DistTensor:
@@ -374,6 +409,13 @@ def dist_pool_leaky_bwd(y: DistTensor, u: DistTensor, slope: float, kind: str, i
     (reference layers/distributed.py:141-147 then :211-214); y is the LeakyReLU
     output, which is also the pool input."""
     g = DistTensor(in_meta, u.grid_rank, zero=False)
+    if isinstance(y, MaskFrame):  # the forward ran fused: signs from the mask (average pool)
+        if kind != "average":
+            raise ShapeMismatch("mask backward needs average pooling")
+        with region(f"{tag}.bwd", 0, 4 * (u.voxels() * u.c + y.voxels() * y.c) + y.voxels() * y.c // 8):
+            _lib.call("vpx_pool_leaky_bwd_mask", y.ptr, y.desc, u.ptr, u.desc, g.ptr, g.desc, float(slope),
+                      stream_ptr())
+        return g
     with region(f"{tag}.bwd", 0, 4 * (u.voxels() * u.c + 2 * y.voxels() * y.c)):
         _lib.call("vpx_pool_leaky_bwd", y.ptr, y.desc, u.ptr, u.desc, g.ptr, g.desc, float(slope),
                   int(kind == "max"), stream_ptr())
@@ -509,7 +551,8 @@ class MaskFrame:
 
     def __init__(self, n, c, d, h, w):
         self.n, self.c, self.d, self.h, self.w = n, c, d, h, w
-        self.t = torch.empty((n, d, h, w), dtype=torch.int16, device="cuda")
+        dt = {8: torch.int8, 16: torch.int16, 32: torch.int32}[c]  # c/8 bytes per voxel
+        self.t = torch.empty((n, d, h, w), dtype=dt, device="cuda")
         self._desc = frame_desc(n, c, d, h, w)
 
     @property
@@ -537,9 +580,26 @@ def first_block_fwd_supported(x: DistTensor, conv_params, pool_kind: str, slope:
     return x.m[2] == 0 and x.w in (128, 256, 512) and x.d % 2 == 0 and x.h % 2 == 0
 
 
+FUSED_POOL_BLOCKS = ((16, 32), (16, 16))  # conv_rowh.cu conv_rowh_pool_kernel instances
+
+
+def block_fwd_pool_supported(x: DistTensor, conv_params, pool_kind: str, slope: float) -> bool:
+    """conv(k3 s1) -> leaky -> average pool of a later block (not the first)
+    in one kernel: pooled output + sign mask; the backward reads the mask
+    (vpx_pool_leaky_bwd_mask) instead of the activation."""
+    if pool_kind != "average" or _lib.load().vpx_get_precision() != 0 or not 0.0 < slope <= 1.0:
+        return False
+    if (conv_params.cin, conv_params.cout) not in FUSED_POOL_BLOCKS:
+        return False
+    if tuple(conv_params.kernel) != (3, 3, 3) or tuple(conv_params.stride) != (1, 1, 1):
+        return False
+    return x.m[2] == 0 and x.w % 128 == 0 and x.d % 2 == 0 and x.h % 2 == 0
+
+
 def first_block_fwd(ctx: RankCtx, x: DistTensor, w: torch.Tensor, conv_params, slope: float, out_radii,
                     tag: str = "c1"):
-    """Pooled output + sign mask of conv -> leaky -> avg pool (conv_c1fwd.cu)."""
+    """Pooled output + sign mask of conv -> leaky -> avg pool in one kernel
+    (conv_c1fwd.cu for Cin 4 -> 16, conv_rowh.cu's pooled variant otherwise)."""
     halo_exchange(ctx, x)
     gs = x.meta.global_shape
     pooled = _out(x.meta, Shape5D(gs.n, conv_params.cout, gs.d // 2, gs.h // 2, gs.w // 2), out_radii,
@@ -550,7 +610,7 @@ def first_block_fwd(ctx: RankCtx, x: DistTensor, w: torch.Tensor, conv_params, s
     nvox = x.voxels()
     with region(f"{tag}.fwd", _conv_flops(conv_params, nvox),
                 4 * (x.voxels() * x.c + pooled.voxels() * pooled.c) + 2 * nvox):
-        _lib.call("vpx_conv3d_fwd_leaky_pool_c4", x.ptr, x.desc, w.data_ptr(), float(slope), pooled.ptr,
+        _lib.call("vpx_conv3d_fwd_leaky_pool", x.ptr, x.desc, w.data_ptr(), float(slope), pooled.ptr,
                   pooled.desc, mask.ptr, ws.data_ptr(), ws.numel() * 4, stream_ptr())
     return pooled, mask
 

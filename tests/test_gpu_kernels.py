@@ -12,7 +12,7 @@ import torch
 
 from oracle import serial as O
 from paper_2007_12856_b200 import _lib, prng
-from paper_2007_12856_b200.frames import Frame, stream_ptr
+from paper_2007_12856_b200.frames import Frame, frame_desc, stream_ptr
 
 pytestmark = pytest.mark.gpu
 
@@ -414,3 +414,71 @@ def test_grouped_wgrad_reads_x_margins(ch, w):
     xpad = np.pad(full, ((0, 0), (0, 0), (0, 0), (0, 0), (1, 1)))
     ref = O.k_conv3d_bwd_filter(xpad, u, (1, 1, 1), (3, 3, 3))
     assert rel(wg.cpu().numpy(), ref) < TF32_RTOL
+
+
+def test_filter_gradient_channel_slices_equal_concat():
+    """wgrad of a conv over a channel concat == the two slice gradients from the
+    concat's sources (vpx_conv3d_bwd_filter_cslice)."""
+    rng = np.random.default_rng(9)
+    n, d, h, w = 1, 3, 4, 128
+    a = rng.uniform(-1, 1, (n, 8, d, h, w)).astype(np.float32)
+    b = rng.uniform(-1, 1, (n, 8, d, h, w)).astype(np.float32)
+    u = rng.uniform(-1, 1, (n, 8, d, h, w)).astype(np.float32)
+    af, bf, uf = _frame_of(a), _frame_of(b), _frame_of(u)
+    cf = _frame_of(np.concatenate([a, b], axis=1))
+    W = ws(16, 8, 3, uf)
+    full = torch.zeros((8, 16, 3, 3, 3), device="cuda")
+    _lib.call("vpx_conv3d_bwd_filter", cf.ptr, cf.desc, uf.ptr, uf.desc, 3, 1, full.data_ptr(), 0, W.data_ptr(),
+              W.numel() * 4, stream_ptr())
+    sl = torch.full((8, 16, 3, 3, 3), 7.0, device="cuda")
+    for ci0, f in ((0, af), (8, bf)):
+        _lib.call("vpx_conv3d_bwd_filter_cslice", f.ptr, f.desc, uf.ptr, uf.desc, 3, 1, sl.data_ptr(), ci0, 16, 0,
+                  W.data_ptr(), W.numel() * 4, stream_ptr())
+    ref = O.conv3d_bwd_filter(np.concatenate([a, b], axis=1), u, (3, 3, 3), (1, 1, 1))
+    assert rel(full.cpu().numpy(), ref) < TF32_RTOL
+    assert rel(sl.cpu().numpy(), ref) < TF32_RTOL
+
+
+@pytest.mark.parametrize("cin,cout,shape,margins", [(16, 32, (1, 4, 6, 256), (0, 0, 0)),
+                                                    (16, 32, (2, 2, 20, 128), (1, 1, 0)),
+                                                    (16, 16, (1, 4, 4, 128), (1, 0, 0))])
+def test_fused_conv_leaky_pool_bit_exact(cin, cout, shape, margins):
+    """conv -> LeakyReLU -> avg pool in one kernel (conv_rowh.cu pooled variant)
+    == the unfused conv(+leaky) and pool kernels, bit for bit; the sign mask ==
+    (activation >= 0); the mask backward == the activation backward."""
+    n, d, h, w = shape
+    rng = np.random.default_rng(12)
+    md, mh, mw = margins
+    full = rng.uniform(-1, 1, (n, cin, d + 2 * md, h + 2 * mh, w)).astype(np.float32)
+    xf = Frame(n, cin, d, h, w, margins, zero=True)
+    xf.t.copy_(torch.from_numpy(full.transpose(0, 2, 3, 4, 1).copy()).cuda())
+    wt = torch.from_numpy((rng.uniform(-1, 1, (cout, cin, 3, 3, 3)) / 12).astype(np.float32)).cuda()
+    slope = 0.3
+    yf = Frame(n, cout, d, h, w)
+    W = ws(cin, cout, 3, yf)
+    _lib.call("vpx_conv3d_fwd_act", xf.ptr, xf.desc, wt.data_ptr(), 3, 1, yf.ptr, yf.desc, 1, slope, W.data_ptr(),
+              W.numel() * 4, stream_ptr())
+    pref = Frame(n, cout, d // 2, h // 2, w // 2)
+    _lib.call("vpx_pool_fwd", yf.ptr, yf.desc, pref.ptr, pref.desc, 0, stream_ptr())
+    pf = Frame(n, cout, d // 2, h // 2, w // 2)
+    dt = {16: torch.int16, 32: torch.int32}[cout]
+    mask = torch.zeros((n, d, h, w), dtype=dt, device="cuda")
+    _lib.call("vpx_conv3d_fwd_leaky_pool", xf.ptr, xf.desc, wt.data_ptr(), slope, pf.ptr, pf.desc,
+              mask.data_ptr(), W.data_ptr(), W.numel() * 4, stream_ptr())
+    torch.cuda.synchronize()
+    assert torch.equal(pf.t.view(torch.int32), pref.t.view(torch.int32))
+    y = yf.t  # (n, d, h, w, c)
+    bits = (y >= 0).to(torch.int64) << torch.arange(cout, device="cuda")
+    want = bits.sum(-1)
+    got = mask.to(torch.int64) & ((1 << cout) - 1)
+    assert torch.equal(got, want)
+    up = rng.uniform(-1, 1, (n, cout, d // 2, h // 2, w // 2)).astype(np.float32)
+    uf = Frame(n, cout, d // 2, h // 2, w // 2).load_ncdhw(up)
+    g1 = Frame(n, cout, d, h, w, (md, mh, 0), zero=True)
+    g2 = Frame(n, cout, d, h, w, (md, mh, 0), zero=True)
+    _lib.call("vpx_pool_leaky_bwd", yf.ptr, yf.desc, uf.ptr, uf.desc, g1.ptr, g1.desc, slope, 0, stream_ptr())
+    mdesc = frame_desc(n, cout, d, h, w)
+    _lib.call("vpx_pool_leaky_bwd_mask", mask.data_ptr(), ctypes.addressof(mdesc), uf.ptr, uf.desc, g2.ptr, g2.desc,
+              slope, stream_ptr())
+    torch.cuda.synchronize()
+    assert torch.equal(g1.t.view(torch.int32), g2.t.view(torch.int32))

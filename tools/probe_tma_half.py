@@ -21,7 +21,7 @@ for sw in (1282, 128, 32):
         strides = (ctypes.c_uint64 * 4)(32, C * 4, W * C * 4, W * C * 4)
         box = (ctypes.c_uint32 * 5)(8, 1, 32, 1, 1)
         coords = (ctypes.c_int32 * 5)(0, half, -1, 0, 0)
-        nbytes = 32 * 32 * 4 if sw != 128 else 32 * 128
+        nbytes = 32 * 32  # box bytes: 8 floats x 32 voxels
         out = torch.full((nbytes // 4,), -1.0, dtype=torch.float32, device="cuda")
         ok = torch.zeros(1, dtype=torch.int32, device="cuda")
         try:
@@ -34,5 +34,5 @@ for sw in (1282, 128, 32):
             continue
         o = out.cpu().numpy().reshape(-1, 4)  # 16-byte chunks
         print(f"sw={sw} half={half} ok={ok.item()}")
-        for row in range(min(len(o) // 8, 10)):
+        for row in range(len(o) // 8):
             print("  row", row, [f"{int(o[row * 8 + k][0])}" for k in range(8)])
