@@ -249,6 +249,11 @@ int vpx_xent(const float* logits, const int* lf, const long long* labels, double
 /* ----------------------------------------------------------------- layout -- */
 int vpx_layout_ncdhw_to_frame(const float* src, const int* ff, float* frame, void* stream);
 int vpx_layout_frame_to_ncdhw(const float* frame, const int* ff, float* dst, void* stream);
+/* Datastore ingest (reference datastore.py:429-444, HSB1 int16 storage):
+ * int16 NCDHW block -> fp32 frame interior (conversion fused into the layout
+ * change; TF32-rounded in TF32 mode), and int16 label slab -> int64 class ids. */
+int vpx_layout_ncdhw_i16_to_frame(const int16_t* src, const int* ff, float* frame, void* stream);
+int vpx_convert_i16_to_i64(const int16_t* src, long long n, long long* dst, void* stream);
 
 /* ---------------------------------------------------------------- probes --
  * Test-only entry points used to pin UMMA/TMA semantics on the device. */

@@ -531,6 +531,37 @@ __global__ void ncdhw_to_frame_kernel(const float* __restrict__ src, Frame f, fl
     fr[fr_off(f, n, z, y, x) + c] = rnd(f, src[i]);
   }
 }
+// int16 NCDHW (the HSB1 storage dtype, reference datastore.py:10-19) -> fp32
+// frame interior: the datastore's conversion to the training dtype
+// (reference datastore.py:429-444) fused into the layout change.  Blocks
+// stride over (n, z, y) rows, threads over x; each channel plane is read
+// coalesced, the voxel's channels are written together.
+__global__ void ncdhw_i16_to_frame_kernel(const int16_t* __restrict__ src, Frame f, float* __restrict__ fr) {
+  const long long nrows = (long long)f.n * f.d * f.h;
+  const long long plane = (long long)f.d * f.h * f.w;
+  for (long long row = blockIdx.x; row < nrows; row += gridDim.x) {
+    const int y = static_cast<int>(row % f.h);
+    const long long t = row / f.h;
+    const int z = static_cast<int>(t % f.d);
+    const int n = static_cast<int>(t / f.d);
+    const int16_t* s = src + (((long long)n * f.c * f.d + z) * f.h + y) * f.w;
+    float* dst = fr + fr_off(f, n, z, y, 0);
+    for (int x = threadIdx.x; x < f.w; x += blockDim.x) {
+      if (f.c % 4 == 0) {
+        for (int c = 0; c < f.c; c += 4) {
+          const float4 v = make_float4(s[c * plane + x], s[(c + 1) * plane + x], s[(c + 2) * plane + x],
+                                       s[(c + 3) * plane + x]);
+          *reinterpret_cast<float4*>(dst + (long long)x * f.c + c) = rnd4(f, v);
+        }
+      } else {
+        for (int c = 0; c < f.c; ++c) dst[(long long)x * f.c + c] = rnd(f, static_cast<float>(s[c * plane + x]));
+      }
+    }
+  }
+}
+__global__ void i16_to_i64_kernel(const int16_t* __restrict__ src, long long n, long long* __restrict__ dst) {
+  GRID_STRIDE(i, n) dst[i] = src[i];
+}
 __global__ void frame_to_ncdhw_kernel(const float* __restrict__ fr, Frame f, float* __restrict__ dst) {
   const long long total = vox_count(f) * f.c;
   GRID_STRIDE(i, total) {
@@ -761,6 +792,18 @@ extern "C" int vpx_xent(const float* logits, const int* lf, const long long* lab
 extern "C" int vpx_layout_ncdhw_to_frame(const float* src, const int* ff, float* fr, void* st) {
   Frame f = F(ff);
   ncdhw_to_frame_kernel<<<grid1d(VC(f) * f.c), 256, 0, S(st)>>>(src, f, fr);
+  LAUNCH_TAIL;
+}
+extern "C" int vpx_layout_ncdhw_i16_to_frame(const int16_t* src, const int* ff, float* fr, void* st) {
+  Frame f = F(ff);
+  const long long rows = (long long)f.n * f.d * f.h;
+  const long long cap = (long long)num_sms() * 16;
+  ncdhw_i16_to_frame_kernel<<<static_cast<int>(rows < cap ? rows : cap), 256, 0, S(st)>>>(src, f, fr);
+  LAUNCH_TAIL;
+}
+extern "C" int vpx_convert_i16_to_i64(const int16_t* src, long long n, long long* dst, void* st) {
+  if (n <= 0) return VPX_OK;
+  i16_to_i64_kernel<<<grid1d(n), 256, 0, S(st)>>>(src, n, dst);
   LAUNCH_TAIL;
 }
 extern "C" int vpx_layout_frame_to_ncdhw(const float* fr, const int* ff, float* dst, void* st) {

@@ -47,3 +47,27 @@ class Unsupported(VoxparError):
 
 class DeviceError(VoxparError):
     """A CUDA runtime/driver or NCCL call failed."""
+
+
+class IoError(VoxparError):
+    """Sample file / manifest could not be read or is malformed."""
+
+
+class BadMagic(IoError):
+    """HSB1 magic mismatch."""
+
+
+class BadVersion(IoError):
+    """Unsupported HSB1 version."""
+
+
+class CacheNotEmpty(VoxparError):
+    """ingest_epoch0 on an already populated cache."""
+
+
+class MissingSample(VoxparError):
+    """A scheduled sample has no owner / cached slab."""
+
+
+class BadBatch(VoxparError):
+    """Batch / group / dataset sizes that cannot form a schedule."""

@@ -73,3 +73,40 @@ def keep_mask_device(key, n: int, keep: float):
     _lib.call("vpx_prng_mask", resolve(key), n, float(keep), out.data_ptr(),
               torch.cuda.current_stream().cuda_stream)
     return out
+
+
+# ----------------------------------------------------------- host (numpy)
+# Vectorised host streams for schedule- and fixture-sized draws (epoch
+# permutations, HSB1 fixture voxels); identical bits to the device streams.
+
+def u64(key, n: int):
+    """First n raw 64-bit words of the stream (reference prng.py:54-62)."""
+    import numpy as np
+
+    k = np.uint64(resolve(key))
+    z = k + (np.arange(n, dtype=np.uint64) + np.uint64(1)) * np.uint64(GOLDEN)
+    z = (z ^ (z >> np.uint64(30))) * np.uint64(M1)
+    z = (z ^ (z >> np.uint64(27))) * np.uint64(M2)
+    return z ^ (z >> np.uint64(31))
+
+
+def randint(key, n: int, lo: int, hi: int):
+    """Integers in [lo, hi), modulo-mapped (reference prng.py:75-78)."""
+    import numpy as np
+
+    return (u64(key, n) % np.uint64(hi - lo)).astype(np.int64) + lo
+
+
+def permutation(key, size: int):
+    """Fisher-Yates shuffle of arange(size), j = stream[i] mod (i+1)
+    (reference prng.py:81-90)."""
+    import numpy as np
+
+    perm = np.arange(size, dtype=np.int64)
+    if size < 2:
+        return perm
+    draws = u64(key, size)
+    for i in range(size - 1, 0, -1):
+        j = int(draws[i] % np.uint64(i + 1))
+        perm[i], perm[j] = perm[j], perm[i]
+    return perm
