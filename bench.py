@@ -352,9 +352,10 @@ def run_ours(args):
         p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         p0.record(stream)
         for _ in range(nprof):
-            eager_step()
+            loss = eager_step()
         p1.record(stream)
         torch.cuda.synchronize()
+    losses = {"eager_profiled": float(loss.item())}
     launches_per_step = (lib.vpx_launch_count() - launches0) / nprof
     ms_eager = p0.elapsed_time(p1)
     ctx.barrier()
@@ -371,6 +372,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         ctx.barrier()
     launches = int(round(launches_per_step * args.steps))
+    losses["timed"] = float(loss.item())
     ms = e0.elapsed_time(e1)
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -399,11 +401,20 @@ def run_ours(args):
         if pipe is not None:
             pipe.start(after=s0)
         loss_host = None
+        first_nan = None
         for i in range(args.steps):
             if pipe is not None:
                 pipe.load(batch, prefetch_next=i + 1 < args.steps)
             loss = step()
             loss_host = float(loss.item())  # D2H of the step's result
+            if first_nan is None and not math.isfinite(loss_host):
+                first_nan = i
+            if os.environ.get("VPX_BENCH_DEBUG") and i < 2:
+                fr = batch.x_block.t
+                print(f"[debug] {note[:12]} step {i}: loss {loss_host} x nan {int(torch.isnan(fr).sum())} "
+                      f"x absmax {float(fr.abs().max())} param nan {int(torch.isnan(state.params.flat).sum())} "
+                      f"grad nan {int(torch.isnan(state.params.grad).sum())} buf {[tuple(b.shape) for b in pipe._buf]} "
+                      f"{[float(b.float().abs().max()) for b in pipe._buf]}", file=sys.stderr, flush=True)
         s1.record(stream)
         torch.cuda.synchronize()
         ctx.barrier()
@@ -413,6 +424,7 @@ def run_ours(args):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return {"value": n_global * args.steps / (float(t[0]) * 1e-3), "unit": "samples/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8, "wall_ms": float(t[1]), "loss": loss_host,
+                "first_nonfinite_step": first_nan,
                 "input_path": note}
 
     e2e = e2e_fp32 = None
@@ -485,7 +497,9 @@ def run_ours(args):
         "flops_per_step": fl["executed"] / n_global * n_global,
         "conv_tflops_achieved": fl["executed"] / (ms_step * 1e-3) / 1e12,
         "kernels": breakdown,
-        "loss": float(loss.item()),
+        "loss": losses["timed"],
+        "loss_by_phase": dict(losses, e2e=(e2e or {}).get("loss"),
+                              e2e_fp32_host_input=(e2e_fp32 or {}).get("loss")),
     }
     print(json.dumps(line), flush=True)
 

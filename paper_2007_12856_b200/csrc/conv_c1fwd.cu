@@ -75,6 +75,15 @@ __global__ void __launch_bounds__(384, 1)
     vpx::tma_prefetch_desc(&xmap);
   }
   if (warp == 2) vpx::tmem_alloc<512>(&tmem_base);
+  // The last K step pairs tap (2,2) with a zero-weight phantom tap whose A rows
+  // start one voxel later: voxel 127 reads 16 bytes past the 130-voxel window,
+  // into the stage padding TMA never writes.  Zero it once so stale shared
+  // memory (possibly NaN bit patterns) cannot turn 0 * x into NaN.
+  for (int i = threadIdx.x; i < kS * (kPlane - 3 * kWin * 16) / 4; i += blockDim.x) {
+    constexpr int kPadWords = (kPlane - 3 * kWin * 16) / 4;
+    reinterpret_cast<uint32_t*>(sa + (i / kPadWords) * kPlane + 3 * kWin * 16)[i % kPadWords] = 0u;
+  }
+  vpx::fence_proxy_async_smem();
   vpx::tc_fence_before();
   __syncthreads();
   vpx::tc_fence_after();

@@ -89,6 +89,14 @@ __global__ void __launch_bounds__(384, 1)
     vpx::tma_prefetch_desc(&xmap);
   }
   if (warp == 2) vpx::tmem_alloc<K::TCOLS>(&tmem_base);
+  if constexpr (K::PAIR) {
+    // the (2,2) + phantom-tap K step reads 16 bytes past each 130-voxel plane
+    // (zero weights); keep that never-loaded padding finite (see conv_c1fwd.cu)
+    constexpr int kPadWords = (kPlane - 3 * kWinH * 16) / 4;
+    for (int i = threadIdx.x; i < S * K::NCH * kPadWords; i += blockDim.x)
+      reinterpret_cast<uint32_t*>(sa + (i / kPadWords) * kPlane + 3 * kWinH * 16)[i % kPadWords] = 0u;
+    vpx::fence_proxy_async_smem();
+  }
   vpx::tc_fence_before();
   __syncthreads();
   vpx::tc_fence_after();

@@ -185,6 +185,51 @@ def test_captured_step_equals_eager_steps(width):
     assert l0 == l1
 
 
+def _poison_free_memory():
+    """Fill every free cached block and most free device memory with NaN, then
+    hand it back to the allocator (exposes reads of never-written memory)."""
+    free, _ = torch.cuda.mem_get_info()
+    cached = torch.cuda.memory_reserved() - torch.cuda.memory_allocated()
+    junk = []
+    for nb in (cached, free - (2 << 30)):
+        if nb > (64 << 20):
+            try:
+                junk.append(torch.full((nb // 4 - (16 << 20),), float("nan"), device="cuda"))
+            except RuntimeError:
+                pass
+    torch.cuda.synchronize()
+    del junk
+    torch.cuda.empty_cache()
+
+
+def test_captured_step_independent_of_stale_memory():
+    """Regression: the Cin=4 first-block kernels pair tap (2,2) with a
+    zero-weight phantom tap that reads 16 bytes past each 130-voxel window, in
+    stage padding TMA never writes.  Stale NaN bit patterns there once turned
+    0*x into NaN in the last voxel of every 128-voxel segment.  Replays after
+    NaN-filling all free memory must match clean replays bit for bit."""
+    width = 128
+    net = build_cosmoflow(width)
+    ctx = RankCtx(0, 1)
+    plan = engine.make_plan(net, ProcessGrid(1, 1, 1, 1), 1, width)
+    x, y, ids = engine.synthetic_batch_full(net, width, 1, 0)
+    runs = []
+    for poisoned in (False, True):
+        state = engine.make_state(net, 0)
+        batch = engine.scatter_batch(plan, x, y, ids, 0)
+        cap = engine.CapturedStep(ctx, plan, state, batch, 1e-3, warmup=1)
+        if poisoned:
+            _poison_free_memory()
+        for _ in range(2):
+            loss = cap(1e-3)
+        torch.cuda.synchronize()
+        runs.append((state.params.flat.clone(), float(loss.item())))
+        del cap
+    (p0, l0), (p1, l1) = runs
+    assert np.isfinite(l1) and l0 == l1
+    assert torch.equal(p0, p1)
+
+
 def test_cosmoflow128_traces_vs_oracle():
     """Exercises the tcgen05 row-window (c1 W=128), tap-box (c2..c7, stride 2)
     and filter-gradient kernels inside the full step, n=1."""
