@@ -120,7 +120,8 @@ def test_first_block_fused_backward_and_c4_wgrad(shape, margins):
     assert rel(wg2.cpu().numpy(), wg.cpu().numpy()) < 1e-5  # same rounded operands, other summation order
 
 
-@pytest.mark.parametrize("shape,margins", [((1, 4, 6, 128), (0, 0, 0)), ((2, 2, 4, 256), (1, 1, 0))])
+@pytest.mark.parametrize("shape,margins", [((1, 4, 6, 128), (0, 0, 0)), ((2, 2, 4, 256), (1, 1, 0)),
+                                           ((1, 2, 34, 128), (0, 0, 0)), ((1, 2, 44, 256), (1, 1, 0))])
 def test_first_block_fused_forward_and_mask_backward(shape, margins):
     """conv(4->16)+leaky+avg-pool in one kernel (pooled output + sign mask)
     equals the unfused conv/pool kernels bit for bit, and the mask-driven
