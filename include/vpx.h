@@ -218,6 +218,23 @@ int vpx_peer_signal(unsigned long long* peer_flag, void* stream);
 int vpx_peer_wait(const unsigned long long* flag, unsigned long long* expected, long long timeout_ns, int* error,
                   void* stream);
 
+/* One halo round (one partitioned dim, both sides) in ONE kernel over the same
+ * mailboxes: pack each face straight into the neighbour's mailbox (peer
+ * stores), release it with a system-scope increment of the neighbour's flag
+ * once every block has packed, wait (acquire) for the neighbours' faces and
+ * unpack (mode 1) or accumulate (mode 2, adjoint round) them into the frame.
+ * Replaces pack + vpx_peer_signal + vpx_peer_wait + unpack per side; one
+ * dimension step of reference fabric.py:380-411 (forward) / :414-443
+ * (reverse).  `faces` = 2 x 32 int64 per face (side -1, side +1):
+ *   [0] send?  [1..8] send box {n0,z0,y0,x0,en,ez,ey,ex}  [9] peer mailbox
+ *   [10] peer flag  [11] recv?  [12..19] recv box  [20] local mailbox
+ *   [21] local flag  [22] local expected count  [23] (face 0 only) three u32
+ *   zero-initialised block counters for the round  [24] recv mode (1|2).
+ * Channels must be a multiple of 4.  A neighbour that never arrives within
+ * timeout_ns sets *error and traps. */
+int vpx_halo_round_peer(float* frame, const int* ff, const long long* faces, long long mailbox_bytes,
+                        long long timeout_ns, int* error, void* stream);
+
 /* ------------------------------------------------------------------- prng --
  * Pinned splitmix64 streams (reference prng.py:28-90), bit-exact with numpy:
  * value i = lo + (hi-lo) * ((mix(key + (i+1)*golden) >> 11) * 2^-53). */

@@ -39,6 +39,9 @@ from .timing import region
 # Profiling switch only (results are wrong with it): VPX_SKIP_HALO=1 skips the
 # halo exchanges to measure what they cost inside a step.
 _SKIP_HALO = os.environ.get("VPX_SKIP_HALO") == "1"
+# PeerHalo rounds as one fused kernel (vpx_halo_round_peer); VPX_HALO_SPLIT=1
+# selects the four-launch pack / signal / wait / unpack sequence per side.
+_FUSED_ROUND = os.environ.get("VPX_HALO_SPLIT") != "1"
 
 
 class RankCtx:
@@ -262,6 +265,36 @@ class PeerHalo:
         _lib.call("vpx_halo_copy", frame.ptr, frame.desc, _box_arg(_box8(frame, box)), dst, mode, st)
         _lib.call("vpx_peer_signal", self.peer_base[(dim, side)] + self.flags_off + 8 * ch, st)
 
+    def round(self, dim, sides, frame, send_boxes, recv_boxes, mode):
+        """One whole round (both sides of `dim`) in one kernel
+        (vpx_halo_round_peer): faces packed into the neighbours' mailboxes,
+        released, awaited and unpacked (mode 1) / accumulated (mode 2).  Same
+        mailboxes, flags and parities as send()/recv()."""
+        import ctypes
+
+        desc = [0] * 64
+        desc[23] = self.base + self.flags_off + 256  # three u32 block counters (zero at rest)
+        for side, sbox, rbox in zip(sides, send_boxes, recv_boxes):
+            d = 32 * ((side + 1) // 2)
+            ch_s = self._chan(dim, -side)
+            par_s = self._parity(("s", dim, side))
+            ch_r = self._chan(dim, side)
+            par_r = self._parity(("r", dim, side))
+            desc[d + 0] = 1
+            desc[d + 1:d + 9] = _box8(frame, sbox)
+            desc[d + 9] = self.peer_base[(dim, side)] + (2 * ch_s + par_s) * self.slab
+            desc[d + 10] = self.peer_base[(dim, side)] + self.flags_off + 8 * ch_s
+            desc[d + 11] = 1
+            desc[d + 12:d + 20] = _box8(frame, rbox)
+            desc[d + 20] = self.base + (2 * ch_r + par_r) * self.slab
+            desc[d + 21] = self.base + self.flags_off + 8 * ch_r
+            desc[d + 22] = self.base + self.flags_off + 64 + 8 * ch_r
+            desc[d + 24] = mode
+        arr = (ctypes.c_longlong * 64)(*desc)
+        st = torch.cuda.current_stream().cuda_stream
+        _lib.call("vpx_halo_round_peer", frame.ptr, frame.desc, ctypes.addressof(arr), self.slab, self.TIMEOUT_NS,
+                  self.base + self.flags_off + 128, st)
+
     def recv(self, dim, side, frame, box, mode):
         """Face from the neighbour on `side` (my channel (dim, side)) -> `box` of `frame`."""
         ch = self._chan(dim, side)
@@ -329,10 +362,14 @@ def halo_exchange(ctx: RankCtx, tensor, pack=_cuda_pack, unpack=_cuda_unpack):
         if peer is not None:
             sides = [s for s in (-1, 1) if meta.neighbor(gr, dim, s) is not None]
             with region("comm.p2p", 0, 0):
-                for side in sides:
-                    peer.send(dim, side, tensor, round_boxes(meta, gr, dim, side)[0], 0)
-                for side in sides:
-                    peer.recv(dim, side, tensor, round_boxes(meta, gr, dim, side)[1], 1)
+                if _FUSED_ROUND and tensor.c % 4 == 0:
+                    boxes = [round_boxes(meta, gr, dim, side) for side in sides]
+                    peer.round(dim, sides, tensor, [b[0] for b in boxes], [b[1] for b in boxes], 1)
+                else:
+                    for side in sides:
+                        peer.send(dim, side, tensor, round_boxes(meta, gr, dim, side)[0], 0)
+                    for side in sides:
+                        peer.recv(dim, side, tensor, round_boxes(meta, gr, dim, side)[1], 1)
             continue
         ops, unpacks = [], []
         for side in (-1, 1):
@@ -370,10 +407,14 @@ def reverse_halo_exchange(ctx: RankCtx, meta, grid_rank: int, frame, pack=_cuda_
         if peer is not None:
             sides = [s for s in (-1, 1) if meta.neighbor(grid_rank, dim, s) is not None]
             with region("comm.p2p", 0, 0):
-                for side in sides:
-                    peer.send(dim, side, frame, round_boxes(meta, grid_rank, dim, side)[1], 0)
-                for side in sides:
-                    peer.recv(dim, side, frame, round_boxes(meta, grid_rank, dim, side)[0], 2)
+                if _FUSED_ROUND and frame.c % 4 == 0:
+                    boxes = [round_boxes(meta, grid_rank, dim, side) for side in sides]
+                    peer.round(dim, sides, frame, [b[1] for b in boxes], [b[0] for b in boxes], 2)
+                else:
+                    for side in sides:
+                        peer.send(dim, side, frame, round_boxes(meta, grid_rank, dim, side)[1], 0)
+                    for side in sides:
+                        peer.recv(dim, side, frame, round_boxes(meta, grid_rank, dim, side)[0], 2)
             continue
         ops, unpacks = [], []
         for side in (-1, 1):
