@@ -71,3 +71,15 @@ class MissingSample(VoxparError):
 
 class BadBatch(VoxparError):
     """Batch / group / dataset sizes that cannot form a schedule."""
+
+
+class InsufficientData(VoxparError):
+    """Too few samples for a performance-model fit."""
+
+
+class DegenerateFit(VoxparError):
+    """A performance-model fit has no spread in its inputs (or a negative slope)."""
+
+
+class NoComparableEntry(VoxparError):
+    """The kernel-time table has no row of the requested kind/phase."""
