@@ -328,6 +328,65 @@ def test_halo_copy_round_trip():
     assert torch.equal(t.t[1:2, 0:4, 1:4, 2:7, :], 2 * before[1:2, 0:4, 1:4, 2:7, :])
 
 
+@pytest.mark.parametrize("dims,margins,c", [((2, 6, 5, 7), (1, 0, 0), 8), ((1, 4, 300, 9), (0, 1, 0), 16)])
+def test_halo_round_peer_loopback(dims, margins, c):
+    """vpx_halo_round_peer on one GPU wired as a ring of one: face -1 sends
+    into mailbox A (read by face +1), face +1 into mailbox B (read by face -1),
+    so the margins receive the opposite boundary slabs (a periodic wrap).
+    Checks the pack/unpack boxes, the accumulate mode, and that the block
+    counters and expected-arrival counts come back consistent across calls."""
+    n, d, h, w = dims
+    t = Frame(n, c, d, h, w, margins, zero=True)
+    interior = torch.randn((n, d, h, w, c), device="cuda")
+    t.interior.copy_(interior)
+    dim = margins.index(1)
+    ext = [d + 2 * margins[0], h + 2 * margins[1], w + 2 * margins[2]]
+    slab = n * c * ext[0] * ext[1] * ext[2]
+    mail = torch.zeros(2 * slab, device="cuda")
+    flags = torch.zeros(64, dtype=torch.int64, device="cuda")  # 0,1 flags; 8,9 expected; 16.. counters; 32 error
+    base = flags.data_ptr()
+
+    def box(lo, size):
+        b = [0, 0, 0, 0, n, ext[0], ext[1], ext[2]]
+        b[1 + dim], b[5 + dim] = lo, size
+        return b
+
+    e = ext[dim]
+    # side -1: send the first interior slab, receive into the low margin
+    # side +1: send the last interior slab, receive into the high margin
+    faces = [(box(1, 1), box(0, 1)), (box(e - 2, 1), box(e - 1, 1))]
+
+    def run(mode):
+        desc = [0] * 64
+        desc[23] = base + 16 * 8
+        for s, (sb, rb) in enumerate(faces):
+            o = 32 * s
+            desc[o + 0], desc[o + 11], desc[o + 24] = 1, 1, mode
+            desc[o + 1:o + 9], desc[o + 12:o + 20] = sb, rb
+            desc[o + 9] = mail.data_ptr() + 4 * slab * s          # face s writes mailbox s
+            desc[o + 10] = base + 8 * s
+            desc[o + 20] = mail.data_ptr() + 4 * slab * (1 - s)   # and reads the other one
+            desc[o + 21] = base + 8 * (1 - s)
+            desc[o + 22] = base + 8 * (8 + s)
+        arr = (ctypes.c_longlong * 64)(*desc)
+        _lib.call("vpx_halo_round_peer", t.ptr, t.desc, ctypes.addressof(arr), 4 * slab, 5_000_000_000,
+                  base + 32 * 8, stream_ptr())
+        torch.cuda.synchronize()
+
+    def sl(lo):
+        idx = [slice(None)] * 5
+        idx[1 + dim] = slice(lo, lo + 1)
+        return tuple(idx)
+
+    run(1)
+    assert torch.equal(t.t[sl(0)], t.t[sl(e - 2)]) and torch.equal(t.t[sl(e - 1)], t.t[sl(1)])
+    run(2)  # accumulate: the margins now hold twice the opposite slab
+    assert torch.equal(t.t[sl(0)], 2 * t.t[sl(e - 2)]) and torch.equal(t.t[sl(e - 1)], 2 * t.t[sl(1)])
+    f = flags.cpu()
+    assert f[0] == f[1] == 2 and f[8] == f[9] == 2  # two arrivals per face, both consumed
+    assert int(f[16]) == 0 and int(f[17]) == 0 and int(f[32]) == 0  # block counters back at rest, no error
+
+
 @pytest.mark.parametrize("cin,cout,spatial", [(16, 8, (3, 4, 40)), (32, 16, (2, 3, 64)), (32, 8, (2, 2, 33))])
 def test_deconv_vectorised_vs_oracle(cin, cout, spatial, fp32_mode):
     """Transposed conv fwd / dgrad / wgrad on the float4 row kernels (ops_unet.cu),
