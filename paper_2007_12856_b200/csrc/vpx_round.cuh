@@ -8,10 +8,11 @@
 #include "conv_simt.h"
 
 namespace vpx {
+// Same result as cvt.rna.tf32.f32 (nearest, ties away from zero) for every
+// non-NaN input, including the carry into the exponent and overflow to inf,
+// in two integer instructions instead of cvt's finite-check sequence.
 __device__ __forceinline__ float tf32_rn(float v) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v));
-  return __uint_as_float(r);
+  return __uint_as_float((__float_as_uint(v) + 0x1000u) & 0xffffe000u);
 }
 __device__ __forceinline__ float rnd(const Frame& f, float v) { return f.rnd ? tf32_rn(v) : v; }
 __device__ __forceinline__ float4 rnd4(const Frame& f, float4 v) {

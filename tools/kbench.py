@@ -59,6 +59,12 @@ def run(case):
         fn = lambda: _lib.call("vpx_conv3d_bwd_data", u.ptr, u.desc, w.data_ptr(), 3, s, g.ptr, g.desc,
                                ws.data_ptr(), ws.numel() * 4, st)
         nbytes = 4 * (u.t.numel() + g.t.numel())
+    elif kind == "pool":  # the fused first block: conv + leaky + avg pool + sign mask
+        pf = Frame(1, cout, O // 2, O // 2, O // 2)
+        mask = torch.empty((1, O, O, O), dtype=torch.int16, device="cuda")
+        fn = lambda: _lib.call("vpx_conv3d_fwd_leaky_pool_c4", x.ptr, x.desc, w.data_ptr(), 0.3, pf.ptr, pf.desc,
+                               mask.data_ptr(), ws.data_ptr(), ws.numel() * 4, st)
+        nbytes = 4 * (x.t.numel() + pf.t.numel()) + 2 * mask.numel()
     elif kind == "wgrad" and layer == "c1":
         up = Frame(1, cout, O // 2, O // 2, O // 2)
         up.t.uniform_(-1, 1)
