@@ -55,6 +55,8 @@ struct C1Params {
 constexpr int kNA = 48;          // N per tap (x chunks k, k+1: 64 > 48 used columns)
 constexpr int kACol = 9 * kNA;   // first A column (432)
 constexpr int kASlots = 8;       // A ring: 8 slots x 8 columns
+constexpr int kProdGroups = 4;   // u producer warps per TMEM lane quarter (power of 2)
+constexpr int kProdWarps = 4 * kProdGroups;
 
 // SRC: 0 = u from the LeakyReLU output y and the pooled gradient, 1 = from the
 // sign mask and the pooled gradient, 2 = u itself (any conv 4 -> 16 whose
@@ -73,7 +75,7 @@ struct C1Cfg {
 };
 
 template <int W, int SRC>
-__global__ void __launch_bounds__(384, 1)
+__global__ void __launch_bounds__(128 + 32 * kProdWarps, 1)
     c1_pooled_wgrad_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap ymap,
                            const __grid_constant__ CUtensorMap upmap, const C1Params p) {
   using Cfg = C1Cfg<W, SRC>;
@@ -95,7 +97,7 @@ __global__ void __launch_bounds__(384, 1)
     for (int i = 0; i < 2; ++i) {
       vpx::mbar_init(&xfull[i], 1);
       vpx::mbar_init(&yfull[i], 1);
-      vpx::mbar_init(&yempty[i], 8);
+      vpx::mbar_init(&yempty[i], kProdWarps);
       vpx::mbar_init(&rowdone[i], 1);
     }
     for (int i = 0; i < kASlots; ++i) {
@@ -214,9 +216,11 @@ __global__ void __launch_bounds__(384, 1)
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------- u producers
-    // two producer warps per TMEM lane quarter (warps 4..7 and 8..11) take
-    // alternate K-step slots; each computes its next slot while the previous
-    // tcgen05.st drains
+    // kProdGroups producer warps per TMEM lane quarter (warps 4..7, 8..11, ...)
+    // take K-step slots round robin; each computes its next slot while the
+    // previous tcgen05.st drains.  The u math is latency-bound, so more warps
+    // in flight is what makes it keep up with the MMAs (2 -> 4 per quarter:
+    // c1 filter gradient 3.16 -> see DESIGN.md).
     const int q = warp & 3, h = (warp - 4) >> 2, m = q * 32 + lane, dd = m >> 4, co = m & 15;
     const uint32_t lane_addr = tbase + (static_cast<uint32_t>(q * 32) << 16) + kACol;
     const float slope = p.slope;
@@ -255,7 +259,7 @@ __global__ void __launch_bounds__(384, 1)
       vpx::mbar_wait_sleep(&yfull[i & 1], (i >> 1) & 1, 64);
       const uint32_t ya0 = vpx::smem_u32(ys + (i & 1) * Cfg::YB) + (MASK ? 0 : co * 4);
       const uint32_t ua0 = vpx::smem_u32(us + (i & 1) * Cfg::UB) + co * 4;
-      int s = ((i * KS) & 1) == h ? 0 : 1;  // first K-step of this row in my slot parity
+      int s = (h - i * KS) & (kProdGroups - 1);  // first K-step g = i KS + s of this row with g = h mod groups
       float v[8];
       if (s < KS) {
         if (p.dbg) {
@@ -266,11 +270,11 @@ __global__ void __launch_bounds__(384, 1)
         }
       }
 #pragma unroll 1
-      for (; s < KS; s += 2) {
+      for (; s < KS; s += kProdGroups) {
         const int g = i * KS + s, slot = g & (kASlots - 1);
         vpx::mbar_wait_sleep(&emptyA[slot], ((g >> 3) & 1) ^ 1);
         if (p.dbg != 2) vpx::tmem_st8(lane_addr + slot * 8, v);
-        if (s + 2 < KS && !p.dbg) make_u(s + 2, ya0, ua0, v);  // overlaps the store
+        if (s + kProdGroups < KS && !p.dbg) make_u(s + kProdGroups, ya0, ua0, v);  // overlaps the store
         if (p.dbg != 2) vpx::tmem_st_wait();
         vpx::tc_fence_before();
         __syncwarp();
@@ -339,7 +343,7 @@ int launch_c1(const CUtensorMap& xm, const CUtensorMap& ym, const CUtensorMap& u
   static_assert(smem <= 227 * 1024, "smem");
   auto kern = c1_pooled_wgrad_kernel<W, SRC>;
   VPX_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  kern<<<p.P, 384, smem, st>>>(xm, ym, um, p);
+  kern<<<p.P, 128 + 32 * kProdWarps, smem, st>>>(xm, ym, um, p);
   VPX_LAUNCH_CHECK();
   return VPX_OK;
 }

@@ -65,6 +65,16 @@ def run(case):
         fn = lambda: _lib.call("vpx_conv3d_fwd_leaky_pool_c4", x.ptr, x.desc, w.data_ptr(), 0.3, pf.ptr, pf.desc,
                                mask.data_ptr(), ws.data_ptr(), ws.numel() * 4, st)
         nbytes = 4 * (x.t.numel() + pf.t.numel()) + 2 * mask.numel()
+    elif kind == "wgm":  # the fused first-block backward: pooled gradient + sign mask -> filter gradient
+        up = Frame(1, cout, O // 2, O // 2, O // 2)
+        up.t.uniform_(-1, 1)
+        mask = torch.randint(-32768, 32767, (1, O, O, O), dtype=torch.int16, device="cuda")
+        wg = torch.empty_like(w)
+        mfr = frame_desc(1, cout, O, O, O)
+        fn = lambda: _lib.call("vpx_conv3d_bwd_filter_c4_pooled_mask", x.ptr, x.desc, mask.data_ptr(),
+                               ctypes.addressof(mfr), up.ptr, up.desc, 0.3, wg.data_ptr(), 0, ws.data_ptr(),
+                               ws.numel() * 4, st)
+        nbytes = 4 * (x.t.numel() + up.t.numel()) + 2 * mask.numel()
     elif kind == "wgrad" and layer == "c1":
         up = Frame(1, cout, O // 2, O // 2, O // 2)
         up.t.uniform_(-1, 1)
