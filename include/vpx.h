@@ -186,6 +186,11 @@ int vpx_bn_stats(const float* sums, int c, double count, float eps, float moment
                  float* inv, float* run_mean, float* run_var, void* stream);
 int vpx_bn_apply(const float* x, const int* xf, const float* mean, const float* inv,
                  const float* gamma, const float* beta, float* y, const int* yf, void* stream);
+/* BatchNorm apply + LeakyReLU in one pass (C % 4 == 0); same bits as
+ * vpx_bn_apply then vpx_leaky_fwd into frames with y's rounding (reference
+ * layers/reference.py:209-214 then :231-233). */
+int vpx_bn_apply_leaky(const float* x, const int* xf, const float* mean, const float* inv, const float* gamma,
+                       const float* beta, float slope, float* y, const int* yf, void* stream);
 int vpx_bn_bwd_apply(const float* x, const int* xf, const float* u, const int* uf, const float* mean,
                      const float* inv, const float* gamma, const float* sums, double count, float* g,
                      const int* gf, void* stream);

@@ -665,6 +665,13 @@ extern "C" int vpx_bn_apply(const float* x, const int* xf, const float* mean, co
   bn_apply_kernel<<<grid1d(VC(a) * a.c), 256, 0, S(st)>>>(x, a, mean, inv, gamma, beta, y, b);
   LAUNCH_TAIL;
 }
+extern "C" int vpx_bn_apply_leaky(const float* x, const int* xf, const float* mean, const float* inv,
+                                  const float* gamma, const float* beta, float slope, float* y, const int* yf,
+                                  void* st) {
+  Frame a = F(xf), b = F(yf);
+  if (a.c % 4) VPX_FAIL(VPX_ERR_UNSUPPORTED, "bn_apply_leaky needs C % 4 == 0");
+  return bn_apply_vec(x, a, mean, inv, gamma, beta, y, b, S(st), true, slope);
+}
 extern "C" int vpx_bn_bwd_apply(const float* x, const int* xf, const float* u, const int* uf,
                                 const float* mean, const float* inv, const float* gamma,
                                 const float* sums, double count, float* g, const int* gf, void* st) {

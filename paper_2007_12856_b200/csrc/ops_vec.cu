@@ -145,9 +145,13 @@ __global__ void pool_bwd_v(const float* __restrict__ x, Frame xf, const float* _
   }
 }
 
+// LEAKY: BatchNorm followed by LeakyReLU in one pass (the normalised value is
+// rounded as its own frame would store it, then activated and rounded again:
+// the same bits as bn_apply + leaky_fwd, without the intermediate tensor).
+template <bool LEAKY>
 __global__ void bn_apply_v(const float* __restrict__ x, Frame xf, const float* __restrict__ mean,
                            const float* __restrict__ inv, const float* __restrict__ gamma,
-                           const float* __restrict__ beta, float* __restrict__ y, Frame yf) {
+                           const float* __restrict__ beta, float* __restrict__ y, Frame yf, float s) {
   const int C = xf.c;
   ROWS2_LOOP(xf) {
     const int off = 4 * jj;
@@ -155,7 +159,13 @@ __global__ void bn_apply_v(const float* __restrict__ x, Frame xf, const float* _
     const float4 v = ld4(x + row_base(xf, row) + off);
     float r[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-    for (int j = 0; j < 4; ++j) r[j] = gamma[c + j] * ((r[j] - mean[c + j]) * inv[c + j]) + beta[c + j];
+    for (int j = 0; j < 4; ++j) {
+      r[j] = gamma[c + j] * ((r[j] - mean[c + j]) * inv[c + j]) + beta[c + j];
+      if (LEAKY) {
+        r[j] = rnd(yf, r[j]);
+        r[j] = r[j] >= 0.f ? r[j] : s * r[j];
+      }
+    }
     st4(yf, y + row_base(yf, row) + off, make_float4(r[0], r[1], r[2], r[3]));
   }
 }
@@ -204,10 +214,11 @@ __global__ void leaky_bwd_flat(const float4* __restrict__ x, const float4* __res
                                 a.z >= 0.f ? b.z : s * b.z, a.w >= 0.f ? b.w : s * b.w));
   }
 }
+template <bool LEAKY>
 __global__ void bn_apply_flat(const float4* __restrict__ x, const float* __restrict__ mean,
                               const float* __restrict__ inv, const float* __restrict__ gamma,
                               const float* __restrict__ beta, float4* __restrict__ y, long long n4, int C4,
-                              Frame yf) {
+                              Frame yf, float s) {
   const int c = 4 * (threadIdx.x % C4);
   float mu[4], iv[4], ga[4], be[4];
 #pragma unroll
@@ -222,7 +233,13 @@ __global__ void bn_apply_flat(const float4* __restrict__ x, const float* __restr
     const float r[4] = {v.x, v.y, v.z, v.w};
     float o[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) o[j] = ga[j] * ((r[j] - mu[j]) * iv[j]) + be[j];
+    for (int j = 0; j < 4; ++j) {
+      o[j] = ga[j] * ((r[j] - mu[j]) * iv[j]) + be[j];
+      if (LEAKY) {
+        o[j] = rnd(yf, o[j]);
+        o[j] = o[j] >= 0.f ? o[j] : s * o[j];
+      }
+    }
     y[i] = rnd4(yf, make_float4(o[0], o[1], o[2], o[3]));
   }
 }
@@ -306,14 +323,16 @@ int pool_bwd_vec(const float* x, const Frame& xf, const float* u, const Frame& u
   return VPX_OK;
 }
 int bn_apply_vec(const float* x, const Frame& xf, const float* mean, const float* inv, const float* gamma,
-                 const float* beta, float* y, const Frame& yf, cudaStream_t st) {
+                 const float* beta, float* y, const Frame& yf, cudaStream_t st, bool leaky, float slope) {
   if (flat_ok(xf) && flat_ok(yf)) {
-    bn_apply_flat<<<grid_v(xf), 256, 0, st>>>(reinterpret_cast<const float4*>(x), mean, inv, gamma, beta,
-                                               reinterpret_cast<float4*>(y), n4_of(xf), xf.c / 4, yf);
+    auto k = leaky ? bn_apply_flat<true> : bn_apply_flat<false>;
+    k<<<grid_v(xf), 256, 0, st>>>(reinterpret_cast<const float4*>(x), mean, inv, gamma, beta,
+                                  reinterpret_cast<float4*>(y), n4_of(xf), xf.c / 4, yf, slope);
     VPX_LAUNCH_CHECK();
     return VPX_OK;
   }
-  bn_apply_v<<<grid_rows(xf), 256, 0, st>>>(x, xf, mean, inv, gamma, beta, y, yf);
+  auto k = leaky ? bn_apply_v<true> : bn_apply_v<false>;
+  k<<<grid_rows(xf), 256, 0, st>>>(x, xf, mean, inv, gamma, beta, y, yf, slope);
   VPX_LAUNCH_CHECK();
   return VPX_OK;
 }

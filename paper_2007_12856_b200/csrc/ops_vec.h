@@ -12,7 +12,7 @@ int pool_fwd_vec(const float* x, const Frame& xf, float* y, const Frame& yf, int
 int pool_bwd_vec(const float* x, const Frame& xf, const float* u, const Frame& uf, float* g, const Frame& gf,
                  int is_max, cudaStream_t st);
 int bn_apply_vec(const float* x, const Frame& xf, const float* mean, const float* inv, const float* gamma,
-                 const float* beta, float* y, const Frame& yf, cudaStream_t st);
+                 const float* beta, float* y, const Frame& yf, cudaStream_t st, bool leaky = false, float slope = 0.f);
 int bn_bwd_apply_vec(const float* x, const Frame& xf, const float* u, const Frame& uf, const float* mean,
                      const float* inv, const float* gamma, const float* sums, float inv_count, float* g,
                      const Frame& gf, cudaStream_t st);

@@ -418,7 +418,12 @@ def forward(ctx: RankCtx, plan: Plan, state: RankState, batch: Batch, mode: str,
             stash.append(cur)
             cur = D.dist_pool3d(ctx, cur, layer.pool_kind, radii, tag=layer.name)
         elif layer.kind == "bn":
-            cur, cache = D.dist_batchnorm(ctx, cur, bn[layer.name], mode, radii, tag=layer.name)
+            nxt = net.layers[i + 1] if i + 1 < len(net.layers) else None
+            fused_act = (trace is None and nxt is not None and nxt.kind == "leaky" and cur.c % 4 == 0
+                         and plan.placement[i + 1] == plan.placement[i] and plan.redist_idx != i + 1)
+            cur, cache = D.dist_batchnorm(ctx, cur, bn[layer.name], mode,
+                                          plan.out_radii[i + 1] if fused_act else radii, tag=layer.name,
+                                          leaky_slope=nxt.slope if fused_act else None)
             stash.append(cache)
         elif layer.kind == "leaky":
             stash.append(cur)

@@ -335,10 +335,12 @@ def _bn_sums(x, u, mean, inv, mode):
 
 
 def dist_batchnorm(ctx: RankCtx, x: DistTensor, state: BNState, mode: str = "train",
-                   out_radii=NO_HALO, tag: str = "bn"):
+                   out_radii=NO_HALO, tag: str = "bn", leaky_slope: float = None):
     """Local (sum x, sum x^2) -> allreduce(2C) over the tensor's whole rank
     group -> normalise (reference layers/distributed.py:152-180).  Returns
-    (y, cache); the cache keeps x and the batch statistics (xhat is recomputed)."""
+    (y, cache); the cache keeps x and the batch statistics (xhat is recomputed).
+    With leaky_slope the following LeakyReLU runs in the same pass (y is then
+    the activation; its signs are the normalised values' signs)."""
     gs = x.meta.global_shape
     c = gs.c
     mean = torch.empty(c, dtype=torch.float32, device="cuda")
@@ -359,8 +361,12 @@ def dist_batchnorm(ctx: RankCtx, x: DistTensor, state: BNState, mode: str = "tra
         raise ShapeMismatch(f"unknown bn mode {mode!r}")
     y = _out(x.meta, gs, out_radii, x.grid_rank)
     with region(f"{tag}.fwd", 0, 8 * x.voxels() * c):
-        _lib.call("vpx_bn_apply", x.ptr, x.desc, mean.data_ptr(), inv.data_ptr(), state.gamma.data_ptr(),
-                  state.beta.data_ptr(), y.ptr, y.desc, stream_ptr())
+        if leaky_slope is not None:
+            _lib.call("vpx_bn_apply_leaky", x.ptr, x.desc, mean.data_ptr(), inv.data_ptr(), state.gamma.data_ptr(),
+                      state.beta.data_ptr(), float(leaky_slope), y.ptr, y.desc, stream_ptr())
+        else:
+            _lib.call("vpx_bn_apply", x.ptr, x.desc, mean.data_ptr(), inv.data_ptr(), state.gamma.data_ptr(),
+                      state.beta.data_ptr(), y.ptr, y.desc, stream_ptr())
     return y, (x, mean, inv, count)
 
 

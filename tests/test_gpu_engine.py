@@ -134,13 +134,15 @@ def _check(precision, loss, loss_o, report):
             assert e2 < TF32["grad_l2"], (key, e2)
 
 
-def test_fused_step_equals_traced_step():
-    """Outside trace mode conv+LeakyReLU run as one kernel; gradients must be
-    identical to the unfused (traced) step."""
-    net = build_cosmoflow(128)
+@pytest.mark.parametrize("kind,width", [("cosmoflow", 128), ("unet", 32)])
+def test_fused_step_equals_traced_step(kind, width):
+    """Outside trace mode conv+LeakyReLU (CosmoFlow) and BatchNorm+LeakyReLU
+    (U-Net) run as one kernel each; gradients must match the unfused (traced)
+    step."""
+    net = build_cosmoflow(width) if kind == "cosmoflow" else build_unet_mini(width)
     ctx = RankCtx(0, 1)
-    plan = engine.make_plan(net, ProcessGrid(1, 1, 1, 1), 1, 128)
-    x, y, ids = engine.synthetic_batch_full(net, 128, 1, 0)
+    plan = engine.make_plan(net, ProcessGrid(1, 1, 1, 1), 1, width)
+    x, y, ids = engine.synthetic_batch_full(net, width, 1, 0)
     grads = []
     for trace in ({}, None):
         state = engine.make_state(net, 0)

@@ -542,3 +542,36 @@ def test_fused_conv_leaky_pool_bit_exact(cin, cout, shape, margins):
               slope, stream_ptr())
     torch.cuda.synchronize()
     assert torch.equal(g1.t.view(torch.int32), g2.t.view(torch.int32))
+
+
+@pytest.mark.parametrize("margins,precision", [((0, 0, 0), "tf32"), ((1, 1, 0), "tf32"), ((0, 0, 0), "fp32")])
+def test_bn_apply_leaky_equals_bn_then_leaky(margins, precision):
+    """vpx_bn_apply_leaky (one pass) == vpx_bn_apply then vpx_leaky_fwd, bit
+    for bit, on flat and margin frames, with and without TF32 storage
+    rounding (reference layers/reference.py:209-214, :231-233)."""
+    rng = np.random.default_rng(11)
+    n, c, d, h, w = 2, 8, 4, 6, 8
+    x = rng.standard_normal((n, c, d, h, w)).astype(np.float32)
+    xf = Frame(n, c, d, h, w, margins, zero=True).load_ncdhw(x)
+    mean = torch.from_numpy(rng.standard_normal(c).astype(np.float32)).cuda()
+    inv = torch.from_numpy(rng.uniform(0.5, 2, c).astype(np.float32)).cuda()
+    gamma = torch.from_numpy(rng.uniform(-1, 1, c).astype(np.float32)).cuda()
+    beta = torch.from_numpy(rng.uniform(-1, 1, c).astype(np.float32)).cuda()
+    mid, ref, got = (Frame(n, c, d, h, w, margins, zero=True) for _ in range(3))
+    import paper_2007_12856_b200 as pkg
+
+    pkg.set_precision(precision)  # TF32 mode rounds every stored value to TF32
+    try:
+        _call_bn_pair(xf, mean, inv, gamma, beta, mid, ref, got)
+    finally:
+        pkg.set_precision("tf32")
+    assert torch.equal(got.t, ref.t)
+
+
+def _call_bn_pair(xf, mean, inv, gamma, beta, mid, ref, got):
+    _lib.call("vpx_bn_apply", xf.ptr, xf.desc, mean.data_ptr(), inv.data_ptr(), gamma.data_ptr(), beta.data_ptr(),
+              mid.ptr, mid.desc, stream_ptr())
+    _lib.call("vpx_leaky_fwd", mid.ptr, mid.desc, ref.ptr, ref.desc, 0.3, stream_ptr())
+    _lib.call("vpx_bn_apply_leaky", xf.ptr, xf.desc, mean.data_ptr(), inv.data_ptr(), gamma.data_ptr(),
+              beta.data_ptr(), 0.3, got.ptr, got.desc, stream_ptr())
+    torch.cuda.synchronize()
