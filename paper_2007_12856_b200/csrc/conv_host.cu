@@ -225,7 +225,7 @@ extern "C" long long vpx_conv3d_workspace_bytes(int cin, int cout, int k, const 
   const long long tc = (long long)vpx::num_sms() * cout * cin * 27 * 4;
   if (tc > parts) parts = tc;
   if (k == 1 || cin == 1) {  // conv_small.cu partials
-    const long long sm = 4LL * vpx::num_sms() * cout * cin * k3 * 4;
+    const long long sm = 8LL * vpx::num_sms() * cout * cin * k3 * 4;
     if (sm > parts) parts = sm;
   }
   const long long tb = vpx::tapbox_workspace_bytes(cin, cout);

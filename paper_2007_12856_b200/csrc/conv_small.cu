@@ -234,47 +234,75 @@ __global__ void __launch_bounds__(256) c1k3_fwd_kernel(const float* __restrict__
 }
 
 // part[block][co][tap] = sum over the block's tiles of u[v][co] x[v + tap - 1].
-// Thread roles: (tap, 4-channel group q) x VG voxel groups.
+// Thread roles: ((a, b) tap row, 4-channel group q) x VG voxel groups.  A role
+// slides along W over 4-voxel segments: per voxel one float4 of u and one new
+// x value feed 12 FMAs (the three width taps of its row x 4 channels), instead
+// of one LDS.128 per FMA quad when every tap re-read u (the kernel was
+// shared-memory bound at 10x its HBM roofline).  Tiles are staged row by row
+// (one index decode per row, not per element).
 template <int CO>
 __global__ void __launch_bounds__(256) c1k3_wgrad_kernel(const float* __restrict__ x, Frame xf,
                                                          const float* __restrict__ u, Frame uf,
                                                          long long ntiles, float* __restrict__ part) {
-  constexpr int PY = kTY + 2, PX = kTX + 2, NQ = CO / 4, ROLES = 27 * NQ, VG = 216 / ROLES;
-  static_assert(ROLES * VG == 216, "role split");
+  constexpr int PY = kTY + 2, PX = kTX + 2, NQ = CO / 4, ROLES = 9 * NQ, VG = 256 / ROLES;
+  constexpr int SEG = 4, ITEMS = kTY * (kTX / SEG);
   __shared__ float xs[3 * PY * PX];
   __shared__ __align__(16) float us[kTX * kTY * CO];
   __shared__ __align__(16) float red[VG * 27 * CO];
   const int role = threadIdx.x % ROLES, vg = threadIdx.x / ROLES;
-  const int tap = role / NQ, q = role % NQ;
-  const int a = tap / 9, b = (tap / 3) % 3, c = tap % 3;
-  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  const int ab = role / NQ, q = role % NQ;
+  const int a = ab / 3, b = ab % 3;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float acc[3][4] = {};
   for (long long ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
     const C1Tile t = c1_tile(uf, ti);
-    c1_load_x(x, xf, t, xs);
-    for (int i = threadIdx.x; i < kTX * kTY * NQ; i += blockDim.x) {
-      const int v = i / NQ, qq = i % NQ;
-      const int oy = t.y0 + v / kTX, ox = t.x0 + v % kTX;
-      float4 val = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (oy < uf.h && ox < uf.w) val = *reinterpret_cast<const float4*>(u + fidx(uf, t.n, t.z, oy, ox) + 4 * qq);
-      *reinterpret_cast<float4*>(us + v * CO + 4 * qq) = val;
+    for (int rr = warp; rr < 3 * PY; rr += 8) {  // x patch rows (depth a, row yy), voxels t.x0-1 .. t.x0+kTX
+      const int aa = rr / PY, yy = rr % PY;
+      const int iz = t.z + aa - 1, iy = t.y0 + yy - 1;
+      const bool rowin = iz >= -xf.md && iz < xf.d + xf.md && iy >= -xf.mh && iy < xf.h + xf.mh;
+      const float* src = x + fidx(xf, t.n, rowin ? iz : 0, rowin ? iy : 0, 0);
+      for (int xx = lane; xx < PX; xx += 32) {
+        const int ix = t.x0 + xx - 1;
+        xs[rr * PX + xx] = rowin && ix >= -xf.mw && ix < xf.w + xf.mw ? __ldg(src + (long long)ix * xf.c) : 0.f;
+      }
+    }
+    for (int r = warp; r < kTY; r += 8) {  // u rows: kTX voxels x CO channels, contiguous in the frame
+      const int oy = t.y0 + r;
+      const float4* src = oy < uf.h ? reinterpret_cast<const float4*>(u + fidx(uf, t.n, t.z, oy, t.x0)) : nullptr;
+      for (int i = lane; i < kTX * NQ; i += 32) {
+        float4 val = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (src != nullptr && t.x0 + i / NQ < uf.w) val = src[i];
+        reinterpret_cast<float4*>(us + r * kTX * CO)[i] = val;
+      }
     }
     __syncthreads();
     if (vg < VG) {
-      const float* xb = xs + (a * PY + b) * PX + c;
-      for (int v = vg; v < kTX * kTY; v += VG) {
-        const float xv = xb[(v / kTX) * PX + (v % kTX)];
-        const float4 uv = *reinterpret_cast<const float4*>(us + v * CO + 4 * q);
-        acc[0] = fmaf(uv.x, xv, acc[0]);
-        acc[1] = fmaf(uv.y, xv, acc[1]);
-        acc[2] = fmaf(uv.z, xv, acc[2]);
-        acc[3] = fmaf(uv.w, xv, acc[3]);
+      for (int it = vg; it < ITEMS; it += VG) {
+        const int r = it / (kTX / SEG), x0 = (it % (kTX / SEG)) * SEG;
+        const float* xb = xs + (a * PY + r + b) * PX + x0;  // x[v + c - 1] for voxel x0 + i is xb[i + c]
+        float xw[SEG + 2];
+#pragma unroll
+        for (int i = 0; i < SEG + 2; ++i) xw[i] = xb[i];
+#pragma unroll
+        for (int i = 0; i < SEG; ++i) {
+          const float4 uv = *reinterpret_cast<const float4*>(us + (r * kTX + x0 + i) * CO + 4 * q);
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            acc[c][0] = fmaf(uv.x, xw[i + c], acc[c][0]);
+            acc[c][1] = fmaf(uv.y, xw[i + c], acc[c][1]);
+            acc[c][2] = fmaf(uv.z, xw[i + c], acc[c][2]);
+            acc[c][3] = fmaf(uv.w, xw[i + c], acc[c][3]);
+          }
+        }
       }
     }
     __syncthreads();
   }
   if (vg < VG) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) red[(vg * CO + 4 * q + j) * 27 + tap] = acc[j];
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) red[(vg * CO + 4 * q + j) * 27 + ab * 3 + c] = acc[c][j];
   }
   __syncthreads();
   for (int i = threadIdx.x; i < 27 * CO; i += blockDim.x) {
@@ -315,7 +343,7 @@ int small_conv_supported(int which, const Frame& xf, const Frame& of, int k, int
 int small_wgrad_parts(const Frame& uf, int k) {
   if (k == 1) return rows_grid(uf, 4);
   const long long ntiles = (long long)uf.n * uf.d * ((uf.h + kTY - 1) / kTY) * ((uf.w + kTX - 1) / kTX);
-  const long long cap = 4LL * num_sms();
+  const long long cap = 8LL * num_sms();  // 8 resident blocks per SM: each block's tile loop is latency-bound
   return static_cast<int>(ntiles < cap ? ntiles : cap);
 }
 

@@ -722,8 +722,11 @@ extern "C" int vpx_deconv_bwd_data(const float* u, const int* uf, const float* w
   deconv_bwd_data_kernel<<<grid1d(VC(B) * B.c), 256, 0, S(st)>>>(u, A, w, g, B);
   LAUNCH_TAIL;
 }
+// partial slices for the filter gradient: 8 per SM for the vectorised kernel
+// (its tile loop is latency-bound), at least 256 for the generic one
+static long long deconv_parts_cap() { return 8LL * num_sms() > 256 ? 8LL * num_sms() : 256; }
 extern "C" long long vpx_deconv_workspace_bytes(int cin, int cout) {
-  return 256LL * cin * cout * 8 * 4;
+  return deconv_parts_cap() * cin * cout * 8 * 4;
 }
 extern "C" int vpx_deconv_bwd_filter(const float* x, const int* xf, const float* u, const int* uf,
                                      float* wg, int accumulate, void* ws, void* st) {
@@ -734,9 +737,10 @@ extern "C" int vpx_deconv_bwd_filter(const float* x, const int* xf, const float*
   const int len = A.c * B.c * 8;
   if (vpx::deconv_vec_supported(A.c, B.c)) {
     int Pv = 0;
-    if (int rc = vpx::deconv_wgrad_vec(x, A, u, B, static_cast<float*>(ws), 256, &Pv, S(st))) return rc;
-    reduce_parts_kernel<<<grid1d(len), 256, 0, S(st)>>>(static_cast<float*>(ws), Pv, len, wg, accumulate);
-    LAUNCH_TAIL;
+    if (int rc = vpx::deconv_wgrad_vec(x, A, u, B, static_cast<float*>(ws), static_cast<int>(deconv_parts_cap()),
+                                       &Pv, S(st)))
+      return rc;
+    return vpx::reduce_partials(static_cast<float*>(ws), Pv, len, wg, accumulate, S(st));
   }
   dim3 grid((len + 255) / 256, P);
   deconv_wgrad_kernel<<<grid, 256, 0, S(st)>>>(x, A, u, B, chunk, static_cast<float*>(ws));

@@ -285,7 +285,7 @@ int deconv_dgrad_vec(const float* u, const Frame& uf, const float* w, float* g, 
 int deconv_wgrad_vec(const float* x, const Frame& xf, const float* u, const Frame& uf, float* part, int max_parts,
                      int* parts, cudaStream_t st) {
   const long long ntiles = (long long)xf.n * xf.d * xf.h * ((xf.w + kDTV - 1) / kDTV);
-  long long P = 4LL * num_sms();
+  long long P = 8LL * num_sms();  // 8 resident blocks per SM hide the per-tile load latency
   if (P > max_parts) P = max_parts;
   if (P > ntiles) P = ntiles;
   if (P < 1) P = 1;
