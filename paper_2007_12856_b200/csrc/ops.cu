@@ -525,6 +525,46 @@ __global__ void xent_kernel(const float* __restrict__ logits, Frame lf, const lo
   if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
 }
 
+// Two classes on margin-free frames (the U-Net head): two voxels per thread
+// as one float4 of logits, one 16-byte label pair and one float4 of
+// gradients -- no per-voxel index decode, same per-voxel arithmetic (and bits)
+// as xent_kernel.
+__global__ void xent2_flat_kernel(const float4* __restrict__ logits, const longlong2* __restrict__ lab,
+                                  long long npairs, double inv_count, float4* __restrict__ g, Frame gf,
+                                  double* __restrict__ part) {
+  double local = 0.0;
+  GRID_STRIDE(i, npairs) {
+    const float4 l = logits[i];
+    const longlong2 y = lab[i];
+    float out[4];
+    const float lv[2][2] = {{l.x, l.y}, {l.z, l.w}};
+    const long long yv[2] = {y.x, y.y};
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+      const float mx = fmaxf(lv[v][0], lv[v][1]);
+      float se = 0.f;
+      se += expf(lv[v][0] - mx);
+      se += expf(lv[v][1] - mx);
+      const float lse = logf(se);
+      local -= (double)(lv[v][yv[v]] - mx - lse);
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const float pr = expf(lv[v][k] - mx - lse);
+        out[2 * v + k] = rnd(gf, static_cast<float>((pr - (k == yv[v] ? 1.f : 0.f)) * inv_count));
+      }
+    }
+    g[i] = make_float4(out[0], out[1], out[2], out[3]);
+  }
+  __shared__ double sh[256];
+  sh[threadIdx.x] = local;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+}
+
 // ------------------------------------------------------------------ layout
 // NCDHW dense <-> NDHWC frame interior.
 __global__ void ncdhw_to_frame_kernel(const float* __restrict__ src, Frame f, float* __restrict__ fr) {
@@ -808,6 +848,15 @@ extern "C" int vpx_sgd(float* p, const float* g, long long n, float lr, void* st
 extern "C" int vpx_xent(const float* logits, const int* lf, const long long* labels, double count,
                         float* g, const int* gf, double* part, int nparts, void* st) {
   Frame A = F(lf), B = F(gf);
+  const bool flat = A.md == 0 && A.mh == 0 && A.mw == 0 && B.md == 0 && B.mh == 0 && B.mw == 0;
+  const bool aligned = (reinterpret_cast<uintptr_t>(logits) | reinterpret_cast<uintptr_t>(labels) |
+                        reinterpret_cast<uintptr_t>(g)) % 16 == 0;
+  if (A.c == 2 && B.c == 2 && flat && aligned && VC(A) % 2 == 0) {
+    xent2_flat_kernel<<<nparts, 256, 0, S(st)>>>(reinterpret_cast<const float4*>(logits),
+                                                 reinterpret_cast<const longlong2*>(labels), VC(A) / 2,
+                                                 1.0 / count, reinterpret_cast<float4*>(g), B, part);
+    LAUNCH_TAIL;
+  }
   xent_kernel<<<nparts, 256, 0, S(st)>>>(logits, A, labels, 1.0 / count, g, B, part);
   LAUNCH_TAIL;
 }

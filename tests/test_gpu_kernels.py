@@ -575,3 +575,30 @@ def _call_bn_pair(xf, mean, inv, gamma, beta, mid, ref, got):
     _lib.call("vpx_bn_apply_leaky", xf.ptr, xf.desc, mean.data_ptr(), inv.data_ptr(), gamma.data_ptr(),
               beta.data_ptr(), 0.3, got.ptr, got.desc, stream_ptr())
     torch.cuda.synchronize()
+
+
+def test_xent_two_class_fast_path_equals_generic():
+    """The vectorised two-class cross entropy (margin-free frames) gives the
+    generic kernel's gradients bit for bit and its loss to double rounding,
+    and both match a numpy log-softmax (reference layers/distributed.py:273-293)."""
+    rng = np.random.default_rng(3)
+    n, d, h, w = 1, 4, 6, 8
+    logits = (rng.standard_normal((n, 2, d, h, w)) * 3).astype(np.float32)
+    labels = torch.from_numpy(rng.integers(0, 2, (n, d, h, w))).cuda()
+    count = n * d * h * w
+    out = []
+    for margins in ((0, 0, 0), (1, 1, 0)):  # flat: fast path; margins: generic kernel
+        lf = Frame(n, 2, d, h, w, margins, zero=True).load_ncdhw(logits)
+        gf = Frame(n, 2, d, h, w, margins, zero=True)
+        part = torch.zeros(64, dtype=torch.float64, device="cuda")
+        _lib.call("vpx_xent", lf.ptr, lf.desc, labels.data_ptr(), float(count), gf.ptr, gf.desc, part.data_ptr(),
+                  64, stream_ptr())
+        torch.cuda.synchronize()
+        out.append((float(part.sum()) / count, gf.to_ncdhw().cpu().numpy()))
+    assert np.array_equal(out[0][1].view(np.uint32), out[1][1].view(np.uint32))
+    assert abs(out[0][0] - out[1][0]) <= 1e-12 * abs(out[1][0])
+    lab = labels.cpu().numpy()
+    lp = logits.astype(np.float64)
+    lse = np.log(np.exp(lp).sum(1))
+    ref = -(np.take_along_axis(lp, lab[:, None], 1)[:, 0] - lse).mean()
+    assert abs(out[0][0] - ref) < 1e-5 * abs(ref)
