@@ -55,6 +55,7 @@ struct C1Params {
 constexpr int kNA = 48;          // N per tap (x chunks k, k+1: 64 > 48 used columns)
 constexpr int kACol = 9 * kNA;   // first A column (432)
 constexpr int kASlots = 8;       // A ring: 8 slots x 8 columns
+constexpr int kRowBlock = 16;    // rows per round-robin block of the CTA row assignment
 constexpr int kProdGroups = 4;   // u producer warps per TMEM lane quarter (power of 2)
 constexpr int kProdWarps = 4 * kProdGroups;
 
@@ -91,7 +92,20 @@ __global__ void __launch_bounds__(128 + 32 * kProdWarps, 1)
   __shared__ uint32_t tmem_base;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int pidx = blockIdx.x;
-  const long long r0 = p.rows * pidx / p.P, r1 = p.rows * (pidx + 1) / p.P;
+  // Rows go to CTAs in round-robin blocks of kRowBlock (not one contiguous
+  // range each): all CTAs then work inside a window of a few depth planes, so
+  // the x rows every depth tap re-reads come from L2 instead of HBM (a
+  // contiguous range per CTA re-read each x plane from DRAM for the next depth).
+  const long long nblk = (p.rows + kRowBlock - 1) / kRowBlock;
+  const long long myblk = pidx < nblk ? (nblk - 1 - pidx) / p.P + 1 : 0;
+  long long nseq = myblk * kRowBlock;
+  if (myblk > 0) {
+    const long long lastend = (pidx + (myblk - 1) * p.P + 1) * kRowBlock;
+    if (lastend > p.rows) nseq -= lastend - p.rows;
+  }
+  auto row_of = [&](long long i) -> long long {
+    return (pidx + (i / kRowBlock) * p.P) * kRowBlock + i % kRowBlock;
+  };
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < 2; ++i) {
@@ -119,17 +133,18 @@ __global__ void __launch_bounds__(128 + 32 * kProdWarps, 1)
   if (warp == 0) {
     // ------------------------------------------------------------ producer
     if (p.dbg < 4 && vpx::elect_one()) {
-      for (long long r = r0; r < r1; ++r) {
-        const int i = static_cast<int>(r - r0);
+      for (long long ii = 0; ii < nseq; ++ii) {
+        const int i = static_cast<int>(ii);
+        const long long r = row_of(ii);
         long long t = r;
         const int y = t % p.h;
         t /= p.h;
         const int z = t % p.d;
         const int n = static_cast<int>(t / p.d);
-        const bool reset = (i == 0) || (y == 0);
+        const bool reset = (i % kRowBlock == 0) || (y == 0);
         // warm L2 with the x rows two steps ahead (the ring only holds one
         // row of lookahead per depth tap)
-        if (r + 2 < r1 && y + 3 < p.h + p.x_off_h)
+        if (i % kRowBlock + 2 < kRowBlock && ii + 2 < nseq && y + 3 < p.h + p.x_off_h)
           for (int a = 0; a < 3; ++a) vpx::tma_prefetch_5d(&xmap, 0, -1, y + 3 + p.x_off_h, z - 1 + a + p.x_off_d, n);
         // the x ring slot of row y+1 last served u row i-2; a reset reloads all
         // three rows per depth tap, so u row i-1 must be done
@@ -150,9 +165,9 @@ __global__ void __launch_bounds__(128 + 32 * kProdWarps, 1)
   } else if (warp == 3) {
     // ------------------------------------- y / pooled-gradient rows (2 stages)
     if (p.dbg < 4 && vpx::elect_one()) {
-      for (long long r = r0; r < r1; ++r) {
-        const int i = static_cast<int>(r - r0);
-        long long t = r;
+      for (long long ii = 0; ii < nseq; ++ii) {
+        const int i = static_cast<int>(ii);
+        long long t = row_of(ii);
         const int y = t % p.h;
         t /= p.h;
         const int z = t % p.d;
@@ -180,9 +195,9 @@ __global__ void __launch_bounds__(128 + 32 * kProdWarps, 1)
     const long long tgl0 = globaltimer_ns();
     if (vpx::elect_one()) {  // one thread issues everything (no per-step warp sync)
       int g = 0;
-      int y = static_cast<int>(r0 % p.h);
-      for (long long r = r0; r < r1; ++r) {
-        const int i = static_cast<int>(r - r0);
+      for (long long ii = 0; ii < nseq; ++ii) {
+        const int i = static_cast<int>(ii);
+        const int y = static_cast<int>(row_of(ii) % p.h);
         if (!skip_waits) vpx::mbar_wait(&xfull[i & 1], (i >> 1) & 1);
         uint64_t bd[9];  // B descriptors of the 9 (depth, height) taps at K-step 0
 #pragma unroll
@@ -203,16 +218,15 @@ __global__ void __launch_bounds__(128 + 32 * kProdWarps, 1)
           vpx::umma_commit(&emptyA[slot]);
         }
         vpx::umma_commit(&rowdone[i & 1]);
-        if (r == r1 - 1) vpx::umma_commit(&tfull);
-        y = (y + 1 == p.h) ? 0 : y + 1;
+        if (ii == nseq - 1) vpx::umma_commit(&tfull);
       }
     }
     __syncwarp();
     if (p.dbg && pidx == 0 && lane == 0) {
       vpx::mbar_wait(&tfull, 0);
       const long long c = clock64() - tclk0, ns = globaltimer_ns() - tgl0;
-      printf("c1 dbg %d: CTA0 %lld MMAs, %.1f cycles/MMA, %.2f GHz\n", p.dbg, (r1 - r0) * KS * 9,
-             double(c) / double((r1 - r0) * KS * 9), double(c) / double(ns));
+      printf("c1 dbg %d: CTA0 %lld MMAs, %.1f cycles/MMA, %.2f GHz\n", p.dbg, nseq * KS * 9,
+             double(c) / double(nseq * KS * 9), double(c) / double(ns));
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------- u producers
@@ -254,8 +268,8 @@ __global__ void __launch_bounds__(128 + 32 * kProdWarps, 1)
         }
       }
     };
-    for (long long r = r0; r < (p.dbg >= 4 ? r0 : r1); ++r) {
-      const int i = static_cast<int>(r - r0);
+    for (long long ii = 0; ii < (p.dbg >= 4 ? 0 : nseq); ++ii) {
+      const int i = static_cast<int>(ii);
       vpx::mbar_wait_sleep(&yfull[i & 1], (i >> 1) & 1, 64);
       const uint32_t ya0 = vpx::smem_u32(ys + (i & 1) * Cfg::YB) + (MASK ? 0 : co * 4);
       const uint32_t ua0 = vpx::smem_u32(us + (i & 1) * Cfg::UB) + co * 4;
@@ -286,7 +300,7 @@ __global__ void __launch_bounds__(128 + 32 * kProdWarps, 1)
   }
 
   // ---------------------------------------------------------------- epilogue
-  const bool have = r1 > r0;
+  const bool have = nseq > 0;
   if (warp >= 4 && warp < 8 && have) {
     vpx::mbar_wait_sleep(&tfull, 0, 256);
     vpx::tc_fence_after();
