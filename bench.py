@@ -240,7 +240,8 @@ def tf32_peak_tflops():
 
 
 def datastore_block(args, net, grid, plan, ctx, W):
-    """This rank's pinned int16 input block from a one-sample HSB1 dataset
+    """This rank's pinned input block (the datastore's transfer copy: int8
+    when the int16 voxels fit, see DataStore.transfer_block) from a one-sample HSB1 dataset
     written for the bench (synthetic voxels in the reference fixture range
     [-8, 8], device PRNG keyed (0, -2, 0)), ingested by the datastore exactly
     as in training: each rank reads only its own hyperslab.  None when the
@@ -276,7 +277,7 @@ def datastore_block(args, net, grid, plan, ctx, W):
     man = DS.load_manifest(root / "manifest.json")
     store = DS.DataStore(man, grid, ctx.rank)
     DS.ingest_epoch0(store, DS.epoch_schedule(0, 0, 1, 1, 1))
-    return store.cache[0].unsqueeze(0)
+    return store.transfer_block(0).unsqueeze(0)
 
 
 def run_ours(args):
@@ -431,10 +432,13 @@ def run_ours(args):
     if not args.no_e2e:
         ds_block = datastore_block(args, net, grid, plan, ctx, W) if batch.x_block is not None else None
         if ds_block is not None:
+            nb = ds_block.element_size()
             e2e = time_e2e(ds_block, "HSB1 sample file -> DataStore.ingest_epoch0 (this rank's hyperslab, pinned "
-                                     "int16 cache) -> engine.HostInputPipeline (H2D 2 B/voxel on a copy stream, "
-                                     "double-buffered) -> vpx_layout_ncdhw_i16_to_frame (int16->fp32 + layout); "
-                                     "loss.item() each step")
+                                     "int16 cache) -> DataStore.transfer_block (" +
+                                     ("pinned int8 copy, made once: the voxels fit int8" if nb == 1 else "the int16 block") +
+                                     f") -> engine.HostInputPipeline (H2D {nb} B/voxel on a copy stream, "
+                                     "double-buffered) -> vpx_layout_ncdhw_i" + ("8" if nb == 1 else "16") +
+                                     "_to_frame (int->fp32 + layout); loss.item() each step")
         e2e_fp32 = time_e2e(x_host, "pinned host fp32 NCDHW array -> engine.HostInputPipeline (copy stream, "
                                     "double-buffered) -> frame; loss.item() each step")
         if e2e is None:

@@ -275,6 +275,9 @@ int vpx_layout_frame_to_ncdhw(const float* frame, const int* ff, float* dst, voi
  * int16 NCDHW block -> fp32 frame interior (conversion fused into the layout
  * change; TF32-rounded in TF32 mode), and int16 label slab -> int64 class ids. */
 int vpx_layout_ncdhw_i16_to_frame(const int16_t* src, const int* ff, float* frame, void* stream);
+/* Same from the datastore's int8 transfer copy (an int16 hyperslab whose
+ * values fit int8: half the host->device bytes, identical fp32 values). */
+int vpx_layout_ncdhw_i8_to_frame(const int8_t* src, const int* ff, float* frame, void* stream);
 int vpx_convert_i16_to_i64(const int16_t* src, long long n, long long* dst, void* stream);
 
 /* ---------------------------------------------------------------- probes --

@@ -587,7 +587,8 @@ __global__ void ncdhw_to_frame_kernel(const float* __restrict__ src, Frame f, fl
 // (reference datastore.py:429-444) fused into the layout change.  Blocks
 // stride over (n, z, y) rows, threads over x; each channel plane is read
 // coalesced, the voxel's channels are written together.
-__global__ void ncdhw_i16_to_frame_kernel(const int16_t* __restrict__ src, Frame f, float* __restrict__ fr) {
+template <typename T>  // int16 (HSB1 storage) or int8 (the datastore's narrowed transfer copy)
+__global__ void ncdhw_int_to_frame_kernel(const T* __restrict__ src, Frame f, float* __restrict__ fr) {
   const long long nrows = (long long)f.n * f.d * f.h;
   const long long plane = (long long)f.d * f.h * f.w;
   for (long long row = blockIdx.x; row < nrows; row += gridDim.x) {
@@ -595,7 +596,7 @@ __global__ void ncdhw_i16_to_frame_kernel(const int16_t* __restrict__ src, Frame
     const long long t = row / f.h;
     const int z = static_cast<int>(t % f.d);
     const int n = static_cast<int>(t / f.d);
-    const int16_t* s = src + (((long long)n * f.c * f.d + z) * f.h + y) * f.w;
+    const T* s = src + (((long long)n * f.c * f.d + z) * f.h + y) * f.w;
     float* dst = fr + fr_off(f, n, z, y, 0);
     for (int x = threadIdx.x; x < f.w; x += blockDim.x) {
       if (f.c % 4 == 0) {
@@ -869,7 +870,14 @@ extern "C" int vpx_layout_ncdhw_i16_to_frame(const int16_t* src, const int* ff, 
   Frame f = F(ff);
   const long long rows = (long long)f.n * f.d * f.h;
   const long long cap = (long long)num_sms() * 16;
-  ncdhw_i16_to_frame_kernel<<<static_cast<int>(rows < cap ? rows : cap), 256, 0, S(st)>>>(src, f, fr);
+  ncdhw_int_to_frame_kernel<int16_t><<<static_cast<int>(rows < cap ? rows : cap), 256, 0, S(st)>>>(src, f, fr);
+  LAUNCH_TAIL;
+}
+extern "C" int vpx_layout_ncdhw_i8_to_frame(const int8_t* src, const int* ff, float* fr, void* st) {
+  Frame f = F(ff);
+  const long long rows = (long long)f.n * f.d * f.h;
+  const long long cap = (long long)num_sms() * 16;
+  ncdhw_int_to_frame_kernel<int8_t><<<static_cast<int>(rows < cap ? rows : cap), 256, 0, S(st)>>>(src, f, fr);
   LAUNCH_TAIL;
 }
 extern "C" int vpx_convert_i16_to_i64(const int16_t* src, long long n, long long* dst, void* st) {

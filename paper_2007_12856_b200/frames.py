@@ -82,16 +82,18 @@ class Frame:
     def load_ncdhw(self, src) -> "Frame":
         """Fill the interior from an NCDHW array/tensor (host or device)."""
         if isinstance(src, np.ndarray):
-            if src.dtype == np.int16:
+            if src.dtype in (np.int16, np.int8):
                 src = torch.from_numpy(np.ascontiguousarray(src))
             else:
                 src = torch.from_numpy(np.ascontiguousarray(src, dtype=np.float32))
         if tuple(src.shape) != (self.n, self.c, self.d, self.h, self.w):
             raise ShapeMismatch(f"block shape {tuple(src.shape)} != {(self.n, self.c) + self.spatial}")
-        if src.dtype == torch.int16:
-            # HSB1 storage dtype: converted to fp32 inside the layout kernel
+        if src.dtype in (torch.int16, torch.int8):
+            # HSB1 storage dtype (or the datastore's int8 transfer copy):
+            # converted to fp32 inside the layout kernel
             src = src.to(device="cuda").contiguous()
-            _lib.call("vpx_layout_ncdhw_i16_to_frame", src.data_ptr(), self.desc, self.ptr, stream_ptr())
+            fn = "vpx_layout_ncdhw_i16_to_frame" if src.dtype == torch.int16 else "vpx_layout_ncdhw_i8_to_frame"
+            _lib.call(fn, src.data_ptr(), self.desc, self.ptr, stream_ptr())
             return self
         src = src.to(device="cuda", dtype=torch.float32).contiguous()
         _lib.call("vpx_layout_ncdhw_to_frame", src.data_ptr(), self.desc, self.ptr, stream_ptr())

@@ -175,3 +175,26 @@ def test_materialize_into_device_frame_and_labels():
     assert np.array_equal(x.to_ncdhw().cpu().numpy(), ref_x)
     ref_l = np.stack([D.read_payload(man.label_path(s)) for s, _, _ in dl])[:, 0].astype(np.int64)
     assert lab.dtype == torch.int64 and np.array_equal(lab.cpu().numpy(), ref_l)
+
+
+def test_transfer_block_narrows_losslessly(tmp_path):
+    """DataStore.transfer_block: int8 copy when the int16 hyperslab fits int8
+    (same values), the int16 block itself when it does not."""
+    import torch
+
+    from paper_2007_12856_b200 import datastore as DS
+    from paper_2007_12856_b200.geometry import ProcessGrid
+
+    dims = (1, 4, 4, 4)
+    vals = {0: np.arange(64, dtype=np.int16).reshape(dims) - 8, 1: np.full(dims, 300, dtype=np.int16)}
+    entries = []
+    for sid, v in vals.items():
+        DS.write_sample(tmp_path / f"s{sid}.hsb", dims, "int16", v)
+        entries.append(DS.SampleEntry(sid, f"s{sid}.hsb", target=(0.0, 0.0, 0.0, 0.0)))
+    man = DS.Manifest(root=str(tmp_path), dtype="int16", dims=dims, loss="mse", samples=tuple(entries))
+    store = DS.DataStore(man, ProcessGrid(1, 1, 1, 1), 0, pin=False)
+    DS.ingest_epoch0(store, DS.epoch_schedule(0, 0, 2, 2, 1))
+    t0, t1 = store.transfer_block(0), store.transfer_block(1)
+    assert t0.dtype == torch.int8 and np.array_equal(t0.numpy().astype(np.int16), vals[0])
+    assert t1.dtype == torch.int16 and np.array_equal(t1.numpy(), vals[1])
+    assert store.transfer_block(0) is t0  # made once

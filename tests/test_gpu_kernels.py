@@ -602,3 +602,16 @@ def test_xent_two_class_fast_path_equals_generic():
     lse = np.log(np.exp(lp).sum(1))
     ref = -(np.take_along_axis(lp, lab[:, None], 1)[:, 0] - lse).mean()
     assert abs(out[0][0] - ref) < 1e-5 * abs(ref)
+
+
+@pytest.mark.parametrize("margins", [(0, 0, 0), (1, 1, 0)])
+def test_int8_transfer_layout_equals_int16(margins):
+    """vpx_layout_ncdhw_i8_to_frame (the datastore's int8 transfer copy) gives
+    the same fp32 frame, bit for bit, as the int16 storage path."""
+    rng = np.random.default_rng(7)
+    v16 = rng.integers(-8, 9, (1, 4, 4, 6, 8)).astype(np.int16)
+    a = Frame(1, 4, 4, 6, 8, margins, zero=True).load_ncdhw(v16)
+    b = Frame(1, 4, 4, 6, 8, margins, zero=True).load_ncdhw(v16.astype(np.int8))
+    torch.cuda.synchronize()
+    assert torch.equal(a.t.view(torch.int32), b.t.view(torch.int32))
+    assert np.array_equal(b.to_ncdhw().cpu().numpy(), v16.astype(np.float32))
