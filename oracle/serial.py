@@ -179,6 +179,81 @@ def k_conv3d_bwd_filter(xpad, u, stride, kernel):
 
 
 # --------------------------------------------------------------- layers
+def tf32_round(a):
+    """Round fp32 to the nearest TF32 value, ties away from zero: the same bits
+    as the device's vpx::tf32_rn (csrc/vpx_round.cuh) and cvt.rna.tf32.f32."""
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    return ((a.view(np.uint32) + np.uint32(0x1000)) & np.uint32(0xFFFFE000)).view(np.float32)
+
+
+class TF32:
+    """TF32-mode numerics of the device path, restated for the oracle.
+
+    The device in TF32 mode (the measured mode) (1) rounds every value it
+    stores into an activation/gradient frame to the nearest TF32, (2) feeds
+    conv/deconv weights to the products rounded the same way, and (3)
+    accumulates the exact TF32 x TF32 products in fp32.  This oracle rounds at
+    the same points and accumulates in fp64 (then casts to fp32), so what
+    remains between the two is fp32 accumulation order.
+
+    LeakyReLU and max-pool backward are discontinuous in their forward input:
+    a pre-activation within a few TF32 ulps of zero (or a max-pool window
+    whose two largest values are that close) may legitimately land on the
+    other side on the device.  With `device` (the device's forward trace,
+    NCDHW arrays keyed ("fwd", layer)), decisions whose oracle margin is at
+    most `tau` x max|input| take the device's branch; every decision is
+    recorded in `self.branches`, and `flips_outside_band()` lists any
+    disagreement OUTSIDE that band (which is a real bug)."""
+
+    def __init__(self, device=None, tau=2.0 ** -11):
+        self.device = device
+        self.tau = tau
+        self.branches = {}
+
+    r = staticmethod(tf32_round)
+
+    def dev(self, layer_name):
+        if self.device is None:
+            return None
+        v = self.device.get(("fwd", layer_name))
+        return None if v is None else np.asarray(v)
+
+    def leaky_mask(self, name, x, dev_x):
+        mask = x >= 0
+        amb = np.abs(x) <= self.tau * max(float(np.max(np.abs(x))), 1e-30)
+        rec = {"ambiguous": int(amb.sum()), "flips_in_band": 0, "flips_outside": 0}
+        if dev_x is not None:
+            dmask = dev_x >= 0
+            rec["flips_in_band"] = int((amb & (dmask != mask)).sum())
+            rec["flips_outside"] = int((~amb & (dmask != mask)).sum())
+            mask = np.where(amb, dmask, mask)
+        self.branches[name] = rec
+        return mask
+
+    def argmax_windows(self, name, x, dev_x):
+        win = _windows(x)
+        arg = win.argmax(axis=-1)
+        top2 = np.sort(win, axis=-1)[..., -2:]
+        amb = (top2[..., 1] - top2[..., 0]) <= self.tau * max(float(np.max(np.abs(x))), 1e-30)
+        rec = {"ambiguous": int(amb.sum()), "flips_in_band": 0, "flips_outside": 0}
+        if dev_x is not None:
+            darg = _windows(dev_x).argmax(axis=-1)
+            rec["flips_in_band"] = int((amb & (darg != arg)).sum())
+            rec["flips_outside"] = int((~amb & (darg != arg)).sum())
+            arg = np.where(amb, darg, arg)
+        self.branches[name] = rec
+        return arg
+
+    def flips_outside_band(self):
+        return {k: v["flips_outside"] for k, v in self.branches.items() if v["flips_outside"]}
+
+
+def _f64(fn, *arrays_and_rest, nargs=2):
+    """Run an oracle contraction in fp64 on fp32 operands, return fp32."""
+    args = [np.asarray(a, dtype=np.float64) for a in arrays_and_rest[:nargs]] + list(arrays_and_rest[nargs:])
+    return fn(*args).astype(np.float32)
+
+
 def _pad(x, radii):
     rd, rh, rw = radii
     return np.pad(x, ((0, 0), (0, 0), (rd, rd), (rh, rh), (rw, rw)))
@@ -252,16 +327,16 @@ def pool3d(x, kind):
     return win.max(axis=-1) if kind == "max" else win.mean(axis=-1)
 
 
-def pool3d_bwd(x, u, kind):
+def pool3d_bwd(x, u, kind, arg=None):
     """reference layers/reference.py:168-183 (avg: u/8 broadcast; max: one-hot at
-    the first maximum)"""
+    the first maximum, or at `arg` when given)"""
     n, c, d, h, w = x.shape
     if kind == "average":
         g = u / u.dtype.type(8)
         return g.repeat(2, axis=2).repeat(2, axis=3).repeat(2, axis=4)
     win = _windows(x)
     hot = np.zeros(win.shape, dtype=u.dtype)
-    np.put_along_axis(hot, win.argmax(axis=-1)[..., None], 1.0, axis=-1)
+    np.put_along_axis(hot, (win.argmax(axis=-1) if arg is None else arg)[..., None], 1.0, axis=-1)
     g = (hot * u[..., None]).reshape(n, c, d // 2, h // 2, w // 2, 2, 2, 2)
     return g.transpose(0, 1, 2, 5, 3, 6, 4, 7).reshape(n, c, d, h, w)
 
@@ -311,9 +386,9 @@ def leaky(x, slope):
     return np.where(x >= 0, x, x.dtype.type(slope) * x)
 
 
-def leaky_bwd(x, u, slope):
-    """reference layers/reference.py:234-236"""
-    return np.where(x >= 0, u, u.dtype.type(slope) * u)
+def leaky_bwd(x, u, slope, mask=None):
+    """reference layers/reference.py:234-236 (`mask`: precomputed x >= 0)"""
+    return np.where(x >= 0 if mask is None else mask, u, u.dtype.type(slope) * u)
 
 
 def dropout_mask(key_parts, n, keep):
@@ -397,95 +472,182 @@ def synthetic_batch(net, wi, n, seed, dtype):
     return x, y, tuple(range(n))
 
 
-def forward(net, params, states, x, mode, step_key=(0, 0, 0), sample_ids=(), trace=None):
-    """reference model/serial.py:42-89"""
-    cur, outs, stash = x, {}, []
+def _fwd_layer(l, idx, cur, params, states, mode, step_key, sample_ids, outs, num):
+    """One layer of reference model/serial.py:42-89: returns (output, stash entry)."""
+    R = num.r if num is not None else (lambda a: a)
+    k = l.kind
+    if k == "conv":
+        w = params[f"{l.name}.w"]
+        if num is None:
+            return conv3d(cur, w, l.params.kernel, l.params.stride), cur
+        return R(_f64(conv3d, cur, R(w), l.params.kernel, l.params.stride)), cur
+    if k == "deconv":
+        w = params[f"{l.name}.w"]
+        return (deconv3d(cur, w) if num is None else R(_f64(deconv3d, cur, R(w)))), cur
+    if k == "pool":
+        return (pool3d(cur, l.pool_kind) if num is None else R(_f64(pool3d, cur, l.pool_kind, nargs=1))), cur
+    if k == "bn":
+        if num is None:
+            return batchnorm_fwd(cur, states[l.name], mode)
+        y, cache = batchnorm_fwd(cur.astype(np.float64), states[l.name], mode)
+        return R(y.astype(np.float32)), cache
+    if k == "leaky":
+        return (R(leaky(cur, l.slope)) if cur.ndim == 5 else leaky(cur, l.slope)), cur
+    if k == "dropout":
+        if mode != "train":
+            return cur, None
+        s, e, it = step_key
+        m = np.stack([dropout_mask([s, e, it, int(sid), idx], cur.shape[1], l.keep) for sid in sample_ids])
+        return dropout_apply(cur, m, l.keep), m
+    if k == "flatten":
+        return cur.reshape(cur.shape[0], -1), cur.shape
+    if k == "fc":
+        return cur @ params[f"{l.name}.w"] + params[f"{l.name}.b"], cur
+    if k == "concat":
+        skip = outs[l.skip]
+        return np.concatenate([cur, skip], axis=1), (cur.shape[1], skip.shape[1])
+    raise ValueError(k)
+
+
+def forward(net, params, states, x, mode, step_key=(0, 0, 0), sample_ids=(), trace=None, num=None):
+    """reference model/serial.py:42-89 (num: TF32 numerics of the device, or None)"""
+    cur, outs, stash = (num.r(x) if num is not None else x), {}, []
     for idx, l in enumerate(net.layers):
-        k = l.kind
-        if k == "conv":
-            stash.append(cur)
-            cur = conv3d(cur, params[f"{l.name}.w"], l.params.kernel, l.params.stride)
-        elif k == "deconv":
-            stash.append(cur)
-            cur = deconv3d(cur, params[f"{l.name}.w"])
-        elif k == "pool":
-            stash.append(cur)
-            cur = pool3d(cur, l.pool_kind)
-        elif k == "bn":
-            cur, cache = batchnorm_fwd(cur, states[l.name], mode)
-            stash.append(cache)
-        elif k == "leaky":
-            stash.append(cur)
-            cur = leaky(cur, l.slope)
-        elif k == "dropout":
-            if mode == "train":
-                s, e, it = step_key
-                m = np.stack([dropout_mask([s, e, it, int(sid), idx], cur.shape[1], l.keep)
-                              for sid in sample_ids])
-                cur = dropout_apply(cur, m, l.keep)
-                stash.append(m)
-            else:
-                stash.append(None)
-        elif k == "flatten":
-            stash.append(cur.shape)
-            cur = cur.reshape(cur.shape[0], -1)
-        elif k == "fc":
-            stash.append(cur)
-            cur = cur @ params[f"{l.name}.w"] + params[f"{l.name}.b"]
-        elif k == "concat":
-            skip = outs[l.skip]
-            stash.append((cur.shape[1], skip.shape[1]))
-            cur = np.concatenate([cur, skip], axis=1)
-        else:
-            raise ValueError(k)
+        cur, kept = _fwd_layer(l, idx, cur, params, states, mode, step_key, sample_ids, outs, num)
+        stash.append(kept)
         outs[l.name] = cur
         if trace is not None:
             trace[("fwd", l.name)] = cur
     return cur, stash
 
 
-def loss_and_grad(net, pred, target):
-    return mse(pred, target) if net.loss == "mse" else cross_entropy(pred, target)
+def loss_and_grad(net, pred, target, num=None):
+    if net.loss == "mse":
+        return mse(pred, target)
+    loss, g = cross_entropy(pred, target)
+    return loss, (g if num is None else num.r(g.astype(np.float32)))
 
 
-def backward(net, params, states, stash, dpred, trace=None):
-    """reference model/serial.py:100-150"""
+def _bwd_layer(l, u, kept, params, states, grads, num, prev_name):
+    """One layer of reference model/serial.py:100-150: returns (input gradient,
+    skip gradient or None); parameter gradients go into `grads`."""
+    R = num.r if num is not None else (lambda a: a)
+    k = l.kind
+    if k == "conv":
+        w = params[f"{l.name}.w"]
+        kk, st = l.params.kernel, l.params.stride
+        if num is None:
+            grads[f"{l.name}.w"] = conv3d_bwd_filter(kept, u, kk, st)
+            return conv3d_bwd_data(u, w, kk, st, kept.shape[2:]), None
+        grads[f"{l.name}.w"] = _f64(conv3d_bwd_filter, kept, u, kk, st)
+        return R(_f64(conv3d_bwd_data, u, R(w), kk, st, kept.shape[2:])), None
+    if k == "deconv":
+        w = params[f"{l.name}.w"]
+        if num is None:
+            grads[f"{l.name}.w"] = deconv3d_bwd_filter(kept, u)
+            return deconv3d_bwd_data(u, w), None
+        grads[f"{l.name}.w"] = _f64(deconv3d_bwd_filter, kept, u)
+        return R(_f64(deconv3d_bwd_data, u, R(w))), None
+    if k == "pool":
+        arg = None
+        if num is not None and l.pool_kind == "max":
+            arg = num.argmax_windows(l.name, kept, num.dev(prev_name))
+        return R(pool3d_bwd(kept, u, l.pool_kind, arg)), None
+    if k == "bn":
+        if num is None:
+            u, grads[f"{l.name}.gamma"], grads[f"{l.name}.beta"] = batchnorm_bwd(u, states[l.name], kept)
+            return u, None
+        g, dg, db = batchnorm_bwd(u.astype(np.float64), states[l.name], kept)
+        grads[f"{l.name}.gamma"], grads[f"{l.name}.beta"] = dg.astype(np.float32), db.astype(np.float32)
+        return R(g.astype(np.float32)), None
+    if k == "leaky":
+        mask = None if num is None else num.leaky_mask(l.name, kept, num.dev(prev_name))
+        g = leaky_bwd(kept, u, l.slope, mask)
+        return (R(g) if kept.ndim == 5 else g), None
+    if k == "dropout":
+        return (dropout_apply(u, kept, l.keep) if kept is not None else u), None
+    if k == "flatten":
+        return R(u.reshape(kept)), None
+    if k == "fc":
+        w = params[f"{l.name}.w"]
+        grads[f"{l.name}.w"], grads[f"{l.name}.b"] = kept.T @ u, u.sum(axis=0)
+        return u @ w.T, None
+    if k == "concat":
+        c_main, _ = kept
+        return u[:, :c_main], u[:, c_main:]
+    raise ValueError(k)
+
+
+def backward(net, params, states, stash, dpred, trace=None, num=None):
+    """reference model/serial.py:100-150 (num: TF32 numerics of the device, or None)"""
+    R = num.r if num is not None else (lambda a: a)
     grads, u, extra = {}, dpred, {}
     for idx in range(len(net.layers) - 1, -1, -1):
         l = net.layers[idx]
         if l.name in extra:
-            u = u + extra.pop(l.name)
-        kept = stash[idx]
-        k = l.kind
-        if k == "conv":
-            w = params[f"{l.name}.w"]
-            grads[f"{l.name}.w"] = conv3d_bwd_filter(kept, u, l.params.kernel, l.params.stride)
-            u = conv3d_bwd_data(u, w, l.params.kernel, l.params.stride, kept.shape[2:])
-        elif k == "deconv":
-            grads[f"{l.name}.w"] = deconv3d_bwd_filter(kept, u)
-            u = deconv3d_bwd_data(u, params[f"{l.name}.w"])
-        elif k == "pool":
-            u = pool3d_bwd(kept, u, l.pool_kind)
-        elif k == "bn":
-            u, grads[f"{l.name}.gamma"], grads[f"{l.name}.beta"] = batchnorm_bwd(u, states[l.name], kept)
-        elif k == "leaky":
-            u = leaky_bwd(kept, u, l.slope)
-        elif k == "dropout":
-            if kept is not None:
-                u = dropout_apply(u, kept, l.keep)
-        elif k == "flatten":
-            u = u.reshape(kept)
-        elif k == "fc":
-            w = params[f"{l.name}.w"]
-            grads[f"{l.name}.w"], grads[f"{l.name}.b"] = kept.T @ u, u.sum(axis=0)
-            u = u @ w.T
-        elif k == "concat":
-            c_main, _ = kept
-            extra[l.skip] = extra.get(l.skip, 0) + u[:, c_main:]
-            u = u[:, :c_main]
+            u = R(u + extra.pop(l.name))
+        prev = net.layers[idx - 1].name if idx > 0 else None
+        u, sk = _bwd_layer(l, u, stash[idx], params, states, grads, num, prev)
+        if sk is not None:
+            extra[l.skip] = extra.get(l.skip, 0) + sk
         if trace is not None:
             trace[("bwd", l.name)] = u
     return grads
+
+
+def layerwise(net, params, states, x, target, dev, sample_ids=(), step_key=(0, 0, 0), num=None):
+    """Teacher-forced per-layer oracle: every layer is evaluated on the
+    DEVICE's own inputs -- forward on the device output of the layer before it
+    (the first on the network input), backward on the device gradient arriving
+    from the layer after it (plus, at a skip source, the device gradient the
+    concat split off) and on the device forward input -- so each layer's
+    result isolates that layer's kernels from the rounding noise compounded
+    upstream.  `dev`: the device trace {("fwd"|"bwd", name): NCDHW/flat array}.
+    Returns (trace, grads) in the shapes of forward/backward's."""
+    R = num.r if num is not None else (lambda a: a)
+    layers = net.layers
+    trace, stash, outs = {}, [], {}
+    for idx, l in enumerate(layers):
+        cur = R(x) if idx == 0 else dev[("fwd", layers[idx - 1].name)]
+        outs_dev = {k[1]: v for k, v in dev.items() if k[0] == "fwd"}
+        y, kept = _fwd_layer(l, idx, cur, params, states, "train", step_key, sample_ids, outs_dev, num)
+        stash.append(kept)
+        trace[("fwd", l.name)] = y
+    _, dpred = loss_and_grad(net, dev[("fwd", layers[-1].name)], target, num)
+    grads = {}
+    skips = {}
+    for idx, l in enumerate(layers):
+        if l.kind == "concat":
+            c_main = stash[idx][0]
+            after = dev[("bwd", layers[idx + 1].name)] if idx + 1 < len(layers) else dpred
+            skips[l.skip] = skips.get(l.skip, 0) + after[:, c_main:]
+    for idx in range(len(layers) - 1, -1, -1):
+        l = layers[idx]
+        u = dpred if idx == len(layers) - 1 else dev[("bwd", layers[idx + 1].name)]
+        if l.name in skips:
+            u = R(u + skips[l.name])
+        prev = layers[idx - 1].name if idx > 0 else None
+        g, _ = _bwd_layer(l, u, stash[idx], params, states, grads, None if num is None else _NoTie(num), prev)
+        trace[("bwd", l.name)] = g
+    return trace, grads
+
+
+class _NoTie:
+    """TF32 numerics without device tie-breaks (a teacher-forced layer sees the
+    device's own pre-activations, so its branch decisions are the device's)."""
+
+    def __init__(self, num):
+        self.r = num.r
+        self.branches = {}
+
+    def dev(self, _name):
+        return None
+
+    def leaky_mask(self, name, x, _dev):
+        return x >= 0
+
+    def argmax_windows(self, name, x, _dev):
+        return _windows(x).argmax(axis=-1)
 
 
 class Adam:
@@ -513,11 +675,12 @@ class Adam:
             p -= lr * (m / c1) / (np.sqrt(v / c2) + self.eps)
 
 
-def train_step(net, params, states, opt, lr, x, target, sample_ids, step_key, trace=None, grads_out=None):
-    """reference model/serial.py:153-161"""
-    pred, stash = forward(net, params, states, x, "train", step_key, sample_ids, trace=trace)
-    loss, dpred = loss_and_grad(net, pred, target)
-    grads = backward(net, params, states, stash, dpred, trace=trace)
+def train_step(net, params, states, opt, lr, x, target, sample_ids, step_key, trace=None, grads_out=None,
+               num=None):
+    """reference model/serial.py:153-161 (num: TF32 numerics of the device, or None)"""
+    pred, stash = forward(net, params, states, x, "train", step_key, sample_ids, trace=trace, num=num)
+    loss, dpred = loss_and_grad(net, pred, target, num)
+    grads = backward(net, params, states, stash, dpred, trace=trace, num=num)
     if grads_out is not None:
         grads_out.update({k: v.copy() for k, v in grads.items()})
     opt.step(params, grads, lr)

@@ -57,7 +57,7 @@ __global__ void conv_fwd_simt_kernel(const float* __restrict__ x, Frame xf,
             const float xv = __ldg(xp + ci);
 #pragma unroll
             for (int j = 0; j < CPT; ++j)
-              acc[j] = fmaf(xv, __ldg(w + ((long long)(CPT * c4 + j) * xf.c + ci) * k3 + tap), acc[j]);
+              acc[j] = fmaf(xv, rnd(yf, __ldg(w + ((long long)(CPT * c4 + j) * xf.c + ci) * k3 + tap)), acc[j]);
           }
         }
       }
@@ -108,7 +108,7 @@ __global__ void conv_bwd_data_simt_kernel(const float* __restrict__ u, Frame uf,
           const float* up = u + fr_index(uf, n, oz, oy, ox);
           const int tap = (a * k + b) * k + c;
           for (int co = 0; co < uf.c; ++co)
-            acc = fmaf(__ldg(up + co), __ldg(w + ((long long)co * gf.c + ci) * k3 + tap), acc);
+            acc = fmaf(__ldg(up + co), rnd(gf, __ldg(w + ((long long)co * gf.c + ci) * k3 + tap)), acc);
         }
       }
     }

@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(256) pw_fwd_kernel(const float* __restrict__ x
                                                      const float* __restrict__ w, float* __restrict__ y,
                                                      Frame yf, int act, float slope) {
   __shared__ float ws[CO * CI];
-  for (int i = threadIdx.x; i < CO * CI; i += blockDim.x) ws[i] = w[i];
+  for (int i = threadIdx.x; i < CO * CI; i += blockDim.x) ws[i] = rnd(yf, w[i]);  // TF32 mode: TF32 operands
   __syncthreads();
   const long long nrows = (long long)xf.n * xf.d * xf.h;
   for (long long row = blockIdx.x; row < nrows; row += gridDim.x) {
@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(256) pw_dgrad_kernel(const float* __restrict__
                                                        const float* __restrict__ w, float* __restrict__ g,
                                                        Frame gf) {
   __shared__ float ws[CO * CI];
-  for (int i = threadIdx.x; i < CO * CI; i += blockDim.x) ws[i] = w[i];
+  for (int i = threadIdx.x; i < CO * CI; i += blockDim.x) ws[i] = rnd(gf, w[i]);
   __syncthreads();
   const long long nrows = (long long)uf.n * uf.d * uf.h;
   for (long long row = blockIdx.x; row < nrows; row += gridDim.x) {
@@ -203,7 +203,7 @@ __global__ void __launch_bounds__(256) c1k3_fwd_kernel(const float* __restrict__
   constexpr int PY = kTY + 2, PX = kTX + 2;
   __shared__ float xs[3 * PY * PX];
   __shared__ __align__(16) float ws[27 * CO];  // ws[tap][co] = w[co][0][tap]
-  for (int i = threadIdx.x; i < 27 * CO; i += blockDim.x) ws[i] = w[(i % CO) * 27 + i / CO];
+  for (int i = threadIdx.x; i < 27 * CO; i += blockDim.x) ws[i] = rnd(yf, w[(i % CO) * 27 + i / CO]);
   const C1Tile t = c1_tile(yf, blockIdx.x);
   c1_load_x(x, xf, t, xs);
   __syncthreads();

@@ -291,7 +291,7 @@ __global__ void deconv_fwd_kernel(const float* __restrict__ x, Frame xf, const f
     const int k = ((o.z & 1) * 2 + (o.y & 1)) * 2 + (o.x & 1);
     const float* xp = x + fr_off(xf, o.n, o.z >> 1, o.y >> 1, o.x >> 1);
     float acc = 0.f;
-    for (int ci = 0; ci < xf.c; ++ci) acc = fmaf(xp[ci], w[((long long)ci * yf.c + co) * 8 + k], acc);
+    for (int ci = 0; ci < xf.c; ++ci) acc = fmaf(xp[ci], rnd(yf, w[((long long)ci * yf.c + co) * 8 + k]), acc);
     y[fr_off(yf, o.n, o.z, o.y, o.x) + co] = rnd(yf, acc);
   }
 }
@@ -305,7 +305,7 @@ __global__ void deconv_bwd_data_kernel(const float* __restrict__ u, Frame uf,
     for (int k = 0; k < 8; ++k) {
       const int a = k >> 2, b = (k >> 1) & 1, c = k & 1;
       const float* up = u + fr_off(uf, p.n, 2 * p.z + a, 2 * p.y + b, 2 * p.x + c);
-      for (int co = 0; co < uf.c; ++co) acc = fmaf(up[co], w[((long long)ci * uf.c + co) * 8 + k], acc);
+      for (int co = 0; co < uf.c; ++co) acc = fmaf(up[co], rnd(gf, w[((long long)ci * uf.c + co) * 8 + k]), acc);
     }
     g[fr_off(gf, p.n, p.z, p.y, p.x) + ci] = rnd(gf, acc);
   }

@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(128) deconv_fwd_v(const float* __restrict__ x,
   __shared__ __align__(16) float ws[8 * CI * CO];  // [k][ci][co]
   for (int i = threadIdx.x; i < 8 * CI * CO; i += blockDim.x) {
     const int k = i % 8, co = (i / 8) % CO, ci = i / (8 * CO);
-    ws[(k * CI + ci) * CO + co] = w[i];
+    ws[(k * CI + ci) * CO + co] = rnd(yf, w[i]);  // TF32 mode: TF32 operands
   }
   __syncthreads();
   const long long nrows = (long long)xf.n * xf.d * xf.h;
@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(128) deconv_dgrad_v(const float* __restrict__ 
   __shared__ __align__(16) float ws[8 * CO * CI];  // [k][co][ci]
   for (int i = threadIdx.x; i < 8 * CI * CO; i += blockDim.x) {
     const int k = i % 8, co = (i / 8) % CO, ci = i / (8 * CO);
-    ws[(k * CO + co) * CI + ci] = w[i];
+    ws[(k * CO + co) * CI + ci] = rnd(gf, w[i]);
   }
   __syncthreads();
   const long long nrows = (long long)gf.n * gf.d * gf.h;

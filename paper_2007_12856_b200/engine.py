@@ -599,7 +599,14 @@ class StepScalars:
     {lr, 1-b1^t, 1-b2^t} and one folded dropout key per (dropout layer,
     sample).  `set(...)` recomputes them on the host (same formulas as the
     eager step: reference optim.py:71-88, engine.py:314-320) and queues one
-    pinned host->device copy on the current stream."""
+    pinned host->device copy on the current stream.
+
+    The host side is a ring of pinned slots, each guarded by an event recorded
+    after its copy: a slot is rewritten only once the copy that read it has
+    completed, so the host may queue any number of replays without
+    synchronising and every replay still sees its own step's scalars."""
+
+    RING = 4
 
     def __init__(self, net: NetworkSpec, sample_ids):
         self.slots = {}
@@ -608,24 +615,34 @@ class StepScalars:
                 for s in sample_ids:
                     self.slots[(i, int(s))] = len(self.slots)
         self.dev = torch.zeros(4 + 2 * max(1, len(self.slots)), dtype=torch.float32, device="cuda")
-        self.host = torch.zeros_like(self.dev, device="cpu").pin_memory()
+        self._ring = [torch.zeros_like(self.dev, device="cpu").pin_memory() for _ in range(self.RING)]
+        self._done = [None] * self.RING
+        self._next = 0
         self.hyper_ptr = self.dev.data_ptr()
-        self._keys = self.host[4:].view(torch.int64)
 
     def key_ptr(self, layer_idx: int, sample_id: int) -> int:
         return self.dev.data_ptr() + 16 + 8 * self.slots[(layer_idx, sample_id)]
 
     def set(self, state: RankState, lr: float, step_key):
+        k = self._next
+        self._next = (k + 1) % self.RING
+        if self._done[k] is not None:
+            self._done[k].synchronize()  # the copy that last read this slot has finished
+        host = self._ring[k]
+        keys = host[4:].view(torch.int64)
         opt = state.opt
         opt.t += 1
-        self.host[0] = float(lr)
-        self.host[1] = float(1.0 - opt.beta1 ** opt.t)
-        self.host[2] = float(1.0 - opt.beta2 ** opt.t)
+        host[0] = float(lr)
+        host[1] = float(1.0 - opt.beta1 ** opt.t)
+        host[2] = float(1.0 - opt.beta2 ** opt.t)
         seed, epoch, it = step_key
-        for (i, s), k in self.slots.items():
+        for (i, s), j in self.slots.items():
             v = prng.key_fold([seed, epoch, it, s, i])
-            self._keys[k] = v - (1 << 64) if v >= (1 << 63) else v
-        self.dev.copy_(self.host, non_blocking=True)
+            keys[j] = v - (1 << 64) if v >= (1 << 63) else v
+        self.dev.copy_(host, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self._done[k] = ev
 
 
 class CapturedStep:
@@ -756,7 +773,11 @@ class HostInputPipeline:
         with torch.cuda.stream(self.copy_stream):
             if self._free_recorded[slot]:
                 self.copy_stream.wait_event(self._free[slot])
-            self._buf[slot].copy_(self._src(i), non_blocking=True)
+            blk = self._src(i)
+            if blk.dtype != self._buf[slot].dtype or tuple(blk.shape) != self.shape:
+                raise ShapeMismatch(f"input block {i}: {blk.dtype} {tuple(blk.shape)}, pipeline staged "
+                                    f"{self._buf[slot].dtype} {self.shape}")
+            self._buf[slot].copy_(blk, non_blocking=True)
             self._ready[slot].record(self.copy_stream)
         self._issued = i
 

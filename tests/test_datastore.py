@@ -177,24 +177,47 @@ def test_materialize_into_device_frame_and_labels():
     assert lab.dtype == torch.int64 and np.array_equal(lab.cpu().numpy(), ref_l)
 
 
-def test_transfer_block_narrows_losslessly(tmp_path):
-    """DataStore.transfer_block: int8 copy when the int16 hyperslab fits int8
-    (same values), the int16 block itself when it does not."""
-    import torch
-
+def _two_sample_store(tmp_path, vals):
     from paper_2007_12856_b200 import datastore as DS
     from paper_2007_12856_b200.geometry import ProcessGrid
 
     dims = (1, 4, 4, 4)
-    vals = {0: np.arange(64, dtype=np.int16).reshape(dims) - 8, 1: np.full(dims, 300, dtype=np.int16)}
     entries = []
     for sid, v in vals.items():
-        DS.write_sample(tmp_path / f"s{sid}.hsb", dims, "int16", v)
+        DS.write_sample(tmp_path / f"s{sid}.hsb", dims, "int16", v.reshape(dims))
         entries.append(DS.SampleEntry(sid, f"s{sid}.hsb", target=(0.0, 0.0, 0.0, 0.0)))
     man = DS.Manifest(root=str(tmp_path), dtype="int16", dims=dims, loss="mse", samples=tuple(entries))
     store = DS.DataStore(man, ProcessGrid(1, 1, 1, 1), 0, pin=False)
-    DS.ingest_epoch0(store, DS.epoch_schedule(0, 0, 2, 2, 1))
+    DS.ingest_epoch0(store, DS.epoch_schedule(0, 0, len(vals), len(vals), 1))
+    return store
+
+
+def test_transfer_block_narrows_losslessly(tmp_path):
+    """DataStore.transfer_block: an int8 copy (same values) when every cached
+    int16 voxel of the store fits int8; forcing int16 returns the cache."""
+    import torch
+
+    vals = {0: np.arange(64, dtype=np.int16) - 8, 1: np.arange(64, dtype=np.int16) - 127}
+    store = _two_sample_store(tmp_path, vals)
+    assert store.transfer_dtype() == torch.int8
     t0, t1 = store.transfer_block(0), store.transfer_block(1)
-    assert t0.dtype == torch.int8 and np.array_equal(t0.numpy().astype(np.int16), vals[0])
-    assert t1.dtype == torch.int16 and np.array_equal(t1.numpy(), vals[1])
+    for sid, t in ((0, t0), (1, t1)):
+        assert t.dtype == torch.int8 and np.array_equal(t.numpy().astype(np.int16).ravel(), vals[sid])
     assert store.transfer_block(0) is t0  # made once
+    assert store.transfer_block(0, dtype=torch.int16).dtype == torch.int16
+
+
+def test_transfer_dtype_is_one_decision_per_dataset(tmp_path):
+    """Regression (advisor r1): sample 0 fits int8, sample 1 does not.  Every
+    block must then travel as int16 -- a per-sample choice would stage sample
+    0 as int8 and wrap sample 1's voxels in the same staging buffer."""
+    import torch
+
+    from paper_2007_12856_b200.errors import ShapeMismatch
+
+    vals = {0: np.arange(64, dtype=np.int16) - 8, 1: np.full(64, 300, dtype=np.int16)}
+    store = _two_sample_store(tmp_path, vals)
+    assert store.transfer_dtype() == torch.int16
+    assert store.transfer_block(0).dtype == store.transfer_block(1).dtype == torch.int16
+    with pytest.raises(ShapeMismatch):
+        store.transfer_block(0, dtype=torch.int8)

@@ -17,9 +17,6 @@ from paper_2007_12856_b200.networks import build_cosmoflow, build_unet_mini
 
 pytestmark = pytest.mark.gpu
 
-RTOL = {"fwd": 1e-3, "bwd": 3e-3, "param": 1e-3}
-
-
 def rel(got, ref):
     ref = np.asarray(ref, dtype=np.float64)
     return float(np.max(np.abs(np.asarray(got, np.float64) - ref)) / max(np.max(np.abs(ref)), 1e-30))
@@ -30,14 +27,28 @@ def rel_l2(got, ref):
     return float(np.linalg.norm(np.asarray(got, np.float64) - ref) / max(np.linalg.norm(ref), 1e-300))
 
 
-# TF32 tolerances (stated in DESIGN.md "Parity"): loss and forward activations
-# in the reference's max-abs metric; gradients in relative L2, because a
-# LeakyReLU whose TF32 pre-activation lands on the other side of zero than the
-# fp32 one switches its gradient between u and 0.3u at that voxel, an O(1)
-# local difference (measured floor: ~1-2% L2 on CosmoFlow-32, ~7% with BN at
-# n=2 where the deepest BN layers normalise 16 values per channel).  FP32 mode
-# is held to the reference's own fp32 tolerance (1e-5) on every tensor.
-TF32 = {"fwd": 2e-3, "loss": 1e-3, "bwd_l2": 1e-1, "grad_l2": 1e-1}
+# Tolerances, in the reference's own metric max|got-ref|/max|ref| per traced
+# tensor (reference cli.py:199-202).
+#  * fp32 mode (CUDA-core kernels): 1e-5 against the fp32 oracle on every
+#    activation, gradient and parameter gradient (reference cli.py:186-187).
+#  * tf32 mode (the measured tcgen05 path): the north-star rtol 1e-3 on EVERY
+#    traced activation, gradient, parameter gradient and the loss, against the
+#    TF32-emulating oracle (oracle.serial.TF32: the same operand/storage
+#    rounding, fp64 accumulation).  Leaky/max-pool branch decisions within one
+#    TF32 ulp of the branch point follow the device; any disagreement outside
+#    that band fails the test.  Against the plain fp32 oracle the loss must
+#    also stay within 1e-3.
+#  * End to end, two TF32 implementations that differ only in fp32
+#    accumulation order drift apart by independent TF32 rounding noise
+#    (~2^-12 per stored value) compounded over every rounding on the path: the
+#    rel-L2 gap grows from ~1e-5 after c1 to ~1e-3 after ~60 roundings
+#    (U-Net-16 fwd+bwd, CosmoFlow-128), and the max-abs metric then reaches
+#    1.0-1.5e-3.  So the 1e-3 end-to-end bound is asserted where the path is
+#    short enough (CosmoFlow-32), E2E_DEEP on the deep nets, and the per-layer
+#    1e-3 bound on EVERY layer of every net by teacher forcing
+#    (test_layerwise_tf32: each layer fed the device's own inputs).
+TOL = {"fp32": 1e-5, "tf32": 1e-3}
+E2E_DEEP = 2e-3
 
 
 def _to_np(v):
@@ -46,21 +57,13 @@ def _to_np(v):
     return v.detach().cpu().numpy()
 
 
-def _run(net, wi, n, lr=1e-3):
+def _run(net, wi, n, lr=1e-3, tf32_oracle=False):
     ctx = RankCtx(0, 1)
     plan = engine.make_plan(net, ProcessGrid(1, 1, 1, 1), n, wi)
     x, y, ids = engine.synthetic_batch_full(net, wi, n, 0)
     state = engine.make_state(net, 0)
+    init = {k: v.cpu().numpy() for k, v in state.params.views.items()}
     batch = engine.scatter_batch(plan, x, y, ids, 0)
-    # oracle on identical inputs
-    xo, yo, _ = O.synthetic_batch(net, wi, n, 0, np.float32)
-    assert np.array_equal(x.cpu().numpy(), xo)
-    po = O.init_params(net, 0, np.float32)
-    for name, v in po.items():
-        assert np.array_equal(state.params.views[name].cpu().numpy(), v), name
-    so = O.make_bn_states(net, po, np.float32)
-    trace_o, grads_o = {}, {}
-    loss_o = O.train_step(net, po, so, O.Adam(po), lr, xo, yo, ids, (0, 0, 0), trace=trace_o, grads_out=grads_o)
     # device
     trace = {}
     state.params.grad.zero_()
@@ -71,7 +74,52 @@ def _run(net, wi, n, lr=1e-3):
     grads = {k: v.clone() for k, v in state.params.grads.items()}
     engine.optimizer_step(state, lr)
     torch.cuda.synchronize()
-    return loss, loss_o, trace, trace_o, grads, grads_o, state, po
+    trace = {k: _to_np(v) for k, v in trace.items() if v is not None}
+    grads = {k: v.cpu().numpy() for k, v in grads.items()}
+    # oracle on identical inputs (bit-identical batch and initial parameters)
+    xo, yo, _ = O.synthetic_batch(net, wi, n, 0, np.float32)
+    assert np.array_equal(x.cpu().numpy(), xo)
+    out = {"loss": float(loss.item()), "trace": trace, "grads": grads, "state": state, "x": xo, "y": yo,
+           "ids": ids}
+    for tag, num in (("fp32", None), ("tf32", O.TF32(device=trace) if tf32_oracle else None)):
+        if tag == "tf32" and num is None:
+            continue
+        po = O.init_params(net, 0, np.float32)
+        for name, v in po.items():
+            assert np.array_equal(init[name], v), name
+        so = O.make_bn_states(net, po, np.float32)
+        tr, gr = {}, {}
+        lo = O.train_step(net, po, so, O.Adam(po), lr, xo, yo, ids, (0, 0, 0), trace=tr, grads_out=gr, num=num)
+        out[tag] = {"loss": lo, "trace": tr, "grads": gr, "params": po, "num": num}
+    return out
+
+
+def _report(out, ref):
+    rep = []
+    for key, r in ref["trace"].items():
+        assert key in out["trace"], key
+        rep.append((key, rel(out["trace"][key], r), rel_l2(out["trace"][key], r)))
+    for name, g in ref["grads"].items():
+        rep.append((("grad", name), rel(out["grads"][name], g), rel_l2(out["grads"][name], g)))
+    return rep
+
+
+def _check_all(which, precision, out, tol=None):
+    ref = out["tf32"] if precision == "tf32" else out["fp32"]
+    rep = _report(out, ref)
+    print(f"\n[{which} {precision}] loss dev {out['loss']!r} oracle fp32 {out['fp32']['loss']!r}"
+          + (f" tf32 {out['tf32']['loss']!r}" if "tf32" in out else ""))
+    print("\n".join(f"{k}: maxabs {e:.2e} l2 {e2:.2e}" for k, e, e2 in rep))
+    tol = TOL[precision] if tol is None else tol
+    assert abs(out["loss"] - ref["loss"]) <= TOL[precision] * abs(ref["loss"]), (out["loss"], ref["loss"])
+    assert abs(out["loss"] - out["fp32"]["loss"]) <= 1e-3 * abs(out["fp32"]["loss"])
+    bad = [(k, e) for k, e, _ in rep if not e < tol]
+    assert not bad, bad
+    if precision == "tf32":
+        num = out["tf32"]["num"]
+        print("branch decisions (ambiguous / followed device in band / outside band):",
+              {k: tuple(v.values()) for k, v in num.branches.items() if v["ambiguous"]})
+        assert not num.flips_outside_band(), num.flips_outside_band()
 
 
 @pytest.fixture
@@ -86,52 +134,25 @@ def precision(request):
 @pytest.mark.parametrize("precision", ["fp32", "tf32"], indirect=True)
 @pytest.mark.parametrize("which", ["cosmoflow32", "cosmoflow32bn", "unet16"])
 def test_train_step_matches_oracle(which, precision):
-    """fp32 mode: every traced activation/gradient and every parameter gradient
-    within the reference's own fp32 verify tolerance (rel 1e-5, reference
-    cli.py:186-187).  tf32 mode: loss and forward activations within the
-    north-star TF32 tolerance rtol 1e-3 (see test_tf32_gradients)."""
+    """One training step, every traced activation/gradient, every parameter
+    gradient and the loss within TOL (above) of the oracle of the same
+    numerics; parameters after Adam within its noise floor."""
     if which == "unet16":
         net, wi = build_unet_mini(16), 16
     else:
         net, wi = build_cosmoflow(32, with_bn=which.endswith("bn")), 32
     lr = 1e-3
-    loss, loss_o, trace, trace_o, grads, grads_o, state, po = _run(net, wi, 2, lr)
-    report = []
-    for key, ref in trace_o.items():
-        got = trace.get(key)
-        assert got is not None, key
-        g = _to_np(got)
-        report.append((key, rel(g, ref), rel_l2(g, ref)))
-    for name, g in grads_o.items():
-        d = grads[name].cpu().numpy()
-        report.append((("grad", name), rel(d, g), rel_l2(d, g)))
-    print(f"\n[{which} {precision}] loss dev {float(loss.item())!r} oracle {loss_o!r}")
-    print("\n".join(f"{k}: maxabs {e:.2e} l2 {e2:.2e}" for k, e, e2 in report))
-    _check(precision, loss, loss_o, report)
+    out = _run(net, wi, 2, lr, tf32_oracle=precision == "tf32")
+    _check_all(which, precision, out, tol=E2E_DEEP if (precision == "tf32" and which != "cosmoflow32") else None)
     # Adam's first step moves every parameter by ~lr*sign(g): a parameter whose
     # gradient sits at the noise floor may flip sign (|dp| <= 2 lr); anything
     # else must agree closely and flips must be rare.
-    for name, p in po.items():
-        d = np.abs(state.params.views[name].cpu().numpy().astype(np.float64) - p)
+    ref = out["tf32"] if precision == "tf32" else out["fp32"]
+    for name, p in ref["params"].items():
+        d = np.abs(out["state"].params.views[name].cpu().numpy().astype(np.float64) - p)
         assert d.max() <= 2.0 * lr * 1.001, name
-        if precision == "fp32":
+        if precision == "fp32":  # in tf32 the noise-floor set is wider (BN gamma/beta of 8-32 channels)
             assert np.mean(d > 1e-2 * lr) < 0.02, (name, float(np.mean(d > 1e-2 * lr)))
-
-
-def _check(precision, loss, loss_o, report):
-    if precision == "fp32":
-        assert abs(float(loss.item()) - loss_o) <= 1e-5 * abs(loss_o)
-        for key, e, _ in report:
-            assert e < 1e-5, (key, e)
-        return
-    assert abs(float(loss.item()) - loss_o) <= TF32["loss"] * abs(loss_o)
-    for key, e, e2 in report:
-        if key[0] == "fwd":
-            assert e < TF32["fwd"], (key, e)
-        elif key[0] == "bwd":
-            assert e2 < TF32["bwd_l2"], (key, e2)
-        else:
-            assert e2 < TF32["grad_l2"], (key, e2)
 
 
 @pytest.mark.parametrize("kind,width", [("cosmoflow", 128), ("unet", 32)])
@@ -161,28 +182,33 @@ def test_fused_step_equals_traced_step(kind, width):
 def test_captured_step_equals_eager_steps(width):
     """engine.CapturedStep (one CUDA graph per step, per-step scalars from
     device memory) takes exactly the same steps as eager train_step calls:
-    parameters, Adam moments and the loss agree bit for bit after 4 steps
-    (2 warm-up steps inside CapturedStep + 2 replays)."""
+    parameters, Adam moments and the loss agree bit for bit after 8 steps
+    (2 warm-up steps inside CapturedStep + 6 replays).  The replays are queued
+    back to back with no host synchronisation and a different lr and iteration
+    (hence dropout keys) each, so a replay that read another step's scalars
+    would show."""
     net = build_cosmoflow(width)
     ctx = RankCtx(0, 1)
     plan = engine.make_plan(net, ProcessGrid(1, 1, 1, 1), 1, width)
     x, y, ids = engine.synthetic_batch_full(net, width, 1, 0)
+    lrs = [1e-3 * (1.0 - 0.07 * i) for i in range(8)]
     runs = []
     for captured in (False, True):
         state = engine.make_state(net, 0)
         batch = engine.scatter_batch(plan, x, y, ids, 0)
         if captured:
-            cap = engine.CapturedStep(ctx, plan, state, batch, 1e-3, warmup=2)
-            for _ in range(2):
-                loss = cap(1e-3)
+            cap = engine.CapturedStep(ctx, plan, state, batch, lrs[0], warmup=2)
+            for i in range(2, 8):
+                loss = cap(lrs[i], iteration=i)
         else:
-            for _ in range(4):
-                loss = engine.train_step(ctx, plan, state, batch, 1e-3)
+            for i in range(8):
+                batch.iteration = i if i >= 2 else 0
+                loss = engine.train_step(ctx, plan, state, batch, lrs[i] if i >= 2 else lrs[0])
         torch.cuda.synchronize()
         runs.append((state.params.flat.clone(), state.opt.m.clone(), state.opt.v.clone(), float(loss.item()),
                      state.opt.t))
     (p0, m0, v0, l0, t0), (p1, m1, v1, l1, t1) = runs
-    assert t0 == t1 == 4
+    assert t0 == t1 == 8
     assert torch.equal(p0, p1) and torch.equal(m0, m1) and torch.equal(v0, v1)
     assert l0 == l1
 
@@ -234,14 +260,35 @@ def test_captured_step_independent_of_stale_memory():
 
 def test_cosmoflow128_traces_vs_oracle():
     """Exercises the tcgen05 row-window (c1 W=128), tap-box (c2..c7, stride 2)
-    and filter-gradient kernels inside the full step, n=1."""
+    and filter-gradient kernels inside the full step, n=1, TF32 mode, every
+    traced tensor and parameter gradient at rtol 1e-3 against the
+    TF32-emulating oracle."""
     net, wi = build_cosmoflow(128), 128
-    loss, loss_o, trace, trace_o, grads, grads_o, state, po = _run(net, wi, 1)
-    report = [(k, rel(_to_np(trace[k]), v), rel_l2(_to_np(trace[k]), v)) for k, v in trace_o.items()]
-    report += [(("grad", k), rel(grads[k].cpu().numpy(), g), rel_l2(grads[k].cpu().numpy(), g))
-               for k, g in grads_o.items()]
-    print("\n".join(f"{k}: maxabs {e:.2e} l2 {e2:.2e}" for k, e, e2 in report))
-    _check("tf32", loss, loss_o, report)
+    out = _run(net, wi, 1, tf32_oracle=True)
+    _check_all("cosmoflow128", "tf32", out, tol=E2E_DEEP)
+
+
+@pytest.mark.parametrize("which", ["cosmoflow32", "cosmoflow32bn", "unet16", "cosmoflow128"])
+def test_layerwise_tf32(which):
+    """Per-layer parity of the measured TF32 path at the north-star rtol 1e-3:
+    every layer's forward output, input gradient and parameter gradient,
+    computed by the TF32-emulating oracle from the DEVICE's own inputs to
+    that layer (oracle.serial.layerwise), against the device's result."""
+    if which == "unet16":
+        net, wi, n = build_unet_mini(16), 16, 2
+    elif which == "cosmoflow128":
+        net, wi, n = build_cosmoflow(128), 128, 1
+    else:
+        net, wi, n = build_cosmoflow(32, with_bn=which.endswith("bn")), 32, 2
+    out = _run(net, wi, n, tf32_oracle=False)
+    po = O.init_params(net, 0, np.float32)
+    tr, gr = O.layerwise(net, po, O.make_bn_states(net, po, np.float32), out["x"], out["y"], out["trace"],
+                         out["ids"], (0, 0, 0), num=O.TF32())
+    rep = _report(out, {"trace": tr, "grads": gr})
+    print(f"\n[{which} layerwise tf32]")
+    print("\n".join(f"{k}: maxabs {e:.2e} l2 {e2:.2e}" for k, e, e2 in rep))
+    bad = [(k, e) for k, e, _ in rep if not e < 1e-3]
+    assert not bad, bad
 
 
 def test_cosmoflow64_loss_matches_reference_value(golden):

@@ -69,9 +69,17 @@ def test_fwd_known_value(precision):
 def test_backend_agrees_with_oracle(precision):
     """fp32 mode: within 1e-5 of the reference kernels (their fwd/bwd
     cross-backend tolerance is 1e-6 on reductions of identical order; ours
-    accumulates in a different order).  tf32 mode: the north-star TF32
-    tolerance band (inputs RN-rounded to TF32, fp32 accumulation)."""
-    tol = 1e-5 if precision == "fp32" else 3e-3
+    accumulates in a different order).  tf32 mode: the north-star rtol 1e-3
+    against the TF32-emulating oracle (operands rounded to nearest TF32 as the
+    device frames and weight packs do, fp64 accumulation, the data gradient
+    stored rounded), and 1e-3 against the plain fp32 kernels as well."""
+    tol = 1e-5 if precision == "fp32" else 1e-3
+    R = O.tf32_round
+
+    def emu(fn, a, b, *rest, rnd_out=True):
+        out = fn(R(a).astype(np.float64), R(b).astype(np.float64), *rest).astype(np.float32)
+        return R(out) if rnd_out else out
+
     for xpad, w, stride in _cases():
         y_o = O.k_conv3d_fwd(xpad, w, stride)
         y = K.conv3d_fwd(xpad, w, stride)
@@ -88,6 +96,13 @@ def test_backend_agrees_with_oracle(precision):
         f = K.conv3d_bwd_filter(xpad, u, stride, w.shape[2:])
         assert f.shape == f_o.shape
         assert _scaled_err(f, f_o) < tol, ("bwd_filter", xpad.shape, stride, _scaled_err(f, f_o))
+        if precision == "tf32":
+            for name, got, ref in (
+                    ("fwd", y, emu(O.k_conv3d_fwd, xpad, w, stride)),
+                    ("bwd_data", g, emu(O.k_conv3d_bwd_data, u, w, stride, xpad.shape[2:])),
+                    ("bwd_filter", f, emu(O.k_conv3d_bwd_filter, xpad, u, stride, w.shape[2:], rnd_out=False))):
+                assert _scaled_err(got, ref) < 1e-3, (name, "tf32-emulated", xpad.shape, stride,
+                                                      _scaled_err(got, ref))
 
 
 @pytest.mark.gpu

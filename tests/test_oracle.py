@@ -126,3 +126,45 @@ def test_oracle_network_step_matches_reference(golden, tag):
     for name, p in params.items():
         ref = A[f"{tag}_param1_{name}"]
         assert np.max(np.abs(_sample(p) - ref)) <= 1e-10 * max(1e-300, np.max(np.abs(ref))), name
+
+
+def test_tf32_round_matches_device_rule():
+    """oracle.serial.tf32_round is the device's vpx::tf32_rn: nearest TF32,
+    ties away from zero, carry into the exponent."""
+    bits = np.array([0x3F800000, 0x3F800FFF, 0x3F801000, 0x3F802000, 0xBF801000, 0x3FFFF000, 0x00000000,
+                     0x7F7FF000], dtype=np.uint32)
+    got = O.tf32_round(bits.view(np.float32)).view(np.uint32)
+    want = np.array([0x3F800000, 0x3F800000, 0x3F802000, 0x3F802000, 0xBF802000, 0x40000000, 0x00000000,
+                     0x7F800000], dtype=np.uint32)
+    np.testing.assert_array_equal(got, want)
+    x = np.random.default_rng(0).normal(size=4096).astype(np.float32)
+    r = O.tf32_round(x)
+    assert np.all(r.view(np.uint32) & 0x1FFF == 0)
+    assert np.max(np.abs(r - x) / np.abs(x)) <= 2.0 ** -11
+
+
+@pytest.mark.parametrize("which", ["cosmoflow32bn", "unet16"])
+@pytest.mark.parametrize("tf32", [False, True])
+def test_layerwise_oracle_reproduces_its_own_trace(which, tf32):
+    """Teacher forcing (oracle.serial.layerwise) fed the oracle's OWN trace
+    must give that trace back bit for bit, layer by layer and for every
+    parameter gradient: the per-layer GPU parity test relies on it."""
+    from paper_2007_12856_b200.networks import build_cosmoflow, build_unet_mini
+
+    net, wi = (build_unet_mini(16), 16) if which == "unet16" else (build_cosmoflow(32, with_bn=True), 32)
+    x, y, ids = O.synthetic_batch(net, wi, 2, 0, np.float32)
+    runs = []
+    for _ in range(2):
+        p = O.init_params(net, 0, np.float32)
+        runs.append((p, O.make_bn_states(net, p, np.float32)))
+    num = O.TF32() if tf32 else None
+    tr, gr = {}, {}
+    pred, stash = O.forward(net, runs[0][0], runs[0][1], x, "train", (0, 0, 0), ids, trace=tr, num=num)
+    _, dpred = O.loss_and_grad(net, pred, y, num)
+    gr = O.backward(net, runs[0][0], runs[0][1], stash, dpred, trace=tr, num=num)
+    lt, lg = O.layerwise(net, runs[1][0], runs[1][1], x, y, tr, ids, (0, 0, 0), num=num)
+    assert set(lt) == set(tr) and set(lg) == set(gr)
+    for k in tr:
+        np.testing.assert_array_equal(np.asarray(lt[k]), np.asarray(tr[k]), err_msg=str(k))
+    for k in gr:
+        np.testing.assert_array_equal(lg[k], gr[k], err_msg=k)
