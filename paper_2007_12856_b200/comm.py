@@ -89,23 +89,47 @@ class RankCtx:
             self.group(m)
 
     # ------------------------------------------------------------- p2p
+    _DTYPES = (torch.float32, torch.float64, torch.int64, torch.int32, torch.int16, torch.int8, torch.uint8)
+
     def send(self, dst: int, tag: int, tensor: torch.Tensor):
+        """Point-to-point send (reference fabric.py:111-119).  A small header
+        (dtype code, ndim, dims) precedes the payload so recv() can allocate
+        the message like the reference's fabric hands over the array."""
         if dst == self.rank:
             raise OutOfBounds("send to self")
-        dist.send(tensor.contiguous(), dst)
+        t = tensor.contiguous()
+        if t.dim() > 8:
+            raise OutOfBounds(f"send of a {t.dim()}-d tensor (at most 8 dims)")
+        hdr = torch.zeros(10, dtype=torch.int64, device=t.device)
+        hdr[0], hdr[1] = self._DTYPES.index(t.dtype), t.dim()
+        if t.dim():
+            hdr[2:2 + t.dim()] = torch.tensor(t.shape, dtype=torch.int64)
+        dist.send(hdr, dst)
+        dist.send(t, dst)
 
-    def recv(self, src: int, tag: int, like: torch.Tensor) -> torch.Tensor:
+    def recv(self, src: int, tag: int, like: torch.Tensor = None) -> torch.Tensor:
+        """Receive the next message from `src` (reference fabric.py:120-121);
+        `like` optionally supplies the destination buffer."""
+        dev = like.device if like is not None else (self.device or torch.device("cpu"))
+        hdr = torch.empty(10, dtype=torch.int64, device=dev)
+        dist.recv(hdr, src)
+        shape = tuple(int(v) for v in hdr[2:2 + int(hdr[1])].tolist())
+        dt = self._DTYPES[int(hdr[0])]
+        if like is None:
+            like = torch.empty(shape, dtype=dt, device=dev)
+        elif tuple(like.shape) != shape or like.dtype != dt:
+            raise OutOfBounds(f"recv buffer {tuple(like.shape)} {like.dtype} != message {shape} {dt}")
         dist.recv(like, src)
         return like
 
-    def exchange(self, ops):
+    def exchange(self, ops, tag: str = "comm.p2p"):
         """ops: list of ("send"|"recv", peer, tensor); one NCCL group."""
         if not ops:
             return
         p2p = [dist.P2POp(dist.isend if kind == "send" else dist.irecv, t, peer)
                for kind, peer, t in ops]
         nbytes = sum(4 * t.numel() for kind, _, t in ops if kind == "send")
-        with region("comm.p2p", 0, nbytes):
+        with region(tag, 0, nbytes):
             for req in dist.batch_isend_irecv(p2p):
                 req.wait()
 
@@ -138,9 +162,19 @@ class RankCtx:
         if self.size == 1 or getattr(self, "_peer_plan", None) is plan:
             return
         self._peer_plan = plan
-        self.peer = None
         if os.environ.get("VPX_NCCL_HALO") == "1" or not torch.cuda.is_available():
+            self.close_peer_halo()
             return
+        need = PeerHalo.requirements(self, plan)
+        if need is None:  # nothing spatially partitioned: no halos to exchange
+            self.close_peer_halo()
+            self.halo_error = None
+            self.no_halo = True
+            return
+        self.no_halo = False
+        if self.peer is not None and self.peer.satisfies(need):
+            return  # same neighbours, mailboxes large enough: keep the mappings
+        self.close_peer_halo()
         ok = 1
         try:
             peer = PeerHalo(self, plan)
@@ -149,12 +183,24 @@ class RankCtx:
             self.halo_error = f"{type(exc).__name__}: {exc}"
         flag = torch.tensor([ok], dtype=torch.int32, device="cuda")
         dist.all_reduce(flag, op=dist.ReduceOp.MIN)
-        self.peer = peer if int(flag.item()) == 1 else None
+        if int(flag.item()) != 1 and peer is not None:
+            peer.close()
+            peer = None
+        self.peer = peer
+
+    def close_peer_halo(self):
+        """Release the peer-halo mailboxes and IPC mappings (collective when a
+        PeerHalo is open: every rank closes together)."""
+        if self.peer is not None:
+            self.peer.close()
+            self.peer = None
 
     @property
     def halo_path(self) -> str:
         if self.size == 1:
             return "none (single rank)"
+        if getattr(self, "no_halo", False):
+            return "none (no spatially partitioned tensor)"
         if self.peer is not None:
             return "CUDA-IPC mailboxes over NVLink (PeerHalo)"
         return "NCCL send/recv" + (f" (IPC setup failed: {self.halo_error})" if getattr(self, "halo_error", None) else "")
@@ -197,23 +243,11 @@ class PeerHalo:
         from cuda.bindings import runtime as rt
 
         self.rt = rt
-        metas = [m for m in plan.in_meta if m is not None and any(p > 1 for p in m.grid.spatial_parts)]
-        if not metas:
+        need = self.requirements(ctx, plan)
+        if need is None:
             raise OutOfBounds("no spatially partitioned tensors")
-        meta = metas[0]
-        gr = meta.grid_rank_of(ctx.rank)
-        # largest face any round can carry: whole frame cross-section, all channels
-        slab = 0
-        for m in metas:
-            try:
-                g = m.grid_rank_of(ctx.rank)
-            except OutOfBounds:
-                continue
-            ls, mg = m.local_shape(g), m.margins()
-            ext = (ls.d + 2 * mg[0], ls.h + 2 * mg[1], ls.w + 2 * mg[2])
-            for dim in range(3):
-                slab = max(slab, ls.n * ls.c * ext[(dim + 1) % 3] * ext[(dim + 2) % 3] * max(1, m.radii[dim]) * 4)
-        self.slab = (slab + 4095) // 4096 * 4096
+        meta, gr, slab, self.neighbours = need
+        self.slab = slab
         self.flags_off = 12 * self.slab
         total = self.flags_off + 4096
         err, ptr = rt.cudaMalloc(total)
@@ -222,6 +256,7 @@ class PeerHalo:
         rt.cudaMemset(ptr, 0, total)
         rt.cudaDeviceSynchronize()
         self.base = int(ptr)
+        self.opened = {}
         err, handle = rt.cudaIpcGetMemHandle(ptr)
         if err != rt.cudaError_t.cudaSuccess:
             raise OutOfBounds(f"cudaIpcGetMemHandle failed: {err}")
@@ -242,8 +277,52 @@ class PeerHalo:
                         raise OutOfBounds(f"cudaIpcOpenMemHandle({peer}) failed: {err}")
                     opened[peer] = int(pptr)
                 self.peer_base[(dim, side)] = opened[peer]
+        self.opened = opened
         self.count = {}
+        self.ctx = ctx
         ctx.barrier()
+
+    @staticmethod
+    def requirements(ctx: "RankCtx", plan):
+        """(first partitioned meta, its grid rank, mailbox bytes, neighbour
+        set) a plan needs, or None when nothing is spatially partitioned."""
+        metas = [m for m in plan.in_meta if m is not None and any(p > 1 for p in m.grid.spatial_parts)]
+        if not metas:
+            return None
+        meta = metas[0]
+        gr = meta.grid_rank_of(ctx.rank)
+        # largest face any round can carry: whole frame cross-section, all channels
+        slab = 0
+        for m in metas:
+            try:
+                g = m.grid_rank_of(ctx.rank)
+            except OutOfBounds:
+                continue
+            ls, mg = m.local_shape(g), m.margins()
+            ext = (ls.d + 2 * mg[0], ls.h + 2 * mg[1], ls.w + 2 * mg[2])
+            for dim in range(3):
+                slab = max(slab, ls.n * ls.c * ext[(dim + 1) % 3] * ext[(dim + 2) % 3] * max(1, m.radii[dim]) * 4)
+        nbrs = tuple((dim, side, meta.fabric_rank(meta.neighbor(gr, dim, side)))
+                     for dim in range(3) for side in (-1, 1) if meta.neighbor(gr, dim, side) is not None)
+        return meta, gr, (slab + 4095) // 4096 * 4096, nbrs
+
+    def satisfies(self, need) -> bool:
+        return need is not None and need[3] == self.neighbours and need[2] <= self.slab
+
+    def close(self):
+        """Close the neighbours' IPC mappings and free this rank's mailbox.
+        Collective: a neighbour may still be writing into our mailbox until
+        every rank has drained its stream, hence the barrier first."""
+        if self.base is None:
+            return
+        torch.cuda.synchronize()
+        self.ctx.barrier()
+        for p in self.opened.values():
+            self.rt.cudaIpcCloseMemHandle(p)
+        self.opened = {}
+        self.ctx.barrier()
+        self.rt.cudaFree(self.base)
+        self.base = None
 
     @staticmethod
     def _chan(dim, side):
@@ -361,7 +440,8 @@ def halo_exchange(ctx: RankCtx, tensor, pack=_cuda_pack, unpack=_cuda_unpack):
             continue
         if peer is not None:
             sides = [s for s in (-1, 1) if meta.neighbor(gr, dim, s) is not None]
-            with region("comm.p2p", 0, 0):
+            nbytes = sum(4 * _box_numel(tensor, round_boxes(meta, gr, dim, side)[0]) for side in sides)
+            with region("comm.halo", 0, nbytes):
                 if _FUSED_ROUND and tensor.c % 4 == 0:
                     boxes = [round_boxes(meta, gr, dim, side) for side in sides]
                     peer.round(dim, sides, tensor, [b[0] for b in boxes], [b[1] for b in boxes], 1)
@@ -385,7 +465,7 @@ def halo_exchange(ctx: RankCtx, tensor, pack=_cuda_pack, unpack=_cuda_unpack):
             ops.append(("send", other, sbuf))
             ops.append(("recv", other, rbuf))
             unpacks.append((mbox, rbuf))
-        ctx.exchange(ops)
+        ctx.exchange(ops, "comm.halo")
         for mbox, rbuf in unpacks:
             unpack(tensor, mbox, rbuf, False)
     return tensor
@@ -406,7 +486,8 @@ def reverse_halo_exchange(ctx: RankCtx, meta, grid_rank: int, frame, pack=_cuda_
             continue
         if peer is not None:
             sides = [s for s in (-1, 1) if meta.neighbor(grid_rank, dim, s) is not None]
-            with region("comm.p2p", 0, 0):
+            nbytes = sum(4 * _box_numel(frame, round_boxes(meta, grid_rank, dim, side)[1]) for side in sides)
+            with region("comm.halo", 0, nbytes):
                 if _FUSED_ROUND and frame.c % 4 == 0:
                     boxes = [round_boxes(meta, grid_rank, dim, side) for side in sides]
                     peer.round(dim, sides, frame, [b[1] for b in boxes], [b[0] for b in boxes], 2)
@@ -430,7 +511,7 @@ def reverse_halo_exchange(ctx: RankCtx, meta, grid_rank: int, frame, pack=_cuda_
             ops.append(("send", other, sbuf))
             ops.append(("recv", other, rbuf))
             unpacks.append((bbox, rbuf))
-        ctx.exchange(ops)
+        ctx.exchange(ops, "comm.halo")
         for bbox, rbuf in unpacks:
             unpack(frame, bbox, rbuf, True)
     return frame

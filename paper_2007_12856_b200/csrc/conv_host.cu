@@ -230,6 +230,11 @@ extern "C" long long vpx_conv3d_workspace_bytes(int cin, int cout, int k, const 
   }
   const long long tb = vpx::tapbox_workspace_bytes(cin, cout);
   if (tb > packed) packed = tb;
+  {  // tap-box split-K partial tiles: ks * base_tiles <= num_sms tiles of 128 x min(N, 256) (conv_tapbox.cu)
+    const int nmax = cin > cout ? cin : cout;
+    const long long tbp = (long long)vpx::num_sms() * 128 * (nmax < 256 ? nmax : 256) * 4;
+    if (tbp > parts) parts = tbp;
+  }
   const long long rh = vpx::rowh_packed_bytes(cin, cout) > vpx::rowh_packed_bytes(cout, cin)
                            ? vpx::rowh_packed_bytes(cin, cout)
                            : vpx::rowh_packed_bytes(cout, cin);

@@ -472,8 +472,13 @@ int conv_tapbox(int mode, const float* in, const Frame& inf, const float* w, int
     if (ks > min_entries / 2) ks = min_entries / 2 > 1 ? min_entries / 2 : 1;
     if (ks > 64) ks = 64;
     const int NTc = ntot <= 256 ? ntot : 256;
-    while (ks > 1 && wbytes + (long long)ks * p.base_tiles * 128 * NTc * 4 > ws_bytes) --ks;
     if (getenv("VPX_NO_KSPLIT")) ks = 1;
+    // the split depends on the shape only (never on how large a workspace the
+    // caller happens to pass), so results are reproducible run to run;
+    // vpx_conv3d_workspace_bytes covers ks * base_tiles <= num_sms partial tiles
+    if (ks > 1 && wbytes + (long long)ks * p.base_tiles * 128 * NTc * 4 > ws_bytes)
+      VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "tapbox: workspace %lld B < %lld B (vpx_conv3d_workspace_bytes)", ws_bytes,
+               wbytes + (long long)ks * p.base_tiles * 128 * NTc * 4);
     if (ks > 1) {
       p.ksplit = ks;
       p.part = reinterpret_cast<float*>(static_cast<char*>(ws) + wbytes);

@@ -209,6 +209,32 @@ class FlatParams:
             pos += n
         self.numel = total
 
+    # the reference's RankState.params is a dict name -> array (reference
+    # engine.py:197-203); the same read/write access by name, on views
+    def __getitem__(self, name):
+        return self.views[name]
+
+    def __setitem__(self, name, value):
+        self.views[name].copy_(torch.as_tensor(value, dtype=torch.float32))
+
+    def __iter__(self):
+        return iter(self.views)
+
+    def __len__(self):
+        return len(self.views)
+
+    def __contains__(self, name):
+        return name in self.views
+
+    def keys(self):
+        return self.views.keys()
+
+    def values(self):
+        return self.views.values()
+
+    def items(self):
+        return self.views.items()
+
 
 def _numel(shape):
     n = 1
@@ -580,10 +606,13 @@ def gradient_allreduce(ctx: RankCtx, state: RankState):
 
 
 def train_step(ctx: RankCtx, plan: Plan, state: RankState, batch: Batch, lr: float, seed: int = 0,
-               scalars: "StepScalars" = None):
-    """One hybrid-parallel training step; returns the loss as a 1-element
-    fp64 CUDA tensor (identical on every rank).  No host synchronisation
-    (except once per plan, when the halo mailboxes are set up)."""
+               scalars: "StepScalars" = None, as_tensor: bool = False):
+    """One hybrid-parallel training step (reference engine.py:465-473).
+    Returns the loss as a float, identical on every rank, like the reference
+    -- which reads it back, i.e. synchronises with the device.  With
+    as_tensor=True it returns the 1-element fp64 CUDA tensor instead and the
+    step queues without any host synchronisation (except once per plan, when
+    the halo mailboxes are set up); CapturedStep and the bench use that."""
     ctx.ensure_peer_halo(plan)
     state.params.grad.zero_()
     pred, stash = forward(ctx, plan, state, batch, "train", seed, scalars=scalars)
@@ -591,7 +620,7 @@ def train_step(ctx: RankCtx, plan: Plan, state: RankState, batch: Batch, lr: flo
     backward(ctx, plan, state, stash, dpred)
     gradient_allreduce(ctx, state)
     optimizer_step(state, lr, scalars)
-    return loss
+    return loss if as_tensor else float(loss.item())
 
 
 class StepScalars:
@@ -662,12 +691,12 @@ class CapturedStep:
         with torch.cuda.stream(side):
             for _ in range(warmup):  # real steps: settles workspaces and allocator state
                 self.scalars.set(state, lr, (seed, batch.epoch, batch.iteration))
-                train_step(ctx, plan, state, batch, lr, seed, scalars=self.scalars)
+                train_step(ctx, plan, state, batch, lr, seed, scalars=self.scalars, as_tensor=True)
         torch.cuda.current_stream().wait_stream(side)
         torch.cuda.synchronize()
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph):
-            self.loss = train_step(ctx, plan, state, batch, lr, seed, scalars=self.scalars)
+            self.loss = train_step(ctx, plan, state, batch, lr, seed, scalars=self.scalars, as_tensor=True)
 
     def __call__(self, lr: float, epoch: int = None, iteration: int = None):
         b = self.batch

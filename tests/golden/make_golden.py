@@ -254,7 +254,10 @@ def halo_fixture():
     (global-coordinate ramp), for bit-exact comparison of the device exchange."""
     A = {}
     for g, shape, radii in (((1, 2, 2, 1), (2, 3, 8, 8, 6), (1, 1, 1)), ((1, 2, 2, 2), (1, 2, 8, 8, 8), (1, 1, 1)),
-                            ((1, 4, 1, 1), (1, 2, 16, 4, 4), (1, 1, 1)), ((2, 2, 1, 1), (2, 2, 8, 4, 4), (1, 0, 0))):
+                            ((1, 4, 1, 1), (1, 2, 16, 4, 4), (1, 1, 1)), ((2, 2, 1, 1), (2, 2, 8, 4, 4), (1, 0, 0)),
+                            # 2-rank grids and channel counts % 4 == 0 (the device's fused peer round)
+                            ((1, 2, 1, 1), (1, 4, 8, 6, 6), (1, 1, 1)), ((1, 1, 2, 1), (2, 8, 6, 8, 6), (1, 1, 1)),
+                            ((1, 1, 1, 2), (1, 4, 6, 6, 8), (1, 1, 1)), ((2, 1, 2, 1), (2, 4, 6, 8, 6), (1, 1, 1))):
         grid = ProcessGrid(*g)
         meta = make_partition(Shape5D(*shape), grid, radii)
         full = np.arange(np.prod(shape), dtype=np.float64).reshape(shape) * 0.5 + 1.0

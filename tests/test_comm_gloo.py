@@ -93,7 +93,7 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("key", ["1x2x2x1", "1x2x2x2", "1x4x1x1", "2x2x1x1"])
+@pytest.mark.parametrize("key", ["1x2x2x1", "1x2x2x2", "1x4x1x1", "2x2x1x1", "1x2x1x1", "1x1x2x1", "1x1x1x2", "2x1x2x1"])
 def test_halo_rounds_bit_exact_vs_reference_fabric(golden, key):
     A = dict(np.load(golden / "halo.npz"))
     size = int(np.prod([int(v) for v in key.split("x")]))

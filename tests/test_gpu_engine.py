@@ -203,7 +203,7 @@ def test_captured_step_equals_eager_steps(width):
         else:
             for i in range(8):
                 batch.iteration = i if i >= 2 else 0
-                loss = engine.train_step(ctx, plan, state, batch, lrs[i] if i >= 2 else lrs[0])
+                loss = engine.train_step(ctx, plan, state, batch, lrs[i] if i >= 2 else lrs[0], as_tensor=True)
         torch.cuda.synchronize()
         runs.append((state.params.flat.clone(), state.opt.m.clone(), state.opt.v.clone(), float(loss.item()),
                      state.opt.t))
@@ -301,4 +301,5 @@ def test_cosmoflow64_loss_matches_reference_value(golden):
     x, y, ids = engine.synthetic_batch_full(net, 64, 2, 0)
     state = engine.make_state(net, 0)
     loss = engine.train_step(ctx, plan, state, engine.scatter_batch(plan, x, y, ids, 0), 1e-3)
-    assert abs(float(loss.item()) - ref) < 1e-3 * abs(ref)
+    assert isinstance(loss, float)  # the reference API returns the loss as a float
+    assert abs(loss - ref) < 1e-3 * abs(ref)

@@ -52,10 +52,10 @@ def main():
         print(f"{tag}: loss {float(loss.item()):.6g} |grad| {gn:.4g} |param| {pn:.4g}", flush=True)
 
     for i in range(a.steps):
-        report(f"eager {i}", engine.train_step(ctx, plan, state, batch, a.lr))
+        report(f"eager {i}", engine.train_step(ctx, plan, state, batch, a.lr, as_tensor=True))
     cap = engine.CapturedStep(ctx, plan, state, batch, a.lr)
     for i in range(a.eager_after_capture):
-        report(f"eager-after-capture {i}", engine.train_step(ctx, plan, state, batch, a.lr))
+        report(f"eager-after-capture {i}", engine.train_step(ctx, plan, state, batch, a.lr, as_tensor=True))
     if a.freed:
         snap = torch.cuda.memory._snapshot()
         last = {}
