@@ -40,6 +40,7 @@ sys.path.insert(0, str(ROOT))
 
 WIDTH = 512
 N_PER_GROUP = 1
+NVLINK_GBS = 900.0  # NVLink 5, per direction per GPU
 
 
 def parse():
@@ -57,6 +58,7 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of the CUDA graph")
     ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of CPU sample work")
+    ap.add_argument("--no-aux", action="store_true", help="skip the CosmoFlow-128 like-for-like step")
     return ap.parse_args()
 
 
@@ -84,6 +86,7 @@ def cpu_sample(width: int, budget_s: float, threads: int, use_ref: bool):
     rng = np.random.default_rng(0)
     t_start = time.time()
     total_est = 0.0
+    done_fl = full_fl = 0
     parts = []
     convs = [(l, i, o) for l, i, o in walk_shapes(net, (1, 4, width, width, width)) if l.kind == "conv"]
     per_layer_budget = budget_s / max(1, len(convs))
@@ -116,14 +119,84 @@ def cpu_sample(width: int, budget_s: float, threads: int, use_ref: bool):
         full = 3 * 2 * 27 * cin * cout * od * oh * ow
         est = dt * full / done
         total_est += est
+        done_fl += done
+        full_fl += full
         parts.append(f"{layer.name}:{rows}x{ow}rows")
     desc = (f"cosmoflow{width} conv layers (fwd+bwd_data+bwd_filter + leaky fwd/bwd) on "
             f"{threads} concurrent 1-plane slabs ({', '.join(parts)}), extrapolated by conv flops "
             f"to a full step of 1 sample; estimated step {total_est:.1f} s")
-    return 1.0 / total_est, desc, time.time() - t_start
+    return 1.0 / total_est, desc, time.time() - t_start, done_fl / full_fl
+
+
+def reference_full_step(width: int = 128, steps: int = 1, threads: int = None):
+    """A REAL full training step of the reference's own implementation: the
+    unmodified reference package installed into baseline/_ref (pip install
+    --target, Cython kernels built), `engine.train_step` on every rank of a
+    spatial grid run as threads by the reference's own fabric
+    (run_ranks(mode="parallel"); its kernels release the GIL, reference
+    fabric.py:337-355), CosmoFlow-`width`, batch 1, the reference's synthetic
+    verify batch (reference cli.py:112-125).  Returns a dict, or None when
+    baseline/_ref is absent."""
+    import copy
+
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "voxpar").exists():
+        return None
+    if str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    os.environ.setdefault("VOXPAR_BACKEND", "cython")
+    import numpy as np
+    from voxpar import kernels as rk
+    from voxpar import prng as rprng
+    from voxpar.fabric import run_ranks
+    from voxpar.model import engine as reng, serial as rserial
+    from voxpar.model.networks import build_cosmoflow as rbuild
+    from voxpar.model.optim import OptimizerState, init_params as rinit
+    from voxpar.tensor import ProcessGrid as RGrid
+
+    cores = threads or os.cpu_count() or 1
+    # as many rank threads as cores, on grids whose every local extent stays even
+    # (1x8x1x1 at 128^3 leaves 1-plane blocks; the reference computes a wrong loss there)
+    grid = (1, 4, 2, 2) if cores >= 16 else (1, 2, 2, 2) if cores >= 8 else (1, 2, 2, 1) if cores >= 4 else (1, 1, 1, 1)
+    net = rbuild(width)
+    plan = reng.make_plan(net, RGrid(*grid), 1, width)
+    shape = (1, 4, width, width, width)
+    x = rprng.uniform([0, -3, 0], math.prod(shape), -1.0, 1.0).reshape(shape).astype(np.float32)
+    y = rprng.uniform([0, -3, 1], 4, -1.0, 1.0).reshape(1, 4).astype(np.float32)
+    params = rinit(net, 0, np.float32)
+    batches = reng.scatter_batch(plan, x, y, (0,))
+
+    def fn(ctx):
+        mine = copy.deepcopy(params)
+        st = reng.RankState(params=mine, bn_states=rserial.make_bn_states(net, mine, np.float32),
+                            opt=OptimizerState.for_params("adam", mine))
+        out = []
+        for _ in range(steps):
+            t0 = time.perf_counter()
+            loss = reng.train_step(ctx, plan, st, batches[ctx.rank], 1e-3, 0)
+            out.append((time.perf_counter() - t0, loss))
+        return out
+
+    res = run_ranks(math.prod(grid), fn, mode="parallel")
+    per_step = [max(r[k][0] for r in res) for k in range(steps)]
+    s_step = sum(per_step) / steps
+    return {"workload": f"cosmoflow{width} n=1 full train step (fwd+bwd+allreduce+adam)", "s_per_step": s_step,
+            "samples_per_s": 1.0 / s_step, "steps_timed": steps, "loss_first_step": float(res[0][0][1]),
+            "grid": "x".join(map(str, grid)), "rank_threads": math.prod(grid), "cores": cores,
+            "backend": getattr(rk, "_active", None) and rk._active.NAME,
+            "source": "baseline/_ref (unmodified reference, reference engine.train_step under run_ranks)"}
 
 
 def run_reference(args):
+    """Reference arm: the reference's own CPU implementation on the host cores.
+    A 512^3 training step of the reference takes ~20 min and ~55 GB, so each
+    timed step here is a BOUNDED SAMPLE of it: thin slabs of every 512^3 conv
+    layer through the reference's compiled kernels (cpu_sample), extrapolated
+    by conv flops -- `ms_per_step` is the measured wall time of one such
+    sample and `value` the extrapolated 512^3 samples/s ("extrapolated":
+    true).  Beside it, `measured_full_step` times REAL full steps of the
+    reference's own engine at 128^3 (no extrapolation), the like-for-like
+    anchor for bench.py's `cosmoflow128_full_step`."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -132,22 +205,35 @@ def run_reference(args):
     use_ref = build_oracle.build_reference_kernels() is not None
     threads = os.cpu_count() or 1
     budget = max(1.0, min(args.cpu_budget, 150.0 / max(1, args.steps + args.warmup)))
-    vals = []
+    vals, walls, fracs = [], [], []
     desc = ""
     for i in range(args.warmup + args.steps):
-        v, desc, _ = cpu_sample(args.width, budget, threads, use_ref)
+        t0 = time.perf_counter()
+        v, desc, _, frac = cpu_sample(args.width, budget, threads, use_ref)
         if i >= args.warmup:
             vals.append(v)
+            walls.append(time.perf_counter() - t0)
+            fracs.append(frac)
     value = sum(vals) / len(vals)
+    ms_sample = 1000.0 * sum(walls) / len(walls)
+    full = reference_full_step(128, 2, threads)
     kind = "reference" if use_ref else "port"
     line = {
         "impl": "reference", "metric": f"CosmoFlow {args.width}^3 samples/sec", "value": value,
         "unit": "samples/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1000.0 / value, "higher_is_better": True, "scaling": "strong",
+        "ms_per_step": ms_sample, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "extrapolated": True,
+        "what_was_timed": (f"{args.steps} timed steps (+{args.warmup} warm-up), each a bounded sample of the "
+                           f"{args.width}^3 step: {desc}; ms_per_step = measured wall ms of one sample "
+                           f"(covering {100.0 * sum(fracs) / len(fracs):.3f}% of the step's conv flops); value = "
+                           f"that sample extrapolated by conv flops to a full {args.width}^3 step"),
+        "extrapolated_s_per_step": 1.0 / value,
+        "measured_full_step": full,
         "config": {"workload": f"cosmoflow{args.width} n=1 train step, CPU slab sample", "global_batch": 1,
                    "width": args.width},
-        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": threads, "kind": kind, "sample": desc},
+        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": threads, "kind": kind, "sample": desc,
+                         "extrapolated": True},
         "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -216,30 +302,17 @@ def ncu_traffic(tag):
     return None if ent is None else ent["dram_bytes"]
 
 
-def tf32_peak_tflops():
-    """cuBLAS TF32 dense GEMM throughput measured live (best of 5, 8192^3)."""
-    import torch
-
-    torch.backends.cuda.matmul.allow_tf32 = True
-    a = torch.randn(8192, 8192, device="cuda")
-    b = torch.randn(8192, 8192, device="cuda")
-    for _ in range(3):
-        a @ b
-    best = 0.0
-    for _ in range(5):
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s.record()
-        a @ b
-        e.record()
-        e.synchronize()
-        best = max(best, 2 * 8192 ** 3 / (s.elapsed_time(e) * 1e-3) / 1e12)
-    torch.backends.cuda.matmul.allow_tf32 = False
-    del a, b
-    torch.cuda.empty_cache()
-    return best
+def tf32_peak_of(peaks):
+    """Dense TF32 tensor-core peak = half the MEASURED dense BF16 peak (the
+    B200's TF32:BF16 dense ratio is 1:2); burst figure, as the roofline kernel
+    is timed per launch.  Committed, not re-measured per run, so the fraction
+    moves only when the kernel does."""
+    if "bf16_tflops" in peaks:
+        return peaks["bf16_tflops"] / 2.0, "MEASURED_PEAKS.json bf16_tflops / 2 (dense TF32 = 1/2 dense BF16)"
+    return 1125.0, "fallback: 2250 TF/s nominal dense BF16 / 2 (MEASURED_PEAKS.json absent)"
 
 
-def datastore_block(args, net, grid, plan, ctx, W):
+def datastore_block(args, net, grid, plan, ctx, W, dtype=None):
     """This rank's pinned input block (the datastore's transfer copy: int8
     when the int16 voxels fit, see DataStore.transfer_block) from a one-sample HSB1 dataset
     written for the bench (synthetic voxels in the reference fixture range
@@ -277,7 +350,40 @@ def datastore_block(args, net, grid, plan, ctx, W):
     man = DS.load_manifest(root / "manifest.json")
     store = DS.DataStore(man, grid, ctx.rank)
     DS.ingest_epoch0(store, DS.epoch_schedule(0, 0, 1, 1, 1))
-    return store.transfer_block(0).unsqueeze(0)
+    return store.transfer_block(0, dtype).unsqueeze(0)
+
+
+def gpu_full_step_128(ctx, steps: int = 20):
+    """Our CosmoFlow-128 (n=1, one GPU) full training step, CUDA-graph replay,
+    device-timed: the like-for-like partner of the reference arm's measured
+    full step at 128^3 (no extrapolation on either side)."""
+    import torch
+
+    from paper_2007_12856_b200 import engine
+    from paper_2007_12856_b200.geometry import ProcessGrid
+    from paper_2007_12856_b200.networks import build_cosmoflow
+
+    net = build_cosmoflow(128)
+    plan = engine.make_plan(net, ProcessGrid(1, 1, 1, 1), 1, 128)
+    state = engine.make_state(net, 0)
+    x, y, ids = engine.synthetic_batch_full(net, 128, 1, 0)
+    batch = engine.scatter_batch(plan, x, y, ids, 0)
+    first_loss = engine.train_step(ctx, plan, state, batch, 1e-3)
+    cap = engine.CapturedStep(ctx, plan, state, batch, 1e-3)
+    for _ in range(3):
+        cap(1e-3)
+    torch.cuda.synchronize()
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record()
+    for _ in range(steps):
+        cap(1e-3)
+    s1.record()
+    torch.cuda.synchronize()
+    ms = s0.elapsed_time(s1) / steps
+    del cap, state, batch
+    torch.cuda.empty_cache()
+    return {"workload": "cosmoflow128 n=1 full train step (fwd+bwd+allreduce+adam), 1 GPU, CUDA-graph replay",
+            "ms_per_step": ms, "samples_per_s": 1000.0 / ms, "steps_timed": steps, "loss_first_step": first_loss}
 
 
 def run_ours(args):
@@ -309,7 +415,7 @@ def run_ours(args):
     plan = engine.make_plan(net, grid, n_global, W)
     ctx.prepare_groups([plan.leads])
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
-    tf32_peak = tf32_peak_tflops() if rank == 0 else 0.0
+    tf32_peak, tf32_src = tf32_peak_of(peaks)
 
     state = engine.make_state(net, 0)
     x, y, ids = engine.synthetic_batch_full(net, W, n_global, 0)
@@ -323,7 +429,7 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
 
     def eager_step():
-        return engine.train_step(ctx, plan, state, batch, 1e-4)
+        return engine.train_step(ctx, plan, state, batch, 1e-4, as_tensor=True)
 
     for _ in range(args.warmup):
         eager_step()
@@ -347,6 +453,7 @@ def run_ours(args):
     # cannot carry per-layer events); also counts this library's launches
     nprof = min(args.steps, 5)
     launches0 = lib.vpx_launch_count()
+    fb0 = lib.vpx_fallback_count()
     rec = Recorder()
     with rec:
         torch.cuda.synchronize()
@@ -358,6 +465,7 @@ def run_ours(args):
         torch.cuda.synchronize()
     losses = {"eager_profiled": float(loss.item())}
     launches_per_step = (lib.vpx_launch_count() - launches0) / nprof
+    fallbacks = (lib.vpx_fallback_count() - fb0) / nprof
     ms_eager = p0.elapsed_time(p1)
     ctx.barrier()
 
@@ -428,7 +536,7 @@ def run_ours(args):
                 "first_nonfinite_step": first_nan,
                 "input_path": note}
 
-    e2e = e2e_fp32 = None
+    e2e = e2e_fp32 = e2e_i16 = None
     if not args.no_e2e:
         ds_block = datastore_block(args, net, grid, plan, ctx, W) if batch.x_block is not None else None
         if ds_block is not None:
@@ -439,16 +547,36 @@ def run_ours(args):
                                      f") -> engine.HostInputPipeline (H2D {nb} B/voxel on a copy stream, "
                                      "double-buffered) -> vpx_layout_ncdhw_i" + ("8" if nb == 1 else "16") +
                                      "_to_frame (int->fp32 + layout); loss.item() each step")
+        if ds_block is not None and ds_block.dtype != torch.int16:
+            # the general case: voxels that do not fit int8 travel in the int16 storage dtype
+            e2e_i16 = time_e2e(datastore_block(args, net, grid, plan, ctx, W, torch.int16),
+                               "HSB1 sample file -> DataStore.ingest_epoch0 (pinned int16 cache) -> "
+                               "DataStore.transfer_block(dtype=int16) -> engine.HostInputPipeline (H2D 2 B/voxel) "
+                               "-> vpx_layout_ncdhw_i16_to_frame; loss.item() each step")
         e2e_fp32 = time_e2e(x_host, "pinned host fp32 NCDHW array -> engine.HostInputPipeline (copy stream, "
                                     "double-buffered) -> frame; loss.item() each step")
         if e2e is None:
             e2e = e2e_fp32
 
+    aux128 = None
+    if world == 1 and args.net == "cosmoflow" and W != 128 and not args.no_aux:
+        aux128 = gpu_full_step_128(ctx)
     if rank != 0:
         return
     # --------------------------------------------------- roofline of top kernel
     hbm = peaks.get("hbm_gbs", 6650.0)
-    top_tag, top = max(kern.items(), key=lambda kv: kv[1]["ms"]) if kern else (None, None)
+    compute = {k: v for k, v in kern.items() if not k.startswith("comm.")}
+    top_tag, top = max(compute.items(), key=lambda kv: kv[1]["ms"]) if compute else (None, None)
+    halo = None
+    if "comm.halo" in kern:
+        h = kern["comm.halo"]
+        gbs_h = h["bytes_total"] / (h["ms"] * 1e-3) / 1e9
+        halo = {"bound": "nvlink", "achieved": gbs_h, "peak": NVLINK_GBS, "unit": "GB/s", "frac": gbs_h / NVLINK_GBS,
+                "bytes_per_step": h["bytes_total"] / nprof, "rounds_per_step": h["launches"] / nprof,
+                "ms_per_step": h["ms"] / nprof, "path": ctx.halo_path,
+                "note": "bytes this rank sends per halo round (both faces) / round duration on the compute "
+                        "stream (pack + NVLink transfer + wait for the neighbour + unpack), eager steps; "
+                        "peak = NVLink 5 per-direction bandwidth per GPU"}
     roof = None
     if top:
         per_launch_s = top["ms"] / top["launches"] * 1e-3
@@ -459,7 +587,7 @@ def run_ours(args):
         if top["flops"] and f_t >= f_h:
             roof = {"bound": "tensor", "achieved": tf, "peak": tf32_peak, "unit": "TFLOP/s", "frac": f_t,
                     "traffic": None, "kernel": top_tag,
-                    "peak_source": "cuBLAS TF32 8192^3 measured live in this run"}
+                    "peak_source": tf32_src}
         else:
             roof = {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": f_h, "traffic": None,
                     "kernel": top_tag, "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"}
@@ -476,9 +604,10 @@ def run_ours(args):
 
         use_ref = build_oracle.build_reference_kernels() is not None
         threads = os.cpu_count() or 1
-        v, desc, _ = cpu_sample(W, args.cpu_budget, threads, use_ref)
+        v, desc, _, frac = cpu_sample(W, args.cpu_budget, threads, use_ref)
         cpu = {"value": v, "unit": "samples/s", "cores": threads, "kind": "reference" if use_ref else "port",
-               "sample": desc}
+               "sample": desc, "extrapolated": True, "sample_conv_flop_fraction": frac,
+               "measured_full_step": reference_full_step(128, 1, threads)}
     line = {
         "metric": (f"U-Net-mini {W}^3 samples/sec" if args.net == "unet" else f"CosmoFlow {W}^3 samples/sec"),
         "value": value, "unit": "samples/s", "n_gpus": world,
@@ -491,9 +620,12 @@ def run_ours(args):
                    "l2": "inputs larger than L2 (no flush needed)",
                    "storage": "fp32 NDHWC, TF32 tensor-core math", "halo": ctx.halo_path},
         "roofline": roof,
+        "halo_roofline": halo,
         "cpu_baseline": cpu,
         "e2e": e2e,
+        "e2e_int16_host_input": e2e_i16,
         "e2e_fp32_host_input": e2e_fp32,
+        "cosmoflow128_full_step": aux128,
         "gpu_launches": launches,
         "step_mode": graph_note,
         "kernel_timing": f"per-layer CUDA events over {nprof} eager steps ({ms_eager / nprof:.3f} ms/step eager)",
@@ -503,7 +635,9 @@ def run_ours(args):
         "kernels": breakdown,
         "loss": losses["timed"],
         "loss_by_phase": dict(losses, e2e=(e2e or {}).get("loss"),
+                              e2e_int16_host_input=(e2e_i16 or {}).get("loss"),
                               e2e_fp32_host_input=(e2e_fp32 or {}).get("loss")),
+        "cuda_core_fallbacks_per_step": fallbacks,
     }
     print(json.dumps(line), flush=True)
 

@@ -42,6 +42,9 @@ const char* vpx_last_error(void);
 const char* vpx_version(void);
 /* Total number of CUDA kernels this library has launched in this process. */
 long long vpx_launch_count(void);
+/* Conv passes that fell back to the generic CUDA-core kernels while in TF32
+ * mode (no tcgen05 kernel covers the shape); bench.py reports it per step. */
+long long vpx_fallback_count(void);
 /* Numeric mode.  0 (default) = TF32: convolutions on tcgen05 tensor cores,
  * activations/gradients stored rounded to nearest TF32 so the MMA operands
  * are exact and the rounding unbiased (north-star tolerance rtol 1e-3).

@@ -287,6 +287,7 @@ static int conv_fwd_impl(const float* x, const int* xfr, const float* w, int k, 
   }
   if (vpx::small_conv_supported(0, xf, yf, k, stride) && !getenv("VPX_NO_SMALL"))
     return vpx::small_conv_fwd(x, xf, w, k, y, yf, act, slope, st);
+  vpx::note_fallback();
   return vpx::conv_fwd_simt(x, xf, w, k, stride, y, yf, st, act, slope);
 }
 
@@ -350,6 +351,7 @@ static int conv_bwd_data_impl(const float* u, const int* ufr, const float* w, in
   }
   if (k == 1 && vpx::small_conv_supported(1, uf, gf, k, stride) && !getenv("VPX_NO_SMALL"))
     return vpx::small_conv_bwd_data(u, uf, w, xg, gf, st);
+  vpx::note_fallback();
   return vpx::conv_bwd_data_simt(u, uf, w, k, stride, xg, gf, st);
 }
 
@@ -403,6 +405,7 @@ static int conv_bwd_filter_impl(const float* x, const int* xfr, const float* u, 
     return finish(vpx::small_wgrad_parts(uf, k));
   }
   if (slice) VPX_FAIL(VPX_ERR_UNSUPPORTED, "conv bwd_filter: channel slices need a partial-sum kernel");
+  vpx::note_fallback();
   return vpx::conv_wgrad_simt(x, xf, u, uf, k, stride, wg, accumulate, part, st);
 }
 

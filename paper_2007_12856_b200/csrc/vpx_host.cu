@@ -5,6 +5,7 @@ namespace vpx {
 
 static thread_local char g_err[1024] = {0};
 std::atomic<long long> g_launches{0};
+std::atomic<long long> g_fallbacks{0};
 static int g_precision = 0;
 int precision() { return g_precision; }
 
@@ -68,6 +69,7 @@ int encode_tiled_strided(CUtensorMap* map, CUtensorMapDataType dtype, int rank, 
 extern "C" const char* vpx_last_error(void) { return vpx::g_err; }
 extern "C" const char* vpx_version(void) { return "libvpx sm_100a " VPX_GIT_REV; }
 extern "C" long long vpx_launch_count(void) { return vpx::g_launches.load(); }
+extern "C" long long vpx_fallback_count(void) { return vpx::g_fallbacks.load(); }
 extern "C" int vpx_set_precision(int mode) {
   if (mode != 0 && mode != 1) VPX_FAIL(VPX_ERR_UNSUPPORTED, "precision mode %d", mode);
   vpx::g_precision = mode;

@@ -19,6 +19,12 @@ void set_error(const char* fmt, ...);
 int precision();
 // Number of kernels this library has launched (vpx_launch_count()).
 extern std::atomic<long long> g_launches;
+// Conv passes that ran on the generic CUDA-core kernels (conv_simt.cu) while the
+// library is in TF32 tensor-core mode: no tcgen05 kernel covers that shape.
+extern std::atomic<long long> g_fallbacks;
+inline void note_fallback() {
+  if (precision() == 0) g_fallbacks.fetch_add(1, std::memory_order_relaxed);
+}
 
 #define VPX_FAIL(code, ...)        \
   do {                             \

@@ -36,12 +36,13 @@ class Recorder:
     def summary(self):
         """{tag: {"ms": total, "launches": k, "flops": per launch, "bytes": per launch}}"""
         torch.cuda.synchronize()
-        out = defaultdict(lambda: {"ms": 0.0, "launches": 0, "flops": 0, "bytes": 0})
+        out = defaultdict(lambda: {"ms": 0.0, "launches": 0, "flops": 0, "bytes": 0, "bytes_total": 0})
         for tag, fl, by, s, e in self.events:
             d = out[tag]
             d["ms"] += s.elapsed_time(e)
             d["launches"] += 1
             d["flops"], d["bytes"] = fl, by
+            d["bytes_total"] += by
         return dict(out)
 
 
