@@ -41,13 +41,13 @@ _CTYPES = {
 }
 
 
-def _parse_header():
+def _parse_header(header: Path = HEADER):
     """{name: (restype, [argtypes])} from the prototypes in include/vpx.h.
 
     Pointers of any type become c_void_p (callers pass torch data_ptr() or
     ctypes addresses); scalars map through _CTYPES.
     """
-    text = re.sub(r"/\*.*?\*/", "", HEADER.read_text(), flags=re.S)
+    text = re.sub(r"/\*.*?\*/", "", Path(header).read_text(), flags=re.S)
     protos = {}
     for m in re.finditer(r"^\s*((?:const\s+)?[\w ]+?\s*\**)\s*(vpx_\w+)\s*\(([^)]*)\)\s*;", text, re.M):
         ret, name, args = m.group(1).strip(), m.group(2), m.group(3)

@@ -252,9 +252,13 @@ namespace vpx {
 // 1 if the tcgen05 wgrad handles this layer (k = 3 checked by the caller).
 // stride 2 is handled in mode B only (Cin >= 64, the CosmoFlow c4 shape).
 int wgrad_tc_supported(const Frame& xf, const Frame& uf, int stride) {
-  if (uf.w % 8 || (uf.w > 128 && uf.w % 128)) return 0;
   if (uf.mw || uf.md || uf.mh) return 0;  // upstream gradients are margin-free
   const int cin = xf.c, cout = uf.c;
+  // W < 8 (CosmoFlow-512 c7 at 4^3): one 8-voxel K step per row, the u rows
+  // past W are TMA zero fill, so they add nothing (mode B only)
+  if (uf.w < 8)
+    return cin % 32 == 0 && cin >= 64 && (stride == 1 || stride == 2) && (cout == 128 || cout % 256 == 0);
+  if (uf.w % 8 || (uf.w > 128 && uf.w % 128)) return 0;
   if (stride == 1 && cin <= 32 && cin % 4 == 0) return cout == 8 || cout == 16 || cout == 32 || cout == 64;
   if (cin % 32 == 0 && cin >= 64 && uf.w <= 32 && (stride == 1 || stride == 2))
     return cout == 128 || cout % 256 == 0;
@@ -264,8 +268,7 @@ int wgrad_tc_supported(const Frame& xf, const Frame& uf, int stride) {
 // Number of partial slices the split-K reduction produces.
 int wgrad_tc_parts(const Frame& xf, const Frame& uf) {
   const int nsub = nsub_of(xf, uf);
-  const int wseg = uf.w < 128 ? uf.w : 128;
-  const long long rows = (long long)uf.n * uf.d * uf.h * (uf.w / wseg);
+  const long long rows = (long long)uf.n * uf.d * uf.h * (uf.w < 8 ? 1 : uf.w / (uf.w < 128 ? uf.w : 128));
   // one CTA per SM (smem-limited): nsub * P must not exceed the SM count, or the
   // leftover CTAs run as a second wave and double the kernel time
   long long P = num_sms() / nsub;
@@ -284,8 +287,8 @@ int conv_wgrad_tc(const float* x, const Frame& xf, const float* u, const Frame& 
   p.w = uf.w;
   p.cin = xf.c;
   p.cout = uf.c;
-  p.wseg = uf.w < 128 ? uf.w : 128;
-  p.nxseg = uf.w / p.wseg;
+  p.wseg = uf.w < 8 ? 8 : uf.w < 128 ? uf.w : 128;
+  p.nxseg = uf.w < 8 ? 1 : uf.w / p.wseg;
   p.rows = (long long)uf.n * uf.d * uf.h * p.nxseg;
   p.nsub = nsub_of(xf, uf);
   p.P = wgrad_tc_parts(xf, uf);

@@ -16,6 +16,8 @@ def test_library_loads_and_exports_all_declared_symbols():
     for n in names:
         assert hasattr(raw, n), n
     assert b"sm_100a" in lib.vpx_version()
+    # measurement probes live in tools/libvpx_probe.so, not in the product library
+    assert not any(hasattr(raw, n) for n in ("vpx_probe_umma", "vpx_probe_tma", "vpx_probe_mma_rate2"))
 
 
 def test_shape_errors_map_to_reference_exceptions():

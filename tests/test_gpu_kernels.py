@@ -80,6 +80,10 @@ CASES = [
     (2, 32, 64, 4, 4, 32, 3, 1),
     (1, 64, 128, 16, 16, 16, 3, 2),
     (1, 256, 256, 8, 8, 8, 3, 1),
+    # W < 8 filter gradients (one zero-padded 8-voxel K step per row): CosmoFlow-512 c7, stride-2 c4 at 8^3
+    (1, 256, 256, 4, 4, 4, 3, 1),
+    (2, 128, 256, 4, 4, 4, 3, 1),
+    (1, 64, 128, 8, 8, 8, 3, 2),
 ]
 
 

@@ -81,6 +81,7 @@ def no_halo(monkeypatch):
 @pytest.mark.parametrize("blk", BLOCKS, ids=[b[0] for b in BLOCKS])
 def test_cosmoflow512_block_slab(blk, split, no_halo):
     name, cin, cout, s, ext, dslab = blk
+    fb0 = _lib.load().vpx_fallback_count()
     if split and name in ("c6", "c7"):
         pytest.skip("8-way split redistributes before these blocks (engine.make_plan)")
     net = build_cosmoflow(512)
@@ -133,6 +134,7 @@ def test_cosmoflow512_block_slab(blk, split, no_halo):
         D.first_block_wgrad(ctx, x, act, up, SLOPE, "average", wg, tag=name)
         wg_ref = O._f64(O.k_conv3d_bwd_filter, xpad, g_ref, (s, s, s), (3, 3, 3))
         assert rel(wg.cpu().numpy(), wg_ref) < RTOL, (name, "wgrad (pooled, mask)", rel(wg.cpu().numpy(), wg_ref))
+        assert _lib.load().vpx_fallback_count() == fb0, "a CUDA-core fallback ran"
         return
     g = D.dist_pool_leaky_bwd(act, up, SLOPE, "average", om, tag=f"{name}_act")
     g_dev = g.numpy()
@@ -146,3 +148,4 @@ def test_cosmoflow512_block_slab(blk, split, no_halo):
     got = _full(gx)
     assert got.shape == ref.shape
     assert rel(got, ref) < RTOL, (name, "dgrad (frame incl. margins)", rel(got, ref))
+    assert _lib.load().vpx_fallback_count() == fb0, f"{name}: a conv pass fell back to the CUDA-core kernels"

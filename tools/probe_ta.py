@@ -16,7 +16,8 @@ import torch
 
 sys.path.insert(0, ".")
 sys.path.insert(0, "tools")
-from paper_2007_12856_b200 import _lib  # noqa: E402
+from paper_2007_12856_b200 import _lib
+import probe_lib  # noqa: E402
 from probe_umma import Img, check, idesc, sdesc, swz, tf32, RESULTS  # noqa: E402
 
 rng = np.random.default_rng(1)
@@ -28,7 +29,7 @@ def run_ta(img_bytes, ops, ta, ncols):
     ops_t = torch.from_numpy(ops_arr.view(np.int64)).cuda()
     ta_t = torch.from_numpy(np.ascontiguousarray(ta, dtype=np.float32)).cuda()
     out = torch.zeros(128 * ncols, dtype=torch.float32, device="cuda")
-    _lib.call("vpx_probe_umma_ta", img.data_ptr(), img.numel(), ops_t.data_ptr(), len(ops), ta_t.data_ptr(),
+    probe_lib.call("vpx_probe_umma_ta", img.data_ptr(), img.numel(), ops_t.data_ptr(), len(ops), ta_t.data_ptr(),
               ta.shape[1], out.data_ptr(), ncols, torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     return out.cpu().numpy().reshape(128, ncols)
@@ -92,7 +93,7 @@ def t_rate():
     res = {}
     for N, n_acc in ((16, 8), (32, 8), (48, 8), (48, 9), (64, 4), (96, 2), (128, 2), (256, 1)):
         for mode in ((0, 2, 3, 5, 6, 7, 8, 9) if (N, n_acc) == (48, 9) else (0, 2, 3)):
-            _lib.call("vpx_probe_mma_rate2", N, n_acc, mode, 4096, cyc.data_ptr(),
+            probe_lib.call("vpx_probe_mma_rate2", N, n_acc, mode, 4096, cyc.data_ptr(),
                       torch.cuda.current_stream().cuda_stream)
             torch.cuda.synchronize()
             c = int(cyc.item()) / 4096

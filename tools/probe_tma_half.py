@@ -7,6 +7,7 @@ import numpy as np
 import torch
 
 from paper_2007_12856_b200 import _lib
+import probe_lib  # noqa: E402
 
 W, C = 64, 16
 X = np.zeros((W, C), np.float32)
@@ -25,7 +26,7 @@ for sw in (1282, 128, 32):
         out = torch.full((nbytes // 4,), -1.0, dtype=torch.float32, device="cuda")
         ok = torch.zeros(1, dtype=torch.int32, device="cuda")
         try:
-            _lib.call("vpx_probe_tma", g.data_ptr(), ctypes.addressof(dims), ctypes.addressof(strides),
+            probe_lib.call("vpx_probe_tma", g.data_ptr(), ctypes.addressof(dims), ctypes.addressof(strides),
                       ctypes.addressof(box), ctypes.addressof(ONES), sw, ctypes.addressof(coords), out.data_ptr(),
                       nbytes, ok.data_ptr(), torch.cuda.current_stream().cuda_stream)
             torch.cuda.synchronize()

@@ -14,7 +14,8 @@ import numpy as np
 import torch
 
 sys.path.insert(0, ".")
-from paper_2007_12856_b200 import _lib  # noqa: E402
+from paper_2007_12856_b200 import _lib
+import probe_lib  # noqa: E402
 
 rng = np.random.default_rng(0)
 RESULTS = {}
@@ -53,7 +54,7 @@ def run(img_bytes: np.ndarray, ops, ncols=64):
     ops_arr = np.array(ops, dtype=np.uint64).reshape(-1)
     ops_t = torch.from_numpy(ops_arr.view(np.int64)).cuda()
     out = torch.zeros(128 * ncols, dtype=torch.float32, device="cuda")
-    _lib.call("vpx_probe_umma", img.data_ptr(), img.numel(), ops_t.data_ptr(), len(ops), out.data_ptr(),
+    probe_lib.call("vpx_probe_umma", img.data_ptr(), img.numel(), ops_t.data_ptr(), len(ops), out.data_ptr(),
               ncols, torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     return out.cpu().numpy().reshape(128, ncols)
@@ -257,7 +258,7 @@ def t_tma():
     nbytes = 4 * 18 * 3 * 2 * 4
     out = torch.zeros(nbytes // 4, dtype=torch.float32, device="cuda")
     ok = torch.zeros(1, dtype=torch.int32, device="cuda")
-    _lib.call("vpx_probe_tma", g.data_ptr(), ctypes.addressof(dims), ctypes.addressof(strides),
+    probe_lib.call("vpx_probe_tma", g.data_ptr(), ctypes.addressof(dims), ctypes.addressof(strides),
               ctypes.addressof(box), ctypes.addressof(ONES), 0, ctypes.addressof(coords), out.data_ptr(), nbytes,
               ok.data_ptr(), torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
@@ -278,7 +279,7 @@ def t_tma():
     nbytes = 16 * 128
     out = torch.zeros(nbytes // 4, dtype=torch.float32, device="cuda")
     ok = torch.zeros(1, dtype=torch.int32, device="cuda")
-    _lib.call("vpx_probe_tma", g2.data_ptr(), ctypes.addressof(dims), ctypes.addressof(strides),
+    probe_lib.call("vpx_probe_tma", g2.data_ptr(), ctypes.addressof(dims), ctypes.addressof(strides),
               ctypes.addressof(box), ctypes.addressof(ONES), 128, ctypes.addressof(coords), out.data_ptr(), nbytes,
               ok.data_ptr(), torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
@@ -301,7 +302,7 @@ def t_rate():
                 if N * nacc > 512:
                     continue
                 it = 1024
-                _lib.call("vpx_probe_mma_rate", N, it, 0, nacc, bf, cyc.data_ptr(),
+                probe_lib.call("vpx_probe_mma_rate", N, it, 0, nacc, bf, cyc.data_ptr(),
                           torch.cuda.current_stream().cuda_stream)
                 torch.cuda.synchronize()
                 c = int(cyc.item())
@@ -317,7 +318,7 @@ def t_rate2():
         for N, accs in ((16, (1, 4, 8)), (32, (1, 4, 8)), (64, (1, 4, 8)), (128, (1, 2)), (256, (1, 2))):
             for nacc in accs:
                 it = 2048
-                _lib.call("vpx_probe_mma_rate2", N, nacc, bf, it, cyc.data_ptr(),
+                probe_lib.call("vpx_probe_mma_rate2", N, nacc, bf, it, cyc.data_ptr(),
                           torch.cuda.current_stream().cuda_stream)
                 torch.cuda.synchronize()
                 c = int(cyc.item())
@@ -392,7 +393,7 @@ def t_tma32b():
     nbytes = 16 * 128
     out = torch.zeros(nbytes // 4, dtype=torch.float32, device="cuda")
     ok = torch.zeros(1, dtype=torch.int32, device="cuda")
-    _lib.call("vpx_probe_tma", g2.data_ptr(), ctypes.addressof(dims), ctypes.addressof(strides),
+    probe_lib.call("vpx_probe_tma", g2.data_ptr(), ctypes.addressof(dims), ctypes.addressof(strides),
               ctypes.addressof(box), ctypes.addressof(ONES), 1282, ctypes.addressof(coords), out.data_ptr(), nbytes,
               ok.data_ptr(), torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
@@ -421,7 +422,7 @@ def t_tma_strided():
     for nbytes in (Wb * Hb * 128, 4 * Wb * Hb * 128):
         out = torch.zeros(nbytes // 4, dtype=torch.float32, device="cuda")
         ok = torch.zeros(1, dtype=torch.int32, device="cuda")
-        _lib.call("vpx_probe_tma", g.data_ptr(), ctypes.addressof(dims), ctypes.addressof(strides),
+        probe_lib.call("vpx_probe_tma", g.data_ptr(), ctypes.addressof(dims), ctypes.addressof(strides),
                   ctypes.addressof(box), ctypes.addressof(est), 128, ctypes.addressof(coords), out.data_ptr(),
                   nbytes, ok.data_ptr(), torch.cuda.current_stream().cuda_stream)
         torch.cuda.synchronize()
@@ -460,7 +461,7 @@ def t_tma_narrow_swz():
         nbytes = box_w * 16
         out = torch.zeros(nbytes // 4, dtype=torch.float32, device="cuda")
         ok = torch.zeros(1, dtype=torch.int32, device="cuda")
-        _lib.call("vpx_probe_tma", g.data_ptr(), ctypes.addressof(dims), ctypes.addressof(strides),
+        probe_lib.call("vpx_probe_tma", g.data_ptr(), ctypes.addressof(dims), ctypes.addressof(strides),
                   ctypes.addressof(box), ctypes.addressof(ONES), 1282, ctypes.addressof(coords), out.data_ptr(),
                   nbytes, ok.data_ptr(), torch.cuda.current_stream().cuda_stream)
         torch.cuda.synchronize()
