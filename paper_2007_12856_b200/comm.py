@@ -205,6 +205,22 @@ class RankCtx:
             return "CUDA-IPC mailboxes over NVLink (PeerHalo)"
         return "NCCL send/recv" + (f" (IPC setup failed: {self.halo_error})" if getattr(self, "halo_error", None) else "")
 
+    def grad_group(self):
+        """A communicator of its own for the bucketed gradient all-reduce, so
+        its kernels (on grad_stream) never queue behind or interleave with the
+        halo / BatchNorm collectives of the world group.  Collective on first
+        use."""
+        g = getattr(self, "_grad_group", None)
+        if g is None and self.size > 1:
+            g = self._grad_group = dist.new_group(list(range(self.size)))
+        return g
+
+    def grad_stream(self):
+        st = getattr(self, "_grad_stream", None)
+        if st is None:
+            st = self._grad_stream = torch.cuda.Stream()
+        return st
+
     def comm_stream(self):
         """Side stream for exchanges overlapped with compute (one per process)."""
         st = getattr(self, "_comm_stream", None)

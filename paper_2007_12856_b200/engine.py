@@ -28,6 +28,7 @@ import os
 from dataclasses import dataclass, field
 
 import torch
+import torch.distributed as dist
 
 from . import _lib, prng
 from .accounting import out_shape
@@ -37,6 +38,7 @@ from .frames import DistTensor, stream_ptr
 from .geometry import DistTensorMeta, ProcessGrid, Shape5D, make_partition
 from . import layers as D
 from .networks import NetworkSpec, param_entries
+from .timing import region
 
 NO_HALO = (0, 0, 0)
 
@@ -485,16 +487,22 @@ def loss_and_grad(ctx: RankCtx, plan: Plan, pred, batch: Batch):
     return loss, g
 
 
-def backward(ctx: RankCtx, plan: Plan, state: RankState, stash, dpred, trace: dict = None):
-    """Backward pass writing gradient partials into the flat bucket."""
+def backward(ctx: RankCtx, plan: Plan, state: RankState, stash, dpred, trace: dict = None,
+             buckets: "GradBuckets" = None):
+    """Backward pass writing gradient partials into the flat bucket; with
+    `buckets`, finished buckets are all-reduced while lower layers run."""
     net = plan.net
     P, G, bn = state.params.views, state.params.grads, state.bn_states
     u = dpred
     extra = {}
     skip_below = None
     skip_one = None
+    if buckets is not None:
+        buckets.start()
     for i in range(len(net.layers) - 1, -1, -1):
         layer = net.layers[i]
+        if buckets is not None:
+            buckets.layers_done_above(i)
         kept = stash[i]
         if skip_below is not None and i >= skip_below:
             continue
@@ -600,8 +608,67 @@ def _skip_meta(plan: Plan, concat_layer):
     return make_partition(Shape5D(*o), src_in.grid, NO_HALO, src_in.rank_map)
 
 
-def gradient_allreduce(ctx: RankCtx, state: RankState):
-    """One flat allreduce over all ranks (reference engine.py:446-462)."""
+BUCKET_BYTES = int(os.environ.get("VPX_BUCKET_MB", "4")) << 20
+
+
+class GradBuckets:
+    """The flat gradient all-reduce (reference engine.py:446-462: one sum over
+    all ranks of the bucket in param_entries order) split into contiguous
+    buckets of >= BUCKET_BYTES at parameter boundaries and overlapped with the
+    backward pass: backward() visits layers last to first, so once it reaches
+    layer i every parameter of layers > i is final, and each bucket whose
+    parameters all belong to finished layers is reduced at once, on a
+    communication stream and a communicator of its own, while the lower
+    layers' kernels run.  The sum is the same (each element is reduced exactly
+    once over the same ranks); finish() joins the stream before the optimizer."""
+
+    def __init__(self, ctx: RankCtx, net: NetworkSpec, params: "FlatParams"):
+        self.ctx, self.params = ctx, params
+        owner = {name: net.layer_index(name.rsplit(".", 1)[0]) for name, _, _ in params.entries}
+        self.buckets = []  # (lo, hi, lowest owning layer)
+        lo, low = 0, None
+        for name, _, _ in params.entries:
+            pos, cnt = params.offsets[name]
+            low = owner[name] if low is None else min(low, owner[name])
+            if 4 * (pos + cnt - lo) >= BUCKET_BYTES:
+                self.buckets.append((lo, pos + cnt, low))
+                lo, low = pos + cnt, None
+        if lo < params.numel:
+            self.buckets.append((lo, params.numel, low))
+        self.pending = []
+        self.group = ctx.grad_group()
+        self.stream = ctx.grad_stream()
+
+    def start(self):
+        self.pending = sorted(range(len(self.buckets)), key=lambda b: -self.buckets[b][2])
+
+    def layers_done_above(self, i: int):
+        """Every layer with index > i has its gradients final: launch the
+        buckets they complete."""
+        while self.pending and self.buckets[self.pending[0]][2] > i:
+            self._launch(self.pending.pop(0))
+
+    def _launch(self, b):
+        lo, hi, _ = self.buckets[b]
+        cur = torch.cuda.current_stream()
+        self.stream.wait_stream(cur)
+        with torch.cuda.stream(self.stream):
+            view = self.params.grad[lo:hi]
+            with region("comm.allreduce_grad", 0, 4 * (hi - lo)):
+                dist.all_reduce(view, op=dist.ReduceOp.SUM, group=self.group)
+
+    def finish(self):
+        self.layers_done_above(-1)
+        torch.cuda.current_stream().wait_stream(self.stream)
+
+
+def gradient_allreduce(ctx: RankCtx, state: RankState, buckets: "GradBuckets" = None):
+    """Sum of the gradient bucket over all ranks (reference engine.py:446-462):
+    the buckets backward() has not launched yet, then the join; without
+    buckets (single rank or a caller-driven backward) one flat all-reduce."""
+    if buckets is not None:
+        buckets.finish()
+        return
     ctx.allreduce_sum_(state.params.grad, None)
 
 
@@ -614,13 +681,26 @@ def train_step(ctx: RankCtx, plan: Plan, state: RankState, batch: Batch, lr: flo
     step queues without any host synchronisation (except once per plan, when
     the halo mailboxes are set up); CapturedStep and the bench use that."""
     ctx.ensure_peer_halo(plan)
+    buckets = _buckets(ctx, plan, state)
     state.params.grad.zero_()
     pred, stash = forward(ctx, plan, state, batch, "train", seed, scalars=scalars)
     loss, dpred = loss_and_grad(ctx, plan, pred, batch)
-    backward(ctx, plan, state, stash, dpred)
-    gradient_allreduce(ctx, state)
+    backward(ctx, plan, state, stash, dpred, buckets=buckets)
+    gradient_allreduce(ctx, state, buckets)
     optimizer_step(state, lr, scalars)
     return loss if as_tensor else float(loss.item())
+
+
+def _buckets(ctx: RankCtx, plan: Plan, state: RankState):
+    """The overlapped bucketed all-reduce (GradBuckets) for multi-rank steps,
+    built once per (plan, state); VPX_FLAT_ALLREDUCE=1 keeps one flat
+    all-reduce after the backward pass."""
+    if ctx.size == 1 or os.environ.get("VPX_FLAT_ALLREDUCE") == "1":
+        return None
+    b = getattr(state, "_buckets", None)
+    if b is None or b[0] is not plan:
+        state._buckets = (plan, GradBuckets(ctx, plan.net, state.params))
+    return state._buckets[1]
 
 
 class StepScalars:
