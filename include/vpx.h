@@ -201,10 +201,14 @@ int vpx_bn_bwd_apply(const float* x, const int* xf, const float* u, const int* u
 /* ------------------------------------------------- transposed conv k2 s2 --
  * reference layers/reference.py:99-144 (w is (cin, cout, 2, 2, 2)). */
 long long vpx_deconv_workspace_bytes(int cin, int cout);
-int vpx_deconv_fwd(const float* x, const int* xf, const float* w, float* y, const int* yf,
-                   void* stream);
-int vpx_deconv_bwd_data(const float* u, const int* uf, const float* w, float* g, const int* gf,
-                        void* stream);
+/* TF32 mode: tcgen05 implicit GEMMs (forward: per fine parity class P a
+ * coarse-voxel x Cout GEMM over Cin with a stride-2 scatter epilogue;
+ * backward-data: a coarse-voxel x Cin GEMM over (P, Cout) gathering the fine
+ * gradient with TMA element stride 2).  ws: vpx_deconv_workspace_bytes. */
+int vpx_deconv_fwd(const float* x, const int* xf, const float* w, float* y, const int* yf, void* ws,
+                   long long ws_bytes, void* stream);
+int vpx_deconv_bwd_data(const float* u, const int* uf, const float* w, float* g, const int* gf, void* ws,
+                        long long ws_bytes, void* stream);
 int vpx_deconv_bwd_filter(const float* x, const int* xf, const float* u, const int* uf, float* wg,
                           int accumulate, void* ws, void* stream);
 

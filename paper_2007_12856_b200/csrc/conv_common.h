@@ -48,9 +48,14 @@ int num_sms();
 int rowwin_config(int cin, int cout, int* R, int* CG);
 struct Frame;
 long long tapbox_workspace_bytes(int cin, int cout);
-int tapbox_supported(int cin, int cout, int mode);
+int tapbox_supported(int cin, int cout, int mode, int kind = 0);
+// k2s2 transposed-conv filter gradient on tcgen05 (deconv_wgrad.cu)
+int deconv_wgrad_tc_supported(const Frame& xf, const Frame& uf);
+int deconv_wgrad_tc_parts(const Frame& xf);
+int deconv_wgrad_tc(const float* x, const Frame& xf, const float* u, const Frame& uf, float* part, cudaStream_t st);
 int conv_tapbox(int mode, const float* in, const Frame& inf, const float* w, int cin, int cout, int stride,
-                float* out, const Frame& of, int act, float slope, void* ws, cudaStream_t st, long long ws_bytes);
+                float* out, const Frame& of, int act, float slope, void* ws, cudaStream_t st, long long ws_bytes,
+                int kind = 0);
 int rowh_supported(int cin, int cout);
 long long rowh_packed_bytes(int cin, int cout);
 int rowh_pack(const float* w, int cout, int cin, int mode, float* dst, cudaStream_t st);

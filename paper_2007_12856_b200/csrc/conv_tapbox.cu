@@ -47,6 +47,8 @@ struct ConvTapParams {
   int act;
   float slope;
   int rnd;
+  int nvalid;                   // output channels actually stored (< NT only for an 8-channel deconv output)
+  int dcout;                    // > 0: transposed-conv forward with all 8 parities in N (n = P*dcout + co)
   int ksplit;                   // split of each tile's K entries across CTAs (1 = none)
   int base_tiles;               // tiles without the split
   float* part;                  // ksplit > 1: raw partial tiles [ks][base_tiles][128][NT]
@@ -57,6 +59,22 @@ struct ConvTapParams {
 namespace {
 
 using vpx::ConvTapParams;
+
+// Destination of output columns [col, col+4) of the voxel q = (qz, qy, qx):
+// the class-P output p = s*q + P, or (merged transposed conv) the parity of
+// the column's block.  nullptr when the position is outside the valid range.
+__device__ __forceinline__ float* tapbox_dst(const ConvTapParams& p, int n, int qz, int qy, int qx, int cls, int col) {
+  int P = cls, c = col;
+  if (p.dcout) {
+    P = col / p.dcout;
+    c = col % p.dcout;
+  }
+  const int pz = p.out_stride * qz + ((P >> 2) & 1), py = p.out_stride * qy + ((P >> 1) & 1),
+            px = p.out_stride * qx + (P & 1);
+  if (pz < p.pd_lo || pz >= p.pd_hi || py < p.ph_lo || py >= p.ph_hi || px < p.pw_lo || px >= p.pw_hi) return nullptr;
+  return p.out + static_cast<long long>(n) * p.out_sn + static_cast<long long>(pz + p.out_off_d) * p.out_sd +
+         static_cast<long long>(py + p.out_off_h) * p.out_sh + static_cast<long long>(px + p.out_off_w) * p.out_sw + c;
+}
 
 template <int NT, int S>
 __global__ void __launch_bounds__(256, 1)
@@ -195,8 +213,8 @@ __global__ void __launch_bounds__(256, 1)
       const int Pd = (cls >> 2) & 1, Ph = (cls >> 1) & 1, Pw = cls & 1;
       const int pz = p.out_stride * qz + Pd, py = p.out_stride * qy + Ph, px = p.out_stride * qx + Pw;
       const bool valid = dz < p.Db && qz < p.qd + p.QD && qy < p.qh + p.QH && qx < p.qw + p.QW &&
-                         pz >= p.pd_lo && pz < p.pd_hi && py >= p.ph_lo && py < p.ph_hi && px >= p.pw_lo &&
-                         px < p.pw_hi;
+                         (p.dcout || (pz >= p.pd_lo && pz < p.pd_hi && py >= p.ph_lo && py < p.ph_hi &&
+                                      px >= p.pw_lo && px < p.pw_hi));
       float* o = p.out + static_cast<long long>(n) * p.out_sn + static_cast<long long>(pz + p.out_off_d) * p.out_sd +
                  static_cast<long long>(py + p.out_off_h) * p.out_sh + static_cast<long long>(px + p.out_off_w) * p.out_sw +
                  nt * NT;
@@ -219,9 +237,19 @@ __global__ void __launch_bounds__(256, 1)
             if (p.act) v[i] = v[i] >= 0.f ? v[i] : p.slope * v[i];
             if (p.rnd) v[i] = vpx::tf32_rn(v[i]);
           }
-          float4* o4 = reinterpret_cast<float4*>(o + cb);
+          if (p.dcout) {
 #pragma unroll
-          for (int i = 0; i < 4; ++i) o4[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+            for (int i = 0; i < 4; ++i) {
+              float* d4 = tapbox_dst(p, n, qz, qy, qx, cls, nt * NT + cb + 4 * i);
+              if (d4) *reinterpret_cast<float4*>(d4) = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+            }
+          } else {
+            float4* o4 = reinterpret_cast<float4*>(o + cb);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              if (nt * NT + cb + 4 * i < p.nvalid)
+                o4[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+          }
         }
       }
       vpx::tc_fence_before();
@@ -260,9 +288,10 @@ __global__ void tapbox_reduce_kernel(const __grid_constant__ ConvTapParams p) {
     const int qz = p.qd + zt * p.Db + dz, qy = p.qh + yt * p.Hb + dy, qx = p.qw + xt * p.Wb + dx;
     const int Pd = (cls >> 2) & 1, Ph = (cls >> 1) & 1, Pw = cls & 1;
     const int pz = p.out_stride * qz + Pd, py = p.out_stride * qy + Ph, px = p.out_stride * qx + Pw;
-    const bool valid = dz < p.Db && qz < p.qd + p.QD && qy < p.qh + p.QH && qx < p.qw + p.QW && pz >= p.pd_lo &&
-                       pz < p.pd_hi && py >= p.ph_lo && py < p.ph_hi && px >= p.pw_lo && px < p.pw_hi;
-    if (!valid) continue;
+    const bool valid = dz < p.Db && qz < p.qd + p.QD && qy < p.qh + p.QH && qx < p.qw + p.QW &&
+                       (p.dcout || (pz >= p.pd_lo && pz < p.pd_hi && py >= p.ph_lo && py < p.ph_hi &&
+                                    px >= p.pw_lo && px < p.pw_hi));
+    if (!valid || nt * NT + 4 * c4 >= p.nvalid) continue;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int ks = 0; ks < p.ksplit; ++ks) {
       const float4 v = reinterpret_cast<const float4*>(
@@ -278,10 +307,12 @@ __global__ void tapbox_reduce_kernel(const __grid_constant__ ConvTapParams p) {
       if (p.act) o[j] = o[j] >= 0.f ? o[j] : p.slope * o[j];
       if (p.rnd) o[j] = vpx::tf32_rn(o[j]);
     }
-    float* dst = p.out + static_cast<long long>(n) * p.out_sn + static_cast<long long>(pz + p.out_off_d) * p.out_sd +
-                 static_cast<long long>(py + p.out_off_h) * p.out_sh + static_cast<long long>(px + p.out_off_w) * p.out_sw +
-                 nt * NT + 4 * c4;
-    *reinterpret_cast<float4*>(dst) = make_float4(o[0], o[1], o[2], o[3]);
+    float* dst = p.dcout ? tapbox_dst(p, n, qz, qy, qx, cls, nt * NT + 4 * c4)
+                         : p.out + static_cast<long long>(n) * p.out_sn +
+                               static_cast<long long>(pz + p.out_off_d) * p.out_sd +
+                               static_cast<long long>(py + p.out_off_h) * p.out_sh +
+                               static_cast<long long>(px + p.out_off_w) * p.out_sw + nt * NT + 4 * c4;
+    if (dst) *reinterpret_cast<float4*>(dst) = make_float4(o[0], o[1], o[2], o[3]);
   }
 }
 
@@ -307,7 +338,10 @@ int launch_tapbox(const CUtensorMap& xm, const CUtensorMap& wm, const ConvTapPar
 // Packed B: [entry][ntot][32]; value = Weff(o = row, i = 32*chunk + j, tap)
 //   mode 0 fwd:   w[o][i][tap]        (ntot = cout, i over cin)
 //   mode 1 dgrad: w[i][o][tap]        (ntot = cin,  i over cout)
-__global__ void pack_tapbox_kernel(const float* __restrict__ w, int cout, int cin, int mode,
+//   kind 1 (k2s2 transposed conv, w = (cin, cout, 8)):
+//   mode 1 fwd:   w[i][o][P]          (ntot = cout, i over cin)
+//   mode 0 dgrad: w[o][i][P]          (ntot = cin,  i over cout)
+__global__ void pack_tapbox_kernel(const float* __restrict__ w, int cout, int cin, int mode, int kind,
                                    const __grid_constant__ ConvTapParams tp, int n_entries, int ntot,
                                    float* __restrict__ out) {
   const long long total = (long long)n_entries * ntot * 32;
@@ -319,10 +353,20 @@ __global__ void pack_tapbox_kernel(const float* __restrict__ w, int cout, int ci
     const int i = 32 * ((tp.entries[e] >> 8) & 0xff) + j;
     const int tap = tp.entries[e] >> 16;
     float v = 0.f;
-    if (mode == 0) {
-      if (i < cin) v = w[((long long)o * cin + i) * 27 + tap];
-    } else {
-      if (i < cout) v = w[((long long)i * cin + o) * 27 + tap];
+    if (o < tp.nvalid) {
+      if (kind == 2) {  // merged transposed-conv forward: row o = P * cout + co
+        if (i < cin) v = w[((long long)i * cout + o % cout) * 8 + o / cout];
+      } else if (kind == 1) {
+        if (mode == 1) {
+          if (i < cin) v = w[((long long)i * cout + o) * 8 + tap];
+        } else {
+          if (i < cout) v = w[((long long)o * cout + i) * 8 + tap];
+        }
+      } else if (mode == 0) {
+        if (i < cin) v = w[((long long)o * cin + i) * 27 + tap];
+      } else {
+        if (i < cout) v = w[((long long)i * cin + o) * 27 + tap];
+      }
     }
     out[idx] = vpx::tf32_rn(v);
   }
@@ -363,24 +407,55 @@ long long tapbox_workspace_bytes(int cin, int cout) {
   return (long long)kMaxEntries * ntot * 32 * 4;
 }
 
-int tapbox_supported(int cin, int cout, int mode) {
-  const int ntot = mode == 0 ? cout : cin;
+int tapbox_supported(int cin, int cout, int mode, int kind) {
+  int ntot = (mode == 0) == (kind == 0) ? cout : cin;
+  if (kind == 1 && ntot == 8) ntot = 16;  // 8-channel deconv outputs: N tile 16, stores masked
   // N tiles with a kernel instance: 16/32/64/128/256, or a multiple of 256
   return ntot == 16 || ntot == 32 || ntot == 64 || ntot == 128 || ntot % 256 == 0;
 }
 
 // mode 0: forward (stride 1 or 2); mode 1: backward-data (stride 1 or 2).
 // in: input frame (x for fwd, u for dgrad); out: output frame.
+// kind 0: 3x3x3 conv, mode 0 forward (stride 1 or 2), mode 1 backward-data.
+// kind 1: k2s2 transposed conv (reference layers/reference.py:99-131, weights
+//   (cin, cout, 2, 2, 2)), stride 2 implied: mode 1 = its forward (eight
+//   parity classes P of the fine output p = 2q + P, one tap each, reading the
+//   coarse input at q), mode 0 = its backward-data (the coarse gradient
+//   gathers the fine one at 2q + P, eight taps, TMA element stride 2).
+// in: the tensor streamed along K; out: the tensor written.
 int conv_tapbox(int mode, const float* in, const Frame& inf, const float* w, int cin, int cout, int stride,
-                float* out, const Frame& of, int act, float slope, void* ws, cudaStream_t st, long long ws_bytes) {
-  const int ntot = mode == 0 ? cout : cin;
-  const int kchan = mode == 0 ? cin : cout;  // channels along K
+                float* out, const Frame& of, int act, float slope, void* ws, cudaStream_t st, long long ws_bytes,
+                int kind) {
+  // transposed-conv forward as ONE GEMM per coarse-voxel tile: N = 8 parities x Cout,
+  // the epilogue scatters column block P to the fine voxel 2q + P
+  const bool merged = kind == 1 && mode == 1 && (8 * cout == 64 || 8 * cout == 128 || 8 * cout == 256);
+  const int nvalid = merged ? 8 * cout : (mode == 0) == (kind == 0) ? cout : cin;
+  const int ntot = (kind == 1 && nvalid == 8) ? 16 : nvalid;
+  const int kchan = (mode == 0) == (kind == 0) ? cin : cout;  // channels along K
   const int nchunks = (kchan + 31) / 32;
   ConvTapParams p{};
+  p.nvalid = nvalid;
+  p.dcout = merged ? cout : 0;
   int ne = 0;
-  const int ncls = (mode == 1 && stride == 2) ? 8 : 1;
+  if (kind == 1) stride = 2;
+  const int ncls = (mode == 1 && stride == 2 && !merged) ? 8 : 1;
   for (int cls = 0; cls < ncls; ++cls) {
     p.cls_start[cls] = ne;
+    if (merged) {
+      for (int ch = 0; ch < nchunks; ++ch) p.entries[ne++] = 1 | (1 << 2) | (1 << 4) | (ch << 8);
+      continue;
+    }
+    if (kind == 1) {
+      for (int P = 0; P < 8; ++P) {
+        if (mode == 1 && P != cls) continue;  // forward: class P uses tap P at offset 0
+        const int off[3] = {mode == 0 ? (P >> 2) & 1 : 0, mode == 0 ? (P >> 1) & 1 : 0, mode == 0 ? P & 1 : 0};
+        for (int ch = 0; ch < nchunks; ++ch) {
+          if (ne >= kMaxEntries) VPX_FAIL(VPX_ERR_UNSUPPORTED, "tapbox: more than %d K entries", kMaxEntries);
+          p.entries[ne++] = (off[0] + 1) | ((off[1] + 1) << 2) | ((off[2] + 1) << 4) | (ch << 8) | (P << 16);
+        }
+      }
+      continue;
+    }
     for (int tap = 0; tap < 27; ++tap) {
       const int t[3] = {tap / 9, (tap / 3) % 3, tap % 3};
       int off[3];
@@ -410,7 +485,7 @@ int conv_tapbox(int mode, const float* in, const Frame& inf, const float* w, int
     const long long total = (long long)ne * ntot * 32;
     int grid = static_cast<int>((total + 255) / 256);
     if (grid > 8192) grid = 8192;
-    pack_tapbox_kernel<<<grid, 256, 0, st>>>(w, cout, cin, mode, p, ne, ntot, wpack);
+    pack_tapbox_kernel<<<grid, 256, 0, st>>>(w, cout, cin, mode, merged ? 2 : kind, p, ne, ntot, wpack);
     VPX_LAUNCH_CHECK();
   }
   p.n = of.n;
@@ -422,6 +497,10 @@ int conv_tapbox(int mode, const float* in, const Frame& inf, const float* w, int
     QD = of.d;
     QH = of.h;
     QW = of.w;
+  } else if (kind == 1) {  // transposed conv: every coarse input voxel, interior outputs only
+    QD = inf.d;
+    QH = inf.h;
+    QW = inf.w;
   } else {
     // cover output positions [-m, e+m) of the xg frame: q in [(-m - 1)/s .. ]
     const int lo[3] = {-of.md, -of.mh, -of.mw};
@@ -500,7 +579,7 @@ int conv_tapbox(int mode, const float* in, const Frame& inf, const float* w, int
   p.out_off_h = of.mh;
   p.out_off_w = of.mw;
   p.out_stride = s_out;
-  if (mode == 0) {
+  if (mode == 0 || kind == 1) {
     p.pd_lo = 0, p.pd_hi = of.d, p.ph_lo = 0, p.ph_hi = of.h, p.pw_lo = 0, p.pw_hi = of.w;
   } else {
     p.pd_lo = -of.md, p.pd_hi = of.d + of.md, p.ph_lo = -of.mh, p.ph_hi = of.h + of.mh;

@@ -7,6 +7,9 @@
 // straight into their consumer's halo-wide frame (no reference-style _wrap
 // copy, reference layers/distributed.py:31-33).  Reductions are deterministic:
 // fixed block partition + fixed-order final sum, accumulated in fp64.
+#include <cstdlib>
+
+#include "conv_common.h"
 #include "conv_simt.h"
 #include "ops_vec.h"
 #include "vpx_round.cuh"
@@ -749,16 +752,37 @@ extern "C" int vpx_copy(const float* x, const int* xf, float* y, const int* yf, 
   copy_kernel<<<grid1d(VC(A) * A.c), 256, 0, S(st)>>>(x, A, y, B);
   LAUNCH_TAIL;
 }
-extern "C" int vpx_deconv_fwd(const float* x, const int* xf, const float* w, float* y, const int* yf,
-                              void* st) {
+static int deconv_shape_check(const Frame& coarse, const Frame& fine, const char* what) {
+  if (coarse.n != fine.n || fine.d != 2 * coarse.d || fine.h != 2 * coarse.h || fine.w != 2 * coarse.w)
+    VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "%s: fine (%d,%d,%d,%d) is not twice coarse (%d,%d,%d,%d)", what, fine.n,
+             fine.d, fine.h, fine.w, coarse.n, coarse.d, coarse.h, coarse.w);
+  return VPX_OK;
+}
+// TF32 mode: the transposed conv runs on tcgen05 through the tap-box implicit
+// GEMM (conv_tapbox.cu kind 1); FP32 mode (and channel counts without a
+// tensor-core tile) on the CUDA-core kernels.
+static bool deconv_tc(int cin, int cout, int mode) {
+  return vpx::precision() == 0 && cin % 4 == 0 && cout % 4 == 0 && vpx::tapbox_supported(cin, cout, mode, 1) &&
+         !getenv("VPX_NO_DECONV_TC");
+}
+extern "C" int vpx_deconv_fwd(const float* x, const int* xf, const float* w, float* y, const int* yf, void* ws,
+                              long long ws_bytes, void* st) {
   Frame A = F(xf), B = F(yf);
+  if (int rc = deconv_shape_check(A, B, "deconv fwd")) return rc;
+  if (deconv_tc(A.c, B.c, 1))
+    return vpx::conv_tapbox(1, x, A, w, A.c, B.c, 2, y, B, 0, 0.f, ws, S(st), ws_bytes, 1);
+  vpx::note_fallback();
   if (vpx::deconv_vec_supported(A.c, B.c)) return vpx::deconv_fwd_vec(x, A, w, y, B, S(st));
   deconv_fwd_kernel<<<grid1d(VC(B) * B.c), 256, 0, S(st)>>>(x, A, w, y, B);
   LAUNCH_TAIL;
 }
-extern "C" int vpx_deconv_bwd_data(const float* u, const int* uf, const float* w, float* g,
-                                   const int* gf, void* st) {
+extern "C" int vpx_deconv_bwd_data(const float* u, const int* uf, const float* w, float* g, const int* gf,
+                                   void* ws, long long ws_bytes, void* st) {
   Frame A = F(uf), B = F(gf);
+  if (int rc = deconv_shape_check(B, A, "deconv bwd_data")) return rc;
+  if (deconv_tc(B.c, A.c, 0))
+    return vpx::conv_tapbox(0, u, A, w, B.c, A.c, 2, g, B, 0, 0.f, ws, S(st), ws_bytes, 1);
+  vpx::note_fallback();
   if (vpx::deconv_vec_supported(B.c, A.c)) return vpx::deconv_dgrad_vec(u, A, w, g, B, S(st));
   deconv_bwd_data_kernel<<<grid1d(VC(B) * B.c), 256, 0, S(st)>>>(u, A, w, g, B);
   LAUNCH_TAIL;
@@ -767,7 +791,12 @@ extern "C" int vpx_deconv_bwd_data(const float* u, const int* uf, const float* w
 // (its tile loop is latency-bound), at least 256 for the generic one
 static long long deconv_parts_cap() { return 8LL * num_sms() > 256 ? 8LL * num_sms() : 256; }
 extern "C" long long vpx_deconv_workspace_bytes(int cin, int cout) {
-  return deconv_parts_cap() * cin * cout * 8 * 4;
+  const long long parts = deconv_parts_cap() * cin * cout * 8 * 4;
+  // tap-box path: packed weights + split-K partial tiles (conv_tapbox.cu)
+  const int nmax = cin > cout ? cin : cout;
+  const long long tb = (vpx::tapbox_workspace_bytes(cin, cout) + 255) / 256 * 256 +
+                       (long long)num_sms() * 128 * (nmax < 16 ? 16 : nmax) * 4;
+  return parts > tb ? parts : tb;
 }
 extern "C" int vpx_deconv_bwd_filter(const float* x, const int* xf, const float* u, const int* uf,
                                      float* wg, int accumulate, void* ws, void* st) {
@@ -776,6 +805,11 @@ extern "C" int vpx_deconv_bwd_filter(const float* x, const int* xf, const float*
   const int P = static_cast<int>(nv < 256 ? nv : 256);
   const long long chunk = (nv + P - 1) / P;
   const int len = A.c * B.c * 8;
+  if (vpx::precision() == 0 && vpx::deconv_wgrad_tc_supported(A, B) && !getenv("VPX_NO_DECONV_TC")) {
+    if (int rc = vpx::deconv_wgrad_tc(x, A, u, B, static_cast<float*>(ws), S(st))) return rc;
+    return vpx::reduce_partials(static_cast<float*>(ws), vpx::deconv_wgrad_tc_parts(A), len, wg, accumulate, S(st));
+  }
+  vpx::note_fallback();
   if (vpx::deconv_vec_supported(A.c, B.c)) {
     int Pv = 0;
     if (int rc = vpx::deconv_wgrad_vec(x, A, u, B, static_cast<float*>(ws), static_cast<int>(deconv_parts_cap()),

@@ -260,14 +260,18 @@ def dist_deconv3d(ctx: RankCtx, x: DistTensor, w: torch.Tensor, out_radii=NO_HAL
     gs = x.meta.global_shape
     y = _out(x.meta, Shape5D(gs.n, w.shape[1], 2 * gs.d, 2 * gs.h, 2 * gs.w), out_radii, x.grid_rank)
     with region(f"{tag}.fwd", 2 * 8 * x.voxels() * x.c * y.c, 4 * (x.voxels() * x.c + y.voxels() * y.c)):
-        _lib.call("vpx_deconv_fwd", x.ptr, x.desc, w.data_ptr(), y.ptr, y.desc, stream_ptr())
+        ws = WS.get(_lib.load().vpx_deconv_workspace_bytes(x.c, y.c))
+        _lib.call("vpx_deconv_fwd", x.ptr, x.desc, w.data_ptr(), y.ptr, y.desc, ws.data_ptr(), ws.numel() * 4,
+                  stream_ptr())
     return y
 
 
 def dist_deconv3d_bwd_data(ctx: RankCtx, u: DistTensor, w: torch.Tensor, in_meta, tag: str = "deconv") -> DistTensor:
     g = DistTensor(in_meta, u.grid_rank, zero=False)
     with region(f"{tag}.dgrad", 2 * u.voxels() * u.c * g.c, 4 * (u.voxels() * u.c + g.voxels() * g.c)):
-        _lib.call("vpx_deconv_bwd_data", u.ptr, u.desc, w.data_ptr(), g.ptr, g.desc, stream_ptr())
+        ws = WS.get(_lib.load().vpx_deconv_workspace_bytes(g.c, u.c))
+        _lib.call("vpx_deconv_bwd_data", u.ptr, u.desc, w.data_ptr(), g.ptr, g.desc, ws.data_ptr(), ws.numel() * 4,
+                  stream_ptr())
     return g
 
 

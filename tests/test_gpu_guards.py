@@ -182,3 +182,33 @@ def test_pointwise_kernels_stay_in_bounds(c, spatial, margins):
     _lib.call("vpx_layout_frame_to_ncdhw", yf.ptr, yf.desc, dst.t.data_ptr(), stream_ptr())
     torch.cuda.synchronize()
     assert dst.guards_intact() and bool(torch.isfinite(dst.t).all())
+
+
+@pytest.mark.parametrize("cin,cout,spatial,margins", [(32, 16, (2, 4, 64), (0, 0, 0)), (16, 8, (3, 2, 32), (1, 1, 0)),
+                                                     (16, 8, (2, 2, 40), (0, 0, 0))])
+def test_deconv_kernels_stay_in_bounds(cin, cout, spatial, margins):
+    """k2s2 transposed conv (tcgen05 tap-box kind 1 + deconv_wgrad.cu, or the
+    CUDA-core kernels where W is not a multiple of the 32-voxel segment)."""
+    rng = np.random.default_rng(4)
+    x = rng.uniform(-1, 1, (2, cin) + spatial).astype(np.float32)
+    fine = tuple(2 * e for e in spatial)
+    xf, gx = gframe(2, cin, *spatial, margins, x)
+    wt = Guarded(cin * cout * 8, torch.from_numpy((rng.uniform(-1, 1, (cin, cout, 2, 2, 2)) / 8).astype(np.float32)).cuda())
+    yf, gy = gframe(2, cout, *fine, margins)
+    yf.t.zero_()
+    W = Guarded(_lib.load().vpx_deconv_workspace_bytes(cin, cout) // 4 + 64)
+    _lib.call("vpx_deconv_fwd", xf.ptr, xf.desc, wt.t.data_ptr(), yf.ptr, yf.desc, W.t.data_ptr(), W.t.numel() * 4,
+              stream_ptr())
+    u = rng.uniform(-1, 1, (2, cout) + fine).astype(np.float32)
+    uf, gu = gframe(2, cout, *fine, (0, 0, 0), u)
+    gf, gg = gframe(2, cin, *spatial, margins)
+    gf.t.zero_()
+    _lib.call("vpx_deconv_bwd_data", uf.ptr, uf.desc, wt.t.data_ptr(), gf.ptr, gf.desc, W.t.data_ptr(),
+              W.t.numel() * 4, stream_ptr())
+    wg = Guarded(cin * cout * 8)
+    _lib.call("vpx_deconv_bwd_filter", xf.ptr, xf.desc, uf.ptr, uf.desc, wg.t.data_ptr(), 0, W.t.data_ptr(),
+              stream_ptr())
+    torch.cuda.synchronize()
+    for g in (gx, wt, gy, W, gu, gg, wg):
+        assert g.guards_intact()
+    assert finite(yf) and finite(gf) and bool(torch.isfinite(wg.t).all())

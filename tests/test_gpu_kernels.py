@@ -306,13 +306,15 @@ def test_pool_leaky_bn_deconv_vs_oracle(golden, fp32_mode):
     xf, uf = _frame_of(dx), _frame_of(du)
     yf = Frame(dx.shape[0], dw.shape[1], *(2 * e for e in dx.shape[2:]))
     wdev = torch.from_numpy(dw).cuda()
-    _lib.call("vpx_deconv_fwd", xf.ptr, xf.desc, wdev.data_ptr(), yf.ptr, yf.desc, stream_ptr())
+    W = torch.empty(_lib.load().vpx_deconv_workspace_bytes(dx.shape[1], dw.shape[1]) // 4, device="cuda")
+    _lib.call("vpx_deconv_fwd", xf.ptr, xf.desc, wdev.data_ptr(), yf.ptr, yf.desc, W.data_ptr(), W.numel() * 4,
+              stream_ptr())
     assert rel(yf.to_ncdhw().cpu().numpy(), A["deconv_y"]) < 1e-5
     gf = Frame(*dx.shape[:2], *dx.shape[2:])
-    _lib.call("vpx_deconv_bwd_data", uf.ptr, uf.desc, wdev.data_ptr(), gf.ptr, gf.desc, stream_ptr())
+    _lib.call("vpx_deconv_bwd_data", uf.ptr, uf.desc, wdev.data_ptr(), gf.ptr, gf.desc, W.data_ptr(), W.numel() * 4,
+              stream_ptr())
     assert rel(gf.to_ncdhw().cpu().numpy(), A["deconv_g"]) < 1e-5
     wg = torch.zeros_like(wdev)
-    W = torch.empty(_lib.load().vpx_deconv_workspace_bytes(dx.shape[1], dw.shape[1]) // 4, device="cuda")
     _lib.call("vpx_deconv_bwd_filter", xf.ptr, xf.desc, uf.ptr, uf.desc, wg.data_ptr(), 0, W.data_ptr(), stream_ptr())
     assert rel(wg.cpu().numpy(), A["deconv_wg"]) < 1e-5
 
@@ -401,16 +403,18 @@ def test_deconv_vectorised_vs_oracle(cin, cout, spatial, fp32_mode):
     xf = _frame_of(x)
     yf = Frame(2, cout, *(2 * e for e in spatial))
     wdev = torch.from_numpy(w).cuda()
-    _lib.call("vpx_deconv_fwd", xf.ptr, xf.desc, wdev.data_ptr(), yf.ptr, yf.desc, stream_ptr())
+    W = torch.empty(_lib.load().vpx_deconv_workspace_bytes(cin, cout) // 4, device="cuda")
+    _lib.call("vpx_deconv_fwd", xf.ptr, xf.desc, wdev.data_ptr(), yf.ptr, yf.desc, W.data_ptr(), W.numel() * 4,
+              stream_ptr())
     assert rel(yf.to_ncdhw().cpu().numpy(), O.deconv3d(x, w)) < 1e-5
     u = rng.standard_normal((2, cout) + tuple(2 * e for e in spatial)).astype(np.float32)
     uf = _frame_of(u)
     gf = Frame(2, cin, *spatial, (1, 1, 1), zero=True)
-    _lib.call("vpx_deconv_bwd_data", uf.ptr, uf.desc, wdev.data_ptr(), gf.ptr, gf.desc, stream_ptr())
+    _lib.call("vpx_deconv_bwd_data", uf.ptr, uf.desc, wdev.data_ptr(), gf.ptr, gf.desc, W.data_ptr(), W.numel() * 4,
+              stream_ptr())
     assert rel(gf.to_ncdhw().cpu().numpy(), O.deconv3d_bwd_data(u, w)) < 1e-5
     assert float(gf.t.abs().sum()) > 0 and gf.t[:, 0].abs().max().item() == 0.0  # margins untouched
     wg = torch.full_like(wdev, 0.5)
-    W = torch.empty(_lib.load().vpx_deconv_workspace_bytes(cin, cout) // 4, device="cuda")
     _lib.call("vpx_deconv_bwd_filter", xf.ptr, xf.desc, uf.ptr, uf.desc, wg.data_ptr(), 1, W.data_ptr(),
               stream_ptr())
     assert rel(wg.cpu().numpy() - 0.5, O.deconv3d_bwd_filter(x, u)) < 1e-5
@@ -619,3 +623,48 @@ def test_int8_transfer_layout_equals_int16(margins):
     torch.cuda.synchronize()
     assert torch.equal(a.t.view(torch.int32), b.t.view(torch.int32))
     assert np.array_equal(b.to_ncdhw().cpu().numpy(), v16.astype(np.float32))
+
+
+@pytest.mark.parametrize("cin,cout,spatial,margins", [(32, 16, (4, 6, 64), (0, 0, 0)), (16, 8, (3, 4, 40), (0, 0, 0)),
+                                                     (32, 16, (2, 8, 16), (1, 1, 0)), (16, 8, (4, 2, 24), (1, 0, 0)),
+                                                     (16, 8, (2, 3, 128), (0, 0, 0)), (32, 16, (3, 2, 32), (1, 1, 0))])
+def test_deconv_tensor_cores_vs_tf32_oracle(cin, cout, spatial, margins):
+    """TF32 mode: the k2s2 transposed conv forward and backward-data run as
+    tcgen05 implicit GEMMs (tap-box kernel, kind 1): rtol 1e-3 against the
+    TF32-emulating oracle (operands rounded to nearest TF32, fp64
+    accumulation), no CUDA-core fallback, output margins untouched by the
+    forward, D/H input margins read correctly.  Reference: reference.py:99-131."""
+    R = O.tf32_round
+    rng = np.random.default_rng(12)
+    x = R(rng.standard_normal((2, cin) + spatial).astype(np.float32))
+    w = (rng.standard_normal((cin, cout, 2, 2, 2)) / np.sqrt(8 * cin)).astype(np.float32)
+    xf = Frame(2, cin, *spatial, margins, zero=True).load_ncdhw(x)
+    fine = tuple(2 * e for e in spatial)
+    yf = Frame(2, cout, *fine, margins, zero=True)
+    wdev = torch.from_numpy(w).cuda()
+    W = torch.empty(_lib.load().vpx_deconv_workspace_bytes(cin, cout) // 4, device="cuda")
+    fb0 = _lib.load().vpx_fallback_count()
+    _lib.call("vpx_deconv_fwd", xf.ptr, xf.desc, wdev.data_ptr(), yf.ptr, yf.desc, W.data_ptr(), W.numel() * 4,
+              stream_ptr())
+    y_ref = R(O.deconv3d(x.astype(np.float64), R(w).astype(np.float64)).astype(np.float32))
+    assert rel(yf.to_ncdhw().cpu().numpy(), y_ref) < 1e-3
+    if any(margins):
+        inner = yf.interior.clone()
+        yf.interior.zero_()
+        assert float(yf.t.abs().max()) == 0.0, "forward wrote into the output margins"
+        yf.interior.copy_(inner)
+    u = R(rng.standard_normal((2, cout) + fine).astype(np.float32))
+    uf = Frame(2, cout, *fine).load_ncdhw(u)
+    gf = Frame(2, cin, *spatial, margins, zero=True)
+    _lib.call("vpx_deconv_bwd_data", uf.ptr, uf.desc, wdev.data_ptr(), gf.ptr, gf.desc, W.data_ptr(), W.numel() * 4,
+              stream_ptr())
+    g_ref = R(O.deconv3d_bwd_data(u.astype(np.float64), R(w).astype(np.float64)).astype(np.float32))
+    assert rel(gf.to_ncdhw().cpu().numpy(), g_ref) < 1e-3
+    assert _lib.load().vpx_fallback_count() == fb0, "deconv fell back to the CUDA-core kernels"
+    if spatial[2] % 32 == 0:  # filter gradient on tcgen05 (deconv_wgrad.cu): 32-voxel W segments
+        wg = torch.full_like(wdev, 0.25)
+        _lib.call("vpx_deconv_bwd_filter", xf.ptr, xf.desc, uf.ptr, uf.desc, wg.data_ptr(), 1, W.data_ptr(),
+                  stream_ptr())
+        wg_ref = O.deconv3d_bwd_filter(x.astype(np.float64), u.astype(np.float64)).astype(np.float32)
+        assert rel(wg.cpu().numpy() - 0.25, wg_ref) < 1e-3
+        assert _lib.load().vpx_fallback_count() == fb0, "deconv filter gradient fell back to CUDA cores"
