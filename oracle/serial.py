@@ -205,12 +205,14 @@ class TF32:
     recorded in `self.branches`, and `flips_outside_band()` lists any
     disagreement OUTSIDE that band (which is a real bug)."""
 
-    def __init__(self, device=None, tau=2.0 ** -11):
+    def __init__(self, device=None, tau=2.0 ** -11, tf32=True):
         self.device = device
         self.tau = tau
         self.branches = {}
-
-    r = staticmethod(tf32_round)
+        # tf32=False: the fp32 path's oracle -- no rounding, fp64 accumulation,
+        # the same tie-breaks with a band at fp32 accumulation noise (large
+        # volumes meet pre-activations that close to zero even in fp32)
+        self.r = tf32_round if tf32 else (lambda a: np.asarray(a, dtype=np.float32))
 
     def dev(self, layer_name):
         if self.device is None:

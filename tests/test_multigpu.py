@@ -86,6 +86,8 @@ STEPS = [  # grid, net, width, batch, precision
     ("2x2x1x1", "cosmoflow_bn", 32, 2, "fp32"),
     ("1x2x2x1", "unet", 16, 2, "tf32"),
     ("1x4x1x1", "cosmoflow", 128, 1, "tf32"),
+    # each rank's blocks, halos and redistribution point are those of the 8-way 512^3 bench grid
+    ("1x4x1x1", "cosmoflow", 256, 1, "fp32"),
 ]
 
 
