@@ -10,7 +10,7 @@ TAG=${1:-r1}
 shift || true
 OUT=gpurun_out
 mkdir -p $OUT
-BENCH="python bench.py --steps 3 --warmup 3 --no-cpu --no-e2e --no-graph $*"
+BENCH="python bench.py --steps 3 --warmup 3 --no-cpu --no-e2e --no-graph --no-aux $*"
 
 timeout 900 python bench.py "$@" > $OUT/${TAG}_bench.json 2> $OUT/${TAG}_bench.err || { echo "bench failed"; tail -5 $OUT/${TAG}_bench.err; exit 1; }
 timeout 300 $BENCH > $OUT/${TAG}_plain.json 2> $OUT/${TAG}_plain.err || { echo "plain bench failed"; exit 1; }
