@@ -212,6 +212,18 @@ int vpx_deconv_bwd_data(const float* u, const int* uf, const float* w, float* g,
 int vpx_deconv_bwd_filter(const float* x, const int* xf, const float* u, const int* uf, float* wg,
                           int accumulate, void* ws, void* stream);
 
+/* -------------------------------------------------------------- BF16 path --
+ * 3x3x3 conv forward / backward-data with bf16 storage (input and output
+ * frames NDHWC bf16, channel counts % 8 == 0) on tcgen05 kind::f16 with fp32
+ * accumulation; weights fp32 OIDHW (rounded to bf16 when packed).  Same
+ * semantics as vpx_conv3d_fwd / vpx_conv3d_bwd_data (reference _hot.pyx:19-67);
+ * north-star tolerance rtol 2e-2 against the fp32 reference.  ws:
+ * vpx_conv3d_workspace_bytes. */
+int vpx_conv3d_fwd_bf16(const void* x, const int* xf, const float* w, int k, int stride, void* y, const int* yf,
+                        void* ws, long long ws_bytes, void* stream);
+int vpx_conv3d_bwd_data_bf16(const void* u, const int* uf, const float* w, int k, int stride, void* g,
+                             const int* gf, void* ws, long long ws_bytes, void* stream);
+
 /* ------------------------------------------------------------------- halo --
  * Copy the box {n0,z0,y0,x0,en,ez,ey,ex} (frame coordinates, margins included)
  * of a frame to a dense (n,z,y,x,c) buffer (mode 0, pack), back (mode 1,

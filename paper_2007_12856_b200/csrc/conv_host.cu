@@ -590,3 +590,37 @@ extern "C" int vpx_conv3d_bwd_filter_c4_pooled(const float* x, const int* xfr, c
   if (int rc = vpx::conv_wgrad_c1_pooled(x, xf, y, yf, up, uf, slope, part, st)) return rc;
   return vpx::reduce_partials(part, P, 16 * 4 * 27, wg, accumulate, st);
 }
+
+// ------------------------------------------------------------------ BF16 path
+// 3x3x3 convolution forward / backward-data with bf16 operands on tcgen05
+// kind::f16 (fp32 accumulation): input frame and output frame in bf16
+// (NDHWC, channel rows of 2-byte elements), weights fp32 OIDHW rounded to
+// bf16 by the pack kernel.  The tap-box implicit GEMM, 64-channel K chunks.
+extern "C" int vpx_conv3d_fwd_bf16(const void* x, const int* xfr, const float* w, int k, int stride, void* y,
+                                   const int* yfr, void* ws, long long ws_bytes, void* stream) {
+  if (int rc = vpx::check_frame(xfr, "bf16 conv fwd input")) return rc;
+  if (int rc = vpx::check_frame(yfr, "bf16 conv fwd output")) return rc;
+  Frame xf = vpx::to_frame(xfr), yf = vpx::to_frame(yfr);
+  if (k != 3 || stride < 1 || stride > 2) VPX_FAIL(VPX_ERR_UNSUPPORTED, "bf16 conv: k=3, stride 1/2 only");
+  if (xf.c % 8 || !vpx::tapbox_supported(xf.c, yf.c, 0))
+    VPX_FAIL(VPX_ERR_UNSUPPORTED, "bf16 conv fwd: channels %d -> %d", xf.c, yf.c);
+  if (yf.n != xf.n || yf.d != (xf.d + stride - 1) / stride || yf.h != (xf.h + stride - 1) / stride ||
+      yf.w != (xf.w + stride - 1) / stride)
+    VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "bf16 conv fwd: output extents");
+  if (ws_bytes < vpx::tapbox_workspace_bytes(xf.c, yf.c)) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "workspace too small");
+  return vpx::conv_tapbox(0, static_cast<const float*>(x), xf, w, xf.c, yf.c, stride, static_cast<float*>(y), yf, 0,
+                          0.f, ws, static_cast<cudaStream_t>(stream), ws_bytes, 0, 3);
+}
+
+extern "C" int vpx_conv3d_bwd_data_bf16(const void* u, const int* ufr, const float* w, int k, int stride, void* g,
+                                        const int* gfr, void* ws, long long ws_bytes, void* stream) {
+  if (int rc = vpx::check_frame(ufr, "bf16 conv bwd_data input")) return rc;
+  if (int rc = vpx::check_frame(gfr, "bf16 conv bwd_data output")) return rc;
+  Frame uf = vpx::to_frame(ufr), gf = vpx::to_frame(gfr);
+  if (k != 3 || stride < 1 || stride > 2) VPX_FAIL(VPX_ERR_UNSUPPORTED, "bf16 conv: k=3, stride 1/2 only");
+  if (uf.c % 8 || !vpx::tapbox_supported(gf.c, uf.c, 1))
+    VPX_FAIL(VPX_ERR_UNSUPPORTED, "bf16 conv bwd_data: channels %d <- %d", gf.c, uf.c);
+  if (ws_bytes < vpx::tapbox_workspace_bytes(gf.c, uf.c)) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "workspace too small");
+  return vpx::conv_tapbox(1, static_cast<const float*>(u), uf, w, gf.c, uf.c, stride, static_cast<float*>(g), gf, 0,
+                          0.f, ws, static_cast<cudaStream_t>(stream), ws_bytes, 0, 3);
+}

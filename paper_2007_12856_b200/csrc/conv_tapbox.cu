@@ -12,6 +12,8 @@
 // stride-1 gather over u with its own list of taps (ConvTapParams.cls_*).
 // B = packed weights [entry][N_total][32] by 2D TMA, N tile <= 256.
 // Reference semantics: reference pkg/src/voxpar/kernels/_hot.pyx:19-67.
+#include <cuda_bf16.h>
+
 #include <cstdlib>
 
 #include "conv_common.h"
@@ -49,6 +51,7 @@ struct ConvTapParams {
   int rnd;
   int nvalid;                   // output channels actually stored (< NT only for an 8-channel deconv output)
   int dcout;                    // > 0: transposed-conv forward with all 8 parities in N (n = P*dcout + co)
+  int out_bf16;                 // 1: the output frame stores bf16 (BF16 path)
   int ksplit;                   // split of each tile's K entries across CTAs (1 = none)
   int base_tiles;               // tiles without the split
   float* part;                  // ksplit > 1: raw partial tiles [ks][base_tiles][128][NT]
@@ -76,11 +79,37 @@ __device__ __forceinline__ float* tapbox_dst(const ConvTapParams& p, int n, int 
          static_cast<long long>(py + p.out_off_h) * p.out_sh + static_cast<long long>(px + p.out_off_w) * p.out_sw + c;
 }
 
-template <int NT, int S>
+// Store 16 consecutive output channels at element offset `off` of the output
+// (fp32, or bf16 on the BF16 path: round to nearest even).
+__device__ __forceinline__ void tapbox_store16(const ConvTapParams& p, long long off, const float (&v)[16], int nmax) {
+  if (p.out_bf16) {
+    uint16_t* o = reinterpret_cast<uint16_t*>(p.out) + off;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (4 * i < nmax) {
+        const __nv_bfloat162 lo = __floats2bfloat162_rn(v[4 * i], v[4 * i + 1]);
+        const __nv_bfloat162 hi = __floats2bfloat162_rn(v[4 * i + 2], v[4 * i + 3]);
+        uint2 w;
+        w.x = *reinterpret_cast<const uint32_t*>(&lo);
+        w.y = *reinterpret_cast<const uint32_t*>(&hi);
+        *reinterpret_cast<uint2*>(o + 4 * i) = w;
+      }
+    return;
+  }
+  float4* o4 = reinterpret_cast<float4*>(p.out + off);
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    if (4 * i < nmax) o4[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+}
+
+// BF16 = true: kind::f16 MMAs on bf16 operands (64-channel K chunks = the same
+// 128-byte SWIZZLE_128B rows, K = 16 per MMA instead of 8), fp32 accumulation.
+template <int NT, int S, bool BF16>
 __global__ void __launch_bounds__(256, 1)
     conv_tapbox_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap wmap,
                        const ConvTapParams p) {
-  constexpr int ABYTES = 128 * 128;  // 128 voxel rows x 32 fp32
+  constexpr int ABYTES = 128 * 128;  // 128 voxel rows x 128 bytes (32 fp32 / 64 bf16 channels)
+  constexpr int CW = BF16 ? 64 : 32; // channels per K chunk
   constexpr int BBYTES = NT * 128;
   constexpr int STAGE = ABYTES + BBYTES;  // multiple of 1024
   constexpr int TCOLS = NT <= 32 ? 32 : NT <= 64 ? 64 : NT <= 128 ? 128 : 256;
@@ -149,7 +178,7 @@ __global__ void __launch_bounds__(256, 1)
           vpx::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * STAGE;
           vpx::mbar_arrive_expect_tx(&full[stage], a_tx + BBYTES);
-          vpx::tma_load_5d(sa, &xmap, &full[stage], 32 * chunk, p.in_stride * qx + ow + p.in_off_w,
+          vpx::tma_load_5d(sa, &xmap, &full[stage], CW * chunk, p.in_stride * qx + ow + p.in_off_w,
                            p.in_stride * qy + oh + p.in_off_h, p.in_stride * qz + od + p.in_off_d, n);
           vpx::tma_load_2d(sa + ABYTES, &wmap, &full[stage], 0, e * p.ntot + nt * NT);
           if (++stage == S) {
@@ -160,7 +189,7 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
   } else if (warp == 1) {
-    constexpr uint32_t idesc = vpx::make_idesc(2, 128, NT, false, false);
+    constexpr uint32_t idesc = vpx::make_idesc(BF16 ? 1 : 2, 128, NT, false, false);
     int stage = 0, acc = 0;
     uint32_t phase = 0, aphase = 0;
     for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
@@ -178,9 +207,13 @@ __global__ void __launch_bounds__(256, 1)
           const uint32_t a = vpx::smem_u32(smem + stage * STAGE);
           const uint32_t b = a + ABYTES;
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            vpx::umma_tf32(d, vpx::make_sdesc(a + 32 * k, 16, 1024, 2), vpx::make_sdesc(b + 32 * k, 16, 1024, 2),
-                           idesc, (e > e0 || k > 0) ? 1u : 0u);
+          for (int k = 0; k < 4; ++k) {
+            const uint64_t ad = vpx::make_sdesc(a + 32 * k, 16, 1024, 2), bd = vpx::make_sdesc(b + 32 * k, 16, 1024, 2);
+            if constexpr (BF16)
+              vpx::umma_f16(d, ad, bd, idesc, (e > e0 || k > 0) ? 1u : 0u);
+            else
+              vpx::umma_tf32(d, ad, bd, idesc, (e > e0 || k > 0) ? 1u : 0u);
+          }
           vpx::umma_commit(&empty[stage]);
           if (e == e1 - 1) vpx::umma_commit(&tfull[acc]);
         }
@@ -235,7 +268,7 @@ __global__ void __launch_bounds__(256, 1)
           for (int i = 0; i < 16; ++i) {
             if (empty_cls) v[i] = 0.f;
             if (p.act) v[i] = v[i] >= 0.f ? v[i] : p.slope * v[i];
-            if (p.rnd) v[i] = vpx::tf32_rn(v[i]);
+            if (p.rnd && !p.out_bf16) v[i] = vpx::tf32_rn(v[i]);
           }
           if (p.dcout) {
 #pragma unroll
@@ -244,11 +277,7 @@ __global__ void __launch_bounds__(256, 1)
               if (d4) *reinterpret_cast<float4*>(d4) = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
             }
           } else {
-            float4* o4 = reinterpret_cast<float4*>(o + cb);
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-              if (nt * NT + cb + 4 * i < p.nvalid)
-                o4[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+            tapbox_store16(p, (o - p.out) + cb, v, p.nvalid - (nt * NT + cb));
           }
         }
       }
@@ -305,22 +334,30 @@ __global__ void tapbox_reduce_kernel(const __grid_constant__ ConvTapParams p) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       if (p.act) o[j] = o[j] >= 0.f ? o[j] : p.slope * o[j];
-      if (p.rnd) o[j] = vpx::tf32_rn(o[j]);
+      if (p.rnd && !p.out_bf16) o[j] = vpx::tf32_rn(o[j]);
     }
     float* dst = p.dcout ? tapbox_dst(p, n, qz, qy, qx, cls, nt * NT + 4 * c4)
                          : p.out + static_cast<long long>(n) * p.out_sn +
                                static_cast<long long>(pz + p.out_off_d) * p.out_sd +
                                static_cast<long long>(py + p.out_off_h) * p.out_sh +
                                static_cast<long long>(px + p.out_off_w) * p.out_sw + nt * NT + 4 * c4;
-    if (dst) *reinterpret_cast<float4*>(dst) = make_float4(o[0], o[1], o[2], o[3]);
+    if (dst && p.out_bf16) {
+      const __nv_bfloat162 lo = __floats2bfloat162_rn(o[0], o[1]), hi = __floats2bfloat162_rn(o[2], o[3]);
+      uint2 w;
+      w.x = *reinterpret_cast<const uint32_t*>(&lo);
+      w.y = *reinterpret_cast<const uint32_t*>(&hi);
+      *reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(p.out) + (dst - p.out)) = w;
+    } else if (dst) {
+      *reinterpret_cast<float4*>(dst) = make_float4(o[0], o[1], o[2], o[3]);
+    }
   }
 }
 
-template <int NT>
+template <int NT, bool BF16 = false>
 int launch_tapbox(const CUtensorMap& xm, const CUtensorMap& wm, const ConvTapParams& p, cudaStream_t st) {
   constexpr int STAGE = 128 * 128 + NT * 128;
   constexpr int S = (200 * 1024) / STAGE >= 6 ? 6 : (200 * 1024) / STAGE;
-  auto kern = conv_tapbox_kernel<NT, S>;
+  auto kern = conv_tapbox_kernel<NT, S, BF16>;
   const int smem = S * STAGE + 1024;
   VPX_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const int grid = p.num_tiles < vpx::num_sms() ? p.num_tiles : vpx::num_sms();
@@ -372,22 +409,48 @@ __global__ void pack_tapbox_kernel(const float* __restrict__ w, int cout, int ci
   }
 }
 
-int encode_in_map(CUtensorMap* map, const float* base, const vpx::Frame& f, int Db, int Hb, int Wb, int s) {
-  const uint64_t Wf = f.w + 2 * f.mw, Hf = f.h + 2 * f.mh, Df = f.d + 2 * f.md;
-  uint64_t dims[5] = {(uint64_t)f.c, Wf, Hf, Df, (uint64_t)f.n};
-  uint64_t strides[4] = {(uint64_t)f.c * 4, Wf * f.c * 4, Hf * Wf * f.c * 4, Df * Hf * Wf * f.c * 4};
-  uint32_t box[5] = {32, (uint32_t)(s * Wb), (uint32_t)(s * Hb), (uint32_t)(s * Db), 1};
-  uint32_t estr[5] = {1, (uint32_t)s, (uint32_t)s, (uint32_t)s, 1};
-  return vpx::encode_tiled_strided(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float*>(base), dims,
-                                   strides, box, estr, CU_TENSOR_MAP_SWIZZLE_128B);
+// BF16 path: packed B [entry][ntot][64] bf16 (128-byte rows), 3x3x3 conv only.
+__global__ void pack_tapbox_bf16_kernel(const float* __restrict__ w, int cout, int cin, int mode,
+                                        const __grid_constant__ ConvTapParams tp, int n_entries, int ntot,
+                                        __nv_bfloat16* __restrict__ out) {
+  const long long total = (long long)n_entries * ntot * 64;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int j = idx % 64;
+    const int o = (idx / 64) % ntot;
+    const int e = static_cast<int>(idx / (64LL * ntot));
+    const int i = 64 * ((tp.entries[e] >> 8) & 0xff) + j;
+    const int tap = tp.entries[e] >> 16;
+    float v = 0.f;
+    if (o < tp.nvalid) {
+      if (mode == 0) {
+        if (i < cin) v = w[((long long)o * cin + i) * 27 + tap];
+      } else {
+        if (i < cout) v = w[((long long)i * cin + o) * 27 + tap];
+      }
+    }
+    out[idx] = __float2bfloat16_rn(v);
+  }
 }
 
-int encode_w_map(CUtensorMap* map, const float* base, long long rows, int NT) {
-  uint64_t dims[2] = {32, (uint64_t)rows};
-  uint64_t strides[1] = {32 * 4};
-  uint32_t box[2] = {32, (uint32_t)NT};
-  return vpx::encode_tiled(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box,
-                           CU_TENSOR_MAP_SWIZZLE_128B);
+int encode_in_map(CUtensorMap* map, const float* base, const vpx::Frame& f, int Db, int Hb, int Wb, int s,
+                  bool bf16 = false) {
+  const uint64_t Wf = f.w + 2 * f.mw, Hf = f.h + 2 * f.mh, Df = f.d + 2 * f.md;
+  const uint64_t eb = bf16 ? 2 : 4;  // bytes per element
+  uint64_t dims[5] = {(uint64_t)f.c, Wf, Hf, Df, (uint64_t)f.n};
+  uint64_t strides[4] = {(uint64_t)f.c * eb, Wf * f.c * eb, Hf * Wf * f.c * eb, Df * Hf * Wf * f.c * eb};
+  uint32_t box[5] = {bf16 ? 64u : 32u, (uint32_t)(s * Wb), (uint32_t)(s * Hb), (uint32_t)(s * Db), 1};
+  uint32_t estr[5] = {1, (uint32_t)s, (uint32_t)s, (uint32_t)s, 1};
+  return vpx::encode_tiled_strided(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5,
+                                   const_cast<float*>(base), dims, strides, box, estr, CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+int encode_w_map(CUtensorMap* map, const float* base, long long rows, int NT, bool bf16 = false) {
+  uint64_t dims[2] = {bf16 ? 64u : 32u, (uint64_t)rows};
+  uint64_t strides[1] = {128};
+  uint32_t box[2] = {bf16 ? 64u : 32u, (uint32_t)NT};
+  return vpx::encode_tiled(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                           const_cast<float*>(base), dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
 void tile_shape(int D, int H, int W, int* Db, int* Hb, int* Wb) {
@@ -425,14 +488,16 @@ int tapbox_supported(int cin, int cout, int mode, int kind) {
 // in: the tensor streamed along K; out: the tensor written.
 int conv_tapbox(int mode, const float* in, const Frame& inf, const float* w, int cin, int cout, int stride,
                 float* out, const Frame& of, int act, float slope, void* ws, cudaStream_t st, long long ws_bytes,
-                int kind) {
+                int kind, int bf16) {
   // transposed-conv forward as ONE GEMM per coarse-voxel tile: N = 8 parities x Cout,
   // the epilogue scatters column block P to the fine voxel 2q + P
   const bool merged = kind == 1 && mode == 1 && (8 * cout == 64 || 8 * cout == 128 || 8 * cout == 256);
   const int nvalid = merged ? 8 * cout : (mode == 0) == (kind == 0) ? cout : cin;
   const int ntot = (kind == 1 && nvalid == 8) ? 16 : nvalid;
   const int kchan = (mode == 0) == (kind == 0) ? cin : cout;  // channels along K
-  const int nchunks = (kchan + 31) / 32;
+  const int cw = (bf16 & 1) ? 64 : 32;                         // channels per K chunk (one 128-byte row)
+  const int nchunks = (kchan + cw - 1) / cw;
+  if ((bf16 & 1) && kind != 0) VPX_FAIL(VPX_ERR_UNSUPPORTED, "tapbox bf16: 3x3x3 conv only");
   ConvTapParams p{};
   p.nvalid = nvalid;
   p.dcout = merged ? cout : 0;
@@ -482,10 +547,14 @@ int conv_tapbox(int mode, const float* in, const Frame& inf, const float* w, int
   p.cls_start[ncls] = ne;
   float* wpack = static_cast<float*>(ws);
   {
-    const long long total = (long long)ne * ntot * 32;
+    const long long total = (long long)ne * ntot * cw;
     int grid = static_cast<int>((total + 255) / 256);
     if (grid > 8192) grid = 8192;
-    pack_tapbox_kernel<<<grid, 256, 0, st>>>(w, cout, cin, mode, merged ? 2 : kind, p, ne, ntot, wpack);
+    if (bf16 & 1)
+      pack_tapbox_bf16_kernel<<<grid, 256, 0, st>>>(w, cout, cin, mode, p, ne, ntot,
+                                                    reinterpret_cast<__nv_bfloat16*>(wpack));
+    else
+      pack_tapbox_kernel<<<grid, 256, 0, st>>>(w, cout, cin, mode, merged ? 2 : kind, p, ne, ntot, wpack);
     VPX_LAUNCH_CHECK();
   }
   p.n = of.n;
@@ -588,9 +657,19 @@ int conv_tapbox(int mode, const float* in, const Frame& inf, const float* w, int
   p.act = act;
   p.slope = slope;
   p.rnd = of.rnd;
+  p.out_bf16 = bf16 >> 1;  // bit 1: bf16 output storage (bit 0: bf16 operands)
   CUtensorMap xm, wm;
-  if (int rc = encode_in_map(&xm, in, inf, Db, Hb, Wb, s_in)) return rc;
-  if (int rc = encode_w_map(&wm, wpack, (long long)ne * ntot, NT)) return rc;
+  if (int rc = encode_in_map(&xm, in, inf, Db, Hb, Wb, s_in, bf16 & 1)) return rc;
+  if (int rc = encode_w_map(&wm, wpack, (long long)ne * ntot, NT, bf16 & 1)) return rc;
+  if (bf16 & 1) {
+    switch (NT) {
+      case 16: return launch_tapbox<16, true>(xm, wm, p, st);
+      case 32: return launch_tapbox<32, true>(xm, wm, p, st);
+      case 64: return launch_tapbox<64, true>(xm, wm, p, st);
+      case 128: return launch_tapbox<128, true>(xm, wm, p, st);
+      case 256: return launch_tapbox<256, true>(xm, wm, p, st);
+    }
+  }
   switch (NT) {
     case 16: return launch_tapbox<16>(xm, wm, p, st);
     case 32: return launch_tapbox<32>(xm, wm, p, st);
