@@ -274,7 +274,8 @@ static int conv_fwd_impl(const float* x, const int* xfr, const float* w, int k, 
     if (int rc = vpx::rowh_pack(w, cout, cin, 0, wpack, st)) return rc;
     return vpx::rowh_run(x, xf, wpack, cin, cout, y, yf, zlo, zhi, 0, yf.h, yf.w, st, act, slope);
   }
-  if (tc && k == 3 && stride == 1 && yf.w % 128 == 0 && vpx::rowwin_config(cin, cout, &R, &CG)) {
+  if (tc && k == 3 && stride == 1 && yf.w % 128 == 0 && vpx::rowwin_config(cin, cout, &R, &CG) &&
+      !getenv("VPX_NO_ROWWIN")) {
     if (ws_bytes < vpx::packed_floats(cin, cout) * 4) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "workspace too small");
     float* wpack = static_cast<float*>(ws);
     if (int rc = vpx::pack(w, cout, cin, 0, wpack, st)) return rc;
@@ -338,7 +339,7 @@ static int conv_bwd_data_impl(const float* u, const int* ufr, const float* w, in
     return vpx::rowh_run(u, uf, wpack, cout, cin, xg, gf, zlo, zhi, -gf.mh, gf.h + gf.mh, gf.w, st);
   }
   if (tc && k == 3 && stride == 1 && gf.mw == 0 && gf.w % 128 == 0 &&
-      vpx::rowwin_config(cout, cin, &R, &CG)) {
+      vpx::rowwin_config(cout, cin, &R, &CG) && !getenv("VPX_NO_ROWWIN")) {
     if (ws_bytes < vpx::packed_floats(cin, cout) * 4) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "workspace too small");
     float* wpack = static_cast<float*>(ws);
     if (int rc = vpx::pack(w, cout, cin, 1, wpack, st)) return rc;
