@@ -312,7 +312,7 @@ int rowwin_config(int cin, int cout, int* R, int* CG) {
   if (cin == 16 && cout == 32) { *R = 4; *CG = 2; return 1; }
   if (cin == 32 && cout == 16) { *R = 4; *CG = 2; return 1; }   // c2 dgrad
   if (cin == 32 && cout == 64) { *R = 2; *CG = 2; return 1; }
-  if (cin == 64 && cout == 32) { *R = 2; *CG = 2; return 1; }   // c3 dgrad
+  if (cin == 64 && cout == 32) { *R = 4; *CG = 2; return 1; }   // c3 dgrad
   if (cin == 16 && cout == 16) { *R = 4; *CG = 2; return 1; }
   if (cin == 8 && cout == 16) { *R = 4; *CG = 2; return 1; }
   if (cin == 16 && cout == 8) { return 0; }
@@ -325,7 +325,7 @@ int launch_rowwin_any(const CUtensorMap& xmap, const ConvRowParams& p, int cin, 
   if (cin == 16 && cout == 32) return launch_rowwin<32, 4, 2, false>(xmap, p, st);
   if (cin == 32 && cout == 16) return launch_rowwin<16, 4, 2, false>(xmap, p, st);
   if (cin == 32 && cout == 64) return launch_rowwin<64, 2, 2, false>(xmap, p, st);
-  if (cin == 64 && cout == 32) return launch_rowwin<32, 2, 2, false>(xmap, p, st);
+  if (cin == 64 && cout == 32) return launch_rowwin<32, 4, 2, false>(xmap, p, st);
   if (cin == 16 && cout == 16) return launch_rowwin<16, 4, 2, false>(xmap, p, st);
   if (cin == 8 && cout == 16) return launch_rowwin<16, 4, 2, false>(xmap, p, st);
   VPX_FAIL(VPX_ERR_UNSUPPORTED, "row-window conv: no instance for cin=%d cout=%d", cin, cout);
