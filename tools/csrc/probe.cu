@@ -121,10 +121,15 @@ __global__ void __launch_bounds__(128, 1)
   const uint32_t tbase = tmem_base;
   const uint32_t s0 = vpx::smem_u32(smem);
   if (tid == 0) {
+    // a_layout 0: no-swizzle K-major, aligned core matrices (LBO 2048); 1: SW128;
+    // 3: no-swizzle with LBO 16 (the conv_c1fwd.cu shifted-window A, core
+    // matrices overlapping at 16-byte offsets); 4: SW32 K-major (SBO 256)
     uint64_t a = a_layout == 0 ? vpx::make_sdesc(s0, 2048, 128, 0)
+               : a_layout == 3 ? vpx::make_sdesc(s0 + 16, 16, 128, 0)
+               : a_layout == 4 ? vpx::make_sdesc(s0, 16, 256, 6)
                                : vpx::make_sdesc(s0, 16, 1024, 2);
-    uint64_t b = a_layout == 0 ? vpx::make_sdesc(s0 + 32768, 4096, 128, 0)
-                               : vpx::make_sdesc(s0 + 32768, 16, 1024, 2);
+    uint64_t b = (a_layout == 0 || a_layout == 3) ? vpx::make_sdesc(s0 + 32768, 4096, 128, 0)
+                                                   : vpx::make_sdesc(s0 + 32768, 16, 1024, 2);
     uint32_t idesc = vpx::make_idesc(bf16 ? 1 : 2, 128, N, false, false);
     long long t0 = clock64();
     if (a_layout == 2) {
@@ -155,6 +160,7 @@ __global__ void __launch_bounds__(128, 1)
 template <int N, int NACC, int MODE>
 __global__ void __launch_bounds__(128, 1) probe_rate2_kernel(int n_iter, long long* cycles) {
   constexpr bool BF16 = MODE == 1;
+  static_assert(MODE != 10 || N % 16 == 0, "");
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bar, bar2;
   __shared__ uint32_t tmem_base;
@@ -204,9 +210,11 @@ __global__ void __launch_bounds__(128, 1) probe_rate2_kernel(int n_iter, long lo
             vpx::umma_tf32_ta(tbase + j * N, tbase + 432 + 8 * (j & 7), bmn + 64 * (j & 3), idesc_mn, i > 0);
           else if (MODE == 8 || MODE == 9)  // 9 B rows 10 KB apart, as in conv_c1bwd.cu
             vpx::umma_tf32_ta(tbase + j * N, tbase + 432 + 8 * (i & 7), bmn9 + 640 * j, idesc_mn, i > 0);
-          else if (MODE >= 3)
+          else if (MODE >= 3 && MODE != 10)
             vpx::umma_tf32_ta(tbase + (j * N) % 256, tbase + 256 + 8 * (j & 7), bmn + 64 * (j & 3), idesc_mn,
                               i > 0);
+          else if (MODE == 10)  // no-swizzle, LBO 16: the c1 forward's shifted 16-byte-pitch window
+            vpx::umma_tf32(tbase + j * N, vpx::make_sdesc(s0 + 16 * (j & 1), 16, 128, 0), b, idesc, i > 0);
           else if (BF16)
             vpx::umma_f16(tbase + j * N, a + 2 * (j & 1), b, idesc, i > 0);
           else
@@ -243,7 +251,8 @@ extern "C" int vpx_probe_mma_rate2(int N, int n_acc, int bf16, int n_iter, long 
   cudaStream_t st = static_cast<cudaStream_t>(stream);
 #define RATE_CASE(n, a)                                                         \
   if (N == n && n_acc == a)                                                     \
-    return bf16 == 9 ? launch_rate2<n, a, 9>(n_iter, cycles, st)                \
+    return bf16 == 10 ? launch_rate2<n, a, 10>(n_iter, cycles, st)              \
+           : bf16 == 9 ? launch_rate2<n, a, 9>(n_iter, cycles, st)              \
            : bf16 == 8 ? launch_rate2<n, a, 8>(n_iter, cycles, st)              \
            : bf16 == 7 ? launch_rate2<n, a, 7>(n_iter, cycles, st)              \
            : bf16 == 6 ? launch_rate2<n, a, 6>(n_iter, cycles, st)              \
