@@ -23,7 +23,7 @@ import torch
 from . import _lib
 from .comm import RankCtx, halo_exchange, reverse_halo_exchange, copy_box
 from .errors import NonDivisible, ShapeMismatch, Unsupported
-from .frames import DistTensor, frame_desc, stream_ptr
+from .frames import DistTensor, Frame, frame_desc, stream_ptr
 from .geometry import DistTensorMeta, Shape5D, make_partition
 from .timing import region
 
@@ -225,13 +225,25 @@ def concat_wgrad_sources(x: DistTensor, sources, u: DistTensor, params):
     are never exchanged)."""
     if sources is None or _cubic(params.kernel) != 3 or _cubic(params.stride) != 1:
         return None
-    if any(any(t.m) for t in (x, u) + tuple(sources)):
+    if _lib.load().vpx_get_precision() != 0 or any(u.m):  # the per-slice kernels are tcgen05 (TF32 mode)
         return None
     if any(t.c != u.c for t in sources) or sum(t.c for t in sources) != x.c:
         return None
     out, c0 = [], 0
+    if not any(any(t.m) for t in (x,) + tuple(sources)):
+        for t in sources:
+            out.append((c0, t))
+            c0 += t.c
+        return out
+    if x.m[2]:  # the grouped-voxel kernel reads whole W rows (no W margins)
+        return None
+    # spatially partitioned: x carries the exchanged halo margins, the concat
+    # sources do not -- take each source's channel range from x itself, as a
+    # dense frame with the same margins (one copy, ~1/4 of the slow
+    # whole-concat kernel's time at U-Net's u1c1)
     for t in sources:
-        out.append((c0, t))
+        sl = x.t[..., c0:c0 + t.c].contiguous()
+        out.append((c0, Frame(x.n, t.c, x.d, x.h, x.w, x.m, tensor=sl)))
         c0 += t.c
     return out
 

@@ -668,3 +668,36 @@ def test_deconv_tensor_cores_vs_tf32_oracle(cin, cout, spatial, margins):
         wg_ref = O.deconv3d_bwd_filter(x.astype(np.float64), u.astype(np.float64)).astype(np.float32)
         assert rel(wg.cpu().numpy() - 0.25, wg_ref) < 1e-3
         assert _lib.load().vpx_fallback_count() == fb0, "deconv filter gradient fell back to CUDA cores"
+
+
+@pytest.mark.parametrize("margins", [(1, 0, 0), (1, 1, 0)])
+def test_concat_wgrad_slices_from_partitioned_frame(margins):
+    """Spatially partitioned U-Net u1c1: the concat frame carries exchanged D/H
+    halo margins the concat sources do not have, so layers.concat_wgrad_sources
+    takes each source's channel range from the concat frame itself (dense copy,
+    margins included) -- the filter gradient must match the oracle over the
+    whole haloed frame and the whole-concat kernel."""
+    from paper_2007_12856_b200 import layers as D
+
+    rng = np.random.default_rng(19)
+    n, d, h, w = 1, 3, 4, 128
+    md, mh, mw = margins
+    full = rng.uniform(-1, 1, (n, 16, d + 2 * md, h + 2 * mh, w)).astype(np.float32)
+    cf = Frame(n, 16, d, h, w, margins, zero=True)
+    cf.t.copy_(torch.from_numpy(full.transpose(0, 2, 3, 4, 1).copy()).cuda())
+    u = rng.uniform(-1, 1, (n, 8, d, h, w)).astype(np.float32)
+    uf = _frame_of(u)
+    srcs = [Frame(n, 8, d, h, w), Frame(n, 8, d, h, w)]  # stand-ins: channel counts only (no margins)
+    params = type("P", (), {"kernel": (3, 3, 3), "stride": (1, 1, 1), "cin": 16, "cout": 8})()
+    slices = D.concat_wgrad_sources(cf, srcs, uf, params)
+    assert slices is not None and [c0 for c0, _ in slices] == [0, 8]
+    W = ws(16, 8, 3, uf)
+    whole = torch.zeros((8, 16, 3, 3, 3), device="cuda")
+    _lib.call("vpx_conv3d_bwd_filter", cf.ptr, cf.desc, uf.ptr, uf.desc, 3, 1, whole.data_ptr(), 0, W.data_ptr(),
+              W.numel() * 4, stream_ptr())
+    sl = torch.full((8, 16, 3, 3, 3), 7.0, device="cuda")
+    D.dist_conv3d_bwd_filter_slices(None, slices, uf, params, sl)
+    xpad = np.pad(full, ((0, 0), (0, 0), (0 if md else 1,) * 2, (0 if mh else 1,) * 2, (1, 1)))
+    ref = O.k_conv3d_bwd_filter(xpad, u, (1, 1, 1), (3, 3, 3))
+    assert rel(sl.cpu().numpy(), ref) < TF32_RTOL
+    assert rel(sl.cpu().numpy(), whole.cpu().numpy()) < 1e-5  # same TF32 products, other summation order
