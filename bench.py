@@ -59,6 +59,9 @@ def parse():
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of the CUDA graph")
     ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of CPU sample work")
     ap.add_argument("--no-aux", action="store_true", help="skip the CosmoFlow-128 like-for-like step")
+    ap.add_argument("--redistribute-before", default=None,
+                    help="layer before which the spatial blocks are gathered to the group lead "
+                         "(reference make_plan's redistribute_before; default: the planner's choice)")
     return ap.parse_args()
 
 
@@ -412,7 +415,7 @@ def run_ours(args):
         net = build_unet_mini(W)
     else:
         net = build_cosmoflow(W, with_bn=args.bn)
-    plan = engine.make_plan(net, grid, n_global, W)
+    plan = engine.make_plan(net, grid, n_global, W, args.redistribute_before)
     ctx.prepare_groups([plan.leads])
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     tf32_peak, tf32_src = tf32_peak_of(peaks)
@@ -618,7 +621,8 @@ def run_ours(args):
                    "global_batch": n_global, "width": W, "grid": f"{grid.groups}x{grid.pd}x{grid.ph}x{grid.pw}",
                    "parallelism": f"dp{grid.groups}xspatial{grid.spatial_size}",
                    "l2": "inputs larger than L2 (no flush needed)",
-                   "storage": "fp32 NDHWC, TF32 tensor-core math", "halo": ctx.halo_path},
+                   "storage": "fp32 NDHWC, TF32 tensor-core math", "halo": ctx.halo_path,
+                   "redistribute_before": net.layers[plan.redist_idx].name if plan.redist_idx >= 0 else None},
         "roofline": roof,
         "halo_roofline": halo,
         "cpu_baseline": cpu,

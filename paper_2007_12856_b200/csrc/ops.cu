@@ -588,9 +588,45 @@ __global__ void ncdhw_to_frame_kernel(const float* __restrict__ src, Frame f, fl
 // int16 NCDHW (the HSB1 storage dtype, reference datastore.py:10-19) -> fp32
 // frame interior: the datastore's conversion to the training dtype
 // (reference datastore.py:429-444) fused into the layout change.  Blocks
-// stride over (n, z, y) rows, threads over x; each channel plane is read
-// coalesced, the voxel's channels are written together.
-template <typename T>  // int16 (HSB1 storage) or int8 (the datastore's narrowed transfer copy)
+// stride over (n, z, y) rows; a thread takes 4 consecutive voxels: one 4-wide
+// vector load per channel plane, a 4x4 register transpose, four 16-byte
+// stores of 4 channels (C % 4 == 0, W % 4 == 0; the scalar loop otherwise).
+// One voxel per thread with scalar loads left this HBM-bound kernel at
+// ~1.75 TB/s (1.5 ms per 512^3 x 4 sample, the e2e step's largest addition).
+template <typename T> struct Vec4;
+template <> struct Vec4<int8_t> { using type = char4; };
+template <> struct Vec4<int16_t> { using type = short4; };
+template <> struct Vec4<float> { using type = float4; };
+
+template <typename T>  // int16 (HSB1 storage), int8 (the datastore's narrowed transfer copy) or fp32
+__global__ void ncdhw_vec_to_frame_kernel(const T* __restrict__ src, Frame f, float* __restrict__ fr) {
+  using V = typename Vec4<T>::type;
+  const long long nrows = (long long)f.n * f.d * f.h;
+  const long long plane = (long long)f.d * f.h * f.w;
+  const int w4 = f.w / 4;
+  for (long long row = blockIdx.x; row < nrows; row += gridDim.x) {
+    const int y = static_cast<int>(row % f.h);
+    const long long t = row / f.h;
+    const int z = static_cast<int>(t % f.d);
+    const int n = static_cast<int>(t / f.d);
+    const T* s = src + (((long long)n * f.c * f.d + z) * f.h + y) * f.w;
+    float* dst = fr + fr_off(f, n, z, y, 0);
+    for (int q = threadIdx.x; q < w4; q += blockDim.x) {
+      for (int c = 0; c < f.c; c += 4) {
+        V v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v[k] = reinterpret_cast<const V*>(s + (c + k) * plane)[q];
+        float* d = dst + (long long)(4 * q) * f.c + c;
+        *reinterpret_cast<float4*>(d) = rnd4(f, make_float4(v[0].x, v[1].x, v[2].x, v[3].x));
+        *reinterpret_cast<float4*>(d + f.c) = rnd4(f, make_float4(v[0].y, v[1].y, v[2].y, v[3].y));
+        *reinterpret_cast<float4*>(d + 2 * f.c) = rnd4(f, make_float4(v[0].z, v[1].z, v[2].z, v[3].z));
+        *reinterpret_cast<float4*>(d + 3 * f.c) = rnd4(f, make_float4(v[0].w, v[1].w, v[2].w, v[3].w));
+      }
+    }
+  }
+}
+
+template <typename T>  // the general shape (C or W not a multiple of 4)
 __global__ void ncdhw_int_to_frame_kernel(const T* __restrict__ src, Frame f, float* __restrict__ fr) {
   const long long nrows = (long long)f.n * f.d * f.h;
   const long long plane = (long long)f.d * f.h * f.w;
@@ -601,18 +637,106 @@ __global__ void ncdhw_int_to_frame_kernel(const T* __restrict__ src, Frame f, fl
     const int n = static_cast<int>(t / f.d);
     const T* s = src + (((long long)n * f.c * f.d + z) * f.h + y) * f.w;
     float* dst = fr + fr_off(f, n, z, y, 0);
-    for (int x = threadIdx.x; x < f.w; x += blockDim.x) {
-      if (f.c % 4 == 0) {
-        for (int c = 0; c < f.c; c += 4) {
-          const float4 v = make_float4(s[c * plane + x], s[(c + 1) * plane + x], s[(c + 2) * plane + x],
-                                       s[(c + 3) * plane + x]);
-          *reinterpret_cast<float4*>(dst + (long long)x * f.c + c) = rnd4(f, v);
+    for (int x = threadIdx.x; x < f.w; x += blockDim.x)
+      for (int c = 0; c < f.c; ++c) dst[(long long)x * f.c + c] = rnd(f, static_cast<float>(s[c * plane + x]));
+  }
+}
+
+// Lane `src` of the warp holds 4 consecutive voxels of one channel plane in a
+// packed vector; return voxel j of it (all lanes take part in the shuffles).
+__device__ __forceinline__ float shfl_voxel(char4 v, int src, int j) {
+  const int w = __shfl_sync(0xffffffffu, *reinterpret_cast<int*>(&v), src);
+  return static_cast<float>(static_cast<signed char>(w >> (8 * j)));
+}
+__device__ __forceinline__ float shfl_voxel(short4 v, int src, int j) {
+  const int lo = __shfl_sync(0xffffffffu, *reinterpret_cast<int*>(&v.x), src);
+  const int hi = __shfl_sync(0xffffffffu, *reinterpret_cast<int*>(&v.z), src);
+  return static_cast<float>(static_cast<short>((j < 2 ? lo : hi) >> (16 * (j & 1))));
+}
+
+// C == 4 (the CosmoFlow input, reference datastore.py:10-19 channels), int8 or
+// int16: a warp loads 128 consecutive voxels as one 4-wide vector per lane and
+// channel plane, then writes them back as four fully coalesced 512-byte runs
+// of float4 (lane L of run k stores voxel 32k + L, gathered with shuffles), so
+// every 32-byte sector is written whole by one instruction.
+template <typename T>
+__global__ void ncdhw_c4_to_frame_kernel(const T* __restrict__ src, Frame f, float* __restrict__ fr) {
+  using V = typename Vec4<T>::type;
+  const long long nrows = (long long)f.n * f.d * f.h;
+  const long long plane = (long long)f.d * f.h * f.w;
+  const int w4 = f.w / 4, lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  for (long long row = blockIdx.x; row < nrows; row += gridDim.x) {
+    const int y = static_cast<int>(row % f.h);
+    const long long t = row / f.h;
+    const int z = static_cast<int>(t % f.d);
+    const int n = static_cast<int>(t / f.d);
+    const T* s = src + (((long long)n * 4 * f.d + z) * f.h + y) * f.w;
+    float4* dst = reinterpret_cast<float4*>(fr + fr_off(f, n, z, y, 0));
+    for (int q0 = 32 * warp; q0 < w4; q0 += 32 * nwarps) {
+      const int q = q0 + lane;
+      V v[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (q < w4) {
+          v[c] = reinterpret_cast<const V*>(s + c * plane)[q];
+        } else {
+          v[c] = V{};
         }
-      } else {
-        for (int c = 0; c < f.c; ++c) dst[(long long)x * f.c + c] = rnd(f, static_cast<float>(s[c * plane + x]));
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int sl = 8 * k + (lane >> 2), j = lane & 3;
+        const float4 o = make_float4(shfl_voxel(v[0], sl, j), shfl_voxel(v[1], sl, j), shfl_voxel(v[2], sl, j),
+                                     shfl_voxel(v[3], sl, j));
+        const int x = 4 * q0 + 32 * k + lane;
+        if (x < f.w) dst[x] = rnd4(f, o);
       }
     }
   }
+}
+
+// C == 1 (the U-Net input): NCDHW and NDHWC coincide, a vectorised convert.
+template <typename T>
+__global__ void ncdhw_c1_to_frame_kernel(const T* __restrict__ src, Frame f, float* __restrict__ fr) {
+  using V = typename Vec4<T>::type;
+  const long long nrows = (long long)f.n * f.d * f.h;
+  const int w4 = f.w / 4;
+  for (long long row = blockIdx.x; row < nrows; row += gridDim.x) {
+    const int y = static_cast<int>(row % f.h);
+    const long long t = row / f.h;
+    const int z = static_cast<int>(t % f.d);
+    const int n = static_cast<int>(t / f.d);
+    const V* s = reinterpret_cast<const V*>(src + (((long long)n * f.d + z) * f.h + y) * f.w);
+    float4* dst = reinterpret_cast<float4*>(fr + fr_off(f, n, z, y, 0));
+    for (int q = threadIdx.x; q < w4; q += blockDim.x) {
+      const V v = s[q];
+      dst[q] = rnd4(f, make_float4(v.x, v.y, v.z, v.w));
+    }
+  }
+}
+
+template <typename T>
+static int layout_to_frame(const T* src, const Frame& f, float* fr, cudaStream_t st) {
+  const long long rows = (long long)f.n * f.d * f.h;
+  const long long cap = (long long)num_sms() * 16;
+  const int grid = static_cast<int>(rows < cap ? rows : cap);
+  const bool vec = f.c % 4 == 0 && f.w % 4 == 0 && (reinterpret_cast<uintptr_t>(src) % (4 * sizeof(T))) == 0;
+  static const bool plain = getenv("VPX_LAYOUT_PLAIN") != nullptr;  // A/B switch (tools/e2e_probe.py)
+  if constexpr (sizeof(T) < 4) {
+    if (vec && f.c == 4 && !plain) {
+      ncdhw_c4_to_frame_kernel<T><<<grid, 128, 0, st>>>(src, f, fr);
+      VPX_LAUNCH_CHECK();
+      return VPX_OK;
+    }
+  }
+  if (vec)
+    ncdhw_vec_to_frame_kernel<T><<<grid, 128, 0, st>>>(src, f, fr);
+  else if (f.c == 1 && f.w % 4 == 0 && f.mw % 4 == 0 && (reinterpret_cast<uintptr_t>(src) % (4 * sizeof(T))) == 0)
+    ncdhw_c1_to_frame_kernel<T><<<grid, 128, 0, st>>>(src, f, fr);
+  else
+    ncdhw_int_to_frame_kernel<T><<<grid, 256, 0, st>>>(src, f, fr);
+  VPX_LAUNCH_CHECK();
+  return VPX_OK;
 }
 __global__ void i16_to_i64_kernel(const int16_t* __restrict__ src, long long n, long long* __restrict__ dst) {
   GRID_STRIDE(i, n) dst[i] = src[i];
@@ -897,22 +1021,16 @@ extern "C" int vpx_xent(const float* logits, const int* lf, const long long* lab
 }
 extern "C" int vpx_layout_ncdhw_to_frame(const float* src, const int* ff, float* fr, void* st) {
   Frame f = F(ff);
+  if ((f.c % 4 == 0 || f.c == 1) && f.w % 4 == 0 && reinterpret_cast<uintptr_t>(src) % 16 == 0)
+    return layout_to_frame<float>(src, f, fr, S(st));
   ncdhw_to_frame_kernel<<<grid1d(VC(f) * f.c), 256, 0, S(st)>>>(src, f, fr);
   LAUNCH_TAIL;
 }
 extern "C" int vpx_layout_ncdhw_i16_to_frame(const int16_t* src, const int* ff, float* fr, void* st) {
-  Frame f = F(ff);
-  const long long rows = (long long)f.n * f.d * f.h;
-  const long long cap = (long long)num_sms() * 16;
-  ncdhw_int_to_frame_kernel<int16_t><<<static_cast<int>(rows < cap ? rows : cap), 256, 0, S(st)>>>(src, f, fr);
-  LAUNCH_TAIL;
+  return layout_to_frame<int16_t>(src, F(ff), fr, S(st));
 }
 extern "C" int vpx_layout_ncdhw_i8_to_frame(const int8_t* src, const int* ff, float* fr, void* st) {
-  Frame f = F(ff);
-  const long long rows = (long long)f.n * f.d * f.h;
-  const long long cap = (long long)num_sms() * 16;
-  ncdhw_int_to_frame_kernel<int8_t><<<static_cast<int>(rows < cap ? rows : cap), 256, 0, S(st)>>>(src, f, fr);
-  LAUNCH_TAIL;
+  return layout_to_frame<int8_t>(src, F(ff), fr, S(st));
 }
 extern "C" int vpx_convert_i16_to_i64(const int16_t* src, long long n, long long* dst, void* st) {
   if (n <= 0) return VPX_OK;

@@ -11,7 +11,7 @@ import pytest
 import torch
 
 from oracle import serial as O
-from paper_2007_12856_b200 import _lib, prng
+from paper_2007_12856_b200 import _lib, get_precision, prng
 from paper_2007_12856_b200.frames import Frame, frame_desc, stream_ptr
 
 pytestmark = pytest.mark.gpu
@@ -623,6 +623,41 @@ def test_int8_transfer_layout_equals_int16(margins):
     torch.cuda.synchronize()
     assert torch.equal(a.t.view(torch.int32), b.t.view(torch.int32))
     assert np.array_equal(b.to_ncdhw().cpu().numpy(), v16.astype(np.float32))
+
+
+@pytest.mark.parametrize("dtype", [np.int8, np.int16, np.float32])
+@pytest.mark.parametrize("c,spatial,margins,offset", [(4, (3, 5, 16), (1, 1, 0), 0), (8, (2, 3, 12), (0, 1, 0), 0),
+                                                      (3, (2, 3, 8), (1, 0, 0), 0), (4, (2, 2, 6), (0, 0, 0), 0),
+                                                      (4, (2, 3, 8), (1, 1, 0), 1), (4, (1, 2, 520), (0, 0, 0), 0),
+                                                      (4, (2, 1, 36), (1, 0, 0), 0), (1, (2, 3, 8), (1, 1, 0), 0),
+                                                      (1, (2, 2, 12), (0, 0, 0), 1), (1, (2, 2, 10), (0, 0, 0), 0)])
+def test_ncdhw_layout_kernels_exact(dtype, c, spatial, margins, offset):
+    """NCDHW -> NDHWC frame layout kernels (C = 4 shuffle-coalesced, C % 4 == 0
+    vector and C = 1 convert paths when W is a multiple of 4 and the source is
+    aligned, scalar path otherwise): exact values in the interior, margins
+    untouched (zero)."""
+    rng = np.random.default_rng(3)
+    n = 2
+    shape = (n, c) + spatial
+    if dtype == np.float32:
+        v = rng.standard_normal(shape).astype(np.float32)
+    else:
+        v = rng.integers(-100, 101, shape).astype(dtype)
+    src = torch.from_numpy(v.ravel()).cuda()
+    if offset:  # a source not 16-byte aligned takes the scalar path
+        buf = torch.zeros(src.numel() + offset, dtype=src.dtype, device="cuda")
+        buf[offset:] = src
+        src = buf[offset:]
+    f = Frame(n, c, *spatial, margins, zero=True).load_ncdhw(src.view(shape))
+    torch.cuda.synchronize()
+    want = v.astype(np.float32)
+    if dtype == np.float32 and get_precision() == "tf32":
+        want = O.tf32_round(v)  # frames store values rounded to nearest TF32 in that mode
+    assert np.array_equal(f.to_ncdhw().cpu().numpy(), want)
+    t = f.t.cpu().numpy()
+    md, mh, mw = f.m
+    inner = t[:, md:md + spatial[0], mh:mh + spatial[1], mw:mw + spatial[2]]
+    assert np.abs(t).sum() == np.abs(inner).sum()
 
 
 @pytest.mark.parametrize("cin,cout,spatial,margins", [(32, 16, (4, 6, 64), (0, 0, 0)), (16, 8, (3, 4, 40), (0, 0, 0)),
