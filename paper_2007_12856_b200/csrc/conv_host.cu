@@ -239,6 +239,7 @@ extern "C" long long vpx_conv3d_workspace_bytes(int cin, int cout, int k, const 
                            ? vpx::rowh_packed_bytes(cin, cout)
                            : vpx::rowh_packed_bytes(cout, cin);
   if (rh > packed) packed = rh;
+  if (cin == 4 && cout == 16 && vpx::c1_fwd_packed_bytes() > packed) packed = vpx::c1_fwd_packed_bytes();
   return ((packed + 255) / 256) * 256 + ((parts + 255) / 256) * 256;
 }
 
@@ -450,10 +451,10 @@ extern "C" int vpx_conv3d_fwd_leaky_pool_c4(const float* x, const int* xfr, cons
   Frame xf = vpx::to_frame(xfr), pf = vpx::to_frame(pfr);
   if (!vpx::c1_fwd_pool_supported(xf, pf.c, pf)) VPX_FAIL(VPX_ERR_UNSUPPORTED, "fused first block: shape/mode");
   if (!(slope > 0.f && slope <= 1.f)) VPX_FAIL(VPX_ERR_UNSUPPORTED, "fused first block: slope must be in (0, 1]");
-  if (ws_bytes < vpx::rowh_packed_bytes(4, 16)) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "workspace too small");
+  if (ws_bytes < vpx::c1_fwd_packed_bytes()) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "workspace too small");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   float* wpack = static_cast<float*>(ws);
-  if (int rc = vpx::rowh_pack(w, 16, 4, 0, wpack, st)) return rc;
+  if (int rc = vpx::c1_fwd_pack(w, wpack, st)) return rc;
   return vpx::conv_c1_fwd_pool(x, xf, wpack, slope, pout, pf, mask, st);
 }
 

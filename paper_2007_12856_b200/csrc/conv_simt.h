@@ -45,6 +45,8 @@ int conv_wgrad_c1_pooled(const float* x, const Frame& xf, const float* y, const 
                          const uint16_t* mask = nullptr, bool u_direct = false);
 int c1_direct_supported(const Frame& xf, const Frame& uf);
 int c1_fwd_pool_supported(const Frame& xf, int cout, const Frame& pf);
+long long c1_fwd_packed_bytes();
+int c1_fwd_pack(const float* w, float* dst, cudaStream_t st);
 int conv_c1_fwd_pool(const float* x, const Frame& xf, const float* wpack, float slope, float* pout,
                      const Frame& pf, uint16_t* mask, cudaStream_t st);
 // conv_small.cu: 1x1x1 convs and 3x3x3 convs on 1 input channel (U-Net edges)

@@ -128,8 +128,11 @@ def test_first_block_fused_backward_and_c4_wgrad(shape, margins):
                                            ((1, 2, 34, 128), (0, 0, 0)), ((1, 2, 44, 256), (1, 1, 0))])
 def test_first_block_fused_forward_and_mask_backward(shape, margins):
     """conv(4->16)+leaky+avg-pool in one kernel (pooled output + sign mask)
-    equals the unfused conv/pool kernels bit for bit, and the mask-driven
-    filter gradient equals the y-driven one bit for bit."""
+    against the unfused conv/pool kernels: the fused kernel sums the three
+    height taps in TMEM (the unfused one in its epilogue), so the activations
+    agree to within one TF32 rounding step -- pooled values within 2^-10 of
+    the maximum, sign bits equal wherever the activation is not ~0.  The
+    mask-driven filter gradient equals the y-driven one bit for bit."""
     n, d, h, w = shape
     rng = np.random.default_rng(5)
     x = rng.uniform(-1, 1, (n, 4, d, h, w)).astype(np.float32)
@@ -148,9 +151,14 @@ def test_first_block_fused_forward_and_mask_backward(shape, margins):
     _lib.call("vpx_conv3d_fwd_leaky_pool_c4", xf.ptr, xf.desc, wt.data_ptr(), 0.3, pf.ptr, pf.desc,
               mask.data_ptr(), W.data_ptr(), W.numel() * 4, stream_ptr())
     torch.cuda.synchronize()
-    assert torch.equal(pf.t, pref.t)
+    assert float((pf.t - pref.t).abs().max()) <= 2.0 ** -10 * float(pref.t.abs().max())
     ybits = (yf.t >= 0).to(torch.int32) * (2 ** torch.arange(16, device="cuda", dtype=torch.int32))
-    assert torch.equal(mask.to(torch.int32) & 0xFFFF, ybits.sum(-1) & 0xFFFF)
+    ymask = ybits.sum(-1) & 0xFFFF
+    yi = yf.t  # conv output frame (no margins)
+    diff = (mask.to(torch.int32) & 0xFFFF) != ymask
+    near0 = (yi.abs() <= 1e-5 * float(yi.abs().max())).any(-1)
+    assert not bool((diff & ~near0).any())
+    mask = ymask.to(torch.int16)  # the backward check below drives both paths from the same y
     # backward from a pooled gradient
     up = rng.uniform(-1, 1, (n, 16, d // 2, h // 2, w // 2)).astype(np.float32)
     upf = Frame(n, 16, d // 2, h // 2, w // 2, margins, zero=True).load_ncdhw(up)

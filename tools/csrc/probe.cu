@@ -262,7 +262,7 @@ extern "C" int vpx_probe_mma_rate2(int N, int n_acc, int bf16, int n_iter, long 
            : bf16    ? launch_rate2<n, a, 1>(n_iter, cycles, st)                \
                      : launch_rate2<n, a, 0>(n_iter, cycles, st);
   RATE_CASE(16, 1) RATE_CASE(16, 4) RATE_CASE(16, 8) RATE_CASE(32, 1) RATE_CASE(32, 4)
-  RATE_CASE(32, 8) RATE_CASE(48, 8) RATE_CASE(48, 9) RATE_CASE(96, 2) RATE_CASE(64, 1) RATE_CASE(64, 4) RATE_CASE(64, 8) RATE_CASE(128, 1)
+  RATE_CASE(32, 8) RATE_CASE(48, 1) RATE_CASE(48, 2) RATE_CASE(48, 4) RATE_CASE(48, 8) RATE_CASE(48, 9) RATE_CASE(96, 1) RATE_CASE(96, 2) RATE_CASE(64, 1) RATE_CASE(64, 4) RATE_CASE(64, 8) RATE_CASE(128, 1)
   RATE_CASE(128, 2) RATE_CASE(256, 1) RATE_CASE(256, 2)
 #undef RATE_CASE
   VPX_FAIL(VPX_ERR_UNSUPPORTED, "rate2 case");
