@@ -102,6 +102,72 @@ __device__ __forceinline__ void tapbox_store16(const ConvTapParams& p, long long
     if (4 * i < nmax) o4[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
 }
 
+// Fixed-order sum of the split-K partial tiles for (base tile tb, row r,
+// channels 4 c4 .. 4 c4 + 3), then the epilogue (LeakyReLU, TF32 rounding,
+// frame store) the single-pass kernel would have applied.
+template <int NT>
+__device__ __forceinline__ void tapbox_reduce_elem(const ConvTapParams& p, int tb, int r, int c4) {
+  int tile = tb;
+  const int nt = tile % p.ntn;
+  tile /= p.ntn;
+  const int cls = tile % p.ncls;
+  tile /= p.ncls;
+  const int xt = tile % p.tw;
+  tile /= p.tw;
+  const int yt = tile % p.th;
+  tile /= p.th;
+  const int zt = tile % p.td;
+  const int n = tile / p.td;
+  const int dx = r % p.Wb, dy = (r / p.Wb) % p.Hb, dz = r / (p.Wb * p.Hb);
+  const int qz = p.qd + zt * p.Db + dz, qy = p.qh + yt * p.Hb + dy, qx = p.qw + xt * p.Wb + dx;
+  const int Pd = (cls >> 2) & 1, Ph = (cls >> 1) & 1, Pw = cls & 1;
+  const int pz = p.out_stride * qz + Pd, py = p.out_stride * qy + Ph, px = p.out_stride * qx + Pw;
+  const bool valid = dz < p.Db && qz < p.qd + p.QD && qy < p.qh + p.QH && qx < p.qw + p.QW &&
+                     (p.dcout || (pz >= p.pd_lo && pz < p.pd_hi && py >= p.ph_lo && py < p.ph_hi &&
+                                  px >= p.pw_lo && px < p.pw_hi));
+  if (!valid || nt * NT + 4 * c4 >= p.nvalid) return;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int ks = 0; ks < p.ksplit; ++ks) {
+    const float4 v = reinterpret_cast<const float4*>(
+        p.part + ((static_cast<long long>(ks) * p.base_tiles + tb) * 128 + r) * NT)[c4];
+    acc.x += v.x;
+    acc.y += v.y;
+    acc.z += v.z;
+    acc.w += v.w;
+  }
+  float o[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    if (p.act) o[j] = o[j] >= 0.f ? o[j] : p.slope * o[j];
+    if (p.rnd && !p.out_bf16) o[j] = vpx::tf32_rn(o[j]);
+  }
+  float* dst = p.dcout ? tapbox_dst(p, n, qz, qy, qx, cls, nt * NT + 4 * c4)
+                       : p.out + static_cast<long long>(n) * p.out_sn +
+                             static_cast<long long>(pz + p.out_off_d) * p.out_sd +
+                             static_cast<long long>(py + p.out_off_h) * p.out_sh +
+                             static_cast<long long>(px + p.out_off_w) * p.out_sw + nt * NT + 4 * c4;
+  if (dst && p.out_bf16) {
+    const __nv_bfloat162 lo = __floats2bfloat162_rn(o[0], o[1]), hi = __floats2bfloat162_rn(o[2], o[3]);
+    uint2 w;
+    w.x = *reinterpret_cast<const uint32_t*>(&lo);
+    w.y = *reinterpret_cast<const uint32_t*>(&hi);
+    *reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(p.out) + (dst - p.out)) = w;
+  } else if (dst) {
+    *reinterpret_cast<float4*>(dst) = make_float4(o[0], o[1], o[2], o[3]);
+  }
+}
+
+template <int NT>
+__global__ void tapbox_reduce_kernel(const __grid_constant__ ConvTapParams p) {
+  const long long total = (long long)p.base_tiles * 128 * (NT / 4);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int c4 = static_cast<int>(i % (NT / 4));
+    const int r = static_cast<int>((i / (NT / 4)) % 128);
+    tapbox_reduce_elem<NT>(p, static_cast<int>(i / (NT / 4) / 128), r, c4);
+  }
+}
+
 // BF16 = true: kind::f16 MMAs on bf16 operands (64-channel K chunks = the same
 // 128-byte SWIZZLE_128B rows, K = 16 per MMA instead of 8), fp32 accumulation.
 template <int NT, int S, bool BF16>
@@ -292,67 +358,6 @@ __global__ void __launch_bounds__(256, 1)
   if (warp == 2) vpx::tmem_dealloc<2 * TCOLS>(tbase);
 }
 
-// Fixed-order sum of the split-K partial tiles, then the epilogue (LeakyReLU,
-// TF32 rounding, frame store) the single-pass kernel would have applied.
-template <int NT>
-__global__ void tapbox_reduce_kernel(const __grid_constant__ ConvTapParams p) {
-  const long long total = (long long)p.base_tiles * 128 * (NT / 4);
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int c4 = static_cast<int>(i % (NT / 4));
-    const int r = static_cast<int>((i / (NT / 4)) % 128);
-    int tile = static_cast<int>(i / (NT / 4) / 128);
-    const int tb = tile;
-    const int nt = tile % p.ntn;
-    tile /= p.ntn;
-    const int cls = tile % p.ncls;
-    tile /= p.ncls;
-    const int xt = tile % p.tw;
-    tile /= p.tw;
-    const int yt = tile % p.th;
-    tile /= p.th;
-    const int zt = tile % p.td;
-    const int n = tile / p.td;
-    const int dx = r % p.Wb, dy = (r / p.Wb) % p.Hb, dz = r / (p.Wb * p.Hb);
-    const int qz = p.qd + zt * p.Db + dz, qy = p.qh + yt * p.Hb + dy, qx = p.qw + xt * p.Wb + dx;
-    const int Pd = (cls >> 2) & 1, Ph = (cls >> 1) & 1, Pw = cls & 1;
-    const int pz = p.out_stride * qz + Pd, py = p.out_stride * qy + Ph, px = p.out_stride * qx + Pw;
-    const bool valid = dz < p.Db && qz < p.qd + p.QD && qy < p.qh + p.QH && qx < p.qw + p.QW &&
-                       (p.dcout || (pz >= p.pd_lo && pz < p.pd_hi && py >= p.ph_lo && py < p.ph_hi &&
-                                    px >= p.pw_lo && px < p.pw_hi));
-    if (!valid || nt * NT + 4 * c4 >= p.nvalid) continue;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int ks = 0; ks < p.ksplit; ++ks) {
-      const float4 v = reinterpret_cast<const float4*>(
-          p.part + ((static_cast<long long>(ks) * p.base_tiles + tb) * 128 + r) * NT)[c4];
-      acc.x += v.x;
-      acc.y += v.y;
-      acc.z += v.z;
-      acc.w += v.w;
-    }
-    float o[4] = {acc.x, acc.y, acc.z, acc.w};
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      if (p.act) o[j] = o[j] >= 0.f ? o[j] : p.slope * o[j];
-      if (p.rnd && !p.out_bf16) o[j] = vpx::tf32_rn(o[j]);
-    }
-    float* dst = p.dcout ? tapbox_dst(p, n, qz, qy, qx, cls, nt * NT + 4 * c4)
-                         : p.out + static_cast<long long>(n) * p.out_sn +
-                               static_cast<long long>(pz + p.out_off_d) * p.out_sd +
-                               static_cast<long long>(py + p.out_off_h) * p.out_sh +
-                               static_cast<long long>(px + p.out_off_w) * p.out_sw + nt * NT + 4 * c4;
-    if (dst && p.out_bf16) {
-      const __nv_bfloat162 lo = __floats2bfloat162_rn(o[0], o[1]), hi = __floats2bfloat162_rn(o[2], o[3]);
-      uint2 w;
-      w.x = *reinterpret_cast<const uint32_t*>(&lo);
-      w.y = *reinterpret_cast<const uint32_t*>(&hi);
-      *reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(p.out) + (dst - p.out)) = w;
-    } else if (dst) {
-      *reinterpret_cast<float4*>(dst) = make_float4(o[0], o[1], o[2], o[3]);
-    }
-  }
-}
-
 template <int NT, bool BF16 = false>
 int launch_tapbox(const CUtensorMap& xm, const CUtensorMap& wm, const ConvTapParams& p, cudaStream_t st) {
   constexpr int STAGE = 128 * 128 + NT * 128;
@@ -406,6 +411,39 @@ __global__ void pack_tapbox_kernel(const float* __restrict__ w, int cout, int ci
       }
     }
     out[idx] = vpx::tf32_rn(v);
+  }
+}
+
+// Same packing, one block per packed row o: the row's source weights
+// (K input channels x T taps) are staged in shared memory with coalesced
+// reads, then every entry's 32-channel segment is written as one 128-byte
+// run.  pack_tapbox_kernel's thread-per-element form reads w with a 27- or
+// 27*cin-float stride between neighbouring threads (~11 us per deep-layer
+// pass, eight passes per CosmoFlow step).  smem row stride Tp = T rounded up
+// to odd keeps the segment reads conflict-free.
+__global__ void pack_tapbox_rows_kernel(const float* __restrict__ w, int cout, int cin, int mode, int kind,
+                                        const __grid_constant__ ConvTapParams tp, int n_entries, int ntot,
+                                        int kchan, float* __restrict__ out) {
+  extern __shared__ float srow[];
+  const int o = blockIdx.x;
+  const int T = kind == 0 ? 27 : kind == 1 ? 8 : 1, Tp = T | 1;
+  const int kpad = (kchan + 31) / 32 * 32;
+  const bool live = o < tp.nvalid;
+  for (int idx = threadIdx.x; idx < kpad * T; idx += blockDim.x) {
+    const int i = idx / T, t = idx % T;
+    float v = 0.f;
+    if (live && i < kchan) {
+      if (kind == 2) v = w[((long long)i * cout + o % cout) * 8 + o / cout];
+      else if (kind == 1) v = mode == 1 ? w[((long long)i * cout + o) * 8 + t] : w[((long long)o * cout + i) * 8 + t];
+      else v = mode == 0 ? w[((long long)o * cin + i) * 27 + t] : w[((long long)i * cin + o) * 27 + t];
+    }
+    srow[i * Tp + t] = v;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  for (int e = threadIdx.x >> 5; e < n_entries; e += blockDim.x >> 5) {
+    const int chunk = (tp.entries[e] >> 8) & 0xff, tap = kind == 2 ? 0 : tp.entries[e] >> 16;
+    out[((long long)e * ntot + o) * 32 + lane] = vpx::tf32_rn(srow[(32 * chunk + lane) * Tp + tap]);
   }
 }
 
@@ -553,8 +591,15 @@ int conv_tapbox(int mode, const float* in, const Frame& inf, const float* w, int
     if (bf16 & 1)
       pack_tapbox_bf16_kernel<<<grid, 256, 0, st>>>(w, cout, cin, mode, p, ne, ntot,
                                                     reinterpret_cast<__nv_bfloat16*>(wpack));
-    else
+    else if (getenv("VPX_PACK_ELEMWISE"))
       pack_tapbox_kernel<<<grid, 256, 0, st>>>(w, cout, cin, mode, merged ? 2 : kind, p, ne, ntot, wpack);
+    else {
+      const int kk = merged ? 2 : kind, T = kk == 0 ? 27 : kk == 1 ? 8 : 1;
+      const int smem = (kchan + 31) / 32 * 32 * (T | 1) * 4;
+      if (smem > 48 * 1024)
+        VPX_CHECK_CUDA(cudaFuncSetAttribute(pack_tapbox_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      pack_tapbox_rows_kernel<<<ntot, 256, smem, st>>>(w, cout, cin, mode, kk, p, ne, ntot, kchan, wpack);
+    }
     VPX_LAUNCH_CHECK();
   }
   p.n = of.n;

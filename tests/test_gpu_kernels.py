@@ -175,6 +175,42 @@ def test_first_block_fused_forward_and_mask_backward(shape, margins):
     assert torch.equal(wg_y, wg_m)
 
 
+@pytest.mark.parametrize("cin,cout,spatial,stride", [(256, 256, (4, 4, 4), 1), (256, 256, (8, 8, 8), 1),
+                                                    (128, 256, (8, 8, 8), 2), (64, 128, (8, 8, 16), 2)])
+def test_tapbox_row_pack_bit_exact(cin, cout, spatial, stride, monkeypatch):
+    """Deep-layer tap-box passes (split K): the row-staged weight pack gives
+    the same bits as the element-wise pack, forward and backward-data, and
+    the forward stays within the TF32 tolerance of the oracle."""
+    rng = np.random.default_rng(17)
+    n = 1
+    x = O.tf32_round(rng.standard_normal((n, cin) + spatial).astype(np.float32))
+    w = (rng.standard_normal((cout, cin, 3, 3, 3)) / np.sqrt(27 * cin)).astype(np.float32)
+    od = tuple(-(-e // stride) for e in spatial)
+    u = O.tf32_round(rng.standard_normal((n, cout) + od).astype(np.float32))
+    wt = torch.from_numpy(w).cuda()
+
+    def run():
+        xf = Frame(n, cin, *spatial, (1, 1, 0), zero=True).load_ncdhw(x)
+        yf = Frame(n, cout, *od)
+        W = ws(cin, cout, 3, yf)
+        _lib.call("vpx_conv3d_fwd", xf.ptr, xf.desc, wt.data_ptr(), 3, stride, yf.ptr, yf.desc, W.data_ptr(),
+                  W.numel() * 4, stream_ptr())
+        uf = Frame(n, cout, *od).load_ncdhw(u)
+        gf = Frame(n, cin, *spatial, (1, 1, 0), zero=True)
+        _lib.call("vpx_conv3d_bwd_data", uf.ptr, uf.desc, wt.data_ptr(), 3, stride, gf.ptr, gf.desc, W.data_ptr(),
+                  W.numel() * 4, stream_ptr())
+        torch.cuda.synchronize()
+        return yf.t.clone(), gf.t.clone()
+
+    y1, g1 = run()
+    monkeypatch.setenv("VPX_PACK_ELEMWISE", "1")
+    y2, g2 = run()
+    assert torch.equal(y1.view(torch.int32), y2.view(torch.int32))
+    assert torch.equal(g1.view(torch.int32), g2.view(torch.int32))
+    assert rel(Frame(n, cout, *od, tensor=y1).to_ncdhw().cpu().numpy(),
+               O.k_conv3d_fwd(np.pad(x, ((0, 0), (0, 0), (1, 1), (1, 1), (1, 1))), w, (stride,) * 3)) < TF32_RTOL
+
+
 def test_tapbox_dgrad_all_margins():
     """W-partitioned frames (margins in all three dims) go through the tap-box
     kernel for both passes."""
