@@ -242,6 +242,28 @@ long long wgrad_simt_parts(const Frame& uf) {
 }
 
 // Few partials (P <= 64): one thread per output walks them in order.
+// Contiguous destination (inner == len, out_off == 0), float4 lanes, P summed
+// in order -- the same sums as reduce_partials_seq_kernel.
+__global__ void reduce_partials_seq4_kernel(const float4* __restrict__ part, int P, long long len4,
+                                            float4* __restrict__ out, int accumulate) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < len4;
+       i += (long long)gridDim.x * blockDim.x) {
+    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int p = 0; p < P; ++p) {
+      const float4 v = part[(long long)p * len4 + i];
+      s.x += v.x;
+      s.y += v.y;
+      s.z += v.z;
+      s.w += v.w;
+    }
+    if (accumulate) {
+      const float4 o = out[i];
+      s = make_float4(o.x + s.x, o.y + s.y, o.z + s.z, o.w + s.w);
+    }
+    out[i] = s;
+  }
+}
+
 __global__ void reduce_partials_seq_kernel(const float* __restrict__ part, int P, long long len, int inner,
                                            long long out_stride, long long out_off, float* __restrict__ out,
                                            int accumulate) {
@@ -257,6 +279,13 @@ __global__ void reduce_partials_seq_kernel(const float* __restrict__ part, int P
 int reduce_partials_slice(const float* part, int P, long long len, int inner, long long out_stride,
                           long long out_off, float* out, int accumulate, cudaStream_t st) {
   if (len <= 0) return VPX_OK;
+  if (P <= 64 && inner == len && out_off == 0 && len % 4 == 0 &&
+      (reinterpret_cast<uintptr_t>(part) | reinterpret_cast<uintptr_t>(out)) % 16 == 0) {
+    reduce_partials_seq4_kernel<<<grid_for(len / 4, 256), 256, 0, st>>>(
+        reinterpret_cast<const float4*>(part), P, len / 4, reinterpret_cast<float4*>(out), accumulate);
+    VPX_LAUNCH_CHECK();
+    return VPX_OK;
+  }
   if (P <= 64) {
     reduce_partials_seq_kernel<<<grid_for(len, 256), 256, 0, st>>>(part, P, len, inner, out_stride, out_off, out,
                                                                      accumulate);

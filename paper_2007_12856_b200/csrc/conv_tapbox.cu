@@ -127,9 +127,23 @@ __device__ __forceinline__ void tapbox_reduce_elem(const ConvTapParams& p, int t
                                   px >= p.pw_lo && px < p.pw_hi));
   if (!valid || nt * NT + 4 * c4 >= p.nvalid) return;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int ks = 0; ks < p.ksplit; ++ks) {
-    const float4 v = reinterpret_cast<const float4*>(
-        p.part + ((static_cast<long long>(ks) * p.base_tiles + tb) * 128 + r) * NT)[c4];
+  const float4* src = reinterpret_cast<const float4*>(p.part + (static_cast<long long>(tb) * 128 + r) * NT) + c4;
+  const long long kstride = static_cast<long long>(p.base_tiles) * 128 * NT / 4;
+  int ks = 0;
+  for (; ks + 4 <= p.ksplit; ks += 4) {  // four independent loads in flight, summed in order
+    float4 v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) v[j] = src[(ks + j) * kstride];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      acc.x += v[j].x;
+      acc.y += v[j].y;
+      acc.z += v[j].z;
+      acc.w += v[j].w;
+    }
+  }
+  for (; ks < p.ksplit; ++ks) {
+    const float4 v = src[ks * kstride];
     acc.x += v.x;
     acc.y += v.y;
     acc.z += v.z;
@@ -324,6 +338,7 @@ __global__ void __launch_bounds__(256, 1)
         float v[16];
         vpx::tmem_ld16(tbase + (static_cast<uint32_t>(q * 32) << 16) + acc * TCOLS + cb, v);
         if (p.ksplit > 1) {
+          if (!valid) continue;  // tapbox_reduce_elem skips these rows too
           float4* o4 = reinterpret_cast<float4*>(prow + cb);
 #pragma unroll
           for (int i = 0; i < 4; ++i)
@@ -414,36 +429,37 @@ __global__ void pack_tapbox_kernel(const float* __restrict__ w, int cout, int ci
   }
 }
 
-// Same packing, one block per packed row o: the row's source weights
-// (K input channels x T taps) are staged in shared memory with coalesced
-// reads, then every entry's 32-channel segment is written as one 128-byte
-// run.  pack_tapbox_kernel's thread-per-element form reads w with a 27- or
-// 27*cin-float stride between neighbouring threads (~11 us per deep-layer
-// pass, eight passes per CosmoFlow step).  smem row stride Tp = T rounded up
-// to odd keeps the segment reads conflict-free.
+// Same packing, one block per (packed row o, 32-channel chunk): the chunk's
+// source weights (32 input channels x T taps -- one contiguous run for the
+// forward layout, 32 runs of T floats for the transposed one) are staged in
+// shared memory with coalesced reads, then each entry of that chunk is
+// written as one 128-byte run.  pack_tapbox_kernel's thread-per-element form
+// reads w with a 27- or 27*cin-float stride between neighbouring threads.
+// smem row stride Tp = T rounded up to odd keeps the segment reads
+// conflict-free.
 __global__ void pack_tapbox_rows_kernel(const float* __restrict__ w, int cout, int cin, int mode, int kind,
                                         const __grid_constant__ ConvTapParams tp, int n_entries, int ntot,
                                         int kchan, float* __restrict__ out) {
-  extern __shared__ float srow[];
-  const int o = blockIdx.x;
+  __shared__ float srow[32 * 27];
+  const int o = blockIdx.x, chunk = blockIdx.y;
   const int T = kind == 0 ? 27 : kind == 1 ? 8 : 1, Tp = T | 1;
-  const int kpad = (kchan + 31) / 32 * 32;
   const bool live = o < tp.nvalid;
-  for (int idx = threadIdx.x; idx < kpad * T; idx += blockDim.x) {
-    const int i = idx / T, t = idx % T;
+  for (int idx = threadIdx.x; idx < 32 * T; idx += blockDim.x) {
+    const int r = idx / T, t = idx % T, i = 32 * chunk + r;
     float v = 0.f;
     if (live && i < kchan) {
       if (kind == 2) v = w[((long long)i * cout + o % cout) * 8 + o / cout];
       else if (kind == 1) v = mode == 1 ? w[((long long)i * cout + o) * 8 + t] : w[((long long)o * cout + i) * 8 + t];
       else v = mode == 0 ? w[((long long)o * cin + i) * 27 + t] : w[((long long)i * cin + o) * 27 + t];
     }
-    srow[i * Tp + t] = v;
+    srow[r * Tp + t] = v;
   }
   __syncthreads();
   const int lane = threadIdx.x & 31;
   for (int e = threadIdx.x >> 5; e < n_entries; e += blockDim.x >> 5) {
-    const int chunk = (tp.entries[e] >> 8) & 0xff, tap = kind == 2 ? 0 : tp.entries[e] >> 16;
-    out[((long long)e * ntot + o) * 32 + lane] = vpx::tf32_rn(srow[(32 * chunk + lane) * Tp + tap]);
+    if (((tp.entries[e] >> 8) & 0xff) != chunk) continue;
+    const int tap = kind == 2 ? 0 : tp.entries[e] >> 16;
+    out[((long long)e * ntot + o) * 32 + lane] = vpx::tf32_rn(srow[lane * Tp + tap]);
   }
 }
 
@@ -594,11 +610,8 @@ int conv_tapbox(int mode, const float* in, const Frame& inf, const float* w, int
     else if (getenv("VPX_PACK_ELEMWISE"))
       pack_tapbox_kernel<<<grid, 256, 0, st>>>(w, cout, cin, mode, merged ? 2 : kind, p, ne, ntot, wpack);
     else {
-      const int kk = merged ? 2 : kind, T = kk == 0 ? 27 : kk == 1 ? 8 : 1;
-      const int smem = (kchan + 31) / 32 * 32 * (T | 1) * 4;
-      if (smem > 48 * 1024)
-        VPX_CHECK_CUDA(cudaFuncSetAttribute(pack_tapbox_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      pack_tapbox_rows_kernel<<<ntot, 256, smem, st>>>(w, cout, cin, mode, kk, p, ne, ntot, kchan, wpack);
+      pack_tapbox_rows_kernel<<<dim3(ntot, nchunks), 128, 0, st>>>(w, cout, cin, mode, merged ? 2 : kind, p, ne,
+                                                                    ntot, kchan, wpack);
     }
     VPX_LAUNCH_CHECK();
   }

@@ -272,6 +272,11 @@ int wgrad_tc_parts(const Frame& xf, const Frame& uf) {
   // one CTA per SM (smem-limited): nsub * P must not exceed the SM count, or the
   // leftover CTAs run as a second wave and double the kernel time
   long long P = num_sms() / nsub;
+  // deep layers (c6, c7 at 8^3 / 4^3): with only a few hundred voxels of K
+  // per CTA the kernel is bound by writing the P partial filter gradients
+  // (7 MB each at 256x256x27), not by the MMAs -- keep >= 256 voxels per slice
+  const long long kvox = rows * (uf.w < 8 ? 8 : uf.w < 128 ? uf.w : 128);
+  if (P > kvox / 256) P = kvox / 256;
   if (P < 1) P = 1;
   if (P > rows) P = rows;
   return static_cast<int>(P);

@@ -24,6 +24,7 @@ kernel over the flat parameter / moment buffers.
 
 from __future__ import annotations
 
+import contextlib
 import os
 from dataclasses import dataclass, field
 
@@ -763,7 +764,7 @@ class CapturedStep:
     loss tensor returned is the graph's static output."""
 
     def __init__(self, ctx: RankCtx, plan: Plan, state: RankState, batch: Batch, lr: float, seed: int = 0,
-                 warmup: int = 2):
+                 warmup: int = 2, recorder=None):
         self.ctx, self.plan, self.state, self.batch, self.seed = ctx, plan, state, batch, seed
         self.scalars = StepScalars(plan.net, batch.sample_ids)
         side = torch.cuda.Stream()
@@ -775,7 +776,9 @@ class CapturedStep:
         torch.cuda.current_stream().wait_stream(side)
         torch.cuda.synchronize()
         self.graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(self.graph):
+        # recorder: a timing.Recorder(graph=True) active during the capture only
+        # (its regions become event nodes re-timed by every replay)
+        with torch.cuda.graph(self.graph), (recorder if recorder is not None else contextlib.nullcontext()):
             self.loss = train_step(ctx, plan, state, batch, lr, seed, scalars=self.scalars, as_tensor=True)
 
     def __call__(self, lr: float, epoch: int = None, iteration: int = None):
