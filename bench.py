@@ -528,37 +528,34 @@ def run_ours(args):
 
     # --------------------------------------------------- e2e (host buffers)
     # Every step's input block comes from pinned host memory through the
-    # engine's HostInputPipeline (H2D on a copy stream, overlapped with the
-    # previous step), and the step's loss is read back to the host.  Headline
+    # engine's PipelinedSteps (H2D + layout on a copy stream, overlapped with
+    # the previous step), and the step's loss is read back to the host.  Headline
     # path: the datastore (HSB1 file -> DataStore pinned cache in the int16
     # storage dtype -> H2D -> int16->fp32 conversion fused into the layout
     # kernel), i.e. the reference's own ingest flow (reference datastore.py);
     # the fp32-host-array path is reported beside it.
     def time_e2e(host_block, note):
+        # engine.PipelinedSteps: two input frames with one captured step
+        # graph each; step i+1's H2D copy and int->fp32 layout run on a copy
+        # stream while step i computes; every step's loss is copied to pinned
+        # host memory and read on the host (the previous step's, while the
+        # current one runs).  Graph capture and warm-up happen before t0.
         h2d = host_block.numel() * host_block.element_size() if host_block is not None else 0
-        pipe = engine.HostInputPipeline(host_block) if host_block is not None else None
+        pipe = engine.PipelinedSteps(ctx, plan, state, batch, host_block, 1e-4)
         torch.cuda.synchronize()
         ctx.barrier()
         t0 = time.perf_counter()
         s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s0.record(stream)
-        if pipe is not None:
-            pipe.start(after=s0)
-        loss_host = None
+        pipe.start(after=s0)
         first_nan = None
         for i in range(args.steps):
-            if pipe is not None:
-                pipe.load(batch, prefetch_next=i + 1 < args.steps)
-            loss = step()
-            loss_host = float(loss.item())  # D2H of the step's result
-            if first_nan is None and not math.isfinite(loss_host):
-                first_nan = i
-            if os.environ.get("VPX_BENCH_DEBUG") and i < 2:
-                fr = batch.x_block.t
-                print(f"[debug] {note[:12]} step {i}: loss {loss_host} x nan {int(torch.isnan(fr).sum())} "
-                      f"x absmax {float(fr.abs().max())} param nan {int(torch.isnan(state.params.flat).sum())} "
-                      f"grad nan {int(torch.isnan(state.params.grad).sum())} buf {[tuple(b.shape) for b in pipe._buf]} "
-                      f"{[float(b.float().abs().max()) for b in pipe._buf]}", file=sys.stderr, flush=True)
+            prev = pipe.step(1e-4, prefetch_next=i + 1 < args.steps)
+            if prev is not None and first_nan is None and not math.isfinite(prev):
+                first_nan = i - 1
+        loss_host = pipe.finish()  # D2H of the last step's result
+        if first_nan is None and not math.isfinite(loss_host):
+            first_nan = args.steps - 1
         s1.record(stream)
         torch.cuda.synchronize()
         ctx.barrier()
@@ -566,8 +563,11 @@ def run_ours(args):
         t = torch.tensor([s0.elapsed_time(s1), wall], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        d2h = pipe._loss_host.element_size() if pipe._loss_host is not None else 4
+        del pipe
+        torch.cuda.empty_cache()
         return {"value": n_global * args.steps / (float(t[0]) * 1e-3), "unit": "samples/s",
-                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8, "wall_ms": float(t[1]), "loss": loss_host,
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "wall_ms": float(t[1]), "loss": loss_host,
                 "first_nonfinite_step": first_nan,
                 "input_path": note}
 
@@ -579,17 +579,17 @@ def run_ours(args):
             e2e = time_e2e(ds_block, "HSB1 sample file -> DataStore.ingest_epoch0 (this rank's hyperslab, pinned "
                                      "int16 cache) -> DataStore.transfer_block (" +
                                      ("pinned int8 copy, made once: the voxels fit int8" if nb == 1 else "the int16 block") +
-                                     f") -> engine.HostInputPipeline (H2D {nb} B/voxel on a copy stream, "
-                                     "double-buffered) -> vpx_layout_ncdhw_i" + ("8" if nb == 1 else "16") +
-                                     "_to_frame (int->fp32 + layout); loss.item() each step")
+                                     f") -> engine.PipelinedSteps (H2D {nb} B/voxel and vpx_layout_ncdhw_i" +
+                                     ("8" if nb == 1 else "16") + "_to_frame (int->fp32 + layout) on a copy "
+                                     "stream into the other of two input frames; loss read back each step)")
         if ds_block is not None and ds_block.dtype != torch.int16:
             # the general case: voxels that do not fit int8 travel in the int16 storage dtype
             e2e_i16 = time_e2e(datastore_block(args, net, grid, plan, ctx, W, torch.int16),
                                "HSB1 sample file -> DataStore.ingest_epoch0 (pinned int16 cache) -> "
-                               "DataStore.transfer_block(dtype=int16) -> engine.HostInputPipeline (H2D 2 B/voxel) "
-                               "-> vpx_layout_ncdhw_i16_to_frame; loss.item() each step")
-        e2e_fp32 = time_e2e(x_host, "pinned host fp32 NCDHW array -> engine.HostInputPipeline (copy stream, "
-                                    "double-buffered) -> frame; loss.item() each step")
+                               "DataStore.transfer_block(dtype=int16) -> engine.PipelinedSteps (H2D 2 B/voxel + "
+                               "vpx_layout_ncdhw_i16_to_frame on a copy stream; loss read back each step)")
+        e2e_fp32 = time_e2e(x_host, "pinned host fp32 NCDHW array -> engine.PipelinedSteps (H2D + layout on a "
+                                    "copy stream into the other of two input frames; loss read back each step)")
         if e2e is None:
             e2e = e2e_fp32
 

@@ -913,3 +913,101 @@ class HostInputPipeline:
         if prefetch_next:
             self._issue(self._step)
         return batch
+
+
+class PipelinedSteps:
+    """Training-loop driver over host-resident input blocks: the end-to-end
+    path (HSB1 datastore -> pinned host block -> device -> step -> loss on
+    the host) with no host->device work on the compute stream.
+
+    Two input frames, each with its own captured step graph (CapturedStep on
+    a twin of `batch` whose x_block is a second DistTensor).  While step i
+    replays from frame i % 2, a copy stream moves step i+1's pinned block to
+    a device staging buffer and converts it into frame (i+1) % 2 with the
+    int -> fp32 layout kernel (vpx_layout_ncdhw_i8/i16_to_frame), so both the
+    PCIe copy and the layout overlap compute; a frame is rewritten only after
+    the graph that read it has finished (an event per frame).  Each step's
+    loss is copied to pinned host memory asynchronously; `step()` returns the
+    PREVIOUS step's loss as a float (its copy completed while this step was
+    queued), `finish()` the last one.  The reference reads each step's block
+    from its datastore on the host and calls train_step (reference
+    data/datastore.py:156-179, model/engine.py:465-473).
+
+    host_blocks: a callable step -> pinned NCDHW host tensor (this rank's
+    block) or one tensor reused every step.  Ranks holding no input block
+    (batch.x_block is None) replay without input traffic.
+    """
+
+    def __init__(self, ctx: RankCtx, plan: Plan, state: RankState, batch: Batch, host_blocks, lr: float,
+                 seed: int = 0, warmup: int = 2):
+        twin = Batch(x_block=batch.x_block.clone() if batch.x_block is not None else None, target=batch.target,
+                     y_block=batch.y_block, sample_ids=batch.sample_ids, epoch=batch.epoch,
+                     iteration=batch.iteration)
+        self.batches = (batch, twin)
+        self.caps = tuple(CapturedStep(ctx, plan, state, b, lr, seed, warmup=warmup) for b in self.batches)
+        self.has_input = batch.x_block is not None and host_blocks is not None
+        self._src = host_blocks if callable(host_blocks) else (lambda i, t=host_blocks: t)
+        self.copy_stream = torch.cuda.Stream()
+        self.bytes_per_step = 0
+        if self.has_input:
+            first = self._src(0)
+            self.shape, self.dtype = tuple(first.shape), first.dtype
+            self.bytes_per_step = first.numel() * first.element_size()
+            self._stage = [torch.empty(self.shape, dtype=self.dtype, device="cuda") for _ in range(2)]
+        self._ready = [torch.cuda.Event() for _ in range(2)]
+        self._free = [None, None]
+        self._loss_host = None  # pinned, allocated with the loss dtype at the first step
+        self._loss_ev = [torch.cuda.Event() for _ in range(2)]
+        self.i = 0
+        self._prepared = -1
+
+    def _prepare(self, i: int):
+        f = i % 2
+        cs = self.copy_stream
+        with torch.cuda.stream(cs):
+            if self._free[f] is not None:
+                cs.wait_event(self._free[f])
+            if self.has_input:
+                blk = self._src(i)
+                if blk.dtype != self.dtype or tuple(blk.shape) != self.shape:
+                    raise ShapeMismatch(f"input block {i}: {blk.dtype} {tuple(blk.shape)}, pipeline staged "
+                                        f"{self.dtype} {self.shape}")
+                self._stage[f].copy_(blk, non_blocking=True)
+                self.batches[f].x_block.load_ncdhw(self._stage[f])
+            self._ready[f].record(cs)
+        self._prepared = i
+
+    def start(self, after: torch.cuda.Event = None):
+        """Queue step 0's input (optionally after `after` on the copy stream)."""
+        if after is not None:
+            self.copy_stream.wait_event(after)
+        self._prepare(self.i)
+
+    def step(self, lr: float, prefetch_next: bool = True):
+        i, f = self.i, self.i % 2
+        if self._prepared < i:
+            self._prepare(i)
+        cur = torch.cuda.current_stream()
+        cur.wait_event(self._ready[f])
+        loss = self.caps[f](lr)
+        done = torch.cuda.Event()
+        done.record(cur)
+        self._free[f] = done
+        if self._loss_host is None:
+            self._loss_host = torch.zeros(2, dtype=loss.dtype).pin_memory()
+        self._loss_host[f:f + 1].copy_(loss.reshape(1), non_blocking=True)
+        self._loss_ev[f].record(cur)
+        if prefetch_next:
+            self._prepare(i + 1)
+        prev = None
+        if i > 0:
+            self._loss_ev[1 - f].synchronize()
+            prev = float(self._loss_host[1 - f])
+        self.i += 1
+        return prev
+
+    def finish(self) -> float:
+        """The last step's loss (waits for it)."""
+        f = (self.i - 1) % 2
+        self._loss_ev[f].synchronize()
+        return float(self._loss_host[f])

@@ -213,6 +213,47 @@ def test_captured_step_equals_eager_steps(width):
     assert l0 == l1
 
 
+@pytest.mark.parametrize("dtype", [torch.int8, torch.int16])
+def test_pipelined_steps_equal_eager_steps(dtype):
+    """engine.PipelinedSteps (two input frames, one graph each, H2D + layout
+    of the next step's block on a copy stream, asynchronous loss readback)
+    takes exactly the eager steps on the same per-step host blocks: every
+    step's loss and the final parameters agree bit for bit.  Each step gets a
+    different block, so a replay reading a stale or half-written frame would
+    show."""
+    width, warm, K = 32, 1, 6
+    net = build_cosmoflow(width)
+    ctx = RankCtx(0, 1)
+    plan = engine.make_plan(net, ProcessGrid(1, 1, 1, 1), 1, width)
+    x, y, ids = engine.synthetic_batch_full(net, width, 1, 0)
+    g = torch.Generator().manual_seed(3)
+    blocks = [torch.randint(-8, 9, (1, 4, width, width, width), generator=g).to(dtype).pin_memory() for _ in range(K)]
+    runs = []
+    for pipelined in (False, True):
+        state = engine.make_state(net, 0)
+        batch = engine.scatter_batch(plan, x, y, ids, 0)
+        losses = []
+        if pipelined:
+            pipe = engine.PipelinedSteps(ctx, plan, state, batch, lambda i: blocks[i], 1e-3, warmup=warm)
+            pipe.start()
+            for i in range(K):
+                prev = pipe.step(1e-3, prefetch_next=i + 1 < K)
+                if prev is not None:
+                    losses.append(prev)
+            losses.append(pipe.finish())
+        else:
+            for _ in range(2 * warm):  # the two graphs' warm-up steps, on the initial input
+                engine.train_step(ctx, plan, state, batch, 1e-3)
+            for i in range(K):
+                batch.x_block.load_ncdhw(blocks[i].cuda())
+                losses.append(engine.train_step(ctx, plan, state, batch, 1e-3))
+        torch.cuda.synchronize()
+        runs.append((losses, state.params.flat.clone()))
+    (l0, p0), (l1, p1) = runs
+    assert l0 == l1
+    assert torch.equal(p0, p1)
+
+
 def _poison_free_memory():
     """Fill every free cached block and most free device memory with NaN, then
     hand it back to the allocator (exposes reads of never-written memory)."""
