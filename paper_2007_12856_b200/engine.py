@@ -939,7 +939,8 @@ class PipelinedSteps:
     """
 
     def __init__(self, ctx: RankCtx, plan: Plan, state: RankState, batch: Batch, host_blocks, lr: float,
-                 seed: int = 0, warmup: int = 2):
+                 seed: int = 0, warmup: int = 2, layout_sms: int = None):
+        self.layout_sms = int(os.environ.get("VPX_PIPE_LAYOUT_SMS", "0")) if layout_sms is None else layout_sms
         twin = Batch(x_block=batch.x_block.clone() if batch.x_block is not None else None, target=batch.target,
                      y_block=batch.y_block, sample_ids=batch.sample_ids, epoch=batch.epoch,
                      iteration=batch.iteration)
@@ -965,15 +966,27 @@ class PipelinedSteps:
         f = i % 2
         cs = self.copy_stream
         with torch.cuda.stream(cs):
-            if self._free[f] is not None:
-                cs.wait_event(self._free[f])
             if self.has_input:
                 blk = self._src(i)
                 if blk.dtype != self.dtype or tuple(blk.shape) != self.shape:
                     raise ShapeMismatch(f"input block {i}: {blk.dtype} {tuple(blk.shape)}, pipeline staged "
                                         f"{self.dtype} {self.shape}")
+                # the PCIe copy needs only the staging buffer (last read by
+                # the previous layout on this stream), so it may start while
+                # the step before the previous one still runs
                 self._stage[f].copy_(blk, non_blocking=True)
-                self.batches[f].x_block.load_ncdhw(self._stage[f])
+            if self._free[f] is not None:  # the frame: once the graph that read it is done
+                cs.wait_event(self._free[f])
+            if self.has_input:
+                # layout_sms: optionally confine the layout kernel to a few
+                # SMs' worth of blocks (vpx_set_sm_limit) while it runs beside the step
+                if self.layout_sms:
+                    _lib.call("vpx_set_sm_limit", self.layout_sms)
+                try:
+                    self.batches[f].x_block.load_ncdhw(self._stage[f])
+                finally:
+                    if self.layout_sms:
+                        _lib.call("vpx_set_sm_limit", 0)
             self._ready[f].record(cs)
         self._prepared = i
 
