@@ -429,37 +429,48 @@ __global__ void pack_tapbox_kernel(const float* __restrict__ w, int cout, int ci
   }
 }
 
-// Same packing, one block per (packed row o, 32-channel chunk): the chunk's
-// source weights (32 input channels x T taps -- one contiguous run for the
-// forward layout, 32 runs of T floats for the transposed one) are staged in
-// shared memory with coalesced reads, then each entry of that chunk is
-// written as one 128-byte run.  pack_tapbox_kernel's thread-per-element form
-// reads w with a 27- or 27*cin-float stride between neighbouring threads.
-// smem row stride Tp = T rounded up to odd keeps the segment reads
-// conflict-free.
-__global__ void pack_tapbox_rows_kernel(const float* __restrict__ w, int cout, int cin, int mode, int kind,
-                                        const __grid_constant__ ConvTapParams tp, int n_entries, int ntot,
-                                        int kchan, float* __restrict__ out) {
-  __shared__ float srow[32 * 27];
-  const int o = blockIdx.x, chunk = blockIdx.y;
+// Same packing, one block per packed row o: the row's K x T source weights
+// are staged in shared memory (one contiguous run for the forward layout),
+// then each warp writes whole 128-byte entry segments.  The thread-per-element
+// form above reads w with a 27- or 27*cin-float stride between neighbouring
+// threads: 14 vs 9 us per CosmoFlow c6/c7 pass (tools/small_pass.py), where
+// the pack is a third of the pass.  Row stride Tp = T rounded up to odd keeps
+// the segment reads conflict-free.
+__global__ void __launch_bounds__(256) pack_tapbox_row_kernel(const float* __restrict__ w, int cout, int cin,
+                                                              int mode, int kind,
+                                                              const __grid_constant__ ConvTapParams tp,
+                                                              int n_entries, int ntot, int kchan,
+                                                              float* __restrict__ out) {
+  extern __shared__ float srow2[];
+  const int o = blockIdx.x;
   const int T = kind == 0 ? 27 : kind == 1 ? 8 : 1, Tp = T | 1;
+  const int kpad = (kchan + 31) / 32 * 32;
   const bool live = o < tp.nvalid;
-  for (int idx = threadIdx.x; idx < 32 * T; idx += blockDim.x) {
-    const int r = idx / T, t = idx % T, i = 32 * chunk + r;
-    float v = 0.f;
-    if (live && i < kchan) {
-      if (kind == 2) v = w[((long long)i * cout + o % cout) * 8 + o / cout];
-      else if (kind == 1) v = mode == 1 ? w[((long long)i * cout + o) * 8 + t] : w[((long long)o * cout + i) * 8 + t];
-      else v = mode == 0 ? w[((long long)o * cin + i) * 27 + t] : w[((long long)i * cin + o) * 27 + t];
+  if (kind == 0 && mode == 0) {  // w[o][i][tap]: one contiguous run of cin * 27 floats
+    const float* src = w + (long long)o * cin * 27;
+    for (int idx = threadIdx.x; idx < kpad * 27; idx += blockDim.x) {
+      const int i = idx / 27, t = idx - i * 27;
+      srow2[i * Tp + t] = (live && i < kchan) ? src[idx] : 0.f;
     }
-    srow[r * Tp + t] = v;
+  } else {
+    for (int idx = threadIdx.x; idx < kpad * T; idx += blockDim.x) {
+      const int i = idx / T, t = idx % T;
+      float v = 0.f;
+      if (live && i < kchan) {
+        if (kind == 2) v = w[((long long)i * cout + o % cout) * 8 + o / cout];
+        else if (kind == 1) v = mode == 1 ? w[((long long)i * cout + o) * 8 + t] : w[((long long)o * cout + i) * 8 + t];
+        else v = w[((long long)i * cin + o) * 27 + t];
+      }
+      srow2[i * Tp + t] = v;
+    }
   }
   __syncthreads();
   const int lane = threadIdx.x & 31;
+#pragma unroll 4
   for (int e = threadIdx.x >> 5; e < n_entries; e += blockDim.x >> 5) {
-    if (((tp.entries[e] >> 8) & 0xff) != chunk) continue;
-    const int tap = kind == 2 ? 0 : tp.entries[e] >> 16;
-    out[((long long)e * ntot + o) * 32 + lane] = vpx::tf32_rn(srow[lane * Tp + tap]);
+    const int ent = tp.entries[e];
+    const int chunk = (ent >> 8) & 0xff, tap = kind == 2 ? 0 : ent >> 16;
+    out[((long long)e * ntot + o) * 32 + lane] = vpx::tf32_rn(srow2[(32 * chunk + lane) * Tp + tap]);
   }
 }
 
@@ -607,11 +618,16 @@ int conv_tapbox(int mode, const float* in, const Frame& inf, const float* w, int
     if (bf16 & 1)
       pack_tapbox_bf16_kernel<<<grid, 256, 0, st>>>(w, cout, cin, mode, p, ne, ntot,
                                                     reinterpret_cast<__nv_bfloat16*>(wpack));
-    else if (getenv("VPX_PACK_ELEMWISE"))
+    // the row-staged form wins once there are >= 256 packed rows (one block
+    // each); below that the element-wise form's parallelism wins (c4, c5 dgrad)
+    else if (ntot < 256 || getenv("VPX_PACK_ELEMWISE"))  // tests compare the two bit for bit
       pack_tapbox_kernel<<<grid, 256, 0, st>>>(w, cout, cin, mode, merged ? 2 : kind, p, ne, ntot, wpack);
     else {
-      pack_tapbox_rows_kernel<<<dim3(ntot, nchunks), 128, 0, st>>>(w, cout, cin, mode, merged ? 2 : kind, p, ne,
-                                                                    ntot, kchan, wpack);
+      const int kk = merged ? 2 : kind, T = kk == 0 ? 27 : kk == 1 ? 8 : 1;
+      const int smem = (kchan + 31) / 32 * 32 * (T | 1) * 4;
+      if (smem > 48 * 1024)
+        VPX_CHECK_CUDA(cudaFuncSetAttribute(pack_tapbox_row_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      pack_tapbox_row_kernel<<<ntot, 256, smem, st>>>(w, cout, cin, mode, kk, p, ne, ntot, kchan, wpack);
     }
     VPX_LAUNCH_CHECK();
   }
