@@ -95,6 +95,19 @@ int vpx_conv3d_bwd_data(const float* u, const int* ufr, const float* w, int k, i
 int vpx_conv3d_bwd_data_range(const float* u, const int* ufr, const float* w, int k, int stride, float* xg,
                               const int* gfr, int zlo, int zhi, void* ws, long long ws_bytes, void* stream);
 
+/* Weight pre-packing (no reference counterpart: the reference convolves from
+ * the OIDHW weights directly).  Every conv pass packs its weights into its
+ * kernel's operand layout; between vpx_prepack_begin and vpx_prepack_end a
+ * pass whose pack was recorded on an earlier step and redone by
+ * vpx_prepack_all reads that buffer instead (the engine runs prepack_all on a
+ * side stream beside the first layer).  owner/owner_numel: the flat weight
+ * buffer (a new owner drops every recorded pack).  prepack_end: the weights
+ * changed, no pack is current.  prepack_entries: the recorded packs. */
+int vpx_prepack_begin(unsigned long long owner, long long owner_numel);
+int vpx_prepack_all(void* stream);
+int vpx_prepack_end(void);
+int vpx_prepack_entries(void);
+
 /* wg (=|+=) sum over voxels of u (x) x-patches; x frame margins must hold the
  * exchanged halos.  Replaces voxpar.kernels.conv3d_bwd_filter(xpad, u, stride,
  * kernel) (reference kernels/__init__.py:71, _hot.pyx:70-93).  Deterministic. */

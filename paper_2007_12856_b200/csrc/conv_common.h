@@ -55,7 +55,11 @@ int deconv_wgrad_tc_parts(const Frame& xf);
 int deconv_wgrad_tc(const float* x, const Frame& xf, const float* u, const Frame& uf, float* part, cudaStream_t st);
 int conv_tapbox(int mode, const float* in, const Frame& inf, const float* w, int cin, int cout, int stride,
                 float* out, const Frame& of, int act, float slope, void* ws, cudaStream_t st, long long ws_bytes,
-                int kind = 0, int bf16 = 0);
+                int kind = 0, int bf16 = 0, const float* wpre = nullptr, bool pack_only = false);
+// Packed-weight cache (conv_host.cu): the pack a conv pass would do, made
+// ahead of time by vpx_prepack_all; nullptr when there is no current one.
+enum PackPath { kPackRowh = 1, kPackRowwin = 2, kPackTapbox = 3 };
+const float* packcache_get(const float* w, int mode, int path, int cin, int cout, int stride, cudaStream_t st);
 int rowh_supported(int cin, int cout);
 long long rowh_packed_bytes(int cin, int cout);
 int rowh_pack(const float* w, int cout, int cin, int mode, float* dst, cudaStream_t st);

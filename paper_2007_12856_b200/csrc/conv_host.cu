@@ -7,6 +7,7 @@
 // host NCDHW arrays, explicit workspace instead of internal allocation.
 #include <climits>
 #include <cstdlib>
+#include <vector>
 
 #include "conv_common.h"
 #include "conv_simt.h"
@@ -205,6 +206,61 @@ static int pack(const float* w, int cout, int cin, int mode, float* dst, cudaStr
   return VPX_OK;
 }
 
+// ---------------------------------------------------------- packed weights
+// Every conv pass packs its weights into the kernel's B layout.  The engine
+// opts in to doing those packs ahead of the step, on a side stream that
+// overlaps the first layer (vpx_prepack_begin / vpx_prepack_all /
+// vpx_prepack_end): a pass whose (weights, direction, kernel, shape) entry
+// was packed under the current weights version reads that buffer and skips
+// its own pack.  Entries are recorded by the passes themselves (outside graph
+// capture), so the engine needs no knowledge of which kernel a pass picks.
+struct PackEntry {
+  const float* w;
+  int mode, path, cin, cout, stride;
+  float* buf;
+  unsigned long long ver;
+};
+static std::vector<PackEntry> g_packs;
+static unsigned long long g_wver = 1;  // entries start at 0: never current
+static int g_pack_on = 0;
+static unsigned long long g_pack_owner = 0;
+
+static long long pack_entry_bytes(int path, int mode, int cin, int cout) {
+  if (path == kPackRowh) return mode ? rowh_packed_bytes(cout, cin) : rowh_packed_bytes(cin, cout);
+  if (path == kPackRowwin) return packed_floats(cin, cout) * 4;
+  return tapbox_workspace_bytes(cin, cout);
+}
+
+static int pack_entry(const PackEntry& e, cudaStream_t st) {
+  if (e.path == kPackRowh) return rowh_pack(e.w, e.cout, e.cin, e.mode, e.buf, st);
+  if (e.path == kPackRowwin) return pack(e.w, e.cout, e.cin, e.mode, e.buf, st);
+  Frame dummy{};
+  return conv_tapbox(e.mode, nullptr, dummy, e.w, e.cin, e.cout, e.stride, nullptr, dummy, 0, 0.f, e.buf, st,
+                     tapbox_workspace_bytes(e.cin, e.cout), 0, 0, nullptr, true);
+}
+
+static void packcache_clear() {
+  for (auto& e : g_packs) cudaFree(e.buf);
+  g_packs.clear();
+}
+
+const float* packcache_get(const float* w, int mode, int path, int cin, int cout, int stride, cudaStream_t st) {
+  if (!g_pack_on) return nullptr;
+  for (const auto& e : g_packs)
+    if (e.w == w && e.mode == mode && e.path == path && e.cin == cin && e.cout == cout && e.stride == stride)
+      return e.ver == g_wver ? e.buf : nullptr;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return nullptr;
+  PackEntry e{w, mode, path, cin, cout, stride, nullptr, 0};
+  if (cudaMalloc(&e.buf, pack_entry_bytes(path, mode, cin, cout)) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  g_packs.push_back(e);
+  return nullptr;
+}
+
+
 }  // namespace vpx
 
 using vpx::Frame;
@@ -212,6 +268,38 @@ using vpx::Frame;
 // Grid budget of the persistent kernels launched after this call (0 = all
 // SMs).  Leaving a few SMs free lets communication kernels (NCCL) run next to
 // a convolution instead of after it.
+
+// Weight pre-packing (see packcache_get): begin a step for the weights
+// owned by `owner` (the flat parameter buffer; a new owner drops every entry)
+// and make a new weights version current; pack every recorded entry; end the
+// step (the optimizer has changed the weights: no entry is current).
+extern "C" int vpx_prepack_begin(unsigned long long owner, long long owner_numel) {
+  const unsigned long long tok = owner ^ (static_cast<unsigned long long>(owner_numel) << 1);
+  if (tok != vpx::g_pack_owner) {
+    vpx::packcache_clear();
+    vpx::g_pack_owner = tok;
+  }
+  vpx::g_pack_on = 1;
+  ++vpx::g_wver;
+  return VPX_OK;
+}
+
+extern "C" int vpx_prepack_all(void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  for (auto& e : vpx::g_packs) {
+    if (int rc = vpx::pack_entry(e, st)) return rc;
+    e.ver = vpx::g_wver;
+  }
+  return VPX_OK;
+}
+
+extern "C" int vpx_prepack_end(void) {
+  ++vpx::g_wver;
+  return VPX_OK;
+}
+
+extern "C" int vpx_prepack_entries(void) { return static_cast<int>(vpx::g_packs.size()); }
+
 extern "C" int vpx_set_sm_limit(int n) {
   vpx::g_sm_limit = n < 0 ? 0 : n;
   return VPX_OK;
@@ -271,21 +359,28 @@ static int conv_fwd_impl(const float* x, const int* xfr, const float* w, int k, 
   }
   if (tc && k == 3 && stride == 1 && yf.w % 128 == 0 && vpx::rowh_supported(cin, cout) && !vpx::rowh_off()) {
     if (ws_bytes < vpx::rowh_packed_bytes(cin, cout)) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "workspace too small");
-    float* wpack = static_cast<float*>(ws);
-    if (int rc = vpx::rowh_pack(w, cout, cin, 0, wpack, st)) return rc;
+    const float* wpack = vpx::packcache_get(w, 0, vpx::kPackRowh, cin, cout, 1, st);
+    if (!wpack) {
+      if (int rc = vpx::rowh_pack(w, cout, cin, 0, static_cast<float*>(ws), st)) return rc;
+      wpack = static_cast<float*>(ws);
+    }
     return vpx::rowh_run(x, xf, wpack, cin, cout, y, yf, zlo, zhi, 0, yf.h, yf.w, st, act, slope);
   }
   if (tc && k == 3 && stride == 1 && yf.w % 128 == 0 && vpx::rowwin_config(cin, cout, &R, &CG) &&
       !getenv("VPX_NO_ROWWIN")) {
     if (ws_bytes < vpx::packed_floats(cin, cout) * 4) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "workspace too small");
-    float* wpack = static_cast<float*>(ws);
-    if (int rc = vpx::pack(w, cout, cin, 0, wpack, st)) return rc;
+    const float* wpack = vpx::packcache_get(w, 0, vpx::kPackRowwin, cin, cout, 1, st);
+    if (!wpack) {
+      if (int rc = vpx::pack(w, cout, cin, 0, static_cast<float*>(ws), st)) return rc;
+      wpack = static_cast<float*>(ws);
+    }
     return vpx::rowwin_run(x, xf, wpack, cin, cout, y, yf, zlo, zhi, 0, yf.h, yf.w, st, act, slope);
   }
   if (!full && (zlo != 0 || zhi != yf.d)) VPX_FAIL(VPX_ERR_UNSUPPORTED, "conv fwd: plane ranges need a row kernel");
   if (tc && k == 3 && cin % 4 == 0 && vpx::tapbox_supported(cin, cout, 0)) {
     if (ws_bytes < vpx::tapbox_workspace_bytes(cin, cout)) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "workspace too small");
-    return vpx::conv_tapbox(0, x, xf, w, cin, cout, stride, y, yf, act, slope, ws, st, ws_bytes);
+    return vpx::conv_tapbox(0, x, xf, w, cin, cout, stride, y, yf, act, slope, ws, st, ws_bytes, 0, 0,
+                            vpx::packcache_get(w, 0, vpx::kPackTapbox, cin, cout, stride, st));
   }
   if (vpx::small_conv_supported(0, xf, yf, k, stride) && !getenv("VPX_NO_SMALL"))
     return vpx::small_conv_fwd(x, xf, w, k, y, yf, act, slope, st);
@@ -335,21 +430,28 @@ static int conv_bwd_data_impl(const float* u, const int* ufr, const float* w, in
   if (tc && k == 3 && stride == 1 && gf.mw == 0 && gf.w % 128 == 0 && vpx::rowh_supported(cout, cin) &&
       !vpx::rowh_off()) {
     if (ws_bytes < vpx::rowh_packed_bytes(cout, cin)) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "workspace too small");
-    float* wpack = static_cast<float*>(ws);
-    if (int rc = vpx::rowh_pack(w, cout, cin, 1, wpack, st)) return rc;
+    const float* wpack = vpx::packcache_get(w, 1, vpx::kPackRowh, cin, cout, 1, st);
+    if (!wpack) {
+      if (int rc = vpx::rowh_pack(w, cout, cin, 1, static_cast<float*>(ws), st)) return rc;
+      wpack = static_cast<float*>(ws);
+    }
     return vpx::rowh_run(u, uf, wpack, cout, cin, xg, gf, zlo, zhi, -gf.mh, gf.h + gf.mh, gf.w, st);
   }
   if (tc && k == 3 && stride == 1 && gf.mw == 0 && gf.w % 128 == 0 &&
       vpx::rowwin_config(cout, cin, &R, &CG) && !getenv("VPX_NO_ROWWIN")) {
     if (ws_bytes < vpx::packed_floats(cin, cout) * 4) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "workspace too small");
-    float* wpack = static_cast<float*>(ws);
-    if (int rc = vpx::pack(w, cout, cin, 1, wpack, st)) return rc;
+    const float* wpack = vpx::packcache_get(w, 1, vpx::kPackRowwin, cin, cout, 1, st);
+    if (!wpack) {
+      if (int rc = vpx::pack(w, cout, cin, 1, static_cast<float*>(ws), st)) return rc;
+      wpack = static_cast<float*>(ws);
+    }
     return vpx::rowwin_run(u, uf, wpack, cout, cin, xg, gf, zlo, zhi, -gf.mh, gf.h + gf.mh, gf.w, st);
   }
   if (!full) VPX_FAIL(VPX_ERR_UNSUPPORTED, "conv bwd_data: plane ranges need a row kernel");
   if (tc && k == 3 && cout % 4 == 0 && vpx::tapbox_supported(cin, cout, 1)) {
     if (ws_bytes < vpx::tapbox_workspace_bytes(cin, cout)) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "workspace too small");
-    return vpx::conv_tapbox(1, u, uf, w, cin, cout, stride, xg, gf, 0, 0.f, ws, st, ws_bytes);
+    return vpx::conv_tapbox(1, u, uf, w, cin, cout, stride, xg, gf, 0, 0.f, ws, st, ws_bytes, 0, 0,
+                            vpx::packcache_get(w, 1, vpx::kPackTapbox, cin, cout, stride, st));
   }
   if (k == 1 && vpx::small_conv_supported(1, uf, gf, k, stride) && !getenv("VPX_NO_SMALL"))
     return vpx::small_conv_bwd_data(u, uf, w, xg, gf, st);
@@ -478,8 +580,11 @@ extern "C" int vpx_conv3d_fwd_leaky_pool(const float* x, const int* xfr, const f
   if (!(slope > 0.f && slope <= 1.f)) VPX_FAIL(VPX_ERR_UNSUPPORTED, "fused conv+pool: slope must be in (0, 1]");
   if (ws_bytes < vpx::rowh_packed_bytes(cin, cout)) VPX_FAIL(VPX_ERR_SHAPE_MISMATCH, "workspace too small");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  float* wpack = static_cast<float*>(ws);
-  if (int rc = vpx::rowh_pack(w, cout, cin, 0, wpack, st)) return rc;
+  const float* wpack = vpx::packcache_get(w, 0, vpx::kPackRowh, cin, cout, 1, st);
+  if (!wpack) {
+    if (int rc = vpx::rowh_pack(w, cout, cin, 0, static_cast<float*>(ws), st)) return rc;
+    wpack = static_cast<float*>(ws);
+  }
   CUtensorMap map;
   {
     const uint64_t Wf = xf.w + 2 * xf.mw, Hf = xf.h + 2 * xf.mh, Df = xf.d + 2 * xf.md;

@@ -553,7 +553,7 @@ int tapbox_supported(int cin, int cout, int mode, int kind) {
 // in: the tensor streamed along K; out: the tensor written.
 int conv_tapbox(int mode, const float* in, const Frame& inf, const float* w, int cin, int cout, int stride,
                 float* out, const Frame& of, int act, float slope, void* ws, cudaStream_t st, long long ws_bytes,
-                int kind, int bf16) {
+                int kind, int bf16, const float* wpre, bool pack_only) {
   // transposed-conv forward as ONE GEMM per coarse-voxel tile: N = 8 parities x Cout,
   // the epilogue scatters column block P to the fine voxel 2q + P
   const bool merged = kind == 1 && mode == 1 && (8 * cout == 64 || 8 * cout == 128 || 8 * cout == 256);
@@ -610,8 +610,9 @@ int conv_tapbox(int mode, const float* in, const Frame& inf, const float* w, int
     }
   }
   p.cls_start[ncls] = ne;
-  float* wpack = static_cast<float*>(ws);
-  {
+  // wpre: weights packed earlier (vpx_prepack_all); pack_only: just the pack, into ws
+  float* wpack = wpre ? const_cast<float*>(wpre) : static_cast<float*>(ws);
+  if (!wpre) {
     const long long total = (long long)ne * ntot * cw;
     int grid = static_cast<int>((total + 255) / 256);
     if (grid > 8192) grid = 8192;
@@ -631,6 +632,7 @@ int conv_tapbox(int mode, const float* in, const Frame& inf, const float* w, int
     }
     VPX_LAUNCH_CHECK();
   }
+  if (pack_only) return VPX_OK;
   p.n = of.n;
   // q grid
   const int s_in = (mode == 0) ? stride : 1;

@@ -354,7 +354,7 @@ def _no_fused_pool() -> bool:
 
 
 def forward(ctx: RankCtx, plan: Plan, state: RankState, batch: Batch, mode: str, seed: int = 0,
-            trace: dict = None, scalars: "StepScalars" = None):
+            trace: dict = None, scalars: "StepScalars" = None, pack_wait: torch.cuda.Event = None):
     net = plan.net
     P, bn = state.params.views, state.bn_states
     me = ctx.rank
@@ -372,7 +372,7 @@ def forward(ctx: RankCtx, plan: Plan, state: RankState, batch: Batch, mode: str,
     for i, layer in enumerate(net.layers):
         if i < skip_to:
             continue
-        if (trace is None and cur is not None and layer.kind == "conv" and i + 3 < len(net.layers)
+        fused_block = (trace is None and cur is not None and layer.kind == "conv" and i + 3 < len(net.layers)
                 and net.layers[i + 1].kind == "leaky" and net.layers[i + 2].kind == "pool"
                 and len({plan.placement[i], plan.placement[i + 1], plan.placement[i + 2]}) == 1
                 and plan.placement[i] != "flat" and plan.redist_idx not in (i, i + 1, i + 2)
@@ -382,7 +382,13 @@ def forward(ctx: RankCtx, plan: Plan, state: RankState, batch: Batch, mode: str,
                                                  net.layers[i + 1].slope) if i == 0 else
                      D.block_fwd_pool_supported(cur, layer.params, net.layers[i + 2].pool_kind,
                                                 net.layers[i + 1].slope))
-                and not _no_fused_pool()):
+                and not _no_fused_pool())
+        if pack_wait is not None and (i > 0 or not fused_block):
+            # weights packed ahead on the side stream (train_step); the fused
+            # first block packs its own and runs while they are being made
+            torch.cuda.current_stream().wait_event(pack_wait)
+            pack_wait = None
+        if fused_block:
             # conv -> leaky -> avg pool in one kernel: pooled output + sign mask
             pooled, mask = D.first_block_fwd(ctx, cur, P[f"{layer.name}.w"], layer.params,
                                              net.layers[i + 1].slope, plan.out_radii[i + 2], tag=layer.name)
@@ -683,13 +689,42 @@ def train_step(ctx: RankCtx, plan: Plan, state: RankState, batch: Batch, lr: flo
     the halo mailboxes are set up); CapturedStep and the bench use that."""
     ctx.ensure_peer_halo(plan)
     buckets = _buckets(ctx, plan, state)
+    pack_wait = _prepack(state)
     state.params.grad.zero_()
-    pred, stash = forward(ctx, plan, state, batch, "train", seed, scalars=scalars)
+    pred, stash = forward(ctx, plan, state, batch, "train", seed, scalars=scalars, pack_wait=pack_wait)
     loss, dpred = loss_and_grad(ctx, plan, pred, batch)
     backward(ctx, plan, state, stash, dpred, buckets=buckets)
     gradient_allreduce(ctx, state, buckets)
     optimizer_step(state, lr, scalars)
+    if pack_wait is not None:
+        _lib.call("vpx_prepack_end")  # the optimizer changed the weights: no pack is current
     return loss if as_tensor else float(loss.item())
+
+
+_PACK_STREAM = {}
+
+
+def _prepack(state: RankState):
+    """Pack every conv pass's weights for this step on a side stream, in
+    parallel with the first layer (vpx_prepack_*, csrc/conv_host.cu): the
+    passes recorded their packs on earlier steps and now read the packed
+    buffers instead of packing inline (~10 us per deep-layer pass).  The
+    returned event is what forward() waits on before its first conv that may
+    read them.  VPX_NO_PREPACK=1 keeps every pack inline."""
+    if os.environ.get("VPX_NO_PREPACK") == "1" or not torch.cuda.is_available():
+        return None
+    _lib.call("vpx_prepack_begin", state.params.flat.data_ptr(), state.params.flat.numel())
+    dev = torch.cuda.current_device()
+    side = _PACK_STREAM.get(dev)
+    if side is None:
+        side = _PACK_STREAM[dev] = torch.cuda.Stream()
+    cur = torch.cuda.current_stream()
+    side.wait_stream(cur)
+    with torch.cuda.stream(side):
+        _lib.call("vpx_prepack_all", stream_ptr())
+        ev = torch.cuda.Event()
+        ev.record(side)
+    return ev
 
 
 def _buckets(ctx: RankCtx, plan: Plan, state: RankState):
