@@ -254,6 +254,41 @@ def test_pipelined_steps_equal_eager_steps(dtype):
     assert torch.equal(p0, p1)
 
 
+def test_prepacked_weights_equal_inline_packs(monkeypatch):
+    """Weight pre-packing (train_step packs every conv pass's operands on a
+    side stream; the passes read those buffers): the same steps, bit for bit,
+    as packing inline in every pass -- losses and parameters after 4 steps,
+    and a forward pass run after the last optimizer update (no stale pack may
+    serve it).  CosmoFlow-128 takes every pack path: row-window, height-taps
+    (rowh, fused conv+pool) and tap-box."""
+    width = 128
+    net = build_cosmoflow(width)
+    ctx = RankCtx(0, 1)
+    plan = engine.make_plan(net, ProcessGrid(1, 1, 1, 1), 1, width)
+    x, y, ids = engine.synthetic_batch_full(net, width, 1, 0)
+    runs = []
+    for inline in (False, True):
+        if inline:
+            monkeypatch.setenv("VPX_NO_PREPACK", "1")
+        state = engine.make_state(net, 0)
+        batch = engine.scatter_batch(plan, x, y, ids, 0)
+        losses = [engine.train_step(ctx, plan, state, batch, 1e-3) for _ in range(4)]
+        if not inline:
+            assert _lib_entries() >= 6  # the passes recorded their packs
+        pred, _ = engine.forward(ctx, plan, state, batch, "eval")
+        torch.cuda.synchronize()
+        runs.append((losses, state.params.flat.clone(), pred.clone()))
+    (l0, p0, f0), (l1, p1, f1) = runs
+    assert l0 == l1
+    assert torch.equal(p0, p1) and torch.equal(f0, f1)
+
+
+def _lib_entries():
+    from paper_2007_12856_b200 import _lib
+
+    return _lib.load().vpx_prepack_entries()
+
+
 def _poison_free_memory():
     """Fill every free cached block and most free device memory with NaN, then
     hand it back to the allocator (exposes reads of never-written memory)."""
