@@ -47,11 +47,14 @@ def _port():
 def _run(nproc, *args, env=None, timeout=600):
     if _ngpu() < nproc:
         pytest.skip(f"needs {nproc} GPUs, {_ngpu()} present")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
-           "--master-addr", "127.0.0.1", f"--master-port={_port()}", os.path.join(ROOT, "tests", "dist_worker.py"),
-           *map(str, args)]
     e = dict(os.environ, **(env or {}))
-    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=timeout, env=e)
+    for _attempt in range(3):  # the free port found by _port() can be taken before torchrun binds it
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+               "--master-addr", "127.0.0.1", f"--master-port={_port()}",
+               os.path.join(ROOT, "tests", "dist_worker.py"), *map(str, args)]
+        r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=timeout, env=e)
+        if "EADDRINUSE" not in r.stderr:
+            break
     lines = [l for l in r.stdout.splitlines() if l.startswith("[dist_worker] ")]
     print(r.stdout[-4000:])
     if not lines:
