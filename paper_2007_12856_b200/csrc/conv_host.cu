@@ -502,6 +502,10 @@ static int conv_bwd_filter_impl(const float* x, const int* xfr, const float* u, 
   }
   if (vpx::precision() == 0 && k == 3 && vpx::wgrad_tc_supported(xf, uf, stride)) {
     if (int rc = vpx::conv_wgrad_tc(x, xf, u, uf, stride, part, st)) return rc;
+    if (k3 == 27 && vpx::wgrad_tc_tapmajor(xf))
+      return vpx::reduce_partials_tapmajor(part, vpx::wgrad_tc_parts(xf, uf), uf.c, xf.c,
+                                           (long long)(slice ? cin_total : xf.c) * 27, slice ? ci0 : 0, wg, accumulate,
+                                           st);
     return finish(vpx::wgrad_tc_parts(xf, uf));
   }
   if (vpx::small_conv_supported(2, xf, uf, k, stride) && !getenv("VPX_NO_SMALL")) {

@@ -276,6 +276,36 @@ __global__ void reduce_partials_seq_kernel(const float* __restrict__ part, int P
   }
 }
 
+// out[co][ci0 + ci][tap] (=|+=) sum_p part[p][tap][co][ci], p in order: one
+// block per (co, 32 input channels) sums the 27 taps' 128-byte runs into
+// shared memory and writes the 32 x 27 result as one contiguous run.
+__global__ void reduce_partials_tapmajor_kernel(const float* __restrict__ part, int P, int cout, int cin,
+                                                long long out_co_stride, int ci0, float* __restrict__ out,
+                                                int accumulate) {
+  __shared__ float t[32 * 27];
+  const int co = blockIdx.y, cb = blockIdx.x * 32;
+  const long long slice = 27LL * cout * cin;
+  for (int i = threadIdx.x; i < 32 * 27; i += blockDim.x) {
+    const int tap = i >> 5, c = i & 31;
+    float s = 0.f;
+    if (cb + c < cin)
+      for (int p = 0; p < P; ++p) s += part[p * slice + ((long long)tap * cout + co) * cin + cb + c];
+    t[c * 27 + tap] = s;
+  }
+  __syncthreads();
+  const int nc = cin - cb < 32 ? cin - cb : 32;
+  float* o = out + co * out_co_stride + (long long)(ci0 + cb) * 27;
+  for (int i = threadIdx.x; i < nc * 27; i += blockDim.x) o[i] = accumulate ? o[i] + t[i] : t[i];
+}
+
+int reduce_partials_tapmajor(const float* part, int P, int cout, int cin, long long out_co_stride, int ci0,
+                             float* out, int accumulate, cudaStream_t st) {
+  reduce_partials_tapmajor_kernel<<<dim3((cin + 31) / 32, cout), 256, 0, st>>>(part, P, cout, cin, out_co_stride,
+                                                                              ci0, out, accumulate);
+  VPX_LAUNCH_CHECK();
+  return VPX_OK;
+}
+
 int reduce_partials_slice(const float* part, int P, long long len, int inner, long long out_stride,
                           long long out_off, float* out, int accumulate, cudaStream_t st) {
   if (len <= 0) return VPX_OK;

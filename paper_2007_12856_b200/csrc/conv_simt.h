@@ -30,6 +30,9 @@ int reduce_partials_slice(const float* part, int P, long long len, int inner, lo
                           long long out_off, float* out, int accumulate, cudaStream_t st);
 int wgrad_tc_supported(const Frame& xf, const Frame& uf, int stride);
 int wgrad_tc_parts(const Frame& xf, const Frame& uf);
+int wgrad_tc_tapmajor(const Frame& xf);
+int reduce_partials_tapmajor(const float* part, int P, int cout, int cin, long long out_co_stride, int ci0,
+                             float* out, int accumulate, cudaStream_t st);
 int conv_wgrad_tc(const float* x, const Frame& xf, const float* u, const Frame& uf, int stride, float* part,
                   cudaStream_t st);
 int wgrad_ut_supported(const Frame& xf, const Frame& uf, int stride);

@@ -196,12 +196,24 @@ __global__ void __launch_bounds__(256, 1)
         for (int j = 0; j < 16; ++j) v[j] = 0.f;
       }
       if (valid) {
+        if (MODE_A) {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const int nn = col + j;
-          const int bb = MODE_A ? nn / NCOUT : b;
-          const int co = MODE_A ? nn % NCOUT : cot * NCOUT + nn;
-          if (co < p.cout) base[(static_cast<long long>(co) * p.cin + ci) * 27 + (a * 3 + bb) * 3 + cc] = v[j];
+          for (int j = 0; j < 16; ++j) {
+            const int nn = col + j;
+            const int bb = nn / NCOUT, co = nn % NCOUT;
+            if (co < p.cout) base[(static_cast<long long>(co) * p.cin + ci) * 27 + (a * 3 + bb) * 3 + cc] = v[j];
+          }
+        } else {
+          // mode B: tap-major partials [tap][co][ci], so a warp's 32 input
+          // channels are one contiguous 128-byte run (the [co][ci][tap] order
+          // scattered every store 108 bytes apart: ~40 us per deep-layer
+          // filter gradient); reduce_partials_tapmajor transposes back
+          float* tb = base + static_cast<long long>((a * 3 + b) * 3 + cc) * p.cout * p.cin;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int co = cot * NCOUT + col + j;
+            if (co < p.cout) tb[static_cast<long long>(co) * p.cin + ci] = v[j];
+          }
         }
       }
     }
@@ -264,6 +276,10 @@ int wgrad_tc_supported(const Frame& xf, const Frame& uf, int stride) {
     return cout == 128 || cout % 256 == 0;
   return 0;
 }
+
+// 1: the partial slices are tap-major ([tap][cout][cin], mode B) and need
+// reduce_partials_tapmajor; 0: [cout][cin][tap] (mode A).
+int wgrad_tc_tapmajor(const Frame& xf) { return xf.c > 32; }
 
 // Number of partial slices the split-K reduction produces.
 int wgrad_tc_parts(const Frame& xf, const Frame& uf) {
