@@ -432,7 +432,17 @@ int small_conv_supported(int which, const Frame& xf, const Frame& of, int k, int
 int small_wgrad_parts(const Frame& uf, int k) {
   if (k == 1) return rows_grid(uf, 4);
   const long long ntiles = (long long)uf.n * uf.d * ((uf.h + kTY - 1) / kTY) * ((uf.w + kTX - 1) / kTX);
-  const long long cap = 8LL * num_sms();  // 8 resident blocks per SM: each block's tile loop is latency-bound
+  // one wave of resident blocks (each loops over tiles): 8 per SM asked for
+  // more than fit (5 by registers for CO = 8), leaving a 0.6-wave tail that
+  // every block's equal share of tiles turned into a second full wave
+  int per_sm = 8;
+  const int co = uf.c;
+  int occ = 0;
+  if (co == 4) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, c1k3_wgrad_kernel<4>, 256, 0);
+  if (co == 8) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, c1k3_wgrad_kernel<8>, 256, 0);
+  if (co == 16) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, c1k3_wgrad_kernel<16>, 256, 0);
+  if (occ > 0 && occ < per_sm) per_sm = occ;
+  const long long cap = (long long)per_sm * num_sms();
   return static_cast<int>(ntiles < cap ? ntiles : cap);
 }
 
