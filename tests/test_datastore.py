@@ -126,6 +126,16 @@ def _exchange_worker(rank, size, port, q):
             res["x_ok"] &= bool(np.array_equal(x, ref)) and t.shape == (2, 4)
         res["got"] = got
         res["exchange"] = st.counters.exchange_bytes
+        # the narrowed exchange (agreed int8 transfer dtype) delivers the same values
+        import torch
+
+        res["agreed"] = str(st.agree_transfer_dtype())
+        res["narrow_ok"] = True
+        for it in range(sched.iterations):
+            dl = D.exchange_for_iteration(None, st, sched, it, device=False, narrow=True)
+            x, t, _ = D.materialize_batch(st, dl)
+            ref = np.stack([D.read_payload(man.path(s)) for s, _, _ in dl]).astype(np.float32)
+            res["narrow_ok"] &= bool(np.array_equal(x, ref)) and all(b.dtype == torch.int8 for _, b, _ in dl)
         q.put((rank, res))
     finally:
         dist.destroy_process_group()
@@ -156,6 +166,8 @@ def test_two_group_exchange_gloo():
         assert [sid for sid, _ in res[r]["got"]] == want
         assert all(ok for _, ok in res[r]["got"]) and res[r]["x_ok"]
     assert res[0]["exchange"] + res[1]["exchange"] > 0
+    assert res[0]["agreed"] == res[1]["agreed"] == "torch.int8"  # the fixture range [-8, 8] fits int8
+    assert res[0]["narrow_ok"] and res[1]["narrow_ok"]
 
 
 @pytest.mark.gpu
