@@ -4,6 +4,7 @@ process per GPU, by tests/test_multigpu.py):
     torchrun --nproc-per-node N tests/dist_worker.py halo KEY
     torchrun --nproc-per-node N tests/dist_worker.py step GRID NET WIDTH N PREC
     torchrun --nproc-per-node N tests/dist_worker.py replay GRID WIDTH N
+    torchrun --nproc-per-node N tests/dist_worker.py pipelined GRID WIDTH N
 
 halo    device halo rounds on the golden frames the REFERENCE fabric produced
         (tests/golden/halo.npz): every exchange path (fused peer round, split
@@ -20,6 +21,10 @@ step    one hybrid-parallel training step on GRID over NCCL; the traces of all
 replay  CapturedStep graph replays over the peer-memory halo path (replays
         queued without host synchronisation) against eager steps over the
         NCCL halo path: parameters, moments and loss bit-identical.
+pipelined  engine.PipelinedSteps (two step graphs, two input frames, the
+        next block's H2D + layout on a copy stream) over the peer halo against
+        eager steps on the same per-step host blocks: losses and parameters
+        bit-identical.
 
 Rank 0 prints one line "[dist_worker] {json}"; exit status 0 = pass.
 """
@@ -345,6 +350,50 @@ def run_stale(ctx, grid_s, width, n):
     return _report(ctx, ok, mode="stale", grid=grid_s, width=width, n=n, per_rank=allinfo)
 
 
+def run_pipelined(ctx, grid_s, width, n):
+    """engine.PipelinedSteps over the peer-halo path (two graphs, two input
+    frames, next block's H2D + layout on a copy stream) against eager steps
+    on the same per-step host blocks: losses and parameters bit-equal."""
+    grid = ProcessGrid.parse(grid_s)
+    net = build_cosmoflow(width)
+    plan = engine.make_plan(net, grid, n, width)
+    ctx.prepare_groups([plan.leads])
+    x, y, ids = engine.synthetic_batch_full(net, width, n, 0)
+    ctx.ensure_peer_halo(plan)
+    K, warm = 5, 1
+    runs = []
+    for pipelined in (False, True):
+        state = engine.make_state(net, 0)
+        batch = engine.scatter_batch(plan, x, y, ids, ctx.rank)
+        shape = (batch.x_block.n, batch.x_block.c) + batch.x_block.spatial if batch.x_block is not None else None
+        g = torch.Generator().manual_seed(11 + ctx.rank)
+        blocks = [torch.randint(-8, 9, shape, generator=g).to(torch.int8).pin_memory() for _ in range(K)] \
+            if shape is not None else None
+        losses = []
+        if pipelined:
+            pipe = engine.PipelinedSteps(ctx, plan, state, batch, (lambda i: blocks[i]) if blocks else None, 1e-3,
+                                         warmup=warm)
+            pipe.start()
+            for i in range(K):
+                prev = pipe.step(1e-3, prefetch_next=i + 1 < K)
+                if prev is not None:
+                    losses.append(prev)
+            losses.append(pipe.finish())
+        else:
+            for _ in range(2 * warm):
+                engine.train_step(ctx, plan, state, batch, 1e-3)
+            for i in range(K):
+                if blocks is not None:
+                    batch.x_block.load_ncdhw(blocks[i].cuda())
+                losses.append(engine.train_step(ctx, plan, state, batch, 1e-3))
+        torch.cuda.synchronize()
+        runs.append((losses, state.params.flat.clone()))
+    (l0, p0), (l1, p1) = runs
+    ok = l0 == l1 and bool(torch.equal(p0, p1)) and all(np.isfinite(l1))
+    return _report(ctx, ok, mode="pipelined", grid=grid_s, width=width, n=n, losses=[l0, l1],
+                   halo=ctx.halo_path, max_param_diff=float((p0 - p1).abs().max()))
+
+
 def main():
     ctx = RankCtx.from_env()
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
@@ -357,6 +406,8 @@ def main():
         rc = run_stale(ctx, sys.argv[2], int(sys.argv[3]), int(sys.argv[4]))
     elif mode == "replay":
         rc = run_replay(ctx, sys.argv[2], int(sys.argv[3]), int(sys.argv[4]))
+    elif mode == "pipelined":
+        rc = run_pipelined(ctx, sys.argv[2], int(sys.argv[3]), int(sys.argv[4]))
     else:
         raise SystemExit(f"unknown mode {mode}")
     dist.destroy_process_group()

@@ -110,3 +110,9 @@ def test_graph_replays_peer_halo_equal_eager_nccl_halo(grid):
 def test_step_independent_of_stale_memory(grid):
     g = [int(v) for v in grid.split("x")]
     _run(g[0] * g[1] * g[2] * g[3], "stale", grid, 32, 1)
+
+
+@pytest.mark.parametrize("grid", ["1x2x1x1", "1x2x2x1"])
+def test_pipelined_steps_equal_eager_steps(grid):
+    g = [int(v) for v in grid.split("x")]
+    _run(g[0] * g[1] * g[2] * g[3], "pipelined", grid, 32, 1)
