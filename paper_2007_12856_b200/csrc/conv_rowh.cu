@@ -495,7 +495,7 @@ __global__ void __launch_bounds__(384, 1)
       for (int i = 0; i < CH; ++i) {
         float s = (__uint_as_float(a0[i]) + __uint_as_float(a1[i])) + __uint_as_float(a2[i]);
         s = fmaxf(s, slope * s);  // LeakyReLU, 0 < slope <= 1 (reference layers/reference.py:231-233)
-        if (rnd) s = vpx::tf32_rn(s);
+        // pooled unrounded (the activation is never stored; the pooled value is rounded)
         v[i] = s;
         bits |= (s >= 0.f ? 1u : 0u) << i;
       }
@@ -542,36 +542,30 @@ __global__ void __launch_bounds__(384, 1)
             mrow[0] = static_cast<uint8_t>(b0);
             mrow[mstep] = static_cast<uint8_t>(b1);
           }
-          // vpx_pool_fwd order: (z,y,x) (z,y,x+1) (z,y+1,x) (z,y+1,x+1), then z+1
-          float n0[CH], n1[CH];
+          // each lane sums its voxel's two rows, one shuffle per channel brings
+          // the W neighbour's sum to the even lane (the pooled voxel's owner);
+          // depth z0's partial waits in shared memory for depth z0+1
+          float part[CH], nb[CH];
 #pragma unroll
-          for (int i = 0; i < CH; ++i) {
-            n0[i] = __shfl_down_sync(0xffffffffu, v0[i], 1);
-            n1[i] = __shfl_down_sync(0xffffffffu, v1[i], 1);
-          }
+          for (int i = 0; i < CH; ++i) part[i] = v0[i] + v1[i];
+#pragma unroll
+          for (int i = 0; i < CH; ++i) nb[i] = __shfl_down_sync(0xffffffffu, part[i], 1);
           if (even) {
             float4* pb4 = reinterpret_cast<float4*>(pb);
             if (pz == 0) {
 #pragma unroll
               for (int i = 0; i < CH / 4; ++i)
-                pb4[i] = make_float4(((v0[4 * i] + n0[4 * i]) + v1[4 * i]) + n1[4 * i],
-                                     ((v0[4 * i + 1] + n0[4 * i + 1]) + v1[4 * i + 1]) + n1[4 * i + 1],
-                                     ((v0[4 * i + 2] + n0[4 * i + 2]) + v1[4 * i + 2]) + n1[4 * i + 2],
-                                     ((v0[4 * i + 3] + n0[4 * i + 3]) + v1[4 * i + 3]) + n1[4 * i + 3]);
+                pb4[i] = make_float4(part[4 * i] + nb[4 * i], part[4 * i + 1] + nb[4 * i + 1],
+                                     part[4 * i + 2] + nb[4 * i + 2], part[4 * i + 3] + nb[4 * i + 3]);
             } else {
 #pragma unroll
               for (int i = 0; i < CH / 4; ++i) {
-                const float4 part = pb4[i];
-                const float pv[4] = {part.x, part.y, part.z, part.w};
+                const float4 pp = pb4[i];
+                const float pv[4] = {pp.x, pp.y, pp.z, pp.w};
                 float fin[4];
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
-                  float t = pv[j];
-                  t = t + v0[4 * i + j];
-                  t = t + n0[4 * i + j];
-                  t = t + v1[4 * i + j];
-                  t = t + n1[4 * i + j];
-                  t = t / 8.0f;
+                  const float t = (pv[j] + (part[4 * i + j] + nb[4 * i + j])) * 0.125f;
                   fin[j] = rnd ? vpx::tf32_rn(t) : t;
                 }
                 reinterpret_cast<float4*>(dp)[i] = make_float4(fin[0], fin[1], fin[2], fin[3]);
