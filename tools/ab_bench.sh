@@ -1,6 +1,6 @@
 #!/usr/bin/env bash
 # A/B the bench step on one box: each argument is an env assignment list
-# ("" = default), e.g. tools/ab_bench.sh "" "VPX_TAPBOX_REDUCE_KERNEL=1"
+# ("" = default), e.g. tools/ab_bench.sh "" "VPX_NO_PREPACK=1"
 i=0
 for envs in "$@"; do
   for rep in 1 2; do
