@@ -156,32 +156,47 @@ __global__ void __launch_bounds__(384, 1)
       vpx::mbar_wait(&wbar, 0);
       const uint32_t wb = vpx::smem_u32(sw);
       const uint32_t ab0 = vpx::smem_u32(sa);
+      // Descriptors built once: B is resident; A differs per stage only in
+      // its start-address field (address >> 4, no carry below 256 KB), so a
+      // row's six MMAs cost one add each -- a single issuing thread that
+      // rebuilt every descriptor spent more cycles issuing than the MMAs took
+      uint64_t adesc0[kKSteps], bdesc[kKSteps];
+#pragma unroll
+      for (int s = 0; s < kKSteps; ++s) {
+        const int t0 = 2 * s, t1 = 2 * s + 1;  // (plane, width tap) t = 3 p + c
+        const uint32_t lbo = ((t1 / 3 - t0 / 3) * kWin + (t1 % 3 - t0 % 3)) * 16;
+        adesc0[s] = vpx::make_sdesc(ab0 + ((t0 / 3) * kWin + t0 % 3) * 16, lbo, 128, 0);
+        bdesc[s] = vpx::make_sdesc(wb + s * kBStep, kN * 16, 128, 0);
+      }
       int stage = 0;
-      uint32_t phase = 0;
-      uint32_t gr = 0;
+      uint32_t phase = 0, soff = 0;           // soff = stage * kStage >> 4
+      uint32_t slot = 0, sphase = 0;          // ring slot of input row gr and its use parity
+      uint32_t d = tbase;
       for (int task = blockIdx.x; task < p.num_tasks; task += gridDim.x) {
         int n, z0, x0, y0, rows;
         decode(task, n, z0, x0, y0, rows);
-        for (int j = 0; j < rows + 2; ++j, ++gr) {
-          const uint32_t slot = gr % kNB;
-          vpx::mbar_wait(&bempty[slot], ((gr / kNB) & 1) ^ 1);
+        for (int j = 0; j < rows + 2; ++j) {
+          vpx::mbar_wait(&bempty[slot], sphase ^ 1);
           vpx::mbar_wait(&full[stage], phase);
           vpx::tc_fence_after();
-          const uint32_t d = tbase + slot * kN;
-          const uint32_t ab = ab0 + stage * kStage;
 #pragma unroll
-          for (int s = 0; s < kKSteps; ++s) {
-            const int t0 = 2 * s, t1 = 2 * s + 1;  // (plane, width tap) t = 3 p + c
-            const uint32_t lbo = ((t1 / 3 - t0 / 3) * kWin + (t1 % 3 - t0 % 3)) * 16;
-            const uint64_t adesc = vpx::make_sdesc(ab + ((t0 / 3) * kWin + t0 % 3) * 16, lbo, 128, 0);
-            const uint64_t bdesc = vpx::make_sdesc(wb + s * kBStep, kN * 16, 128, 0);
-            vpx::umma_tf32(d, adesc, bdesc, idesc, s > 0 ? 1u : 0u);
-          }
+          for (int s = 0; s < kKSteps; ++s)
+            vpx::umma_tf32(d, adesc0[s] + soff, bdesc[s], idesc, s > 0 ? 1u : 0u);
           vpx::umma_commit(&empty[stage]);
           vpx::umma_commit(&bfull[slot]);
           if (++stage == kS) {
             stage = 0;
             phase ^= 1;
+            soff = 0;
+          } else {
+            soff += kStage >> 4;
+          }
+          if (++slot == kNB) {
+            slot = 0;
+            sphase ^= 1;
+            d = tbase;
+          } else {
+            d += kN;
           }
         }
       }
