@@ -151,6 +151,7 @@ __global__ void __launch_bounds__(384, 1)
       vpx::mbar_wait(&wbar, 0);
       const uint32_t wb = vpx::smem_u32(sw);
       const uint32_t ab0 = vpx::smem_u32(sa);
+      const uint64_t bbase = vpx::make_sdesc(wb, N * 16, 128, 0);
       int stage = 0;
       uint32_t phase = 0;
       uint32_t gr = 0;  // E blocks produced by this CTA
@@ -174,14 +175,19 @@ __global__ void __launch_bounds__(384, 1)
               vpx::umma_tf32(d, adesc, bdesc, idesc, q > 0 ? 1u : 0u);
             }
           } else {
+            // descriptors = a per-row base + a compile-time offset in the
+            // 16-byte address field (no carry below 256 KB): one add per
+            // operand instead of rebuilding both for each of the 9 x CIN/8
+            // MMAs -- the single issuing thread is otherwise slower than the
+            // N = 48 MMAs it feeds
+            const uint64_t arow = vpx::make_sdesc(ab, 16, 8 * K::RB, K::LAYOUT);
 #pragma unroll
             for (int t = 0; t < 9; ++t) {
 #pragma unroll
               for (int jp = 0; jp < CIN / 8; ++jp) {
                 // row (plane a, voxel c) of the swizzled window, K step jp = 8 channels (32 B)
-                const uint64_t adesc = vpx::make_sdesc(ab + ((t / 3) * kWinH + t % 3) * K::RB + jp * 32, 16,
-                                                       8 * K::RB, K::LAYOUT);
-                const uint64_t bdesc = vpx::make_sdesc(wb + (t * (CIN / 8) + jp) * K::BSTEP, N * 16, 128, 0);
+                const uint64_t adesc = arow + (((t / 3) * kWinH + t % 3) * K::RB + jp * 32) / 16;
+                const uint64_t bdesc = bbase + ((t * (CIN / 8) + jp) * K::BSTEP) / 16;
                 vpx::umma_tf32(d, adesc, bdesc, idesc, (t | jp) != 0 ? 1u : 0u);
               }
             }
@@ -432,6 +438,7 @@ __global__ void __launch_bounds__(384, 1)
       vpx::mbar_wait(&wbar, 0);
       const uint32_t wb = vpx::smem_u32(sw);
       const uint32_t ab0 = vpx::smem_u32(sa);
+      const uint64_t bbase = vpx::make_sdesc(wb, N * 16, 128, 0);
       int stage = 0;
       uint32_t phase = 0;
       uint32_t gr = 0;
@@ -446,13 +453,13 @@ __global__ void __launch_bounds__(384, 1)
             vpx::tc_fence_after();
             const uint32_t d = tbase + slot * N;
             const uint32_t ab = ab0 + stage * K::STAGE;
+            const uint64_t arow = vpx::make_sdesc(ab, 16, 8 * K::RB, K::LAYOUT);  // + per-MMA address offsets
 #pragma unroll
             for (int t = 0; t < 9; ++t) {
 #pragma unroll
               for (int jp = 0; jp < CIN / 8; ++jp) {
-                const uint64_t adesc = vpx::make_sdesc(ab + ((t / 3) * kWinH + t % 3) * K::RB + jp * 32, 16,
-                                                       8 * K::RB, K::LAYOUT);
-                const uint64_t bdesc = vpx::make_sdesc(wb + (t * (CIN / 8) + jp) * K::BSTEP, N * 16, 128, 0);
+                const uint64_t adesc = arow + (((t / 3) * kWinH + t % 3) * K::RB + jp * 32) / 16;
+                const uint64_t bdesc = bbase + ((t * (CIN / 8) + jp) * K::BSTEP) / 16;
                 vpx::umma_tf32(d, adesc, bdesc, idesc, (t | jp) != 0 ? 1u : 0u);
               }
             }
