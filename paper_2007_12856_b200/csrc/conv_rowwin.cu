@@ -179,19 +179,23 @@ __global__ void __launch_bounds__(256, 1)
               }
             }
           } else {
-#pragma unroll 1
+            // fully unrolled: every descriptor is the stage's base descriptor
+            // plus a compile-time offset in the 16-byte address field (one add)
+            // -- rebuilding them per MMA kept the single issuing thread behind
+            // the N = 32 / 64 MMAs
+            const uint64_t a0desc = vpx::make_sdesc(aBase, 16, 256, 6);
+            const uint64_t b0desc = vpx::make_sdesc(bBase, COUT * 16, 128, 0);
+#pragma unroll
             for (int t = 0; t < 27; ++t) {
               const int a = t / 9, b = (t / 3) % 3, c = t % 3;
 #pragma unroll
               for (int jp = 0; jp < CG / 2; ++jp) {
-                const uint64_t bdesc =
-                    vpx::make_sdesc(bBase + (t * CG + 2 * jp) * COUT * 16, COUT * 16, 128, 0);
+                const uint64_t bdesc = b0desc + (t * CG + 2 * jp) * COUT;
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
                   // 8-channel plane jp, voxel row (a, r+b, c): 32-byte SW32 rows, 8-row atoms
-                  const uint32_t as = aBase + jp * PLANE + ((a * (R + 2) + r + b) * kWin + c) * 32;
-                  vpx::umma_tf32(dacc + r * COUT, vpx::make_sdesc(as, 16, 256, 6), bdesc, idesc,
-                                 (g | t | jp) != 0);
+                  const uint64_t adesc = a0desc + (jp * PLANE + ((a * (R + 2) + r + b) * kWin + c) * 32) / 16;
+                  vpx::umma_tf32(dacc + r * COUT, adesc, bdesc, idesc, (g | t | jp) != 0);
                 }
               }
             }
