@@ -286,9 +286,10 @@ __global__ void __launch_bounds__(256, 1)
         if (vpx::elect_one()) {
           const uint32_t a = vpx::smem_u32(smem + stage * STAGE);
           const uint32_t b = a + ABYTES;
+          const uint64_t ad0 = vpx::make_sdesc(a, 16, 1024, 2), bd0 = vpx::make_sdesc(b, 16, 1024, 2);
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
-            const uint64_t ad = vpx::make_sdesc(a + 32 * k, 16, 1024, 2), bd = vpx::make_sdesc(b + 32 * k, 16, 1024, 2);
+            const uint64_t ad = ad0 + 2 * k, bd = bd0 + 2 * k;  // +32 B per K step
             if constexpr (BF16)
               vpx::umma_f16(d, ad, bd, idesc, (e > e0 || k > 0) ? 1u : 0u);
             else

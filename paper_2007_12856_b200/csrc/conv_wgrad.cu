@@ -144,20 +144,24 @@ __global__ void __launch_bounds__(256, 1)
       if (vpx::elect_one()) {
         const uint32_t xb = vpx::smem_u32(smem + stage * STAGE);
         const uint32_t ub = xb + XB;
-        for (int k = 0; k < wseg; k += 8) {
-          const uint64_t bdesc = vpx::make_sdesc(ub + k * kRow, UPLANE, 512, 1);
-          const uint32_t first = (r == r0 && k == 0) ? 0u : 1u;
-          if (MODE_A) {
+        // descriptors advanced by 8 rows (1024 B = 64 in the address field)
+        // per K step instead of rebuilt for every MMA by the issuing thread
+        uint64_t bdesc = vpx::make_sdesc(ub, UPLANE, 512, 1);
+        uint64_t adesc[MODE_A ? 3 : 1];
+        if (MODE_A) {
 #pragma unroll
-            for (int bb = 0; bb < 3; ++bb) {
-              const uint64_t adesc = vpx::make_sdesc(xb + bb * xpitch + k * kRow, kRow, 512, 1);
-              vpx::umma_tf32(tbase + bb * NCOUT, adesc, bdesc, idesc, first);
-            }
-          } else {
-            const int coff = p.stride == 1 ? c : 0;
-            const uint64_t adesc = vpx::make_sdesc(xb + (k + coff) * kRow, XPLANE, 512, 1);
-            vpx::umma_tf32(tbase, adesc, bdesc, idesc, first);
+          for (int bb = 0; bb < (MODE_A ? 3 : 1); ++bb) adesc[bb] = vpx::make_sdesc(xb + bb * xpitch, kRow, 512, 1);
+        } else {
+          adesc[0] = vpx::make_sdesc(xb + (p.stride == 1 ? c : 0) * kRow, XPLANE, 512, 1);
+        }
+        for (int k = 0; k < wseg; k += 8) {
+          const uint32_t first = (r == r0 && k == 0) ? 0u : 1u;
+#pragma unroll
+          for (int bb = 0; bb < (MODE_A ? 3 : 1); ++bb) {
+            vpx::umma_tf32(tbase + bb * NCOUT, adesc[bb], bdesc, idesc, first);
+            adesc[bb] += 8 * kRow / 16;
           }
+          bdesc += 8 * kRow / 16;
         }
         vpx::umma_commit(&empty[stage]);
         if (r == r1 - 1) vpx::umma_commit(&tfull);
