@@ -102,14 +102,15 @@ __global__ void __launch_bounds__(256, 1)
       vpx::tc_fence_after();
       if (vpx::elect_one()) {
         const uint32_t sb = vpx::smem_u32(smem + stage * kStage);
+        // base descriptors + address-field offsets (8 voxel rows = 1024 B per K step)
+        const uint64_t b0 = vpx::make_sdesc(sb + 8 * kTile, kTile, 512, 1);
+        const uint64_t a0 = vpx::make_sdesc(sb, kTile, 512, 1);
+#pragma unroll
         for (int k = 0; k < kSeg; k += 8) {
-          const uint64_t bdesc = vpx::make_sdesc(sb + 8 * kTile + k * kRow, kTile, 512, 1);
           const uint32_t first = (r == r0 && k == 0) ? 0u : 1u;
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const uint64_t adesc = vpx::make_sdesc(sb + 4 * h * kTile + k * kRow, kTile, 512, 1);
-            vpx::umma_tf32(tbase + 32 * h, adesc, bdesc, idesc, first);
-          }
+          for (int h = 0; h < 2; ++h)
+            vpx::umma_tf32(tbase + 32 * h, a0 + (4 * h * kTile + k * kRow) / 16, b0 + k * kRow / 16, idesc, first);
         }
         vpx::umma_commit(&empty[stage]);
         if (r == r1 - 1) vpx::umma_commit(&tfull);
