@@ -6,6 +6,7 @@
 // extent ceil(e/stride).  Tensors are NDHWC halo frames (see include/vpx.h).
 #include "conv_simt.h"
 #include "vpx_host.h"
+#include "vpx_ptx.cuh"
 #include "vpx_round.cuh"
 
 namespace vpx {
@@ -246,10 +247,24 @@ long long wgrad_simt_parts(const Frame& uf) {
 // in order -- the same sums as reduce_partials_seq_kernel.
 __global__ void reduce_partials_seq4_kernel(const float4* __restrict__ part, int P, long long len4,
                                             float4* __restrict__ out, int accumulate) {
+  vpx::pdl_wait();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < len4;
        i += (long long)gridDim.x * blockDim.x) {
     float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int p = 0; p < P; ++p) {
+    int p = 0;
+    for (; p + 8 <= P; p += 8) {  // eight loads in flight, summed in order
+      float4 v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = part[(long long)(p + j) * len4 + i];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        s.x += v[j].x;
+        s.y += v[j].y;
+        s.z += v[j].z;
+        s.w += v[j].w;
+      }
+    }
+    for (; p < P; ++p) {
       const float4 v = part[(long long)p * len4 + i];
       s.x += v.x;
       s.y += v.y;
@@ -267,6 +282,7 @@ __global__ void reduce_partials_seq4_kernel(const float4* __restrict__ part, int
 __global__ void reduce_partials_seq_kernel(const float* __restrict__ part, int P, long long len, int inner,
                                            long long out_stride, long long out_off, float* __restrict__ out,
                                            int accumulate) {
+  vpx::pdl_wait();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < len;
        i += (long long)gridDim.x * blockDim.x) {
     float s = 0.f;
@@ -285,11 +301,22 @@ __global__ void reduce_partials_tapmajor_kernel(const float* __restrict__ part, 
   __shared__ float t[32 * 27];
   const int co = blockIdx.y, cb = blockIdx.x * 32;
   const long long slice = 27LL * cout * cin;
+  vpx::pdl_wait();
   for (int i = threadIdx.x; i < 32 * 27; i += blockDim.x) {
     const int tap = i >> 5, c = i & 31;
     float s = 0.f;
-    if (cb + c < cin)
-      for (int p = 0; p < P; ++p) s += part[p * slice + ((long long)tap * cout + co) * cin + cb + c];
+    if (cb + c < cin) {
+      const float* src = part + ((long long)tap * cout + co) * cin + cb + c;
+      int p = 0;
+      for (; p + 8 <= P; p += 8) {  // eight loads in flight, summed in order
+        float v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = src[(p + j) * slice];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) s += v[j];
+      }
+      for (; p < P; ++p) s += src[p * slice];
+    }
     t[c * 27 + tap] = s;
   }
   __syncthreads();
@@ -300,8 +327,8 @@ __global__ void reduce_partials_tapmajor_kernel(const float* __restrict__ part, 
 
 int reduce_partials_tapmajor(const float* part, int P, int cout, int cin, long long out_co_stride, int ci0,
                              float* out, int accumulate, cudaStream_t st) {
-  reduce_partials_tapmajor_kernel<<<dim3((cin + 31) / 32, cout), 256, 0, st>>>(part, P, cout, cin, out_co_stride,
-                                                                              ci0, out, accumulate);
+  VPX_CHECK_CUDA(vpx::launch_pdl(reduce_partials_tapmajor_kernel, dim3((cin + 31) / 32, cout), 256, 0, st, part, P,
+                                 cout, cin, out_co_stride, ci0, out, accumulate));
   VPX_LAUNCH_CHECK();
   return VPX_OK;
 }
@@ -311,14 +338,15 @@ int reduce_partials_slice(const float* part, int P, long long len, int inner, lo
   if (len <= 0) return VPX_OK;
   if (P <= 64 && inner == len && out_off == 0 && len % 4 == 0 &&
       (reinterpret_cast<uintptr_t>(part) | reinterpret_cast<uintptr_t>(out)) % 16 == 0) {
-    reduce_partials_seq4_kernel<<<grid_for(len / 4, 256), 256, 0, st>>>(
-        reinterpret_cast<const float4*>(part), P, len / 4, reinterpret_cast<float4*>(out), accumulate);
+    VPX_CHECK_CUDA(vpx::launch_pdl(reduce_partials_seq4_kernel, grid_for(len / 4, 256), 256, 0, st,
+                                   reinterpret_cast<const float4*>(part), P, len / 4, reinterpret_cast<float4*>(out),
+                                   accumulate));
     VPX_LAUNCH_CHECK();
     return VPX_OK;
   }
   if (P <= 64) {
-    reduce_partials_seq_kernel<<<grid_for(len, 256), 256, 0, st>>>(part, P, len, inner, out_stride, out_off, out,
-                                                                     accumulate);
+    VPX_CHECK_CUDA(vpx::launch_pdl(reduce_partials_seq_kernel, grid_for(len, 256), 256, 0, st, part, P, len, inner,
+                                   out_stride, out_off, out, accumulate));
     VPX_LAUNCH_CHECK();
     return VPX_OK;
   }

@@ -130,6 +130,18 @@ __device__ __forceinline__ void tapbox_reduce_elem(const ConvTapParams& p, int t
   const float4* src = reinterpret_cast<const float4*>(p.part + (static_cast<long long>(tb) * 128 + r) * NT) + c4;
   const long long kstride = static_cast<long long>(p.base_tiles) * 128 * NT / 4;
   int ks = 0;
+  for (; ks + 16 <= p.ksplit; ks += 16) {  // deep splits: 16 loads in flight, summed in order
+    float4 v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = src[(ks + j) * kstride];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      acc.x += v[j].x;
+      acc.y += v[j].y;
+      acc.z += v[j].z;
+      acc.w += v[j].w;
+    }
+  }
   for (; ks + 4 <= p.ksplit; ks += 4) {  // four independent loads in flight, summed in order
     float4 v[4];
 #pragma unroll
@@ -174,6 +186,7 @@ __device__ __forceinline__ void tapbox_reduce_elem(const ConvTapParams& p, int t
 template <int NT>
 __global__ void tapbox_reduce_kernel(const __grid_constant__ ConvTapParams p) {
   const long long total = (long long)p.base_tiles * 128 * (NT / 4);
+  vpx::pdl_wait();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
     const int c4 = static_cast<int>(i % (NT / 4));
@@ -218,6 +231,7 @@ __global__ void __launch_bounds__(256, 1)
   __syncthreads();
   vpx::tc_fence_after();
   const uint32_t tbase = tmem_base;
+  vpx::pdl_wait();
 
   // tile -> (k split, n-tile, class, n, zt, yt, xt)
   auto decode = [&](int tile, int& nt, int& cls, int& n, int& zt, int& yt, int& xt) {
@@ -382,12 +396,12 @@ int launch_tapbox(const CUtensorMap& xm, const CUtensorMap& wm, const ConvTapPar
   const int smem = S * STAGE + 1024;
   VPX_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const int grid = p.num_tiles < vpx::num_sms() ? p.num_tiles : vpx::num_sms();
-  kern<<<grid, 256, smem, st>>>(xm, wm, p);
+  VPX_CHECK_CUDA(vpx::launch_pdl(kern, grid, 256, smem, st, xm, wm, p));
   VPX_LAUNCH_CHECK();
   if (p.ksplit > 1) {
     const long long total = (long long)p.base_tiles * 128 * (NT / 4);
     const int rg = static_cast<int>((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);
-    tapbox_reduce_kernel<NT><<<rg, 256, 0, st>>>(p);
+    VPX_CHECK_CUDA(vpx::launch_pdl(tapbox_reduce_kernel<NT>, rg, 256, 0, st, p));
     VPX_LAUNCH_CHECK();
   }
   return VPX_OK;

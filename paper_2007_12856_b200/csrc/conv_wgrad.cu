@@ -95,6 +95,7 @@ __global__ void __launch_bounds__(256, 1)
   __syncthreads();
   vpx::tc_fence_after();
   const uint32_t tbase = tmem_base;
+  vpx::pdl_wait();
 
   if (warp == 0) {
     if (vpx::elect_one()) {
@@ -250,7 +251,7 @@ int launch_wgrad(const CUtensorMap& xm, const CUtensorMap& um, const WgradParams
   auto kern = wgrad_kernel<MODE_A, NCOUT, S, WMAX>;
   const int smem = S * STAGE + 1024;
   VPX_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  kern<<<p.nsub * p.P, 256, smem, st>>>(xm, um, p);
+  VPX_CHECK_CUDA(vpx::launch_pdl(kern, p.nsub * p.P, 256, smem, st, xm, um, p));
   VPX_LAUNCH_CHECK();
   return VPX_OK;
 }

@@ -9,7 +9,9 @@
 #include <cstdarg>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <string>
+#include <utility>
 
 #include "../../include/vpx.h"
 
@@ -44,6 +46,32 @@ inline void note_fallback() {
     cudaError_t _e = cudaGetLastError();                                             \
     if (_e != cudaSuccess) VPX_FAIL(VPX_ERR_CUDA, "launch: %s", cudaGetErrorString(_e)); \
   } while (0)
+
+// Programmatic dependent launch for the deep-layer conv chain: the kernel may
+// be scheduled while its predecessor in the stream drains, runs its prologue
+// (barrier init, TMEM alloc, tensor-map prefetch) and then blocks in
+// vpx::pdl_wait() until the predecessor has completed and its writes are
+// visible.  Only kernels that call pdl_wait() before touching global memory
+// are launched this way.  VPX_NO_PDL=1 launches them with plain serialization.
+inline bool pdl_enabled() {
+  static const bool on = std::getenv("VPX_NO_PDL") == nullptr;
+  return on;
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // Encode a tiled TMA map. dims/box are innermost-first; strides_bytes has
 // rank-1 entries (stride of dims 1..rank-1).  Returns 0 or VPX_ERR_CUDA.

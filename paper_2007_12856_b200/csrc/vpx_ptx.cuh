@@ -49,6 +49,15 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, 
 }
 
 // One lane of the (converged) warp returns true.
+// Programmatic dependent launch (vpx::launch_pdl): wait until the previous
+// kernel in the stream has completed and flushed (a no-op for a plain launch),
+// then allow the next kernel to be scheduled.  Called by every thread before
+// its first global-memory access.
+__device__ __forceinline__ void pdl_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred = 0;
   asm volatile(

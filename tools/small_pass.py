@@ -2,7 +2,9 @@
 GPU): 50 back-to-back passes captured in one CUDA graph, replayed; reports
 microseconds per pass for forward, backward-data and backward-filter
 (each = the C-ABI call: weight pack + kernel + split-K reduce).
-python tools/small_pass.py"""
+python tools/small_pass.py
+SMALL_PASS_EAGER=1 runs each pass 3 times eagerly instead (for an ncu launch list)."""
+import os
 import sys
 
 import numpy as np
@@ -17,6 +19,11 @@ REPS = 50
 
 
 def timed(fn):
+    if os.environ.get("SMALL_PASS_EAGER"):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        return 0.0
     s = torch.cuda.Stream()
     s.wait_stream(torch.cuda.current_stream())
     with torch.cuda.stream(s):
