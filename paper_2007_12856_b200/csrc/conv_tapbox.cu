@@ -701,7 +701,10 @@ int conv_tapbox(int mode, const float* in, const Frame& inf, const float* w, int
   p.ntn = ntot / NT;
   p.base_tiles = of.n * p.td * p.th * p.tw * ncls * p.ntn;
   // few tiles (deep layers): split each tile's K entries over otherwise idle
-  // SMs; partial tiles go after the packed weights in the workspace
+  // SMs; partial tiles go after the packed weights in the workspace.  At most
+  // 16 ways (VPX_KSPLIT_MAX): on the 4^3/8^3 CosmoFlow layers a 64-way split
+  // saved less in the conv than its partial tiles cost the reduce (c7 forward
+  // 24.8 -> 21.7 us per pass, tools/small_pass.py)
   p.ksplit = 1;
   p.part = nullptr;
   {
@@ -709,7 +712,8 @@ int conv_tapbox(int mode, const float* in, const Frame& inf, const float* w, int
     int ks = 2 * p.base_tiles <= num_sms() ? num_sms() / p.base_tiles : 1;
     const int min_entries = ne / ncls;
     if (ks > min_entries / 2) ks = min_entries / 2 > 1 ? min_entries / 2 : 1;
-    if (ks > 64) ks = 64;
+    static const int ks_cap = getenv("VPX_KSPLIT_MAX") ? atoi(getenv("VPX_KSPLIT_MAX")) : 16;
+    if (ks > ks_cap) ks = ks_cap > 1 ? ks_cap : 1;
     const int NTc = ntot <= 256 ? ntot : 256;
     if (getenv("VPX_NO_KSPLIT")) ks = 1;
     // the split depends on the shape only (never on how large a workspace the
