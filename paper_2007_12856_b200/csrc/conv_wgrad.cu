@@ -11,6 +11,10 @@
 //       zero-fill), so one MMA covers the three W taps at once.
 //     mode B (Cin % 128 == 0): block i = channel block i of a 128-channel
 //       tile (LBO = plane stride); W taps are separate MMAs.
+//     mode B, Cin = 64 (tap pairs): blocks 0-1 = the 64 channels at tap t,
+//       blocks 2-3 = the same channels at tap t + 1 (each tap applied in the
+//       TMA coordinates), so all 128 rows are useful: 14 sub-tasks instead of
+//       27 half-empty ones, every element summed in the same K order.
 //   B (N = Cout tile <= 256) = u: 32-channel blocks at LBO = plane stride.
 //
 // Split-K: CTA (sub, p) owns sub-task `sub` (mode A: depth tap a, the three H
@@ -36,6 +40,7 @@ struct WgradParams {
   int x_off_d, x_off_h, x_off_w;  // x frame margins
   int stride;                     // 1 or 2 (mode B only): x voxel = stride*o + tap - 1
   int ci_tiles, co_tiles;         // mode B tiling
+  int pair;                       // mode B, Cin = 64: two taps per 128-row tile
   float* part;                    // [P][cout][cin][27]
 };
 
@@ -66,8 +71,16 @@ __global__ void __launch_bounds__(256, 1)
   const int sub = blockIdx.x % p.nsub, pidx = blockIdx.x / p.nsub;
   const long long r0 = p.rows * pidx / p.P, r1 = p.rows * (pidx + 1) / p.P;
   int a, b = 0, c = 0, cit = 0, cot = 0;
+  int t0 = 0, t1 = -1;  // pair mode: taps of M rows 0-63 / 64-127 (-1: none)
   if (MODE_A) {
     a = sub;
+  } else if (p.pair) {
+    cot = sub % p.co_tiles;
+    t0 = 2 * (sub / p.co_tiles);
+    t1 = t0 + 1 < 27 ? t0 + 1 : -1;
+    a = t0 / 9;
+    b = (t0 / 3) % 3;
+    c = t0 % 3;
   } else {
     cot = sub % p.co_tiles;
     int t = sub / p.co_tiles;
@@ -106,7 +119,8 @@ __global__ void __launch_bounds__(256, 1)
       const int npl = MODE_A ? XPL : min(XPL, (p.cin - 128 * cit) / 32);
       const int xrows = (MODE_A || p.stride == 1) ? wseg + 4 : wseg;
       const int xw0 = (MODE_A || p.stride == 1) ? -1 : c - 1;
-      const uint32_t tx = npl * XROWS * xrows * kRow + NCO * wseg * kRow;
+      const int nplx = (!MODE_A && p.pair) ? (t1 >= 0 ? 4 : 2) : npl;
+      const uint32_t tx = nplx * XROWS * xrows * kRow + NCO * wseg * kRow;
       int stage = 0;
       uint32_t phase = 0;
       for (long long r = r0; r < r1; ++r) {
@@ -123,9 +137,17 @@ __global__ void __launch_bounds__(256, 1)
         uint8_t* su = sx + XB;
         vpx::mbar_arrive_expect_tx(&full[stage], tx);
         const int s = MODE_A ? 1 : p.stride;
-        for (int pl = 0; pl < npl; ++pl)
-          vpx::tma_load_5d(sx + pl * XPLANE, &xmap, &full[stage], 32 * (cit * 4 + pl), s * x0 + xw0 + p.x_off_w,
-                           s * y - 1 + b + p.x_off_h, s * z - 1 + a + p.x_off_d, n);
+        if (!MODE_A && p.pair) {
+          for (int pl = 0; pl < nplx; ++pl) {  // planes 0-1: tap t0, planes 2-3: tap t1
+            const int t = pl < 2 ? t0 : t1;
+            vpx::tma_load_5d(sx + pl * XPLANE, &xmap, &full[stage], 32 * (pl & 1), s * x0 + t % 3 - 1 + p.x_off_w,
+                             s * y - 1 + (t / 3) % 3 + p.x_off_h, s * z - 1 + t / 9 + p.x_off_d, n);
+          }
+        } else {
+          for (int pl = 0; pl < npl; ++pl)
+            vpx::tma_load_5d(sx + pl * XPLANE, &xmap, &full[stage], 32 * (cit * 4 + pl), s * x0 + xw0 + p.x_off_w,
+                             s * y - 1 + b + p.x_off_h, s * z - 1 + a + p.x_off_d, n);
+        }
 #pragma unroll
         for (int cb = 0; cb < NCO; ++cb)
           vpx::tma_load_5d(su + cb * UPLANE, &umap, &full[stage], 32 * (cot * NCO + cb), x0, y, z, n);
@@ -153,7 +175,7 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
           for (int bb = 0; bb < (MODE_A ? 3 : 1); ++bb) adesc[bb] = vpx::make_sdesc(xb + bb * xpitch, kRow, 512, 1);
         } else {
-          adesc[0] = vpx::make_sdesc(xb + (p.stride == 1 ? c : 0) * kRow, XPLANE, 512, 1);
+          adesc[0] = vpx::make_sdesc(xb + (p.stride == 1 && !p.pair ? c : 0) * kRow, XPLANE, 512, 1);
         }
         for (int k = 0; k < wseg; k += 8) {
           const uint32_t first = (r == r0 && k == 0) ? 0u : 1u;
@@ -181,13 +203,18 @@ __global__ void __launch_bounds__(256, 1)
       vpx::mbar_wait(&tfull, 0);
       vpx::tc_fence_after();
     }
-    int ci, cc;
+    int ci, cc, tap = 0;
     if (MODE_A) {
       cc = m >> 5;
       ci = m & 31;
+    } else if (p.pair) {
+      ci = m & 63;
+      tap = m < 64 ? t0 : t1;
+      cc = tap < 0 ? 3 : 0;
     } else {
       cc = c;
       ci = cit * 128 + m;
+      tap = (a * 3 + b) * 3 + c;
     }
     const bool valid = ci < p.cin && cc < 3;
     float* base = p.part + static_cast<long long>(pidx) * p.cout * p.cin * 27;
@@ -213,7 +240,7 @@ __global__ void __launch_bounds__(256, 1)
           // channels are one contiguous 128-byte run (the [co][ci][tap] order
           // scattered every store 108 bytes apart: ~40 us per deep-layer
           // filter gradient); reduce_partials_tapmajor transposes back
-          float* tb = base + static_cast<long long>((a * 3 + b) * 3 + cc) * p.cout * p.cin;
+          float* tb = base + static_cast<long long>(tap) * p.cout * p.cin;
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
             const int co = cot * NCOUT + col + j;
@@ -256,10 +283,15 @@ int launch_wgrad(const CUtensorMap& xm, const CUtensorMap& um, const WgradParams
   return VPX_OK;
 }
 
+// mode B with 64 input channels: two taps share the 128-row tile
+bool pair_mode(const vpx::Frame& xf) {
+  return xf.c == 64 && getenv("VPX_WGRAD_NOPAIR") == nullptr;
+}
+
 int nsub_of(const vpx::Frame& xf, const vpx::Frame& uf) {
   if (xf.c <= 32) return 3;
   const int nco = uf.c == 128 ? 128 : 256;
-  return 27 * ((xf.c + 127) / 128) * (uf.c / nco);
+  return (pair_mode(xf) ? 14 : 27 * ((xf.c + 127) / 128)) * (uf.c / nco);
 }
 
 }  // namespace
@@ -326,6 +358,7 @@ int conv_wgrad_tc(const float* x, const Frame& xf, const float* u, const Frame& 
   if (!modeA) {
     p.ci_tiles = (xf.c + 127) / 128;
     p.co_tiles = uf.c / (uf.c == 128 ? 128 : 256);
+    p.pair = pair_mode(xf) ? 1 : 0;
   }
   CUtensorMap xm, um;
   if (modeA || stride == 1) {

@@ -258,6 +258,36 @@ def test_conv_passes_vs_oracle(case):
     assert rel(wg.cpu().numpy(), wg_ref) < TF32_RTOL
 
 
+@pytest.mark.parametrize("cout,spatial,stride", [(128, (8, 8, 16), 2), (128, (4, 6, 8), 1), (256, (4, 4, 16), 1),
+                                                 (128, (6, 8, 64), 2), (128, (4, 4, 8), 2)])
+def test_wgrad_tap_pairs(cout, spatial, stride, monkeypatch):
+    """64-input-channel filter gradients (CosmoFlow c4) put two taps in the
+    128-row MMA tile; same result as the one-tap tiles (VPX_WGRAD_NOPAIR, a
+    different split-K partition, so equal up to fp32 summation order) and the
+    oracle, on a frame with D/H margins as under a spatial split."""
+    rng = np.random.default_rng(11)
+    n, cin = 1, 64
+    x = O.tf32_round(rng.uniform(-1, 1, (n, cin) + spatial).astype(np.float32))
+    od = tuple(-(-e // stride) for e in spatial)
+    u = O.tf32_round(rng.uniform(-1, 1, (n, cout) + od).astype(np.float32))
+    xf = Frame(n, cin, *spatial, (1, 1, 0), zero=True).load_ncdhw(x)
+    uf = Frame(n, cout, *od).load_ncdhw(u)
+    W = ws(cin, cout, 3, uf)
+
+    def run():
+        wg = torch.zeros(cout, cin, 3, 3, 3, device="cuda")
+        _lib.call("vpx_conv3d_bwd_filter", xf.ptr, xf.desc, uf.ptr, uf.desc, 3, stride, wg.data_ptr(), 0,
+                  W.data_ptr(), W.numel() * 4, stream_ptr())
+        torch.cuda.synchronize()
+        return wg.cpu().numpy()
+
+    got = run()
+    monkeypatch.setenv("VPX_WGRAD_NOPAIR", "1")
+    one = run()
+    assert np.abs(got - one).max() <= 1e-5 * np.abs(one).max()
+    assert rel(got, O.conv3d_bwd_filter(x, u, (3,) * 3, (stride,) * 3)) < TF32_RTOL
+
+
 def test_conv_fwd_frame_margins_and_dgrad_margins():
     """D/H-partitioned frames: the kernel must read the margin rows (here
     filled with neighbour data) and write dgrad over the margins too."""
