@@ -17,6 +17,8 @@
 #include <cstdlib>
 
 #include "conv_common.h"
+#include <algorithm>
+
 #include "conv_simt.h"
 #include "vpx_host.h"
 #include "vpx_ptx.cuh"
@@ -41,6 +43,8 @@ struct ConvTapParams {
   // per K entry: (od+1) | (oh+1)<<2 | (ow+1)<<4 | chunk<<8 | tap<<16
   int entries[kMaxEntries];
   int cls_start[9];             // entry ranges per parity class
+  int balance;                  // 1: tiles handed out heaviest class first, serpentine over CTAs
+  int cls_order[8];             // balance: classes by descending K entries
   float* out;
   long long out_sn, out_sd, out_sh, out_sw;
   int out_off_d, out_off_h, out_off_w;  // frame margins of the output
@@ -247,6 +251,19 @@ __global__ void __launch_bounds__(256, 1)
     zt = tile % p.td;
     n = tile / p.td;
   };
+  // j-th tile of this CTA.  Plain: round robin.  Balanced (stride-2 backward
+  // data: the 8 parity classes carry 1..8 taps, and round robin gave every
+  // CTA the same two classes -- up to 4x the work of the lightest CTAs): the
+  // tiles sorted heaviest class first, dealt out serpentine.  Every tile is
+  // still computed whole by one CTA, so the results are the same bits.
+  auto tile_of = [&](int j) -> int {
+    const int G = gridDim.x, b = blockIdx.x;
+    if (!p.balance) return b + j * G;
+    const int q = j * G + ((j & 1) ? G - 1 - b : b);
+    if (q >= p.num_tiles) return p.num_tiles;
+    const int per = p.num_tiles / p.ncls, rem = q % per;
+    return ((rem / p.ntn) * p.ncls + p.cls_order[q / per]) * p.ntn + rem % p.ntn;
+  };
   // K entries of this tile's class, restricted to its split
   auto krange = [&](int tile, int cls, int& e0, int& e1) {
     const int c0 = p.cls_start[cls], len = p.cls_start[cls + 1] - c0, ks = tile / p.base_tiles;
@@ -259,7 +276,7 @@ __global__ void __launch_bounds__(256, 1)
       const uint32_t a_tx = p.Db * p.Hb * p.Wb * 128;
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+      for (int j = 0, tile = tile_of(0); tile < p.num_tiles; tile = tile_of(++j)) {
         int nt, cls, n, zt, yt, xt;
         decode(tile, nt, cls, n, zt, yt, xt);
         const int qz = p.qd + zt * p.Db, qy = p.qh + yt * p.Hb, qx = p.qw + xt * p.Wb;
@@ -286,7 +303,7 @@ __global__ void __launch_bounds__(256, 1)
     constexpr uint32_t idesc = vpx::make_idesc(BF16 ? 1 : 2, 128, NT, false, false);
     int stage = 0, acc = 0;
     uint32_t phase = 0, aphase = 0;
-    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+    for (int j = 0, tile = tile_of(0); tile < p.num_tiles; tile = tile_of(++j)) {
       int nt, cls, n, zt, yt, xt;
       decode(tile, nt, cls, n, zt, yt, xt);
       int e0, e1;
@@ -328,7 +345,7 @@ __global__ void __launch_bounds__(256, 1)
     const int r = q * 32 + lane;  // row of the M tile
     int acc = 0;
     uint32_t aphase = 0;
-    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+    for (int j = 0, tile = tile_of(0); tile < p.num_tiles; tile = tile_of(++j)) {
       int nt, cls, n, zt, yt, xt;
       decode(tile, nt, cls, n, zt, yt, xt);
       int e0, e1;
@@ -728,6 +745,12 @@ int conv_tapbox(int mode, const float* in, const Frame& inf, const float* w, int
     }
   }
   p.num_tiles = p.base_tiles * p.ksplit;
+  p.balance = (ncls == 8 && p.ksplit == 1 && !getenv("VPX_TAPBOX_RR")) ? 1 : 0;
+  for (int c = 0; c < 8; ++c) p.cls_order[c] = c < ncls ? c : 0;
+  if (p.balance)  // stable: classes with equal entry counts keep their order
+    std::stable_sort(p.cls_order, p.cls_order + ncls, [&](int a, int b) {
+      return p.cls_start[a + 1] - p.cls_start[a] > p.cls_start[b + 1] - p.cls_start[b];
+    });
   p.in_stride = s_in;
   p.in_off_d = inf.md;
   p.in_off_h = inf.mh;

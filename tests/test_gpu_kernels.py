@@ -288,6 +288,36 @@ def test_wgrad_tap_pairs(cout, spatial, stride, monkeypatch):
     assert rel(got, O.conv3d_bwd_filter(x, u, (3,) * 3, (stride,) * 3)) < TF32_RTOL
 
 
+@pytest.mark.parametrize("cin,cout,spatial", [(64, 128, (16, 16, 16)), (64, 128, (6, 10, 32)), (128, 256, (8, 8, 8))])
+def test_tapbox_stride2_dgrad_balanced_tiles_bit_exact(cin, cout, spatial, monkeypatch):
+    """Stride-2 backward-data deals its tiles heaviest parity class first,
+    serpentine over the CTAs; every tile is still computed whole by one CTA,
+    so the gradient has the same bits as the round-robin order
+    (VPX_TAPBOX_RR) and stays within the TF32 tolerance of the oracle."""
+    rng = np.random.default_rng(5)
+    n = 1
+    w = (rng.standard_normal((cout, cin, 3, 3, 3)) / np.sqrt(27 * cin)).astype(np.float32)
+    od = tuple(-(-e // 2) for e in spatial)
+    u = O.tf32_round(rng.standard_normal((n, cout) + od).astype(np.float32))
+    wt = torch.from_numpy(w).cuda()
+    uf = Frame(n, cout, *od).load_ncdhw(u)
+
+    def run():
+        gf = Frame(n, cin, *spatial, (1, 1, 0), zero=True)
+        W = ws(cin, cout, 3, gf)
+        _lib.call("vpx_conv3d_bwd_data", uf.ptr, uf.desc, wt.data_ptr(), 3, 2, gf.ptr, gf.desc, W.data_ptr(),
+                  W.numel() * 4, stream_ptr())
+        torch.cuda.synchronize()
+        return gf
+
+    g1 = run()
+    monkeypatch.setenv("VPX_TAPBOX_RR", "1")
+    g2 = run()
+    assert torch.equal(g1.t, g2.t)
+    g_ref = O.conv3d_bwd_data(u, O.tf32_round(w), (3,) * 3, (2,) * 3, spatial)
+    assert rel(g1.to_ncdhw().cpu().numpy(), g_ref) < TF32_RTOL
+
+
 def test_conv_fwd_frame_margins_and_dgrad_margins():
     """D/H-partitioned frames: the kernel must read the margin rows (here
     filled with neighbour data) and write dgrad over the margins too."""
